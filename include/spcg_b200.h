@@ -1,0 +1,162 @@
+/*
+ * spcg_b200.h — C-ABI of the B200-native fp64 CG solve path.
+ *
+ * This is the drop-in boundary for the solve path of the reference package
+ * `spcg` (arxiv/paper_1010_4639).  The reference binds its hot path from
+ * Python into a Cython/OpenMP extension, one call per kernel:
+ *
+ *   reference call site                               replaced by
+ *   ------------------------------------------------  -----------------------------
+ *   _ckernels.csr_gather     (_ckernels.pyx:31-47)     spcg_spmv(CSR)
+ *   _ckernels.scatter_atomic (_ckernels.pyx:50-62)     spcg_spmv(SCSR, ATOMIC),
+ *                                                      spcg_spmv(CSC)
+ *   _ckernels.scatter_privatized (_ckernels.pyx:65-91) spcg_spmv(SCSR, PRIVATIZED)
+ *   _ckernels.dot_partials + config.pairwise_merge
+ *                (_ckernels.pyx:94-108, config.py:43-56) spcg_dot
+ *   _ckernels.axpy_kernel    (_ckernels.pyx:111-117)   spcg_axpy
+ *   solver.cg_solve loop body (solver.py:107-162)      spcg_cg_solve / spcg_cg_solve_host
+ *   core.CsrMatrix / SymHalfMatrix (core.py:57-156)    spcg_matrix_create_host
+ *   genprob.poisson2d/3d (genprob.py:50-93)            spcg_matrix_generate
+ *
+ * Conventions: plain pointers and sizes only.  Pointers named d_* are device
+ * pointers (any allocator: cudaMalloc, a torch tensor's data_ptr, ...); h_*
+ * are host pointers.  `stream` is a cudaStream_t passed as void* (0 = legacy
+ * default stream).  Every call returns an spcg_status; spcg_last_error()
+ * gives the message of the most recent failure on the calling thread.
+ * No call falls back to the CPU: without a usable sm_100 device every call
+ * returns SPCG_ERR_CUDA.
+ */
+#ifndef SPCG_B200_H
+#define SPCG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPCG_ABI_VERSION 1
+
+typedef enum {
+  SPCG_OK = 0,
+  SPCG_ERR_ARG = 1,          /* invalid argument (ValueError in Python)            */
+  SPCG_ERR_CUDA = 2,         /* CUDA runtime failure / no device                   */
+  SPCG_ERR_NOT_SPD = 3,      /* p'Ap <= 0  -> NotPositiveDefiniteError (solver.py:135) */
+  SPCG_ERR_NONFINITE_ALPHA = 4, /* solver.py:138-139 */
+  SPCG_ERR_NONFINITE_RESIDUAL = 5, /* solver.py:144-145 */
+  SPCG_ERR_NONFINITE_BETA = 6,  /* solver.py:154-155 */
+  SPCG_ERR_UNSUPPORTED = 7
+} spcg_status;
+
+/* Storage formats (core.py:57 CsrMatrix, core.py:103 SymHalfMatrix; CSC is new). */
+typedef enum {
+  SPCG_FMT_CSR = 0,   /* full CSR: row_start[n+1], col_idx[nnz], values[nnz]          */
+  SPCG_FMT_SCSR = 1,  /* symmetric half: CSR of L+D, col<=row, diagonal last per row  */
+  SPCG_FMT_CSC = 2    /* full CSC: col_start[n+1], row_idx[nnz], values[nnz]          */
+} spcg_format;
+
+/* Accumulation contract of the symmetric scatter (config.py:13-35). */
+typedef enum {
+  SPCG_ACC_ATOMIC = 0,      /* single pass over L+D, transpose scattered with fp64 red.add */
+  SPCG_ACC_PRIVATIZED = 1   /* deterministic owner-computes gather over a stored L^T;
+                               bitwise equal to the reference privatized mode at workers=1 */
+} spcg_accumulation;
+
+typedef struct spcg_matrix_s* spcg_matrix_t;
+
+/* ---- matrix handles ---------------------------------------------------- */
+
+/* Upload host CSR/SCSR/CSC arrays (int64 offsets and indices as in
+ * core.INDEX_DTYPE, fp64 values).  The device copy uses int32 indices,
+ * 16-byte-aligned arrays padded to a multiple of 4 entries, and a row-tile
+ * table (rows binned into tiles of <= 512 rows / <= 4096 entries).
+ * For SCSR the privatized-mode transpose L^T is built on the device lazily. */
+int spcg_matrix_create_host(int fmt, int64_t n, int64_t nnz,
+                            const int64_t* h_ptr, const int64_t* h_idx,
+                            const double* h_val, spcg_matrix_t* out);
+
+/* Same, from the u64 offsets / u32 indices of a .spcg container
+ * (matio.py:162-168) without widening to int64 first. */
+int spcg_matrix_create_host_u32(int fmt, int64_t n, int64_t nnz,
+                                const uint64_t* h_ptr, const uint32_t* h_idx,
+                                const double* h_val, spcg_matrix_t* out);
+
+/* Generate a reference-identical matrix directly in HBM.
+ * kind: 0 = poisson2d(d0,d1)      (genprob.py:50-70, diag 4, -1 per neighbour)
+ *       1 = poisson3d(d0,d1,d2)   (genprob.py:73-93, diag 6)
+ *       2 = stencil27(d0,d1,d2)   (27-point, diag 26, off-diagonal -1; new)
+ * fmt CSR emits the full matrix, SCSR its L+D (same as core.extract_lower). */
+int spcg_matrix_generate(int kind, int fmt, int64_t d0, int64_t d1, int64_t d2,
+                         spcg_matrix_t* out);
+
+int spcg_matrix_destroy(spcg_matrix_t m);
+
+/* n, stored entries, format, number of row tiles, device bytes held. */
+int spcg_matrix_info(spcg_matrix_t m, int64_t* n, int64_t* nnz, int* fmt,
+                     int64_t* ntiles, int64_t* device_bytes);
+
+/* Copy the device arrays back (int64 offsets/indices) — test helper. */
+int spcg_matrix_download(spcg_matrix_t m, int64_t* h_ptr, int64_t* h_idx, double* h_val);
+
+/* ---- kernel API (kernels/__init__.py:67-103) --------------------------- */
+
+/* y = A x.  CSR: sequential per-row sums, bitwise equal to csr_gather.
+ * SCSR: (L+D)x + L^T x per `accumulation`.  CSC: column scatter (atomic). */
+int spcg_spmv(spcg_matrix_t m, const double* d_x, double* d_y, int accumulation,
+              void* stream);
+
+/* *d_out = sum u[i] v[i], fixed-order two-level reduction (deterministic). */
+int spcg_dot(int64_t n, const double* d_u, const double* d_v, double* d_out,
+             void* stream);
+
+/* d_out = v + alpha*u elementwise (mul then add, no FMA: bitwise equal to
+ * axpy_kernel); alpha == 0 copies v (_compiled.py:50-51). */
+int spcg_axpy(int64_t n, double alpha, const double* d_u, const double* d_v,
+              double* d_out, void* stream);
+
+/* ---- CG solve (solver.py:65-172) -------------------------------------- */
+
+typedef struct {
+  double tol;                    /* CgOptions.tol (> 0)                        */
+  int64_t max_iter;              /* <= 0 -> max(1, n)  (solver.py:96)          */
+  int32_t record_history;        /* write rel residual per iteration to hist   */
+  int32_t recompute_final_residual; /* default 1 (solver.py:159-162)           */
+  int32_t accumulation;          /* spcg_accumulation, SCSR only               */
+  int32_t engine;                /* 0 = auto, 1 = persistent cooperative grid,
+                                    2 = per-pass kernels (multi-launch)        */
+} spcg_cg_options;
+
+typedef struct {
+  int64_t iterations;
+  int32_t converged;
+  int32_t status;                /* spcg_status of the solve                   */
+  int64_t fail_iteration;        /* iteration k named in breakdown messages    */
+  double final_relative_residual;
+  double b_norm;
+  double device_ms;              /* CUDA-event time of the solve on `stream`   */
+  int64_t kernel_launches;       /* kernels launched by this solve             */
+} spcg_cg_result;
+
+/* Device-resident solve.  d_x0 may be NULL (zeros).  d_x receives x.
+ * d_hist (may be NULL unless record_history) must hold max_iter doubles.
+ * Breakdowns are reported in result->status and returned. */
+int spcg_cg_solve(spcg_matrix_t m, const double* d_b, const double* d_x0,
+                  double* d_x, double* d_hist, const spcg_cg_options* opts,
+                  spcg_cg_result* result, void* stream);
+
+/* Same from host buffers: H2D of b (and x0), solve, D2H of x (and history). */
+int spcg_cg_solve_host(spcg_matrix_t m, const double* h_b, const double* h_x0,
+                       double* h_x, double* h_hist, const spcg_cg_options* opts,
+                       spcg_cg_result* result, void* stream);
+
+/* ---- library ------------------------------------------------------------ */
+
+const char* spcg_last_error(void);
+int spcg_abi_version(void);
+/* SMs of the current device and the cooperative grid the solver uses. */
+int spcg_device_info(int* sm_count, int* coop_grid, int* cc_major, int* cc_minor);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPCG_B200_H */

@@ -1,0 +1,225 @@
+// lines.cuh — per-line SpMV bodies over a staged tile (one thread per line).
+//
+// The gathered vector is abstracted as a "source":
+//   SrcPlain  x_j            (y = A x; r0 = b - A x0; true residual)
+//   SrcFirst  r_j            (CG iteration 1: p_1 = r_0, solver.py:123)
+//   SrcFold   r_j + beta*p_j (CG iteration k>1: the p-update of solver.py:156
+//                             folded into the next SpMV's gather, so p is never
+//                             re-read and re-written in a separate pass)
+// Row sums are formed sequentially in storage order with IEEE mul-then-add, so
+// a CSR row equals _ckernels.csr_gather (_ckernels.pyx:42-47) bit for bit.
+#pragma once
+#include "tiles.cuh"
+
+namespace spcg {
+
+struct SrcPlain {
+  const double* x;
+  __device__ __forceinline__ double get(int j) const { return x[j]; }
+};
+struct SrcFirst {
+  const double* r;
+  __device__ __forceinline__ double get(int j) const { return r[j]; }
+};
+struct SrcFold {
+  const double* r;
+  const double* p;
+  double beta;
+  __device__ __forceinline__ double get(int j) const {
+    return __dadd_rn(r[j], __dmul_rn(beta, p[j]));
+  }
+};
+
+constexpr int kUnroll = 8;
+
+// acc = sum_k v[k]*src(ix[k]) over [ks,ke), sequential order; loads batched
+// kUnroll-deep so each thread keeps many gathers in flight.
+template <class Src>
+__device__ __forceinline__ double seq_row(const double* v, const int* ix, int ks, int ke,
+                                          const Src& src) {
+  double acc = 0.0;
+  for (int k = ks; k < ke; k += kUnroll) {
+    double pr[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      pr[u] = (k + u < ke) ? __dmul_rn(v[k + u], src.get(ix[k + u])) : 0.0;
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (k + u < ke) acc = __dadd_rn(acc, pr[u]);
+  }
+  return acc;
+}
+
+// Symmetric L+D row i (diagonal last): g = sum_{j<=i} a_ij x_j, and the
+// transpose contributions a_ij * x_i scattered into y_j (j<i) with fp64 red.
+template <class Src>
+__device__ __forceinline__ double sym_row_atomic(const double* v, const int* ix, int ks, int ke,
+                                                 int i, double xi, const Src& src, double* y) {
+  double acc = 0.0;
+  for (int k = ks; k < ke; k += kUnroll) {
+    double pr[kUnroll];
+    int jj[kUnroll];
+    double vv[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const bool ok = k + u < ke;
+      jj[u] = ok ? ix[k + u] : i;
+      vv[u] = ok ? v[k + u] : 0.0;
+      pr[u] = ok ? __dmul_rn(vv[u], src.get(jj[u])) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      if (k + u < ke) {
+        acc = __dadd_rn(acc, pr[u]);
+        if (jj[u] != i) red_add_f64(y + jj[u], __dmul_rn(vv[u], xi));
+      }
+    }
+  }
+  return acc;
+}
+
+// CSC column j: y[row_k] += a_kj * xj (red), and (if GATHER) the transposed
+// gather g = sum_k a_kj x_{row_k} that makes p.Ap = sum_j p_j g_j.
+template <bool GATHER, class Src>
+__device__ __forceinline__ double csc_col(const double* v, const int* ix, int ks, int ke,
+                                          double xj, const Src& src, double* y) {
+  double acc = 0.0;
+  for (int k = ks; k < ke; k += kUnroll) {
+    double pr[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      if (k + u < ke) {
+        const int row = ix[k + u];
+        const double a = v[k + u];
+        red_add_f64(y + row, __dmul_rn(a, xj));
+        pr[u] = GATHER ? __dmul_rn(a, src.get(row)) : 0.0;
+      } else {
+        pr[u] = 0.0;
+      }
+    }
+    if (GATHER) {
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u)
+        if (k + u < ke) acc = __dadd_rn(acc, pr[u]);
+    }
+  }
+  return acc;
+}
+
+// ---- long lines: one line with > kTileNnz entries, read from global by the
+// whole CTA (strided partial sums + fixed-order block reduction).
+template <class Src>
+__device__ __forceinline__ double long_gather(const double* val, const int* idx, int k0, int k1,
+                                              const Src& src, Smem& sm) {
+  double part = 0.0;
+  for (int k = k0 + (int)threadIdx.x; k < k1; k += blockDim.x)
+    part = __dadd_rn(part, __dmul_rn(ld_stream_f64(val + k), src.get(ld_stream_s32(idx + k))));
+  return block_sum(part, sm);
+}
+
+// Result of one line of a tile pass: the line's output value and the line's
+// p.Ap contribution pieces (only meaningful where the caller needs them).
+struct LineOut {
+  double q;    // (A x)_i for CSR / SCSR_PRIV; g_i for SCSR_ATOMIC / CSC
+  double xi;   // src(i): the gathered-vector value of the line itself
+  double dg;   // SCSR_ATOMIC: diagonal a_ii
+};
+
+// Computes line i (the tid-th line of staged tile s).  For FMT in
+// {SCSR_ATOMIC, CSC} the scatter goes to y (must be zeroed beforehand) and
+// the line's own gather is returned in q; for CSR / SCSR_PRIV the caller
+// stores q.  `active` = this thread owns a line.  Long tiles: every thread
+// must call (CTA-wide reductions); the line's result is valid in thread 0.
+template <int FMT, bool GATHER_CSC, class Src>
+__device__ __forceinline__ LineOut tile_line(Smem& sm, int s, const MatView& M, const Src& src,
+                                             double* y, bool& active, int& line) {
+  const StageMeta& mt = sm.meta[s];
+  LineOut o{0.0, 0.0, 0.0};
+  if (!mt.is_long) {
+    const int i = mt.row0 + (int)threadIdx.x;
+    active = i < mt.row1;
+    line = i;
+    if (!active) return o;
+    const int lr = i - mt.r0a;
+    const int ks = sm.rpA[s][lr] - mt.kA0a;
+    const int ke = sm.rpA[s][lr + 1] - mt.kA0a;
+    const double* v = sm.val[s];
+    const int* ix = sm.idx[s];
+    if (FMT == K_CSR) {
+      o.q = seq_row(v, ix, ks, ke, src);
+      o.xi = src.get(i);
+    } else if (FMT == K_SCSR_PRIV) {
+      const int kb = sm.rpB[s][lr] - mt.kB0a + mt.offB;
+      const int kbe = sm.rpB[s][lr + 1] - mt.kB0a + mt.offB;
+      const double g = seq_row(v, ix, ks, ke, src);
+      const double t = seq_row(v, ix, kb, kbe, src);
+      o.q = __dadd_rn(g, t);
+      o.xi = src.get(i);
+    } else if (FMT == K_SCSR_ATOMIC) {
+      o.xi = src.get(i);
+      o.q = sym_row_atomic(v, ix, ks, ke, i, o.xi, src, y);
+      o.dg = (ke > ks) ? v[ke - 1] : 0.0;
+    } else {  // K_CSC
+      o.xi = src.get(i);
+      o.q = csc_col<GATHER_CSC>(v, ix, ks, ke, o.xi, src, y);
+    }
+    return o;
+  }
+  // long tile: one line, entries from global memory
+  const int i = mt.row0;
+  line = i;
+  active = threadIdx.x == 0;
+  const int k0 = M.ptrA[i], k1 = M.ptrA[i + 1];
+  if (FMT == K_CSR) {
+    o.q = long_gather(M.valA, M.idxA, k0, k1, src, sm);
+    o.xi = src.get(i);
+  } else if (FMT == K_SCSR_PRIV) {
+    const double g = long_gather(M.valA, M.idxA, k0, k1, src, sm);
+    const double t = long_gather(M.valB, M.idxB, M.ptrB[i], M.ptrB[i + 1], src, sm);
+    o.q = __dadd_rn(g, t);
+    o.xi = src.get(i);
+  } else if (FMT == K_SCSR_ATOMIC) {
+    const double xi = src.get(i);
+    double part = 0.0;
+    for (int k = k0 + (int)threadIdx.x; k < k1; k += blockDim.x) {
+      const int j = ld_stream_s32(M.idxA + k);
+      const double a = ld_stream_f64(M.valA + k);
+      part = __dadd_rn(part, __dmul_rn(a, src.get(j)));
+      if (j != i) red_add_f64(y + j, __dmul_rn(a, xi));
+    }
+    o.q = block_sum(part, sm);
+    o.xi = xi;
+    o.dg = (k1 > k0) ? M.valA[k1 - 1] : 0.0;
+  } else {
+    const double xj = src.get(i);
+    double part = 0.0;
+    for (int k = k0 + (int)threadIdx.x; k < k1; k += blockDim.x) {
+      const int row = ld_stream_s32(M.idxA + k);
+      const double a = ld_stream_f64(M.valA + k);
+      red_add_f64(y + row, __dmul_rn(a, xj));
+      if (GATHER_CSC) part = __dadd_rn(part, __dmul_rn(a, src.get(row)));
+    }
+    o.q = GATHER_CSC ? block_sum(part, sm) : 0.0;
+    o.xi = xj;
+  }
+  return o;
+}
+
+// Finish a line of a plain SpMV y = A x (no CG bookkeeping).
+template <int FMT>
+__device__ __forceinline__ void finish_plain(const LineOut& o, int i, double* y) {
+  if (FMT == K_CSR || FMT == K_SCSR_PRIV) y[i] = o.q;
+  else if (FMT == K_SCSR_ATOMIC) red_add_f64(y + i, o.q);
+  // CSC: the column scatter already wrote everything
+}
+
+// p.Ap contribution of a line (p_i = o.xi):
+//   CSR / SCSR_PRIV: p_i q_i;  SCSR_ATOMIC: p_i (2 g_i - a_ii p_i)
+//   (p'Ap = 2 p'(L+D)p - p'Dp);  CSC: p_j g_j  (p'A p = p'A^T p).
+template <int FMT>
+__device__ __forceinline__ double line_pq(const LineOut& o) {
+  if (FMT == K_SCSR_ATOMIC) return o.xi * (2.0 * o.q - o.dg * o.xi);
+  return o.xi * o.q;
+}
+
+}  // namespace spcg

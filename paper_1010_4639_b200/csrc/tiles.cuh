@@ -1,0 +1,200 @@
+// tiles.cuh — row-tile staging of CSR/SCSR/CSC arrays into shared memory.
+//
+// HBM layout (built by matrix.cu at upload):
+//   ptr  int32[n+1 (+8 pad)]   idx int32[nnz (+8 pad)]   val f64[nnz (+8 pad)]
+//   every array 256-byte aligned; pads are zero so 16-byte-rounded bulk copies
+//   never read past an allocation.
+//   tdesc int4[ntiles] = {row0, row1, k0, k1}: lines [row0,row1) hold stored
+//   entries [k0,k1); a tile has <= kTileLines lines and <= kTileNnz entries,
+//   except a "long" tile = one line with more entries than kTileNnz.
+//   For the privatized symmetric mode a second segment (CSR of L^T) rides in
+//   the same tile: tdescB int2[ntiles] = {k0B, k1B}.
+//
+// One tile = one stage of the shared-memory ring: its row-pointer slice, index
+// slice and value slice arrive by 1-D bulk async copies (cp.async.bulk,
+// completion on an mbarrier), issued by thread 0 one or more tiles ahead of the
+// consumer, so HBM streaming overlaps the x-gathers and the grid barriers.
+#pragma once
+#include "ptx.cuh"
+
+namespace spcg {
+
+constexpr int kBlock = 512;        // threads per CTA == lines per tile
+constexpr int kTileLines = kBlock;
+constexpr int kTileNnz = 4096;     // stored entries per tile (both segments)
+constexpr int kStages = 2;
+constexpr int kRpCap = kTileLines + 8;
+constexpr int kNzCap = kTileNnz + 16;
+
+// Kernel-level storage variants.
+enum KFmt : int { K_CSR = 0, K_SCSR_ATOMIC = 1, K_SCSR_PRIV = 2, K_CSC = 3 };
+
+struct MatView {
+  int n;
+  int ntiles;
+  const int4* tdesc;     // {row0,row1,k0,k1}
+  const int2* tdescB;    // {k0B,k1B} (K_SCSR_PRIV only)
+  const int* ptrA;
+  const int* idxA;
+  const double* valA;
+  const int* ptrB;       // CSR of L^T (K_SCSR_PRIV only)
+  const int* idxB;
+  const double* valB;
+};
+
+struct StageMeta {
+  int row0, row1;   // lines [row0,row1)
+  int r0a;          // row-pointer slice starts at ptr[r0a]
+  int kA0a, kB0a;   // first staged entry of each segment (4-aligned)
+  int offB;         // segment B's offset inside the stage buffers
+  int is_long;      // 1: entries not staged, read from global
+  int pad;
+};
+
+struct __align__(16) Smem {
+  double val[kStages][kNzCap];
+  int idx[kStages][kNzCap];
+  int rpA[kStages][kRpCap];
+  int rpB[kStages][kRpCap];
+  uint64_t full[kStages];
+  StageMeta meta[kStages];
+  double red[32];
+  double bcast;
+};
+
+__device__ __forceinline__ int my_tile(int j) { return blockIdx.x + j * gridDim.x; }
+__device__ __forceinline__ int my_tile_count(int ntiles) {
+  return (ntiles > (int)blockIdx.x) ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+}
+
+// Thread 0 only: stage tile `t` into ring slot `s`.
+template <bool TWO>
+__device__ __forceinline__ void issue_tile(Smem& sm, const MatView& M, int t, int s) {
+  const int4 d = M.tdesc[t];
+  const int row0 = d.x, row1 = d.y, kA0 = d.z, kA1 = d.w;
+  int kB0 = 0, kB1 = 0;
+  if (TWO) {
+    const int2 e = M.tdescB[t];
+    kB0 = e.x;
+    kB1 = e.y;
+  }
+  StageMeta& mt = sm.meta[s];
+  mt.row0 = row0;
+  mt.row1 = row1;
+  const int r0a = row0 & ~3;
+  const int rcnt = ((row1 + 1 + 3) & ~3) - r0a;
+  mt.r0a = r0a;
+  const int nA = kA1 - kA0, nB = kB1 - kB0;
+  const bool is_long = (nA + nB) > kTileNnz;
+  mt.is_long = is_long;
+  uint32_t bytes = (uint32_t)rcnt * 4u * (TWO ? 2u : 1u);
+  int kA0a = kA0 & ~3, cA = 0, kB0a = kB0 & ~3, cB = 0;
+  if (!is_long) {
+    cA = (nA > 0) ? ((kA1 + 3) & ~3) - kA0a : 0;
+    cB = (TWO && nB > 0) ? ((kB1 + 3) & ~3) - kB0a : 0;
+    bytes += (uint32_t)(cA + cB) * 12u;
+  }
+  mt.kA0a = kA0a;
+  mt.kB0a = kB0a;
+  mt.offB = cA;
+  fence_proxy_async_smem();
+  mbar_arrive_expect_tx(&sm.full[s], bytes);
+  bulk_g2s(sm.rpA[s], M.ptrA + r0a, (uint32_t)rcnt * 4u, &sm.full[s]);
+  if (TWO) bulk_g2s(sm.rpB[s], M.ptrB + r0a, (uint32_t)rcnt * 4u, &sm.full[s]);
+  if (cA > 0) {
+    bulk_g2s(sm.idx[s], M.idxA + kA0a, (uint32_t)cA * 4u, &sm.full[s]);
+    bulk_g2s(sm.val[s], M.valA + kA0a, (uint32_t)cA * 8u, &sm.full[s]);
+  }
+  if (TWO && cB > 0) {
+    bulk_g2s(sm.idx[s] + cA, M.idxB + kB0a, (uint32_t)cB * 4u, &sm.full[s]);
+    bulk_g2s(sm.val[s] + cA, M.valB + kB0a, (uint32_t)cB * 8u, &sm.full[s]);
+  }
+}
+
+// Ring of kStages stages over this CTA's tile list (t = blockIdx.x + j*gridDim.x).
+// If the CTA owns <= kStages tiles they are loaded once and stay resident in
+// shared memory for the whole kernel (the 30880-row matrix fits this way);
+// otherwise the list is streamed cyclically, prefetching kStages tiles ahead,
+// across pass and iteration boundaries.
+struct Pipe {
+  int m;
+  bool resident;
+  long long c;  // tiles consumed (streaming mode)
+};
+
+template <bool TWO>
+__device__ __forceinline__ void pipe_start(Pipe& P, Smem& sm, const MatView& M) {
+  P.m = my_tile_count(M.ntiles);
+  P.resident = P.m <= kStages;
+  P.c = 0;
+  if (threadIdx.x == 0) {
+    const int pre = P.m < kStages ? P.m : kStages;
+    for (int j = 0; j < pre; ++j) issue_tile<TWO>(sm, M, my_tile(j), j);
+  }
+}
+
+// Stage holding the j-th tile of the current pass (waits for its bytes).
+__device__ __forceinline__ int pipe_acquire(Pipe& P, Smem& sm, int j) {
+  if (P.resident) {
+    mbar_wait(&sm.full[j], 0);
+    return j;
+  }
+  const int s = (int)(P.c % kStages);
+  mbar_wait(&sm.full[s], (uint32_t)((P.c / kStages) & 1));
+  return s;
+}
+
+// Done with the stage returned by pipe_acquire: recycle it for a later tile.
+template <bool TWO>
+__device__ __forceinline__ void pipe_release(Pipe& P, Smem& sm, const MatView& M, int s) {
+  if (P.resident) return;
+  __syncthreads();
+  if (threadIdx.x == 0) issue_tile<TWO>(sm, M, my_tile((int)((P.c + kStages) % P.m)), s);
+  P.c++;
+}
+
+// Wait for copies still in flight before the CTA exits.
+__device__ __forceinline__ void pipe_drain(Pipe& P, Smem& sm) {
+  if (P.m == 0) return;
+  if (P.resident) {
+    for (int j = 0; j < P.m; ++j) mbar_wait(&sm.full[j], 0);
+    return;
+  }
+  for (int u = 0; u < kStages; ++u) {
+    const long long q = P.c + u;
+    mbar_wait(&sm.full[q % kStages], (uint32_t)((q / kStages) & 1));
+  }
+}
+
+__device__ __forceinline__ void smem_init(Smem& sm) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&sm.full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+}
+
+// ---- deterministic reductions ------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Fixed-order block sum, result broadcast to every thread.
+__device__ __forceinline__ double block_sum(double v, Smem& sm) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();  // protects sm.red / sm.bcast reuse
+  if (lane == 0) sm.red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    double t = (lane < (int)(blockDim.x >> 5)) ? sm.red[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) sm.bcast = t;
+  }
+  __syncthreads();
+  return sm.bcast;
+}
+
+}  // namespace spcg

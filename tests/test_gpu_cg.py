@@ -1,0 +1,249 @@
+"""cg_solve on the B200 vs the reference's behaviour (tests/test_solver.py and
+test_acceptance.py of the reference, re-pointed at the device path) and vs
+the oracle / golden reference runs on the benchmark matrices."""
+
+import numpy as np
+import pytest
+
+from conftest import rel_inf_err
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def two_by_two():
+    from paper_1010_4639_b200 import build_csr_from_triplets
+
+    return build_csr_from_triplets([(0, 0, 4.0), (0, 1, 1.0), (1, 0, 1.0), (1, 1, 3.0)], 2)
+
+
+def diag_matrix(values):
+    from paper_1010_4639_b200 import build_csr_from_triplets
+
+    return build_csr_from_triplets([(i, i, float(v)) for i, v in enumerate(values)], len(values))
+
+
+STORAGES = ["csr", "sym_priv", "sym_atomic", "csc"]
+
+
+def as_storage(a, kind):
+    from paper_1010_4639_b200 import KernelConfig, extract_lower
+
+    if kind == "csr":
+        return a, KernelConfig()
+    if kind == "csc":
+        return a.to_csc(), KernelConfig()
+    acc = "privatized" if kind == "sym_priv" else "atomic"
+    return extract_lower(a), KernelConfig(accumulation=acc)
+
+
+@pytest.mark.parametrize("kind", STORAGES)
+def test_identity_one_iteration(kind):
+    from paper_1010_4639_b200 import cg_solve
+
+    m, cfg = as_storage(diag_matrix(np.ones(7)), kind)
+    b = np.random.default_rng(0).standard_normal(7)
+    r = cg_solve(m, b, cfg=cfg)
+    assert r.converged and r.iterations == 1
+    assert np.allclose(r.x, b, atol=1e-14)
+
+
+@pytest.mark.parametrize("kind", STORAGES)
+def test_2x2_direct(kind):
+    from paper_1010_4639_b200 import cg_solve
+
+    m, cfg = as_storage(two_by_two(), kind)
+    r = cg_solve(m, np.array([1.0, 2.0]), cfg=cfg)
+    assert r.converged and r.iterations <= 2
+    assert np.allclose(r.x, [1 / 11, 7 / 11], atol=1e-10)
+
+
+@pytest.mark.parametrize("k", [1, 2, 5, 10])
+def test_distinct_eigenvalue_bound(k):
+    from paper_1010_4639_b200 import cg_solve
+
+    rng = np.random.default_rng(k)
+    a = diag_matrix([1.0 + (i % k) for i in range(32)])
+    b = rng.standard_normal(32)
+    r = cg_solve(a, b)
+    assert r.converged and r.iterations <= k + 2
+    assert np.allclose(r.x, np.linalg.solve(a.to_dense(), b), atol=1e-9)
+
+
+def test_zero_rhs_returns_zero_even_with_x0():
+    from paper_1010_4639_b200 import cg_solve
+
+    r = cg_solve(two_by_two(), np.zeros(2), x0=np.ones(2))
+    assert r.converged and r.iterations == 0
+    assert (r.x == 0.0).all() and r.final_relative_residual == 0.0
+
+
+def test_x0_already_converged():
+    from paper_1010_4639_b200 import CgOptions, cg_solve
+
+    a = two_by_two()
+    x = np.array([1 / 11, 7 / 11])
+    b = a.to_dense() @ x
+    r = cg_solve(a, b, x0=x, opts=CgOptions(tol=1e-6, record_history=True))
+    assert r.converged and r.iterations == 0 and r.residual_history == []
+
+
+def test_random_spd_finite_termination():
+    from paper_1010_4639_b200 import cg_solve
+    from paper_1010_4639_b200.genprob import random_spd
+
+    rng = np.random.default_rng(77)
+    for _ in range(15):
+        n = int(rng.integers(2, 65))
+        a = random_spd(n, 0.2, int(rng.integers(1 << 30)))
+        x_ref = rng.standard_normal(n)
+        r = cg_solve(a, a.to_dense() @ x_ref)
+        assert r.converged and r.iterations <= n + 5
+        assert np.allclose(r.x, x_ref, atol=1e-7)
+
+
+def test_history_and_truncation():
+    from paper_1010_4639_b200 import CgOptions, cg_solve
+    from paper_1010_4639_b200.genprob import poisson2d
+
+    a = poisson2d(5, 5)
+    r = cg_solve(a, np.ones(25), opts=CgOptions(record_history=True))
+    assert len(r.residual_history) == r.iterations
+    t = cg_solve(a, np.ones(25), opts=CgOptions(record_history=True, max_iter=3))
+    assert not t.converged and t.iterations == 3 and len(t.residual_history) == 3
+    assert set(r.timings) == {"spmv", "dot", "axpy", "total"} and r.timings["total"] > 0
+
+
+def test_not_positive_definite():
+    from paper_1010_4639_b200 import NotPositiveDefiniteError, cg_solve
+
+    with pytest.raises(NotPositiveDefiniteError, match="not positive definite"):
+        cg_solve(diag_matrix([1.0, -1.0]), np.array([1.0, 2.0]))
+
+
+def test_dimension_mismatch():
+    from paper_1010_4639_b200 import cg_solve
+
+    with pytest.raises(ValueError):
+        cg_solve(two_by_two(), np.ones(3))
+    with pytest.raises(ValueError):
+        cg_solve(two_by_two(), np.ones(2), x0=np.ones(3))
+    with pytest.raises(TypeError):
+        cg_solve(np.eye(2), np.ones(2))
+
+
+def test_golden_poisson32_all_storages(golden):
+    """Acceptance criterion 4 against the reference's own CG run."""
+    from paper_1010_4639_b200 import CgOptions, cg_solve
+    from paper_1010_4639_b200.genprob import poisson2d
+
+    g = golden("cg_small")
+    a = poisson2d(32, 32)
+    its = []
+    for kind in STORAGES:
+        m, cfg = as_storage(a, kind)
+        r = cg_solve(m, g["p2_b"], opts=CgOptions(max_iter=1029, record_history=True), cfg=cfg)
+        ref_it = int(g["p2_full_it"])
+        assert abs(r.iterations - ref_it) <= max(1, 0.01 * ref_it), kind
+        assert np.linalg.norm(r.x - g["p2_full_x"]) / np.linalg.norm(g["p2_full_x"]) <= 1e-8
+        assert np.max(np.abs(r.x - g["p2_xgen"])) <= 1e-8
+        its.append(r.iterations)
+    assert max(its) - min(its) <= 1
+
+
+def test_golden_x0_and_truncation(golden):
+    from paper_1010_4639_b200 import CgOptions, cg_solve
+    from paper_1010_4639_b200.genprob import poisson3d
+
+    g = golden("cg_small")
+    a = poisson3d(12, 12, 12)
+    r = cg_solve(a, g["p3_b"], x0=g["p3_x0"], opts=CgOptions(tol=1e-9, record_history=True))
+    assert abs(r.iterations - int(g["p3_it"])) <= 1
+    assert np.linalg.norm(r.x - g["p3_x"]) / np.linalg.norm(g["p3_x"]) <= 1e-8
+    t = cg_solve(a, g["p3_b"], x0=g["p3_x0"],
+                 opts=CgOptions(max_iter=7, recompute_final_residual=False))
+    assert t.iterations == 7 and not t.converged
+    assert abs(t.final_relative_residual - float(g["p3t_final"])) <= 1e-10 * float(g["p3t_final"])
+    assert rel_inf_err(t.x, g["p3t_x"]) <= 1e-12
+
+
+@pytest.mark.parametrize("kind", STORAGES)
+def test_fem_mesh_parity(golden, kind):
+    """The paper-sized FEM-shaped matrix (30880 rows, 449,798 nnz): same
+    iteration count +-1% and ||x - x_ref|| / ||x_ref|| <= 1e-8 against the
+    reference CG's own output."""
+    from paper_1010_4639_b200 import CgOptions, cg_solve
+    from paper_1010_4639_b200.genprob import fem_mesh
+
+    g = golden("fem")
+    F = fem_mesh()
+    m, cfg = as_storage(F, kind)
+    r = cg_solve(m, g["F_b"], opts=CgOptions(record_history=True), cfg=cfg)
+    ref_it = int(g["F_full_it"])
+    assert abs(r.iterations - ref_it) <= max(1, int(0.01 * ref_it)), r.iterations
+    xr = g["F_full_x"]
+    assert np.linalg.norm(r.x - xr) / np.linalg.norm(xr) <= 1e-8
+    assert r.converged and r.final_relative_residual <= 1e-10
+    h = np.array(r.residual_history)
+    k = min(len(h), 200)
+    assert np.allclose(h[:k], g["F_full_hist"][:k], rtol=1e-6)
+
+
+def test_fem_rand_parity(golden):
+    from paper_1010_4639_b200 import cg_solve
+    from paper_1010_4639_b200.genprob import random_spd
+
+    g = golden("fem")
+    R = random_spd(30880, 418918 / 30880**2, 1)
+    b = O.spmv_full(R.row_start, R.col_idx, R.values, np.random.default_rng(1).standard_normal(R.n))
+    r = cg_solve(R, b)
+    assert abs(r.iterations - int(g["R_it"])) <= 1
+    assert np.linalg.norm(r.x - g["R_x"]) / np.linalg.norm(g["R_x"]) <= 1e-8
+
+
+def test_sym_privatized_is_deterministic():
+    from paper_1010_4639_b200 import KernelConfig, cg_solve, extract_lower
+    from paper_1010_4639_b200.genprob import poisson2d
+
+    s = extract_lower(poisson2d(40, 40))
+    b = np.random.default_rng(13).standard_normal(s.n)
+    runs = [cg_solve(s, b, cfg=KernelConfig(accumulation="privatized")) for _ in range(4)]
+    assert len({r.iterations for r in runs}) == 1
+    assert len({r.final_relative_residual for r in runs}) == 1
+    assert all((r.x == runs[0].x).all() for r in runs)
+
+
+def test_streaming_engine_matches_oracle():
+    """A matrix too large for the resident kernel exercises the streamed
+    tile pipeline; compare a 20-iteration window against the oracle."""
+    from paper_1010_4639_b200 import CgOptions, cg_solve
+    from paper_1010_4639_b200.genprob import poisson3d
+
+    a = poisson3d(64, 64, 64)
+    dev = a.device()
+    assert dev.info()["ntiles"] > 2 * 148
+    b = np.random.default_rng(3).standard_normal(a.n)
+    r = cg_solve(a, b, opts=CgOptions(max_iter=20, record_history=True))
+    o = O.cg_solve("csr", a.row_start, a.col_idx, a.values, b, max_iter=20, record_history=True,
+                   workers=8)
+    assert r.iterations == o.iterations == 20
+    assert np.linalg.norm(r.x - o.x) / np.linalg.norm(o.x) <= 1e-12
+    assert np.allclose(r.residual_history, o.residual_history, rtol=1e-10)
+    full = cg_solve(a, b)
+    of = O.cg_solve("csr", a.row_start, a.col_idx, a.values, b, workers=8)
+    assert abs(full.iterations - of.iterations) <= max(1, of.iterations // 100)
+    assert np.linalg.norm(full.x - of.x) / np.linalg.norm(of.x) <= 1e-8
+
+
+def test_torch_resident_solve():
+    import torch
+
+    from paper_1010_4639_b200 import cg_solve
+    from paper_1010_4639_b200.genprob import poisson2d
+
+    a = poisson2d(30, 30)
+    b = torch.randn(a.n, dtype=torch.float64, device="cuda")
+    r = cg_solve(a, b)
+    assert r.x.is_cuda and r.converged
+    o = O.cg_solve("csr", a.row_start, a.col_idx, a.values, b.cpu().numpy())
+    assert np.linalg.norm(r.x.cpu().numpy() - o.x) / np.linalg.norm(o.x) <= 1e-8
