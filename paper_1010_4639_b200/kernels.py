@@ -84,8 +84,9 @@ def get_backend() -> str:
     return _active
 
 
-set_backend(os.environ.get("SPCG_BACKEND", "auto") if os.environ.get("SPCG_BACKEND") in
-            (None, "auto", "cuda") else "cuda")
+# SPCG_BACKEND (kernels/__init__.py:50) may name a reference backend; the
+# only implementation here is the device one.
+set_backend("auto")
 
 
 # ---- device buffer plumbing --------------------------------------------------
