@@ -1,0 +1,430 @@
+"""Benchmark: fp64 CG iterations/s (and SpMV HBM GB/s, % of roofline) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload p3|p2|q27|f|s|csc] [--max-iter M]
+
+Workload (BASELINE.json configs[3]; the largest single-GPU config and the one
+the metric's 1/2/4/8-GPU scaling is quoted on): 3-D 7-point Poisson 400^3
+(n = 64,000,000, nnz = 447,040,000), full CSR, fp64, x0 = 0, b = A x_gen with
+x_gen = default_rng(1).standard_normal(n), tol 1e-10.  One step = one complete
+cg_solve (944 iterations + the true-residual recompute).  Inputs (5.6 GB of
+matrix) are far larger than L2 (126 MB), so no L2 flush is needed.
+
+`value` = total CG iterations / device time of K solves (CUDA events on the
+solve stream, barrier + synchronize on both sides, max over ranks);
+`e2e` = the same through the C-ABI host entry point spcg_cg_solve_host with
+b in pinned host memory and x copied back every step.
+`roofline` = algorithmic bytes of one solve-kernel launch / its CUDA-event
+duration vs MEASURED_PEAKS.json hbm_gbs.  `cpu_baseline` = the reference's own
+compiled kernels (oracle/_ref, built from the reference sources) driven by
+the reference CG loop on this host, on a 20-iteration window of the same
+system.  `--impl reference` times that CPU path alone (the driver's reference
+arm).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    # name: (generator kind, dims, storage, accumulation, description)
+    "p3": ("poisson3d", (400, 400, 400), "csr", 1, "3D 7-point Poisson 400^3, CSR fp64 CG"),
+    "p2": ("poisson2d", (4096, 4096), "csr", 1, "2D 5-point Poisson 4096^2, CSR fp64 CG"),
+    "q27": ("stencil27", (256, 256, 256), "scsr", 0,
+            "3D 27-point stencil 256^3, symmetric CSR (L+D, atomic scatter) fp64 CG"),
+    "f": ("fem", None, "csr", 1, "FEM-shaped 30880x30880 / 449,798 nnz, full CSR fp64 CG"),
+    "s": ("fem", None, "scsr", 1, "FEM-shaped 30880, symmetric CSR (L+D) fp64 CG"),
+    "csc": ("fem", None, "csc", 1, "FEM-shaped 30880, CSC fp64 CG"),
+}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def iter_bytes(n, nnz):
+    """algorithmic bytes of one CG iteration."""
+    return 12 * nnz + 4 * (n + 1) + 88 * n
+
+
+def spmv_bytes(n, nnz):
+    return 12 * nnz + 4 * (n + 1) + 16 * n
+
+
+def solve_bytes(n, nnz, iterations, recompute=True):
+    """Algorithmic bytes of one solve-kernel launch: ||b|| (8n), x=0 & r=b
+    (24n), r.r (8n); per iteration iter_bytes; x += alpha p (24n); true
+    residual = SpMV + b - q (spmv_bytes + 16n)."""
+    b = 40 * n + iterations * iter_bytes(n, nnz) + 24 * n
+    if recompute:
+        b += spmv_bytes(n, nnz) + 16 * n
+    return b
+
+
+# ---- clocks ---------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        except OSError:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k] == "Active"})
+        loaded = [s for s in sm if s > 0.5 * mx] or sm
+        pw = [float(r[3]) for r in rows if r[3].replace(".", "").isdigit()]
+        return {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(pw) if pw else None}
+
+
+# ---- system construction ----------------------------------------------------------
+def build_device_system(workload: str):
+    """(DeviceMatrix, b (cuda tensor), n, stored nnz, x_gen numpy)."""
+    import torch
+
+    from paper_1010_4639_b200 import _native as N
+    from paper_1010_4639_b200.core import extract_lower
+    from paper_1010_4639_b200.device import DeviceMatrix
+    from paper_1010_4639_b200.genprob import fem_mesh, rhs_for
+
+    kind, dims, fmt, acc, _ = WORKLOADS[workload]
+    if kind == "fem":
+        F = fem_mesh()
+        b, xg = rhs_for(F, seed=1)
+        m = {"csr": F, "scsr": extract_lower(F) if fmt == "scsr" else None,
+             "csc": F.to_csc() if fmt == "csc" else None}[fmt]
+        dm = m.device()
+        return dm, torch.from_numpy(b).cuda(), m.n, m.nnz, xg, acc
+    dm = DeviceMatrix.generate(kind, dims, fmt)
+    n = dm.n
+    xg = np.random.default_rng(1).standard_normal(n)
+    xt = torch.from_numpy(xg).cuda()
+    full = dm if fmt == "csr" else DeviceMatrix.generate(kind, dims, "csr")
+    bt = torch.empty_like(xt)
+    N.check(N.load().spcg_spmv(full.handle, xt.data_ptr(), bt.data_ptr(), 1,
+                               torch.cuda.current_stream().cuda_stream), "rhs spmv")
+    torch.cuda.synchronize()
+    if full is not dm:
+        full.close()
+    del xt
+    return dm, bt, n, dm.nnz, xg, acc
+
+
+def host_system(workload: str):
+    """Host int64 arrays of the same system for the CPU path: (kind, rs, ci, v, b)."""
+    from oracle import oracle as O
+    from paper_1010_4639_b200.core import extract_lower
+    from paper_1010_4639_b200.genprob import fem_mesh, rhs_for
+
+    kind, dims, fmt, acc, _ = WORKLOADS[workload]
+    if kind == "fem":
+        F = fem_mesh()
+        b, _ = rhs_for(F, seed=1)
+        if fmt == "scsr":
+            s = extract_lower(F)
+            return "sym", s.row_start, s.col_idx, s.values, b
+        return "csr", F.row_start, F.col_idx, F.values, b
+    rs, ci, v = O.stencil(kind, dims, "full")
+    xg = np.random.default_rng(1).standard_normal(len(rs) - 1)
+    b = O.spmv_full(rs, ci, v, xg, workers=O.host_cores())
+    if fmt == "scsr":
+        rs, ci, v = O.stencil(kind, dims, "lower")
+        return "sym", rs, ci, v, b
+    return "csr", rs, ci, v, b
+
+
+def cpu_sample(workload: str, steps: int, warmup: int, window: int):
+    """Time the reference's compiled kernels (reference CG loop) on host cores."""
+    from oracle import oracle as O
+
+    kind, rs, ci, v, b = host_system(workload)
+    n = len(rs) - 1
+    cores = O.host_cores()
+    acc = "atomic" if WORKLOADS[workload][3] == 0 else "privatized"
+    use_ref = O.load_ref() is not None
+    solve = O.cg_solve_ref if use_ref else O.cg_solve
+    full_solve = kind != "sym" and n < 100_000  # small systems: whole solve
+    mi = None if full_solve else window
+    times, its = [], []
+    for k in range(warmup + steps):
+        t0 = time.perf_counter()
+        r = solve(kind, rs, ci, v, b, max_iter=mi, recompute=full_solve, workers=cores,
+                  accumulation=acc)
+        dt = time.perf_counter() - t0
+        if k >= warmup:
+            times.append(dt)
+            its.append(r.iterations)
+    value = sum(its) / sum(times)
+    sample = (f"{'full solve' if full_solve else f'{window}-iteration window (max_iter={window}, x0=0)'}"
+              f" of the same {n}-row system, {steps} timed + {warmup} warm-up, "
+              f"{'reference _ckernels (oracle/_ref) + reference CG loop' if use_ref else 'oracle C port'}")
+    return {"value": value, "unit": "iterations/s", "cores": cores,
+            "kind": "reference" if use_ref else "port", "sample": sample,
+            "iterations_per_step": its[0], "s_per_step": float(np.median(times))}
+
+
+# ---- our arm ---------------------------------------------------------------------
+def run_ours(args):
+    import torch
+
+    from paper_1010_4639_b200 import _native as N
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1 or args.gpus > 1:
+        from paper_1010_4639_b200 import distributed as D
+
+        return D.bench_main(args, WORKLOADS, peaks)
+    torch.cuda.set_device(0)
+    torch.cuda.init()
+    lib = N.load()
+    peak, peak_src = peaks()
+    t0 = time.time()
+    dm, bt, n, nnz, xg, acc = build_device_system(args.workload)
+    setup_s = time.time() - t0
+    st = torch.cuda.current_stream()
+    x = torch.empty_like(bt)
+    opts = N.CgOptionsC(tol=1e-10, max_iter=args.max_iter, record_history=0,
+                        recompute_final_residual=1, accumulation=acc, engine=0)
+
+    def solve_dev():
+        r = N.CgResultC()
+        N.check(lib.spcg_cg_solve(dm.handle, bt.data_ptr(), None, x.data_ptr(), None, opts, r,
+                                  st.cuda_stream), "spcg_cg_solve")
+        return r
+
+    for _ in range(args.warmup):
+        solve_dev()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    results = []
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        torch.cuda.synchronize()
+        e0.record(st)
+        for _ in range(args.steps):
+            results.append(solve_dev())
+        e1.record(st)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    clocks = clk.summary()
+    iters = sum(r.iterations for r in results)
+    value = iters / (ms / 1e3)
+    kern_ms = float(np.mean([r.device_ms for r in results]))
+    it_per = results[-1].iterations
+    alg = solve_bytes(n, nnz, it_per)
+    achieved = alg / (kern_ms / 1e3) / 1e9
+
+    # e2e through the C-ABI host entry point: pinned b in, x out, every step
+    b_host = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    b_host.copy_(bt.cpu())
+    x_host = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    bh, xh = b_host.numpy(), x_host.numpy()
+
+    def solve_host():
+        r = N.CgResultC()
+        N.check(lib.spcg_cg_solve_host(dm.handle, bh.ctypes.data, None, xh.ctypes.data, None,
+                                       opts, r, st.cuda_stream), "spcg_cg_solve_host")
+        return r
+
+    solve_host()
+    torch.cuda.synchronize()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record(st)
+    e2e_its = 0
+    for _ in range(args.steps):
+        e2e_its += solve_host().iterations
+    e3.record(st)
+    torch.cuda.synchronize()
+    e2e_ms = e2.elapsed_time(e3)
+    x_check = xh.copy()
+
+    # standalone SpMV kernel (the metric's "SpMV HBM GB/s")
+    y = torch.empty_like(bt)
+    for _ in range(3):
+        lib.spcg_spmv(dm.handle, bt.data_ptr(), y.data_ptr(), acc, st.cuda_stream)
+    reps = 20 if n > 1_000_000 else 200
+    e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e4.record(st)
+    for _ in range(reps):
+        lib.spcg_spmv(dm.handle, bt.data_ptr(), y.data_ptr(), acc, st.cuda_stream)
+    e5.record(st)
+    torch.cuda.synchronize()
+    sp_ms = e4.elapsed_time(e5) / reps
+    sp_gbs = spmv_bytes(n, nnz) / (sp_ms / 1e3) / 1e9
+
+    err_gen = float(np.max(np.abs(x_check - xg)) / max(1.0, np.max(np.abs(xg))))
+    _, _, _, _, desc = WORKLOADS[args.workload]
+    line = {
+        "metric": "fp64 CG iterations/sec (and SpMV HBM GB/s, % of roofline)",
+        "value": round(value, 3),
+        "unit": "iterations/s",
+        "n_gpus": 1,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (reference generators rebuilt in HBM; b = A x_gen, x_gen ~ N(0,1) seed 1)",
+        "config": {"workload": desc, "n": n, "nnz_stored": nnz, "tol": 1e-10, "x0": "zeros",
+                   "iterations_per_solve": it_per, "step": "one full cg_solve",
+                   "l2": "inputs (matrix %.1f GB) >> 126 MB L2, no flush needed" % (12 * nnz / 1e9),
+                   "parallelism": "1 GPU, one persistent cooperative kernel per solve"},
+        "e2e": {"value": round(e2e_its / (e2e_ms / 1e3), 3), "unit": "iterations/s",
+                "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n + 40,
+                "path": "spcg_cg_solve_host (C-ABI, pinned host b -> x), matrix handle resident"},
+        "gpu_launches": args.steps,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "peak_source": peak_src,
+                     "kernel": "cg_kernel (persistent cooperative CG solve)",
+                     "algorithmic_bytes_per_launch": alg, "kernel_ms": kern_ms,
+                     "bytes_model": "per iteration 12*nnz + 4*(n+1) + 88*n (SURVEY 8d)"},
+        "spmv": {"ms": sp_ms, "GBs": round(sp_gbs, 1), "frac": round(sp_gbs / peak, 4),
+                 "bytes": spmv_bytes(n, nnz)},
+        "clocks": clocks,
+        "final_relative_residual": results[-1].final_relative_residual,
+        "converged": bool(results[-1].converged),
+        "max_abs_err_vs_xgen": err_gen,
+        "setup_s": round(setup_s, 2),
+    }
+    if not args.no_secondary and args.workload == "p3":
+        line["secondary"] = secondary(peak)
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_sample(args.workload, steps=1, warmup=0, window=20)
+    print(json.dumps(line), flush=True)
+
+
+def secondary(peak):
+    """The 30880-row FEM-shaped configs (BASELINE configs[0..1]): full solves."""
+    import torch
+
+    from paper_1010_4639_b200 import _native as N
+
+    lib = N.load()
+    out = {}
+    for w in ("f", "s", "csc"):
+        dm, bt, n, nnz, _, acc = build_device_system(w)
+        x = torch.empty_like(bt)
+        o = N.CgOptionsC(tol=1e-10, max_iter=0, record_history=0, recompute_final_residual=1,
+                         accumulation=acc, engine=0)
+        rs = []
+        for k in range(8):
+            r = N.CgResultC()
+            N.check(lib.spcg_cg_solve(dm.handle, bt.data_ptr(), None, x.data_ptr(), None, o, r,
+                                      torch.cuda.current_stream().cuda_stream), "solve")
+            if k >= 3:
+                rs.append((r.device_ms, r.iterations))
+        ms = float(np.median([a for a, _ in rs]))
+        its = rs[-1][1]
+        us = ms * 1e3 / its
+        gbs = iter_bytes(n, nnz) / (us * 1e-6) / 1e9
+        out[w] = {"workload": WORKLOADS[w][4], "iterations": its, "solve_ms": round(ms, 4),
+                  "us_per_iteration": round(us, 3), "iterations_per_s": round(its / (ms / 1e3), 1),
+                  "GBs_algorithmic": round(gbs, 1), "frac": round(gbs / peak, 4)}
+    return out
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    _, _, _, _, desc = WORKLOADS[args.workload]
+    s = cpu_sample(args.workload, steps=args.steps, warmup=min(args.warmup, 1), window=20)
+    line = {
+        "impl": "reference",
+        "metric": "fp64 CG iterations/sec (and SpMV HBM GB/s, % of roofline)",
+        "value": round(s["value"], 4),
+        "unit": "iterations/s",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "steps": args.steps,
+        "warmup": min(args.warmup, 1),
+        "ms_per_step": s["s_per_step"] * 1e3,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (same system as the ours arm)",
+        "config": {"workload": desc},
+        "cpu_baseline": {k: s[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": round(s["value"], 4), "unit": "iterations/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", choices=tuple(WORKLOADS), default="p3")
+    ap.add_argument("--max-iter", type=int, default=0, help="cap iterations (profiling only)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours" and args.max_iter == 0:
+        print("note: contract requires warmup >= 3", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
