@@ -14,7 +14,7 @@ import os
 import threading
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libspcg_b200.so"
+LIB_PATH = Path(os.environ.get("SPCG_LIB") or Path(__file__).resolve().parent / "_lib" / "libspcg_b200.so")
 HEADER_PATH = Path(__file__).resolve().parent.parent / "include" / "spcg_b200.h"
 
 # spcg_status (spcg_b200.h)

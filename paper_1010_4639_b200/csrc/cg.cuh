@@ -40,6 +40,7 @@ struct CgArgs {
   double* p1;
   double* q;  // zero on entry for atomic formats
   double* hist;
+  unsigned long long* trace;  // nullable: per-CTA phase nanoseconds [G][4]
   unsigned long long* slots;  // 2 * gridDim.x * 2 words, zero on entry
   CgDevResult* res;
   double tol;
@@ -57,36 +58,85 @@ enum : int {
 };
 
 // Grid-wide all-reduce + barrier.  Each CTA publishes its fixed-order block
-// sum in a slot of two 64-bit words {hi32(sum)|epoch, lo32(sum)|epoch}; each
-// word is single-copy atomic, so a reader that sees the epoch in both words
-// has the whole value (one polling round trip, no atomics, no counter).
-// Slots alternate between two banks by epoch parity, which makes reuse safe.
-// The writer's fence.acq_rel.gpu (after the CTA barrier inside block_sum)
-// publishes all of the CTA's prior global writes; each polling thread's fence
-// after observing the epochs acquires them for the whole CTA.
+// sum in its own 256-byte slot (one L2 line per CTA, so polls spread over
+// many L2 slices instead of hammering a few lines) as two 64-bit words
+// {hi32(sum)|epoch, lo32(sum)|epoch}; each word is single-copy atomic, so a
+// reader that sees the epoch in both words has the whole value: one polling
+// round trip, no atomics, no counter, no second hop.  Slots alternate between
+// two banks by epoch parity, which makes reuse safe (a CTA can only run one
+// barrier ahead of the slowest reader).
+// Release: thread 0's fence.acq_rel.gpu after the CTA barrier publishes all
+// of the CTA's prior global writes.  Acquire: warp 0 polls every slot (lane
+// l reads slots l, l+32, ...), then fences once for the CTA.
+// The total is summed in the same fixed order in every CTA (bitwise equal).
+constexpr int kSlotWords = 32;  // 256 bytes per CTA slot
+constexpr int kPollWarps = (kBlock / 32) < 8 ? (kBlock / 32) : 8;  // warps polling the slots
+constexpr int kPollPer = 3;  // slots per polling lane: grids up to 32*kPollWarps*3 CTAs
+
 __device__ __forceinline__ double grid_allreduce(double v, Smem& sm, unsigned long long* slots,
                                                  uint32_t& epoch) {
   ++epoch;
-  const double bs = block_sum(v, sm);
-  unsigned long long* bank = slots + (size_t)(epoch & 1u) * gridDim.x * 2;
-  if (threadIdx.x == 0) {
-    fence_acq_rel_gpu();
-    const unsigned long long bits = (unsigned long long)__double_as_longlong(bs);
-    st_relaxed_v2_u64(bank + 2 * blockIdx.x, (bits & 0xffffffff00000000ull) | epoch,
-                      (bits << 32) | epoch);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0) sm.red[w] = v;
+  __syncthreads();
+  unsigned long long* bank = slots + (size_t)(epoch & 1u) * gridDim.x * kSlotWords;
+  if (w == 0) {
+    double bs = lane < (int)(blockDim.x >> 5) ? sm.red[lane] : 0.0;
+    bs = warp_sum(bs);
+    if (lane == 0) {
+      fence_acq_rel_gpu();
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(bs);
+      st_relaxed_v2_u64(bank + (size_t)kSlotWords * blockIdx.x,
+                        (bits & 0xffffffff00000000ull) | epoch, (bits << 32) | epoch);
+    }
   }
-  double s = 0.0;
-  for (int t = threadIdx.x; t < (int)gridDim.x; t += blockDim.x) {
-    unsigned long long a, c;
+  if (w < kPollWarps) {
+    // slot t = 32*w + lane + 128*u; all of a lane's loads are in flight at once
+    unsigned long long a[kPollPer], c[kPollPer];
+    bool pend[kPollPer];
+    const int base = 32 * w + lane;
+#pragma unroll
+    for (int u = 0; u < kPollPer; ++u) pend[u] = base + 32 * kPollWarps * u < (int)gridDim.x;
+    bool any = true;
     unsigned long long spins = 0;
-    do {
-      ld_relaxed_v2_u64(bank + 2 * t, a, c);
+    while (any) {
+#pragma unroll
+      for (int u = 0; u < kPollPer; ++u)
+        if (pend[u])
+          ld_relaxed_v2_u64(bank + (size_t)kSlotWords * (base + 32 * kPollWarps * u), a[u], c[u]);
+      any = false;
+#pragma unroll
+      for (int u = 0; u < kPollPer; ++u)
+        if (pend[u]) {
+          pend[u] = (uint32_t)a[u] != epoch || (uint32_t)c[u] != epoch;
+          any |= pend[u];
+        }
       if (++spins > kSpinLimit) asm volatile("trap;");
-    } while ((uint32_t)a != epoch || (uint32_t)c != epoch);
-    s += __longlong_as_double((long long)((a & 0xffffffff00000000ull) | (c >> 32)));
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int u = 0; u < kPollPer; ++u)
+      if (base + 32 * kPollWarps * u < (int)gridDim.x)
+        s += __longlong_as_double((long long)((a[u] & 0xffffffff00000000ull) | (c[u] >> 32)));
+    fence_acq_rel_gpu();
+    s = warp_sum(s);
+    if (lane == 0) sm.red[16 + w] = s;  // red[0..15] is not reread after the barrier
   }
-  if (threadIdx.x < gridDim.x) fence_acq_rel_gpu();
-  return block_sum(s, sm);
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int k = 0; k < kPollWarps; ++k) t += sm.red[16 + k];  // fixed order, every thread
+  __syncthreads();  // red reuse by the next call
+  return t;
+}
+
+// Resident tiles keep their values: the CSR-stream products go to a separate
+// shared-memory buffer placed after Smem (kResProdBytes extra dynamic smem).
+constexpr size_t kResProdBytes = sizeof(double) * kStages * kNzCap;
+__device__ __forceinline__ double* res_prod(Smem& sm, int j) {
+  return reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(&sm) + sizeof(Smem)) +
+         (size_t)j * kNzCap;
 }
 
 // Iterate this CTA's tiles; fn(j, line, LineOut) for every owned line.
@@ -94,7 +144,7 @@ __device__ __forceinline__ double grid_allreduce(double v, Smem& sm, unsigned lo
 // compile-time index into the per-thread register arrays.
 template <int FMT, bool GATHER_CSC, bool TWO, bool RES, class Src, class Fn>
 __device__ __forceinline__ void run_tiles(Pipe& P, Smem& sm, const MatView& M, const Src& src,
-                                          double* y, Fn fn) {
+                                          double* y, Fn fn, const double* xpre = nullptr) {
   if (RES) {
 #pragma unroll
     for (int j = 0; j < kStages; ++j) {
@@ -102,7 +152,8 @@ __device__ __forceinline__ void run_tiles(Pipe& P, Smem& sm, const MatView& M, c
         mbar_wait(&sm.full[j], 0);
         bool active = false;
         int line = -1;
-        const LineOut o = tile_line<FMT, GATHER_CSC>(sm, j, M, src, y, active, line);
+        const LineOut o =
+            tile_line<FMT, GATHER_CSC>(sm, j, M, src, y, active, line, res_prod(sm, j));
         if (active) fn(j, line, o);
       }
     }
@@ -112,14 +163,15 @@ __device__ __forceinline__ void run_tiles(Pipe& P, Smem& sm, const MatView& M, c
     const int s = pipe_acquire(P, sm, j);
     bool active = false;
     int line = -1;
-    const LineOut o = tile_line<FMT, GATHER_CSC>(sm, s, M, src, y, active, line);
+    const LineOut o =
+        tile_line<FMT, GATHER_CSC>(sm, s, M, src, y, active, line, sm.val[s], xpre);
     if (active) fn(j, line, o);
     pipe_release<TWO>(P, sm, M, s);
   }
 }
 
 template <int FMT, bool RES>
-__global__ void __launch_bounds__(kBlock, RES ? 1 : 2) cg_kernel(const CgArgs A) {
+__global__ void __launch_bounds__(kBlock, RES ? 1 : kStreamMinBlocks) cg_kernel(const CgArgs A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   constexpr bool TWO = (FMT == K_SCSR_PRIV);
@@ -132,7 +184,7 @@ __global__ void __launch_bounds__(kBlock, RES ? 1 : 2) cg_kernel(const CgArgs A)
 
   smem_init(sm);
   Pipe P;
-  pipe_start<TWO>(P, sm, M);
+  pipe_start<TWO>(P, sm, M, /*allow_resident=*/RES);
   uint32_t epoch = 0;
 
   // RES: per-thread owned lines and their register-resident vector entries.
@@ -259,6 +311,15 @@ __global__ void __launch_bounds__(kBlock, RES ? 1 : 2) cg_kernel(const CgArgs A)
   double* p_new = A.p0;
   double* p_cur = nullptr;
 
+  unsigned long long tr[4] = {0, 0, 0, 0};
+  unsigned long long tlast = A.trace ? globaltimer_ns() : 0;
+  auto mark = [&](int ph) {
+    if (A.trace && threadIdx.x == 0) {
+      const unsigned long long t = globaltimer_ns();
+      tr[ph] += t - tlast;
+      tlast = t;
+    }
+  };
   for (long long k = 1; k <= max_it; ++k) {
     // pass A
     double pq = 0.0;
@@ -268,7 +329,7 @@ __global__ void __launch_bounds__(kBlock, RES ? 1 : 2) cg_kernel(const CgArgs A)
         pg[j] = o.xi;
         if (!ATOM) qg[j] = o.q;
       } else {
-        if (k > 1) A.x[i] = mul_add_rn(A.x[i], alpha, p_old[i]);
+        if (k > 1) A.x[i] = mul_add_rn(o.xo, alpha, p_old[i]);
         if (!ATOM) A.q[i] = o.q;
       }
       p_new[i] = o.xi;
@@ -280,10 +341,12 @@ __global__ void __launch_bounds__(kBlock, RES ? 1 : 2) cg_kernel(const CgArgs A)
       run_tiles<FMT, true, TWO, RES>(P, sm, M, sf, A.q, lineA);
     } else {
       SrcFold sf{A.r, p_old, beta};
-      run_tiles<FMT, true, TWO, RES>(P, sm, M, sf, A.q, lineA);
+      run_tiles<FMT, true, TWO, RES>(P, sm, M, sf, A.q, lineA, RES ? nullptr : A.x);
     }
     p_cur = p_new;
+    mark(0);
     pq = grid_allreduce(pq, sm, A.slots, epoch);
+    mark(1);
     if (pq <= 0.0) {
       status = ST_NOT_SPD;
       fail_iter = k;
@@ -312,15 +375,55 @@ __global__ void __launch_bounds__(kBlock, RES ? 1 : 2) cg_kernel(const CgArgs A)
           part = fma(rg[u], rg[u], part);
         }
     } else {
-      for (long long i = gtid; i < n; i += gstride) {
+      // r -= alpha q over 16-byte pairs, two pairs in flight per thread
+      // (q, r are 256-byte-aligned workspace arrays).
+      const double2* q2 = reinterpret_cast<const double2*>(A.q);
+      double2* r2 = reinterpret_cast<double2*>(A.r);
+      double2* z2 = reinterpret_cast<double2*>(A.q);
+      const long long np = (long long)n >> 1;
+      const double na = -alpha;
+      long long pi = gtid;
+      for (; pi + gstride < np; pi += 2 * gstride) {
+        const double2 qa = q2[pi], qb = q2[pi + gstride];
+        const double2 ra = r2[pi], rb = r2[pi + gstride];
+        double2 oa, ob;
+        oa.x = mul_add_rn(ra.x, na, qa.x);
+        oa.y = mul_add_rn(ra.y, na, qa.y);
+        ob.x = mul_add_rn(rb.x, na, qb.x);
+        ob.y = mul_add_rn(rb.y, na, qb.y);
+        r2[pi] = oa;
+        r2[pi + gstride] = ob;
+        if (ATOM) {
+          z2[pi] = make_double2(0.0, 0.0);
+          z2[pi + gstride] = make_double2(0.0, 0.0);
+        }
+        part = fma(oa.x, oa.x, part);
+        part = fma(oa.y, oa.y, part);
+        part = fma(ob.x, ob.x, part);
+        part = fma(ob.y, ob.y, part);
+      }
+      if (pi < np) {
+        const double2 qa = q2[pi], ra = r2[pi];
+        double2 oa;
+        oa.x = mul_add_rn(ra.x, na, qa.x);
+        oa.y = mul_add_rn(ra.y, na, qa.y);
+        r2[pi] = oa;
+        if (ATOM) z2[pi] = make_double2(0.0, 0.0);
+        part = fma(oa.x, oa.x, part);
+        part = fma(oa.y, oa.y, part);
+      }
+      if ((n & 1) && gtid == 0) {
+        const long long i = n - 1;
         const double qi = A.q[i];
         if (ATOM) A.q[i] = 0.0;
-        const double ri = mul_add_rn(A.r[i], -alpha, qi);
+        const double ri = mul_add_rn(A.r[i], na, qi);
         A.r[i] = ri;
         part = fma(ri, ri, part);
       }
     }
+    mark(2);
     const double rr_new = grid_allreduce(part, sm, A.slots, epoch);
+    mark(3);
     rel = sqrt(rr_new) / b_norm;
     if (!isfinite(rel)) {
       status = ST_NF_RES;
@@ -346,6 +449,10 @@ __global__ void __launch_bounds__(kBlock, RES ? 1 : 2) cg_kernel(const CgArgs A)
     p_new = t;
   }
 
+  if (A.trace && threadIdx.x == 0) {
+#pragma unroll
+    for (int ph = 0; ph < 4; ++ph) A.trace[blockIdx.x * 4 + ph] = tr[ph];
+  }
   if (status != ST_OK) {
     if (leader) {
       A.res->iterations = iterations;

@@ -30,7 +30,10 @@ struct SrcFold {
   }
 };
 
-constexpr int kUnroll = 8;
+#ifndef SPCG_UNROLL
+#define SPCG_UNROLL 8
+#endif
+constexpr int kUnroll = SPCG_UNROLL;
 
 // acc = sum_k v[k]*src(ix[k]) over [ks,ke), sequential order; loads batched
 // kUnroll-deep so each thread keeps many gathers in flight.
@@ -47,6 +50,40 @@ __device__ __forceinline__ double seq_row(const double* v, const int* ix, int ks
     for (int u = 0; u < kUnroll; ++u)
       if (k + u < ke) acc = __dadd_rn(acc, pr[u]);
   }
+  return acc;
+}
+
+// Phase 1 of a CSR / SCSR_PRIV tile ("CSR-stream"): every thread forms
+// products prod[k] = val[k] * src(idx[k]) for staged entries k = tid,
+// tid+kBlock, ...  (kUnroll of them in flight), so all 512 threads gather
+// regardless of row lengths; phase 2 sums each line's products sequentially
+// in storage order (same bits as a sequential row sum).  prod may alias
+// sm.val[s] (streamed tiles) or be a separate buffer (resident tiles).
+template <class Src>
+__device__ __forceinline__ void stream_products(const Smem& sm, int s, const Src& src,
+                                                double* prod) {
+  const int cnt = sm.meta[s].cnt;
+  const double* v = sm.val[s];
+  const int* ix = sm.idx[s];
+  for (int k0 = threadIdx.x; k0 < cnt; k0 += kBlock * kUnroll) {
+    double pr[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int k = k0 + u * kBlock;
+      pr[u] = (k < cnt) ? __dmul_rn(v[k], src.get(ix[k])) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int k = k0 + u * kBlock;
+      if (k < cnt) prod[k] = pr[u];
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ double seq_sum(const double* prod, int ks, int ke) {
+  double acc = 0.0;
+  for (int k = ks; k < ke; ++k) acc = __dadd_rn(acc, prod[k]);
   return acc;
 }
 
@@ -123,7 +160,13 @@ struct LineOut {
   double q;    // (A x)_i for CSR / SCSR_PRIV; g_i for SCSR_ATOMIC / CSC
   double xi;   // src(i): the gathered-vector value of the line itself
   double dg;   // SCSR_ATOMIC: diagonal a_ii
+  double xo;   // xpre[i] prefetched with the line's loads (CG x update)
 };
+
+// Tiles averaging more than this many entries per line use the two-phase
+// CSR-stream body; shorter rows (e.g. the 7-point stencil) keep one thread
+// per row, which already has all of its gathers in flight.
+constexpr int kStreamMinPerLine = 8;
 
 // Computes line i (the tid-th line of staged tile s).  For FMT in
 // {SCSR_ATOMIC, CSC} the scatter goes to y (must be zeroed beforehand) and
@@ -132,19 +175,41 @@ struct LineOut {
 // must call (CTA-wide reductions); the line's result is valid in thread 0.
 template <int FMT, bool GATHER_CSC, class Src>
 __device__ __forceinline__ LineOut tile_line(Smem& sm, int s, const MatView& M, const Src& src,
-                                             double* y, bool& active, int& line) {
+                                             double* y, bool& active, int& line, double* prod,
+                                             const double* xpre = nullptr) {
   const StageMeta& mt = sm.meta[s];
-  LineOut o{0.0, 0.0, 0.0};
+  LineOut o{0.0, 0.0, 0.0, 0.0};
   if (!mt.is_long) {
     const int i = mt.row0 + (int)threadIdx.x;
     active = i < mt.row1;
     line = i;
-    if (!active) return o;
-    const int lr = i - mt.r0a;
-    const int ks = sm.rpA[s][lr] - mt.kA0a;
-    const int ke = sm.rpA[s][lr + 1] - mt.kA0a;
+    const bool stream = (FMT == K_CSR || FMT == K_SCSR_PRIV) &&
+                        mt.cnt > kStreamMinPerLine * (mt.row1 - mt.row0);
     const double* v = sm.val[s];
     const int* ix = sm.idx[s];
+    const int lr = i - mt.r0a;
+    if (stream) {
+      if (active) {  // own-line loads go out before the gather phase
+        o.xi = src.get(i);
+        if (xpre) o.xo = xpre[i];
+      }
+      stream_products(sm, s, src, prod);
+      if (!active) return o;
+      const int ks = sm.rpA[s][lr] - mt.kA0a;
+      const int ke = sm.rpA[s][lr + 1] - mt.kA0a;
+      if (FMT == K_CSR) {
+        o.q = seq_sum(prod, ks, ke);
+      } else {
+        const int kb = sm.rpB[s][lr] - mt.kB0a + mt.offB;
+        const int kbe = sm.rpB[s][lr + 1] - mt.kB0a + mt.offB;
+        o.q = __dadd_rn(seq_sum(prod, ks, ke), seq_sum(prod, kb, kbe));
+      }
+      return o;
+    }
+    if (!active) return o;
+    if (xpre) o.xo = xpre[i];
+    const int ks = sm.rpA[s][lr] - mt.kA0a;
+    const int ke = sm.rpA[s][lr + 1] - mt.kA0a;
     if (FMT == K_CSR) {
       o.q = seq_row(v, ix, ks, ke, src);
       o.xi = src.get(i);
@@ -169,6 +234,7 @@ __device__ __forceinline__ LineOut tile_line(Smem& sm, int s, const MatView& M, 
   const int i = mt.row0;
   line = i;
   active = threadIdx.x == 0;
+  if (xpre) o.xo = xpre[i];
   const int k0 = M.ptrA[i], k1 = M.ptrA[i + 1];
   if (FMT == K_CSR) {
     o.q = long_gather(M.valA, M.idxA, k0, k1, src, sm);

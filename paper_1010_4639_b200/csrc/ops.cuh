@@ -20,7 +20,7 @@ __global__ void __launch_bounds__(kBlock, 1) spmv_kernel(const MatView M, const 
     const int s = pipe_acquire(P, sm, j);
     bool active = false;
     int line = -1;
-    const LineOut o = tile_line<FMT, false>(sm, s, M, src, y, active, line);
+    const LineOut o = tile_line<FMT, false>(sm, s, M, src, y, active, line, sm.val[s]);
     if (active) finish_plain<FMT>(o, line, y);
     pipe_release<TWO>(P, sm, M, s);
   }

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -46,12 +47,12 @@ std::mutex g_dev_mutex;
 DevInfo g_dev[64];
 
 template <class K>
-int occupancy(K kernel, int* blocks) {
-  CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)sizeof(Smem)));
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, kernel, kBlock, sizeof(Smem)));
+int occupancy(K kernel, int* blocks, size_t smem = sizeof(Smem)) {
+  CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, kernel, kBlock, smem));
   return SPCG_OK;
 }
+constexpr size_t kSmemRes = sizeof(Smem) + kResProdBytes;
 
 int dev_info(DevInfo** out) {
   int dev = 0;
@@ -71,14 +72,14 @@ int dev_info(DevInfo** out) {
     d.minor = prop.minor;
     int br = 0, bs = 0, bp = 0, t = 0;
     int rc;
-    if ((rc = occupancy(cg_kernel<K_CSR, true>, &br))) return rc;
+    if ((rc = occupancy(cg_kernel<K_CSR, true>, &br, kSmemRes))) return rc;
     if ((rc = occupancy(cg_kernel<K_CSR, false>, &bs))) return rc;
     // every instantiation shares the same block/smem shape; check the rest
-    if ((rc = occupancy(cg_kernel<K_SCSR_ATOMIC, true>, &t))) return rc;
+    if ((rc = occupancy(cg_kernel<K_SCSR_ATOMIC, true>, &t, kSmemRes))) return rc;
     br = std::min(br, t);
-    if ((rc = occupancy(cg_kernel<K_SCSR_PRIV, true>, &t))) return rc;
+    if ((rc = occupancy(cg_kernel<K_SCSR_PRIV, true>, &t, kSmemRes))) return rc;
     br = std::min(br, t);
-    if ((rc = occupancy(cg_kernel<K_CSC, true>, &t))) return rc;
+    if ((rc = occupancy(cg_kernel<K_CSC, true>, &t, kSmemRes))) return rc;
     br = std::min(br, t);
     if ((rc = occupancy(cg_kernel<K_SCSR_ATOMIC, false>, &t))) return rc;
     bs = std::min(bs, t);
@@ -91,8 +92,8 @@ int dev_info(DevInfo** out) {
     if ((rc = occupancy(spmv_kernel<K_SCSR_PRIV>, &t))) return rc;
     if ((rc = occupancy(spmv_kernel<K_CSC>, &t))) return rc;
     if (br < 1 || bs < 1 || bp < 1) return fail(SPCG_ERR_CUDA, "CG kernel does not fit on an SM");
-    d.coop_res = br * d.sms;
-    d.coop_stream = bs * d.sms;
+    d.coop_res = std::min(br * d.sms, 32 * kPollWarps * kPollPer);
+    d.coop_stream = std::min(bs * d.sms, 32 * kPollWarps * kPollPer);
     d.spmv_grid = bp * d.sms;
     d.device = dev;
   }
@@ -374,7 +375,7 @@ int ensure_ws(spcg_matrix_s* m, int grid) {
   }
   if (w.slots_g < grid) {
     if (w.slots) cudaFree(w.slots);
-    if ((rc = dmalloc((void**)&w.slots, sizeof(unsigned long long) * 4 * (size_t)grid, nullptr)))
+    if ((rc = dmalloc((void**)&w.slots, sizeof(unsigned long long) * 2 * kSlotWords * (size_t)grid, nullptr)))
       return rc;
     w.slots_g = grid;
   }
@@ -385,7 +386,8 @@ template <int FMT>
 int launch_cg(const CgArgs& a, bool res, int grid, cudaStream_t st) {
   void* args[] = {(void*)&a};
   const void* fn = res ? (const void*)cg_kernel<FMT, true> : (const void*)cg_kernel<FMT, false>;
-  CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBlock), args, sizeof(Smem), st));
+  CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBlock), args,
+                                       res ? kSmemRes : sizeof(Smem), st));
   return SPCG_OK;
 }
 
@@ -433,7 +435,7 @@ int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double
   const long long max_iter = o->max_iter > 0 ? o->max_iter : std::max(1, m->n);
   if (o->record_history && hist == nullptr)
     return fail(SPCG_ERR_ARG, "record_history needs a history buffer");
-  CUDA_TRY(cudaMemsetAsync(w.slots, 0, sizeof(unsigned long long) * 4 * (size_t)grid, st));
+  CUDA_TRY(cudaMemsetAsync(w.slots, 0, sizeof(unsigned long long) * 2 * kSlotWords * (size_t)grid, st));
   if (kf == K_SCSR_ATOMIC || kf == K_CSC)
     CUDA_TRY(cudaMemsetAsync(w.q, 0, sizeof(double) * (size_t)std::max(1, m->n), st));
   CgArgs a{};
@@ -447,6 +449,13 @@ int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double
   a.q = w.q;
   a.hist = hist;
   a.slots = w.slots;
+  unsigned long long* trace = nullptr;
+  static const bool tracing = getenv("SPCG_TRACE") != nullptr;
+  if (tracing) {
+    CUDA_TRY(cudaMalloc((void**)&trace, sizeof(unsigned long long) * 4 * (size_t)grid));
+    CUDA_TRY(cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * 4 * (size_t)grid, st));
+  }
+  a.trace = trace;
   a.res = w.res;
   a.tol = o->tol;
   a.max_iter = max_iter;
@@ -466,6 +475,25 @@ int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double
   float ms = 0.f;
   CUDA_TRY(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
   const CgDevResult& r = *w.h_res;
+  if (trace) {
+    std::vector<unsigned long long> tv(4 * (size_t)grid);
+    CUDA_TRY(cudaMemcpy(tv.data(), trace, sizeof(unsigned long long) * tv.size(),
+                        cudaMemcpyDeviceToHost));
+    cudaFree(trace);
+    double mean[4] = {0, 0, 0, 0}, mx[4] = {0, 0, 0, 0};
+    for (int b = 0; b < grid; ++b)
+      for (int ph = 0; ph < 4; ++ph) {
+        mean[ph] += (double)tv[4 * b + ph] / grid;
+        mx[ph] = std::max(mx[ph], (double)tv[4 * b + ph]);
+      }
+    const double it = (double)std::max<long long>(1, r.iterations);
+    fprintf(stderr,
+            "[spcg trace] grid=%d res=%d iters=%lld us/iter mean(max): passA %.3f(%.3f) "
+            "reduce1 %.3f(%.3f) passB %.3f(%.3f) reduce2 %.3f(%.3f)\n",
+            grid, (int)res, r.iterations, mean[0] / it / 1e3, mx[0] / it / 1e3, mean[1] / it / 1e3,
+            mx[1] / it / 1e3, mean[2] / it / 1e3, mx[2] / it / 1e3, mean[3] / it / 1e3,
+            mx[3] / it / 1e3);
+  }
   out->iterations = r.iterations;
   out->converged = r.converged;
   out->status = r.status;

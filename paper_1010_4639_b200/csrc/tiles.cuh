@@ -19,10 +19,20 @@
 
 namespace spcg {
 
-constexpr int kBlock = 512;        // threads per CTA == lines per tile
+#ifndef SPCG_BLOCK
+#define SPCG_BLOCK 512
+#endif
+#ifndef SPCG_TILE_NNZ
+#define SPCG_TILE_NNZ 4096
+#endif
+constexpr int kBlock = SPCG_BLOCK;     // threads per CTA == lines per tile
 constexpr int kTileLines = kBlock;
-constexpr int kTileNnz = 4096;     // stored entries per tile (both segments)
+constexpr int kTileNnz = SPCG_TILE_NNZ;  // stored entries per tile (both segments)
 constexpr int kStages = 2;
+#ifndef SPCG_STREAM_MINB
+#define SPCG_STREAM_MINB (1024 / SPCG_BLOCK)
+#endif
+constexpr int kStreamMinBlocks = SPCG_STREAM_MINB;  // CTAs/SM targeted by streaming kernels
 constexpr int kRpCap = kTileLines + 8;
 constexpr int kNzCap = kTileNnz + 16;
 
@@ -48,7 +58,7 @@ struct StageMeta {
   int kA0a, kB0a;   // first staged entry of each segment (4-aligned)
   int offB;         // segment B's offset inside the stage buffers
   int is_long;      // 1: entries not staged, read from global
-  int pad;
+  int cnt;          // staged entries (both segments)
 };
 
 struct __align__(16) Smem {
@@ -97,6 +107,7 @@ __device__ __forceinline__ void issue_tile(Smem& sm, const MatView& M, int t, in
   mt.kA0a = kA0a;
   mt.kB0a = kB0a;
   mt.offB = cA;
+  mt.cnt = cA + cB;
   fence_proxy_async_smem();
   mbar_arrive_expect_tx(&sm.full[s], bytes);
   bulk_g2s(sm.rpA[s], M.ptrA + r0a, (uint32_t)rcnt * 4u, &sm.full[s]);
@@ -122,14 +133,18 @@ struct Pipe {
   long long c;  // tiles consumed (streaming mode)
 };
 
+// allow_resident=false forces cyclic streaming even for <= kStages tiles
+// (needed when a pass overwrites staged values in place and the tiles are
+// visited again, e.g. every CG iteration).
 template <bool TWO>
-__device__ __forceinline__ void pipe_start(Pipe& P, Smem& sm, const MatView& M) {
+__device__ __forceinline__ void pipe_start(Pipe& P, Smem& sm, const MatView& M,
+                                           bool allow_resident = true) {
   P.m = my_tile_count(M.ntiles);
-  P.resident = P.m <= kStages;
+  P.resident = allow_resident && P.m <= kStages;
   P.c = 0;
-  if (threadIdx.x == 0) {
-    const int pre = P.m < kStages ? P.m : kStages;
-    for (int j = 0; j < pre; ++j) issue_tile<TWO>(sm, M, my_tile(j), j);
+  if (threadIdx.x == 0 && P.m > 0) {
+    const int pre = P.resident ? P.m : kStages;
+    for (int j = 0; j < pre; ++j) issue_tile<TWO>(sm, M, my_tile(j % P.m), j);
   }
 }
 
