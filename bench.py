@@ -92,8 +92,9 @@ class ClockSampler:
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
         try:
+            sel = ["-i", str(self.idx)] if self.idx >= 0 else []
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                ["nvidia-smi", *sel, f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
@@ -222,11 +223,8 @@ def run_ours(args):
     from paper_1010_4639_b200 import _native as N
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    if world > 1 or args.gpus > 1:
-        from paper_1010_4639_b200 import distributed as D
-
-        return D.bench_main(args, WORKLOADS, peaks)
+    if world > 1 or args.gpus > 1 or args.engine == "sharded":
+        return run_distributed(args)
     torch.cuda.set_device(0)
     torch.cuda.init()
     lib = N.load()
@@ -349,6 +347,157 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
 
 
+def run_distributed(args):
+    """N ranks (torchrun, one per GPU).  Stencil workloads are row-sharded
+    (contiguous z-slabs; halo exchange + 2 all-reduces per iteration over
+    NCCL): strong scaling of one global solve.  The 30880-row FEM configs do
+    not shard (SURVEY §8e "replicas only"): each rank solves its own copy."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1010_4639_b200 import _native as N
+    from paper_1010_4639_b200 import distributed as D
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        gather, bcast = D.torch_collectives()
+    else:
+        gather, bcast = (lambda o: [o]), (lambda o: o)
+    peak, peak_src = peaks()
+    kind, dims, fmt, acc, desc = WORKLOADS[args.workload]
+    st = torch.cuda.current_stream()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def max_over_ranks(v):
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    if kind == "fem":  # replicas
+        dm, bt, n, nnz, xg, acc = build_device_system(args.workload)
+        lib = N.load()
+        x = torch.empty_like(bt)
+        o = N.CgOptionsC(tol=1e-10, max_iter=args.max_iter, record_history=0,
+                         recompute_final_residual=1, accumulation=acc, engine=0)
+
+        def step():
+            r = N.CgResultC()
+            N.check(lib.spcg_cg_solve(dm.handle, bt.data_ptr(), None, x.data_ptr(), None, o, r,
+                                      st.cuda_stream), "solve")
+            return r
+        for _ in range(args.warmup):
+            step()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        its = sum(step().iterations for _ in range(args.steps))
+        e1.record(st)
+        barrier()
+        ms = max_over_ranks(e0.elapsed_time(e1))
+        if rank == 0:
+            print(json.dumps({
+                "metric": "fp64 CG iterations/sec (and SpMV HBM GB/s, % of roofline)",
+                "value": round(world * its / (ms / 1e3), 3), "unit": "iterations/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": desc, "parallelism": f"{world} independent replicas"},
+                "gpu_launches": args.steps}), flush=True)
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    comm = D.Comm(rank, world, bcast)
+    t0 = time.time()
+    sm = D.ShardedMatrix.from_stencil(kind, dims, fmt, rank, world, gather)
+    n = sm.n_global
+    xg = np.random.default_rng(1).standard_normal(n)
+    x_ext = torch.from_numpy(np.concatenate([xg[sm.row0:sm.row1], xg[sm.halo]])).cuda()
+    b_loc = sm.spmv_ext(x_ext)
+    del x_ext
+    torch.cuda.synchronize()
+    setup_s = time.time() - t0
+    nnz_loc = sm.dm.nnz
+    nnz_tot = int(sum(gather(nnz_loc))) if world > 1 else nnz_loc
+
+    def step():
+        x, res, _ = D.dist_cg_solve(sm, comm, b_loc, max_iter=args.max_iter or None)
+        return x, res
+
+    for _ in range(args.warmup):
+        step()
+    results = []
+    with ClockSampler(local if world == 1 else -1) as clk:
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(args.steps):
+            x, r = step()
+            results.append((r.iterations, r.device_ms, r.kernel_launches, r.final_relative_residual))
+        e1.record(st)
+        barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    clocks = clk.summary() if rank == 0 else None
+    its = sum(r[0] for r in results)
+    it_per = results[-1][0]
+    kern_ms = max_over_ranks(float(np.mean([r[1] for r in results])))
+    alg = solve_bytes(n, nnz_tot, it_per)
+    achieved = alg / (kern_ms / 1e3) / 1e9
+    err = float(np.max(np.abs(x.cpu().numpy() - xg[sm.row0:sm.row1])))
+    err = max_over_ranks(err)
+    # e2e: pinned host b in, x out, every step, through the sharded entry point
+    bh = torch.empty(sm.nloc, dtype=torch.float64, pin_memory=True)
+    bh.copy_(b_loc.cpu())
+    xh = torch.empty(sm.nloc, dtype=torch.float64, pin_memory=True)
+    barrier()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(st)
+    e2e_its = 0
+    for _ in range(args.steps):
+        bd = bh.to("cuda", non_blocking=True)
+        xd, r, _ = D.dist_cg_solve(sm, comm, bd, max_iter=args.max_iter or None)
+        xh.copy_(xd, non_blocking=True)
+        e2e_its += r.iterations
+    e3.record(st)
+    barrier()
+    e2e_ms = max_over_ranks(e2.elapsed_time(e3))
+    if rank == 0:
+        print(json.dumps({
+            "metric": "fp64 CG iterations/sec (and SpMV HBM GB/s, % of roofline)",
+            "value": round(its / (ms / 1e3), 3), "unit": "iterations/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference generator rebuilt in HBM per shard; b = A x_gen)",
+            "config": {"workload": desc, "n": n, "nnz_stored": nnz_tot, "tol": 1e-10,
+                       "iterations_per_solve": it_per, "step": "one full cg_solve",
+                       "parallelism": f"row-sharded over {world} GPU(s): z-slabs, NCCL halo "
+                                      "send/recv + 2 all-reduces per iteration",
+                       "engine": "per-pass kernels + NCCL (spcg_dist_cg_solve)"},
+            "e2e": {"value": round(e2e_its / (e2e_ms / 1e3), 3), "unit": "iterations/s",
+                    "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+                    "path": "spcg_dist_cg_solve per rank, pinned host b -> x"},
+            "gpu_launches": int(sum(r[2] for r in results)),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1),
+                         "peak": round(peak * world, 1), "unit": "GB/s",
+                         "frac": round(achieved / (peak * world), 4), "traffic": None,
+                         "peak_source": peak_src + f" x {world} GPUs",
+                         "algorithmic_bytes_per_launch": alg, "kernel_ms": kern_ms},
+            "clocks": clocks, "final_relative_residual": results[-1][3],
+            "max_abs_err_vs_xgen": err, "setup_s": round(setup_s, 2)}), flush=True)
+    comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def secondary(peak):
     """The 30880-row FEM-shaped configs (BASELINE configs[0..1]): full solves."""
     import torch
@@ -417,6 +566,8 @@ def main():
     ap.add_argument("--max-iter", type=int, default=0, help="cap iterations (profiling only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--engine", choices=("auto", "sharded"), default="auto",
+                    help="sharded: run the row-sharded engine even on one GPU")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours" and args.max_iter == 0:
         print("note: contract requires warmup >= 3", file=sys.stderr)

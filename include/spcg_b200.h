@@ -149,6 +149,46 @@ int spcg_cg_solve_host(spcg_matrix_t m, const double* h_b, const double* h_x0,
                        double* h_x, double* h_hist, const spcg_cg_options* opts,
                        spcg_cg_result* result, void* stream);
 
+/* ---- row-sharded multi-GPU solve (new: the reference has no distribution,
+ *      SPEC.md:489) ---------------------------------------- */
+
+/* NCCL bootstrap: rank 0 makes an id, the host framework broadcasts the 128
+ * bytes, every rank creates its communicator (one rank per GPU; the current
+ * CUDA device is used).  nranks == 1 needs no NCCL. */
+#define SPCG_COMM_ID_BYTES 128
+typedef struct spcg_comm_s* spcg_comm_t;
+int spcg_comm_unique_id(unsigned char* out_id);
+int spcg_comm_create(int nranks, int rank, const unsigned char* id, spcg_comm_t* out);
+int spcg_comm_destroy(spcg_comm_t comm);
+
+/* Rows [row0,row1) of an n_global-row matrix, GLOBAL column ids (int64 host
+ * arrays; ptr may be a slice of a global offsets array).  SCSR: A = the L+D
+ * rows, B = the same rows of L^T (strict upper), needed for sharded solves. */
+int spcg_matrix_create_rows(int fmt, int64_t n_global, int64_t row0, int64_t row1,
+                            int64_t nnzA, const int64_t* ptrA, const int64_t* idxA,
+                            const double* valA, int64_t nnzB, const int64_t* ptrB,
+                            const int64_t* idxB, const double* valB, spcg_matrix_t* out);
+/* Same rows of an in-HBM generated stencil (kinds of spcg_matrix_generate). */
+int spcg_matrix_generate_rows(int kind, int fmt, int64_t d0, int64_t d1, int64_t d2,
+                              int64_t row0, int64_t row1, spcg_matrix_t* out);
+/* Remap columns: owned -> [0,nloc), others -> nloc + rank in the sorted halo
+ * list.  After this the handle gathers from extended vectors of nloc+nhalo. */
+int spcg_matrix_localize(spcg_matrix_t m, int64_t* nhalo);
+int spcg_matrix_halo(spcg_matrix_t m, int64_t* halo_global_cols);
+
+/* One rank's share of a row-sharded CG solve (solver.py:65-172 semantics on
+ * the global system).  Halo plan: peers[npeers] (ranks, ascending);
+ * recv_off[npeers+1] partitions the halo list by owner; send_off[npeers+1]
+ * partitions send_idx (local rows each peer needs).  Per iteration: pack +
+ * ncclSend/ncclRecv of the halo, pass A, ncclAllReduce(p.q), pass B,
+ * ncclAllReduce(r.r); scalars stay on the device.  d_b/d_x0/d_x are local
+ * (nloc); d_hist (max_iter) is written identically on every rank. */
+int spcg_dist_cg_solve(spcg_matrix_t local, spcg_comm_t comm, int npeers,
+                       const int32_t* peers, const int64_t* recv_off,
+                       const int64_t* send_off, const int32_t* send_idx,
+                       const double* d_b, const double* d_x0, double* d_x, double* d_hist,
+                       const spcg_cg_options* opts, spcg_cg_result* result, void* stream);
+
 /* ---- library ------------------------------------------------------------ */
 
 const char* spcg_last_error(void);

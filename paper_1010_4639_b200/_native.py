@@ -88,6 +88,22 @@ SIGNATURES = {
         _i32,
         [_vp, _vp, _vp, _vp, _vp, ctypes.POINTER(CgOptionsC), ctypes.POINTER(CgResultC), _vp],
     ),
+    "spcg_comm_unique_id": (_i32, [_vp]),
+    "spcg_comm_create": (_i32, [_i32, _i32, _vp, ctypes.POINTER(_vp)]),
+    "spcg_comm_destroy": (_i32, [_vp]),
+    "spcg_matrix_create_rows": (
+        _i32,
+        [_i32, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, ctypes.POINTER(_vp)],
+    ),
+    "spcg_matrix_generate_rows": (_i32, [_i32, _i32, _i64, _i64, _i64, _i64, _i64,
+                                         ctypes.POINTER(_vp)]),
+    "spcg_matrix_localize": (_i32, [_vp, ctypes.POINTER(_i64)]),
+    "spcg_matrix_halo": (_i32, [_vp, _vp]),
+    "spcg_dist_cg_solve": (
+        _i32,
+        [_vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.POINTER(CgOptionsC),
+         ctypes.POINTER(CgResultC), _vp],
+    ),
     "spcg_last_error": (ctypes.c_char_p, []),
     "spcg_abi_version": (_i32, []),
     "spcg_device_info": (

@@ -108,21 +108,22 @@ __device__ __forceinline__ int stencil_row(int kind, int part, long long i, int 
   return c;
 }
 
-__global__ void stencil_count_kernel(int kind, int part, long long n, int nx, int ny, int nz,
-                                     int* counts) {
+// Rows [row0, row0+nrows) of the global stencil (global column ids).
+__global__ void stencil_count_kernel(int kind, int part, long long row0, long long nrows, int nx,
+                                     int ny, int nz, int* counts) {
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    counts[i] = stencil_row(kind, part, i, nx, ny, nz, nullptr, nullptr);
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < nrows; t += stride)
+    counts[t] = stencil_row(kind, part, row0 + t, nx, ny, nz, nullptr, nullptr);
 }
 
-__global__ void stencil_fill_kernel(int kind, int part, long long n, int nx, int ny, int nz,
-                                    const int* ptr, int* idx, double* val) {
+__global__ void stencil_fill_kernel(int kind, int part, long long row0, long long nrows, int nx,
+                                    int ny, int nz, const int* ptr, int* idx, double* val) {
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < nrows; t += stride) {
     int cols[27];
     double vals[27];
-    const int c = stencil_row(kind, part, i, nx, ny, nz, cols, vals);
-    const int k0 = ptr[i];
+    const int c = stencil_row(kind, part, row0 + t, nx, ny, nz, cols, vals);
+    const int k0 = ptr[t];
     for (int u = 0; u < c; ++u) {
       idx[k0 + u] = cols[u];
       val[k0 + u] = vals[u];

@@ -12,8 +12,12 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include "../../include/spcg_b200.h"
 #include "cg.cuh"
+#include "dist.cuh"
 #include "ops.cuh"
 
 using namespace spcg;
@@ -91,6 +95,10 @@ int dev_info(DevInfo** out) {
     if ((rc = occupancy(spmv_kernel<K_SCSR_ATOMIC>, &t))) return rc;
     if ((rc = occupancy(spmv_kernel<K_SCSR_PRIV>, &t))) return rc;
     if ((rc = occupancy(spmv_kernel<K_CSC>, &t))) return rc;
+    if ((rc = occupancy(dist_pass_a<K_CSR>, &t))) return rc;
+    if ((rc = occupancy(dist_pass_a<K_SCSR_PRIV>, &t))) return rc;
+    if ((rc = occupancy(dist_spmv<K_CSR>, &t))) return rc;
+    if ((rc = occupancy(dist_spmv<K_SCSR_PRIV>, &t))) return rc;
     if (br < 1 || bs < 1 || bp < 1) return fail(SPCG_ERR_CUDA, "CG kernel does not fit on an SM");
     d.coop_res = std::min(br * d.sms, 32 * kPollWarps * kPollPer);
     d.coop_stream = std::min(bs * d.sms, 32 * kPollWarps * kPollPer);
@@ -134,11 +142,28 @@ struct Workspace {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
 
+// Workspace of the row-sharded (per-pass) engine.
+struct DistWorkspace {
+  long long next = -1;  // nloc + nhalo
+  double* r_ext = nullptr;
+  double* p_ext[2] = {nullptr, nullptr};
+  double* tmp_ext = nullptr;
+  double* q = nullptr;
+  double* part = nullptr;
+  StepState* S = nullptr;
+  StepState* h_S = nullptr;  // pinned
+  double* send_buf = nullptr;
+  long long send_cap = 0;
+  int* send_idx = nullptr;
+  long long send_idx_cap = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
 }  // namespace
 
 struct spcg_matrix_s {
   int fmt = 0;
-  int n = 0;
+  int n = 0;          // lines held (all rows, or the rows block of a shard)
   long long nnz = 0;
   int device = 0;
   Seg A, B;
@@ -146,7 +171,18 @@ struct spcg_matrix_s {
   Tiles t1, t2;
   long long bytes = 0;
   Workspace ws;
+  // row block of a sharded matrix (rows [row0,row1) of an n_global system)
+  bool is_rows = false;
+  bool localized = false;
+  long long row0 = 0, row1 = 0, n_global = 0;
+  std::vector<long long> halo;  // sorted global ids of the halo columns
+  DistWorkspace dw;
   std::mutex mu;  // one solve at a time per handle (workspace reuse)
+};
+
+struct spcg_comm_s {
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
 };
 
 namespace {
@@ -333,6 +369,12 @@ void free_matrix(spcg_matrix_s* m) {
   if (w.h_res) cudaFreeHost(w.h_res);
   if (w.ev0) cudaEventDestroy(w.ev0);
   if (w.ev1) cudaEventDestroy(w.ev1);
+  DistWorkspace& d = m->dw;
+  F(d.r_ext); F(d.p_ext[0]); F(d.p_ext[1]); F(d.tmp_ext); F(d.q); F(d.part); F(d.S);
+  F(d.send_buf); F(d.send_idx);
+  if (d.h_S) cudaFreeHost(d.h_S);
+  if (d.ev0) cudaEventDestroy(d.ev0);
+  if (d.ev1) cudaEventDestroy(d.ev1);
 }
 
 MatView view(const spcg_matrix_s* m, bool priv) {
@@ -417,12 +459,20 @@ int do_spmv(spcg_matrix_s* m, const double* x, double* y, int accumulation, cuda
   }
 }
 
+int do_dist_cg(spcg_matrix_s* m, spcg_comm_s* comm, int npeers, const int32_t* peers,
+               const int64_t* recv_off, const int64_t* send_off, const int32_t* send_idx,
+               const double* b, const double* x0, double* x, double* hist,
+               const spcg_cg_options* o, spcg_cg_result* out, cudaStream_t st);
+
 int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double* hist,
           const spcg_cg_options* o, spcg_cg_result* out, cudaStream_t st) {
   DevInfo* d;
   int rc;
   if ((rc = dev_info(&d))) return rc;
   if (!(o->tol > 0.0)) return fail(SPCG_ERR_ARG, "tol must be > 0");
+  if (o->engine == 2)  // per-pass engine on one GPU (the sharded engine with no peers)
+    return do_dist_cg(m, nullptr, 0, nullptr, nullptr, nullptr, nullptr, b, x0, x, hist, o, out, st);
+  if (m->is_rows) return fail(SPCG_ERR_ARG, "a row block is solved with spcg_dist_cg_solve");
   const int kf = kfmt_of(m, o->accumulation);
   if (kf == K_SCSR_PRIV && !m->hasB) return fail(SPCG_ERR_UNSUPPORTED, "no L^T for privatized mode");
   const MatView v = view(m, kf == K_SCSR_PRIV);
@@ -580,14 +630,14 @@ int create_from_host(int fmt, int64_t n, int64_t nnz, const PT* hp, const IT* hi
 }
 
 // Device generator: counts -> host prefix sum -> ptr upload -> device fill.
-int gen_seg(int kind, int part, long long n, int nx, int ny, int nz, Seg& s, std::vector<int>& ptr,
-            long long* acct) {
+int gen_seg(int kind, int part, long long row0, long long n, int nx, int ny, int nz, Seg& s,
+            std::vector<int>& ptr, long long* acct) {
   int rc;
   int* counts = nullptr;
   if ((rc = dmalloc((void**)&counts, sizeof(int) * (size_t)std::max<long long>(1, n), nullptr)))
     return rc;
   const int grid = 148 * 8;
-  stencil_count_kernel<<<grid, 256>>>(kind, part, n, nx, ny, nz, counts);
+  stencil_count_kernel<<<grid, 256>>>(kind, part, row0, n, nx, ny, nz, counts);
   CUDA_TRY(cudaGetLastError());
   std::vector<int> c((size_t)n);
   CUDA_TRY(cudaMemcpy(c.data(), counts, sizeof(int) * (size_t)n, cudaMemcpyDeviceToHost));
@@ -600,12 +650,362 @@ int gen_seg(int kind, int part, long long n, int nx, int ny, int nz, Seg& s, std
     ptr[(size_t)i + 1] = (int)acc;
   }
   if ((rc = upload_seg(s, (int)n, ptr, nullptr, nullptr, acc, acct))) return rc;
-  stencil_fill_kernel<<<grid, 256>>>(kind, part, n, nx, ny, nz, s.ptr, s.idx, s.val);
+  stencil_fill_kernel<<<grid, 256>>>(kind, part, row0, n, nx, ny, nz, s.ptr, s.idx, s.val);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaDeviceSynchronize());
   return SPCG_OK;
 }
 
+
+// ---- NCCL, loaded at run time ---------------------------------------------
+// dlopen keeps the library loadable without NCCL and lets it share the NCCL
+// a host framework (torch) already loaded (RTLD_NOLOAD first).
+struct NcclApi {
+  bool ok = false;
+  std::string err;
+  decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclAllReduce) AllReduce = nullptr;
+  decltype(&ncclSend) Send = nullptr;
+  decltype(&ncclRecv) Recv = nullptr;
+  decltype(&ncclGroupStart) GroupStart = nullptr;
+  decltype(&ncclGroupEnd) GroupEnd = nullptr;
+  decltype(&ncclGetErrorString) GetErrorString = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.err = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return a;
+    }
+#define SPCG_NCCL_SYM(f)                                     \
+  a.f = reinterpret_cast<decltype(a.f)>(dlsym(h, "nccl" #f)); \
+  if (!a.f) {                                                \
+    a.err = "libnccl.so.2 lacks nccl" #f;                    \
+    return a;                                                \
+  }
+    SPCG_NCCL_SYM(GetUniqueId)
+    SPCG_NCCL_SYM(CommInitRank)
+    SPCG_NCCL_SYM(CommDestroy)
+    SPCG_NCCL_SYM(AllReduce)
+    SPCG_NCCL_SYM(Send)
+    SPCG_NCCL_SYM(Recv)
+    SPCG_NCCL_SYM(GroupStart)
+    SPCG_NCCL_SYM(GroupEnd)
+    SPCG_NCCL_SYM(GetErrorString)
+#undef SPCG_NCCL_SYM
+    a.ok = true;
+    return a;
+  }();
+  return api;
+}
+
+#define NCCL_TRY(expr)                                                                   \
+  do {                                                                                   \
+    ncclResult_t _r = (expr);                                                            \
+    if (_r != ncclSuccess)                                                               \
+      return fail(SPCG_ERR_CUDA, std::string(#expr " failed: ") + nccl().GetErrorString(_r)); \
+  } while (0)
+
+// ---- row blocks ------------------------------------------------------------
+// Rows [row0,row1) of an n_global system with GLOBAL column ids; becomes
+// solvable after localize().
+template <class IT>
+int seg_from_host(int nrows, const IT* hp, const IT* hi, long long nnz, long long ncols,
+                  std::vector<int>& ptr, std::vector<int>& idx) {
+  ptr.assign((size_t)nrows + 1, 0);
+  if (nrows > 0) {
+    const long long base = (long long)hp[0];
+    if ((long long)hp[nrows] - base != nnz) return fail(SPCG_ERR_ARG, "offsets do not span nnz");
+    for (int i = 0; i <= nrows; ++i) {
+      if (i > 0 && hp[i] < hp[i - 1]) return fail(SPCG_ERR_ARG, "offsets must be non-decreasing");
+      ptr[(size_t)i] = (int)((long long)hp[i] - base);
+    }
+  }
+  idx.resize((size_t)nnz);
+  for (long long k = 0; k < nnz; ++k) {
+    const long long c = (long long)hi[k];
+    if (c < 0 || c >= ncols) return fail(SPCG_ERR_ARG, "column index out of range");
+    idx[(size_t)k] = (int)c;
+  }
+  return SPCG_OK;
+}
+
+// Map global column ids to [0,nloc) (owned) / nloc + rank in the sorted halo
+// list, for segment A (and B).  Host pass over the indices: O(nnz + n/64).
+int localize(spcg_matrix_s* m) {
+  if (!m->is_rows) return fail(SPCG_ERR_ARG, "localize needs a row-block matrix");
+  if (m->localized) return SPCG_OK;
+  const long long N = m->n_global, r0 = m->row0, r1 = m->row1;
+  const size_t words = (size_t)((N + 63) / 64);
+  std::vector<unsigned long long> bits(words, 0ull);
+  Seg* segs[2] = {&m->A, m->hasB ? &m->B : nullptr};
+  std::vector<std::vector<int>> host(2);
+  for (int t = 0; t < 2; ++t) {
+    if (!segs[t]) continue;
+    host[t].resize((size_t)segs[t]->nnz);
+    if (segs[t]->nnz)
+      CUDA_TRY(cudaMemcpy(host[t].data(), segs[t]->idx, sizeof(int) * (size_t)segs[t]->nnz,
+                          cudaMemcpyDeviceToHost));
+    for (int c : host[t])
+      if (c < r0 || c >= r1) bits[(size_t)c >> 6] |= 1ull << (c & 63);
+  }
+  std::vector<long long> prefix(words + 1, 0);
+  for (size_t w = 0; w < words; ++w) prefix[w + 1] = prefix[w] + __builtin_popcountll(bits[w]);
+  m->halo.clear();
+  m->halo.reserve((size_t)prefix[words]);
+  for (size_t w = 0; w < words; ++w)
+    for (unsigned long long b = bits[w]; b; b &= b - 1)
+      m->halo.push_back((long long)(w * 64 + __builtin_ctzll(b)));
+  const long long nloc = r1 - r0;
+  if (nloc + (long long)m->halo.size() >= (1LL << 31) - 16)
+    return fail(SPCG_ERR_UNSUPPORTED, "local extended vector exceeds int32");
+  for (int t = 0; t < 2; ++t) {
+    if (!segs[t]) continue;
+    for (int& c : host[t]) {
+      if (c >= r0 && c < r1) {
+        c = (int)(c - r0);
+      } else {
+        const size_t w = (size_t)c >> 6;
+        const unsigned long long below = bits[w] & ((1ull << (c & 63)) - 1ull);
+        c = (int)(nloc + prefix[w] + __builtin_popcountll(below));
+      }
+    }
+    if (segs[t]->nnz)
+      CUDA_TRY(cudaMemcpy(segs[t]->idx, host[t].data(), sizeof(int) * (size_t)segs[t]->nnz,
+                          cudaMemcpyHostToDevice));
+  }
+  m->localized = true;
+  return SPCG_OK;
+}
+
+int ensure_dist_ws(spcg_matrix_s* m, long long send_total) {
+  DistWorkspace& d = m->dw;
+  int rc;
+  const long long next = (long long)m->n + (long long)m->halo.size();
+  if (d.next != next) {
+    const size_t eb = sizeof(double) * (size_t)std::max<long long>(1, next);
+    if ((rc = dmalloc((void**)&d.r_ext, eb, nullptr))) return rc;
+    if ((rc = dmalloc((void**)&d.p_ext[0], eb, nullptr))) return rc;
+    if ((rc = dmalloc((void**)&d.p_ext[1], eb, nullptr))) return rc;
+    if ((rc = dmalloc((void**)&d.tmp_ext, eb, nullptr))) return rc;
+    if ((rc = dmalloc((void**)&d.q, sizeof(double) * (size_t)std::max(1, m->n), nullptr)))
+      return rc;
+    if ((rc = dmalloc((void**)&d.part, sizeof(double) * 4096, nullptr))) return rc;
+    if ((rc = dmalloc((void**)&d.S, sizeof(StepState), nullptr))) return rc;
+    CUDA_TRY(cudaMallocHost((void**)&d.h_S, sizeof(StepState)));
+    CUDA_TRY(cudaEventCreate(&d.ev0));
+    CUDA_TRY(cudaEventCreate(&d.ev1));
+    d.next = next;
+  }
+  if (d.send_cap < std::max(1LL, send_total)) {
+    if (d.send_buf) cudaFree(d.send_buf);
+    if (d.send_idx) cudaFree(d.send_idx);
+    d.send_buf = nullptr;
+    d.send_idx = nullptr;
+    d.send_cap = std::max(1LL, send_total);
+    if ((rc = dmalloc((void**)&d.send_buf, sizeof(double) * (size_t)d.send_cap, nullptr))) return rc;
+    if ((rc = dmalloc((void**)&d.send_idx, sizeof(int) * (size_t)d.send_cap, nullptr))) return rc;
+  }
+  return SPCG_OK;
+}
+
+struct HaloPlan {
+  ncclComm_t comm = nullptr;
+  int npeers = 0;
+  const int32_t* peers = nullptr;
+  const int64_t* recv_off = nullptr;
+  const int64_t* send_off = nullptr;
+  long long nloc = 0;
+};
+
+// Pack values from `src` at the send rows, then exchange into dst_ext's halo.
+int halo_exchange(const HaloPlan& H, DistWorkspace& d, int mode, StepState* S, const double* r,
+                  const double* p, double* dst_ext, cudaStream_t st, long long* launches) {
+  if (H.npeers == 0) return SPCG_OK;
+  const long long total = H.send_off[H.npeers];
+  if (total > 0) {
+    const int g = (int)std::min<long long>(1184, (total + 255) / 256);
+    dist_pack<<<g, 256, 0, st>>>(mode, S, total, d.send_idx, r, p, d.send_buf);
+    CUDA_TRY(cudaGetLastError());
+    ++*launches;
+  }
+  NcclApi& N = nccl();
+  NCCL_TRY(N.GroupStart());
+  for (int k = 0; k < H.npeers; ++k) {
+    const long long sc = H.send_off[k + 1] - H.send_off[k];
+    const long long rc = H.recv_off[k + 1] - H.recv_off[k];
+    if (sc > 0)
+      NCCL_TRY(N.Send(d.send_buf + H.send_off[k], (size_t)sc, ncclDouble, H.peers[k], H.comm, st));
+    if (rc > 0)
+      NCCL_TRY(N.Recv(dst_ext + H.nloc + H.recv_off[k], (size_t)rc, ncclDouble, H.peers[k], H.comm,
+                      st));
+  }
+  NCCL_TRY(N.GroupEnd());
+  return SPCG_OK;
+}
+
+int allreduce_red(const HaloPlan& H, StepState* S, cudaStream_t st) {
+  if (!H.comm) return SPCG_OK;
+  NCCL_TRY(nccl().AllReduce(&S->red, &S->red, 1, ncclDouble, ncclSum, H.comm, st));
+  return SPCG_OK;
+}
+
+template <int FMT>
+int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const double* x0, double* x,
+                 double* hist, const spcg_cg_options* o, spcg_cg_result* out, cudaStream_t st) {
+  DevInfo* di;
+  int rc;
+  if ((rc = dev_info(&di))) return rc;
+  DistWorkspace& d = m->dw;
+  const MatView v = view(m, FMT == K_SCSR_PRIV);
+  const long long nloc = m->n, next = d.next;
+  const int G = std::max(1, std::min(std::max(1, v.ntiles), di->spmv_grid));
+  const int GE = 2 * di->sms;
+  const size_t sm = sizeof(Smem);
+  long long launches = 0;
+  StepState init{};
+  init.tol = o->tol;
+  init.max_it = o->max_iter > 0 ? o->max_iter : std::max<long long>(1, std::max<long long>(m->n_global, m->n));
+  init.record = o->record_history && hist;
+  init.x0_given = x0 != nullptr;
+  CUDA_TRY(cudaMemcpyAsync(d.S, &init, sizeof(StepState), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemsetAsync(d.p_ext[0], 0, sizeof(double) * (size_t)next, st));
+  CUDA_TRY(cudaMemsetAsync(d.p_ext[1], 0, sizeof(double) * (size_t)next, st));
+  CUDA_TRY(cudaMemsetAsync(d.r_ext, 0, sizeof(double) * (size_t)next, st));
+  CUDA_TRY(cudaEventRecord(d.ev0, st));
+  // ||b|| (solver.py:107)
+  dist_elem<<<GE, kBlock, 0, st>>>(0, nloc, d.S, b, nullptr, nullptr, d.part);
+  ++launches;
+  if ((rc = allreduce_red(H, d.S, st))) return rc;
+  dist_scalar<<<1, 1, 0, st>>>(0, d.S, hist);
+  ++launches;
+  // x = x0, r = b - A x0 (solver.py:120-124)
+  dist_x<<<GE, kBlock, 0, st>>>(0, nloc, d.S, x0, x);
+  ++launches;
+  if (x0) {
+    CUDA_TRY(cudaMemcpyAsync(d.tmp_ext, x0, sizeof(double) * (size_t)nloc,
+                             cudaMemcpyDeviceToDevice, st));
+    if ((rc = halo_exchange(H, d, 0, d.S, x0, nullptr, d.tmp_ext, st, &launches))) return rc;
+    dist_spmv<FMT><<<G, kBlock, sm, st>>>(v, d.tmp_ext, d.q);
+    ++launches;
+    dist_elem<<<GE, kBlock, 0, st>>>(1, nloc, d.S, b, d.q, d.r_ext, d.part);
+  } else {
+    dist_elem<<<GE, kBlock, 0, st>>>(1, nloc, d.S, b, nullptr, d.r_ext, d.part);
+  }
+  ++launches;
+  if ((rc = allreduce_red(H, d.S, st))) return rc;
+  dist_scalar<<<1, 1, 0, st>>>(1, d.S, hist);
+  ++launches;
+  CUDA_TRY(cudaGetLastError());
+  // CG loop: iteration k writes its direction into p_ext[(k-1)&1]; the host
+  // enqueues chunks of iterations and polls the device-side done flag between
+  // chunks (iterations after `done` are no-ops on every rank).
+  const int chunk = 16;
+  long long it = 0;
+  for (;;) {
+    for (int c = 0; c < chunk; ++c, ++it) {
+      double* p_new = d.p_ext[it & 1];
+      double* p_old = d.p_ext[(it + 1) & 1];
+      if ((rc = halo_exchange(H, d, 1, d.S, d.r_ext, p_old, d.r_ext, st, &launches))) return rc;
+      dist_pass_a<FMT><<<G, kBlock, sm, st>>>(v, d.S, d.r_ext, p_old, p_new, x, d.q, d.part);
+      if ((rc = allreduce_red(H, d.S, st))) return rc;
+      dist_scalar<<<1, 1, 0, st>>>(2, d.S, hist);
+      dist_elem<<<GE, kBlock, 0, st>>>(2, nloc, d.S, nullptr, d.q, d.r_ext, d.part);
+      if ((rc = allreduce_red(H, d.S, st))) return rc;
+      dist_scalar<<<1, 1, 0, st>>>(3, d.S, hist);
+      launches += 4;
+    }
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(d.h_S, d.S, sizeof(StepState), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (d.h_S->done) break;
+  }
+  const long long K = d.h_S->k;
+  // x += alpha_K p_K (p_K in p_ext[(K-1)&1]), then the true residual
+  dist_x<<<GE, kBlock, 0, st>>>(1, nloc, d.S, d.p_ext[(K - 1) & 1], x);
+  ++launches;
+  if (o->recompute_final_residual && d.h_S->status == 0 && d.h_S->b_norm != 0.0) {
+    CUDA_TRY(cudaMemcpyAsync(d.tmp_ext, x, sizeof(double) * (size_t)nloc,
+                             cudaMemcpyDeviceToDevice, st));
+    if ((rc = halo_exchange(H, d, 0, d.S, x, nullptr, d.tmp_ext, st, &launches))) return rc;
+    dist_spmv<FMT><<<G, kBlock, sm, st>>>(v, d.tmp_ext, d.q);
+    dist_elem<<<GE, kBlock, 0, st>>>(3, nloc, d.S, b, d.q, nullptr, d.part);
+    if ((rc = allreduce_red(H, d.S, st))) return rc;
+    dist_true_rel<<<1, 1, 0, st>>>(d.S);
+    launches += 3;
+  }
+  CUDA_TRY(cudaEventRecord(d.ev1, st));
+  CUDA_TRY(cudaMemcpyAsync(d.h_S, d.S, sizeof(StepState), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  CUDA_TRY(cudaGetLastError());
+  float ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&ms, d.ev0, d.ev1));
+  const StepState& S = *d.h_S;
+  out->iterations = S.k;
+  out->converged = S.converged;
+  out->status = S.status;
+  out->fail_iteration = S.fail_iter;
+  out->final_relative_residual = S.rel;
+  out->b_norm = S.b_norm;
+  out->device_ms = ms;
+  out->kernel_launches = launches;
+  if (S.status != 0) {
+    const char* what = S.status == SPCG_ERR_NOT_SPD ? "matrix not positive definite"
+                       : S.status == SPCG_ERR_NONFINITE_ALPHA ? "non-finite alpha"
+                       : S.status == SPCG_ERR_NONFINITE_RESIDUAL ? "non-finite residual"
+                                                                  : "non-finite beta";
+    return fail(S.status, std::string(what) + " at iteration " + std::to_string(S.fail_iter));
+  }
+  return SPCG_OK;
+}
+
+int do_dist_cg(spcg_matrix_s* m, spcg_comm_s* comm, int npeers, const int32_t* peers,
+               const int64_t* recv_off, const int64_t* send_off, const int32_t* send_idx,
+               const double* b, const double* x0, double* x, double* hist,
+               const spcg_cg_options* o, spcg_cg_result* out, cudaStream_t st) {
+  if (!(o->tol > 0.0)) return fail(SPCG_ERR_ARG, "tol must be > 0");
+  if (m->fmt == SPCG_FMT_CSC) return fail(SPCG_ERR_UNSUPPORTED, "sharded CSC is not supported");
+  const bool priv = m->fmt == SPCG_FMT_SCSR;
+  if (priv && !m->hasB) return fail(SPCG_ERR_UNSUPPORTED, "sharded SCSR needs its L^T rows");
+  if (m->is_rows && !m->localized) return fail(SPCG_ERR_ARG, "call spcg_matrix_localize first");
+  if (npeers > 0 && (!comm || !comm->comm)) return fail(SPCG_ERR_ARG, "peers need a communicator");
+  if (npeers > 0 && !nccl().ok) return fail(SPCG_ERR_CUDA, nccl().err);
+  if (o->record_history && !hist) return fail(SPCG_ERR_ARG, "record_history needs a history buffer");
+  HaloPlan H;
+  H.comm = comm ? comm->comm : nullptr;
+  H.npeers = npeers;
+  H.peers = peers;
+  H.recv_off = recv_off;
+  H.send_off = send_off;
+  H.nloc = m->n;
+  const long long nhalo = (long long)m->halo.size();
+  if (npeers > 0 && recv_off[npeers] != nhalo)
+    return fail(SPCG_ERR_ARG, "receive plan does not cover the halo");
+  const long long send_total = npeers > 0 ? send_off[npeers] : 0;
+  int rc;
+  if ((rc = ensure_dist_ws(m, send_total))) return rc;
+  if (send_total > 0) {
+    for (long long s = 0; s < send_total; ++s)
+      if (send_idx[s] < 0 || send_idx[s] >= m->n) return fail(SPCG_ERR_ARG, "send index out of range");
+    CUDA_TRY(cudaMemcpyAsync(m->dw.send_idx, send_idx, sizeof(int) * (size_t)send_total,
+                             cudaMemcpyHostToDevice, st));
+  }
+  if (m->n == 0 && npeers == 0) {
+    out->iterations = 0;
+    out->converged = 1;
+    out->status = 0;
+    out->final_relative_residual = 0.0;
+    return SPCG_OK;
+  }
+  return priv ? dist_solve_t<K_SCSR_PRIV>(m, H, b, x0, x, hist, o, out, st)
+              : dist_solve_t<K_CSR>(m, H, b, x0, x, hist, o, out, st);
+}
 }  // namespace
 
 // ============================================================================
@@ -657,7 +1057,7 @@ int spcg_matrix_generate(int kind, int fmt, int64_t d0, int64_t d1, int64_t d2,
   std::vector<int> ptr, tptr;
   // CSC of a symmetric stencil is its CSR
   const int part = fmt == SPCG_FMT_SCSR ? 1 : 0;
-  if ((rc = gen_seg(kind, part, n, (int)d0, (int)d1, (int)d2, m->A, ptr, &m->bytes)) ||
+  if ((rc = gen_seg(kind, part, 0, n, (int)d0, (int)d1, (int)d2, m->A, ptr, &m->bytes)) ||
       (rc = finish_matrix(m, ptr, nullptr, nullptr, true))) {
     free_matrix(m);
     delete m;
@@ -665,7 +1065,7 @@ int spcg_matrix_generate(int kind, int fmt, int64_t d0, int64_t d1, int64_t d2,
   }
   m->nnz = m->A.nnz;
   if (fmt == SPCG_FMT_SCSR) {
-    if ((rc = gen_seg(kind, 2, n, (int)d0, (int)d1, (int)d2, m->B, tptr, &m->bytes)) ||
+    if ((rc = gen_seg(kind, 2, 0, n, (int)d0, (int)d1, (int)d2, m->B, tptr, &m->bytes)) ||
         (rc = finish_transpose(m, ptr, tptr, nullptr, nullptr, true))) {
       free_matrix(m);
       delete m;
@@ -812,6 +1212,156 @@ int spcg_cg_solve_host(spcg_matrix_t m, const double* h_b, const double* h_x0, d
   CUDA_TRY(cudaStreamSynchronize(st));
   g_last_error = err;
   return rc;
+}
+
+// ---- row-sharded multi-GPU solve ------------------------------------------
+int spcg_comm_unique_id(unsigned char* out) {
+  if (!out) return fail(SPCG_ERR_ARG, "null out");
+  NcclApi& N = nccl();
+  if (!N.ok) return fail(SPCG_ERR_CUDA, N.err);
+  ncclUniqueId id;
+  NCCL_TRY(N.GetUniqueId(&id));
+  memcpy(out, id.internal, SPCG_COMM_ID_BYTES);
+  return SPCG_OK;
+}
+
+int spcg_comm_create(int nranks, int rank, const unsigned char* id_bytes, spcg_comm_t* out) {
+  if (!out || nranks < 1 || rank < 0 || rank >= nranks) return fail(SPCG_ERR_ARG, "bad comm args");
+  spcg_comm_s* c = new spcg_comm_s();
+  c->nranks = nranks;
+  c->rank = rank;
+  if (nranks > 1) {
+    NcclApi& N = nccl();
+    if (!N.ok) {
+      delete c;
+      return fail(SPCG_ERR_CUDA, N.err);
+    }
+    if (!id_bytes) {
+      delete c;
+      return fail(SPCG_ERR_ARG, "null unique id");
+    }
+    ncclUniqueId id;
+    memcpy(id.internal, id_bytes, SPCG_COMM_ID_BYTES);
+    ncclResult_t r = N.CommInitRank(&c->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+      delete c;
+      return fail(SPCG_ERR_CUDA, std::string("ncclCommInitRank: ") + N.GetErrorString(r));
+    }
+  }
+  *out = c;
+  return SPCG_OK;
+}
+
+int spcg_comm_destroy(spcg_comm_t c) {
+  if (!c) return SPCG_OK;
+  if (c->comm) nccl().CommDestroy(c->comm);
+  delete c;
+  return SPCG_OK;
+}
+
+int spcg_matrix_create_rows(int fmt, int64_t n_global, int64_t row0, int64_t row1, int64_t nnzA,
+                            const int64_t* ptrA, const int64_t* idxA, const double* valA,
+                            int64_t nnzB, const int64_t* ptrB, const int64_t* idxB,
+                            const double* valB, spcg_matrix_t* out) {
+  if (!out) return fail(SPCG_ERR_ARG, "null out");
+  int rc;
+  if ((rc = check_csr_host(fmt, n_global, nnzA))) return rc;
+  if (fmt == SPCG_FMT_CSC) return fail(SPCG_ERR_UNSUPPORTED, "row blocks are CSR / SCSR");
+  if (row0 < 0 || row1 < row0 || row1 > n_global) return fail(SPCG_ERR_ARG, "bad row range");
+  const int nrows = (int)(row1 - row0);
+  std::vector<int> pA, iA, pB, iB;
+  if ((rc = seg_from_host(nrows, ptrA, idxA, nnzA, n_global, pA, iA))) return rc;
+  const bool hasB = fmt == SPCG_FMT_SCSR && ptrB != nullptr;
+  if (hasB && (rc = seg_from_host(nrows, ptrB, idxB, nnzB, n_global, pB, iB))) return rc;
+  DevInfo* d;
+  if ((rc = dev_info(&d))) return rc;
+  spcg_matrix_s* m = new spcg_matrix_s();
+  m->fmt = fmt;
+  m->n = nrows;
+  m->nnz = nnzA;
+  m->is_rows = true;
+  m->row0 = row0;
+  m->row1 = row1;
+  m->n_global = n_global;
+  CUDA_TRY(cudaGetDevice(&m->device));
+  if ((rc = finish_matrix(m, pA, iA.data(), valA, false)) ||
+      (hasB && (rc = finish_transpose(m, pA, pB, iB.data(), valB, false)))) {
+    free_matrix(m);
+    delete m;
+    return rc;
+  }
+  *out = m;
+  return SPCG_OK;
+}
+
+int spcg_matrix_generate_rows(int kind, int fmt, int64_t d0, int64_t d1, int64_t d2, int64_t row0,
+                              int64_t row1, spcg_matrix_t* out) {
+  if (!out) return fail(SPCG_ERR_ARG, "null out");
+  if (kind < 0 || kind > 2) return fail(SPCG_ERR_ARG, "unknown generator kind");
+  if (fmt != SPCG_FMT_CSR && fmt != SPCG_FMT_SCSR) return fail(SPCG_ERR_ARG, "row blocks are CSR / SCSR");
+  if (kind == 0) d2 = 1;
+  if (d0 < 1 || d1 < 1 || d2 < 1) return fail(SPCG_ERR_ARG, "extents must be >= 1");
+  const long long N = d0 * d1 * d2;
+  if (N >= (1LL << 31) - 16) return fail(SPCG_ERR_UNSUPPORTED, "grid exceeds int32 rows");
+  if (row0 < 0 || row1 < row0 || row1 > N) return fail(SPCG_ERR_ARG, "bad row range");
+  DevInfo* d;
+  int rc;
+  if ((rc = dev_info(&d))) return rc;
+  spcg_matrix_s* m = new spcg_matrix_s();
+  m->fmt = fmt;
+  m->n = (int)(row1 - row0);
+  m->is_rows = true;
+  m->row0 = row0;
+  m->row1 = row1;
+  m->n_global = N;
+  CUDA_TRY(cudaGetDevice(&m->device));
+  std::vector<int> ptr, tptr;
+  const int part = fmt == SPCG_FMT_SCSR ? 1 : 0;
+  if ((rc = gen_seg(kind, part, row0, m->n, (int)d0, (int)d1, (int)d2, m->A, ptr, &m->bytes)) ||
+      (rc = finish_matrix(m, ptr, nullptr, nullptr, true))) {
+    free_matrix(m);
+    delete m;
+    return rc;
+  }
+  m->nnz = m->A.nnz;
+  if (fmt == SPCG_FMT_SCSR) {
+    if ((rc = gen_seg(kind, 2, row0, m->n, (int)d0, (int)d1, (int)d2, m->B, tptr, &m->bytes)) ||
+        (rc = finish_transpose(m, ptr, tptr, nullptr, nullptr, true))) {
+      free_matrix(m);
+      delete m;
+      return rc;
+    }
+  }
+  *out = m;
+  return SPCG_OK;
+}
+
+int spcg_matrix_localize(spcg_matrix_t m, int64_t* nhalo) {
+  if (!m) return fail(SPCG_ERR_ARG, "null matrix");
+  std::lock_guard<std::mutex> lk(m->mu);
+  int rc = localize(m);
+  if (rc) return rc;
+  if (nhalo) *nhalo = (int64_t)m->halo.size();
+  return SPCG_OK;
+}
+
+int spcg_matrix_halo(spcg_matrix_t m, int64_t* halo_cols) {
+  if (!m) return fail(SPCG_ERR_ARG, "null matrix");
+  if (!m->localized) return fail(SPCG_ERR_ARG, "matrix is not localized");
+  for (size_t k = 0; k < m->halo.size(); ++k) halo_cols[k] = m->halo[k];
+  return SPCG_OK;
+}
+
+int spcg_dist_cg_solve(spcg_matrix_t local, spcg_comm_t comm, int npeers, const int32_t* peers,
+                       const int64_t* recv_off, const int64_t* send_off, const int32_t* send_idx,
+                       const double* d_b, const double* d_x0, double* d_x, double* d_hist,
+                       const spcg_cg_options* opts, spcg_cg_result* result, void* stream) {
+  if (!local || !opts || !result) return fail(SPCG_ERR_ARG, "null argument");
+  if (npeers < 0 || (npeers > 0 && (!peers || !recv_off || !send_off)))
+    return fail(SPCG_ERR_ARG, "bad halo plan");
+  std::lock_guard<std::mutex> lk(local->mu);
+  return do_dist_cg(local, comm, npeers, peers, recv_off, send_off, send_idx, d_b, d_x0, d_x,
+                    d_hist, opts, result, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -196,8 +196,10 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Fixed-order block sum, result broadcast to every thread.
-__device__ __forceinline__ double block_sum(double v, Smem& sm) {
+// Fixed-order block sum, result broadcast to every thread.  S: any shared
+// struct with `double red[32]; double bcast;`.
+template <class S>
+__device__ __forceinline__ double block_sum(double v, S& sm) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   v = warp_sum(v);
   __syncthreads();  // protects sm.red / sm.bcast reuse

@@ -1,0 +1,287 @@
+"""Row-sharded CG across the GPUs of one node (new — the
+reference has no distribution).
+
+One process per GPU (torchrun).  Rows are split into contiguous blocks; each
+rank holds its block as a *localized* matrix handle (owned columns ->
+[0, nloc), halo columns -> nloc + position in the sorted halo list).  Per CG
+iteration the C++ engine (spcg_dist_cg_solve) exchanges the halo of the next
+search direction with ncclSend/ncclRecv and sums the two dot products with
+ncclAllReduce; all scalars stay on the device and are bitwise identical on
+every rank, so all ranks stop at the same iteration.
+
+Host-side logic here is plain numpy + torch.distributed object collectives
+(works with the gloo backend on CPU, which tests/test_distributed.py uses):
+  * `row_partition`  — contiguous, balanced by stored entries (+ optional
+    alignment, e.g. whole z-planes of a stencil);
+  * `localize_columns` — the halo numbering (also done in C for device
+    handles; both must agree);
+  * `halo_plan` — receive lists by owner and the matching send lists.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+
+
+# ---- partition & plan (host logic) ---------------------------------------------
+def row_partition(n: int, nranks: int, row_start: np.ndarray | None = None,
+                  align: int = 1) -> np.ndarray:
+    """Boundaries b[0..nranks] of contiguous row blocks.  Balanced by stored
+    entries + rows when offsets are given, by rows otherwise; every interior
+    boundary is a multiple of `align` (rounded to the nearest)."""
+    if nranks < 1:
+        raise ValueError("nranks must be >= 1")
+    b = np.zeros(nranks + 1, dtype=np.int64)
+    b[-1] = n
+    if row_start is not None:
+        w = np.asarray(row_start, dtype=np.int64) + np.arange(n + 1, dtype=np.int64)
+        for k in range(1, nranks):
+            b[k] = int(np.searchsorted(w, (w[-1] * k) // nranks))
+    else:
+        for k in range(1, nranks):
+            b[k] = (n * k) // nranks
+    if align > 1:
+        b[1:-1] = np.clip(np.rint(b[1:-1] / align).astype(np.int64) * align, 0, n)
+    return np.maximum.accumulate(b)
+
+
+def localize_columns(cols: np.ndarray, row0: int, row1: int) -> tuple[np.ndarray, np.ndarray]:
+    """(local column ids, sorted halo global ids) — the numbering the C
+    library's spcg_matrix_localize produces."""
+    cols = np.asarray(cols, dtype=np.int64)
+    own = (cols >= row0) & (cols < row1)
+    halo = np.unique(cols[~own])
+    loc = np.empty_like(cols)
+    nloc = row1 - row0
+    loc[own] = cols[own] - row0
+    loc[~own] = nloc + np.searchsorted(halo, cols[~own])
+    return loc, halo
+
+
+@dataclass
+class HaloPlan:
+    peers: np.ndarray      # int32, ascending ranks exchanged with
+    recv_off: np.ndarray   # int64[npeers+1] into the halo list
+    send_off: np.ndarray   # int64[npeers+1] into send_idx
+    send_idx: np.ndarray   # int32 local rows to send, grouped by peer
+
+    @property
+    def npeers(self) -> int:
+        return int(self.peers.shape[0])
+
+
+def halo_plan(halo: np.ndarray, bounds: np.ndarray, rank: int, all_gather_object) -> HaloPlan:
+    """Build the exchange plan.  `all_gather_object(obj) -> list` gathers one
+    picklable object per rank (torch.distributed.all_gather_object)."""
+    halo = np.asarray(halo, dtype=np.int64)
+    owners = np.searchsorted(bounds, halo, side="right") - 1
+    nranks = len(bounds) - 1
+    if halo.size and (owners.min() < 0 or owners.max() >= nranks or (owners == rank).any()):
+        raise ValueError("halo column outside the partition or owned by this rank")
+    want = {int(q): halo[owners == q] for q in np.unique(owners)}
+    everyone = all_gather_object(want)
+    row0 = int(bounds[rank])
+    send = {q: np.asarray(everyone[q][rank], dtype=np.int64) - row0
+            for q in range(nranks) if q != rank and rank in everyone[q]}
+    peers = sorted(set(want) | set(send))
+    recv_off = [0]
+    send_off = [0]
+    send_idx = []
+    for q in peers:
+        recv_off.append(recv_off[-1] + (want[q].size if q in want else 0))
+        s = send.get(q, np.empty(0, dtype=np.int64))
+        send_off.append(send_off[-1] + s.size)
+        send_idx.append(s)
+    # receive order must follow the sorted halo list
+    if halo.size and not np.array_equal(
+            np.concatenate([want[q] for q in peers if q in want]), halo):
+        raise AssertionError("halo is not grouped by ascending owner")
+    si = np.concatenate(send_idx) if send_idx else np.empty(0, dtype=np.int64)
+    if si.size and (si.min() < 0 or si.max() >= bounds[rank + 1] - row0):
+        raise ValueError("a peer requested rows this rank does not own")
+    return HaloPlan(np.asarray(peers, dtype=np.int32), np.asarray(recv_off, dtype=np.int64),
+                    np.asarray(send_off, dtype=np.int64), si.astype(np.int32))
+
+
+# ---- communicator ----------------------------------------------------------------
+class Comm:
+    """NCCL communicator of the C library, bootstrapped over torch.distributed."""
+
+    def __init__(self, rank: int, world: int, broadcast_object=None):
+        self.rank, self.world = rank, world
+        lib = N.load()
+        h = ctypes.c_void_p()
+        if world > 1:
+            idbuf = (ctypes.c_ubyte * 128)()
+            if rank == 0:
+                N.check(lib.spcg_comm_unique_id(idbuf), "spcg_comm_unique_id")
+            data = broadcast_object(bytes(idbuf) if rank == 0 else None)
+            idbuf = (ctypes.c_ubyte * 128).from_buffer_copy(data)
+            N.check(lib.spcg_comm_create(world, rank, idbuf, ctypes.byref(h)), "spcg_comm_create")
+        else:
+            N.check(lib.spcg_comm_create(1, 0, None, ctypes.byref(h)), "spcg_comm_create")
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            N.load().spcg_comm_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def torch_collectives():
+    """(all_gather_object, broadcast_object) over the default process group."""
+    import torch.distributed as dist
+
+    def gather(obj):
+        out = [None] * dist.get_world_size()
+        dist.all_gather_object(out, obj)
+        return out
+
+    def bcast(obj):
+        box = [obj]
+        dist.broadcast_object_list(box, src=0)
+        return box[0]
+
+    return gather, bcast
+
+
+# ---- sharded matrices and the solve ------------------------------------------------
+class ShardedMatrix:
+    """This rank's localized row block + its halo plan."""
+
+    def __init__(self, dm, row0: int, row1: int, n_global: int, halo: np.ndarray, plan: HaloPlan):
+        self.dm, self.row0, self.row1, self.n_global = dm, row0, row1, n_global
+        self.halo, self.plan = halo, plan
+
+    @property
+    def nloc(self) -> int:
+        return self.row1 - self.row0
+
+    @staticmethod
+    def _finish(dm, bounds, rank, all_gather_object):
+        lib = N.load()
+        nh = ctypes.c_int64()
+        N.check(lib.spcg_matrix_localize(dm.handle, ctypes.byref(nh)), "spcg_matrix_localize")
+        halo = np.empty(nh.value, dtype=np.int64)
+        N.check(lib.spcg_matrix_halo(dm.handle, halo.ctypes.data if halo.size else None),
+                "spcg_matrix_halo")
+        plan = halo_plan(halo, bounds, rank, all_gather_object)
+        return ShardedMatrix(dm, int(bounds[rank]), int(bounds[rank + 1]), int(bounds[-1]), halo,
+                             plan)
+
+    @classmethod
+    def from_stencil(cls, kind: str, dims, fmt: str, rank: int, world: int, all_gather_object,
+                     align_planes: bool = True) -> "ShardedMatrix":
+        """Rows of an in-HBM generated stencil; blocks aligned to whole
+        z-planes (x-y planes for 2-D) so each halo is one plane per side."""
+        from .device import DeviceMatrix
+
+        kinds = {"poisson2d": N.GEN_POISSON2D, "poisson3d": N.GEN_POISSON3D,
+                 "stencil27": N.GEN_STENCIL27}
+        d = list(dims) + [1] * (3 - len(dims))
+        n = d[0] * d[1] * d[2]
+        plane = d[0] if kind == "poisson2d" else d[0] * d[1]
+        bounds = row_partition(n, world, align=plane if align_planes else 1)
+        h = ctypes.c_void_p()
+        N.check(N.load().spcg_matrix_generate_rows(kinds[kind], DeviceMatrix.FORMATS[fmt], d[0], d[1],
+                                                   d[2], int(bounds[rank]), int(bounds[rank + 1]),
+                                                   ctypes.byref(h)), "spcg_matrix_generate_rows")
+        dm = DeviceMatrix(h.value, DeviceMatrix.FORMATS[fmt], 0, 0)
+        dm._refresh()
+        return cls._finish(dm, bounds, rank, all_gather_object)
+
+    @classmethod
+    def from_host(cls, a, rank: int, world: int, all_gather_object) -> "ShardedMatrix":
+        """Rows of a host CsrMatrix / SymHalfMatrix (SCSR also ships the rows
+        of L^T, needed by the owner-computes transpose)."""
+        from .core import CsrMatrix, SymHalfMatrix, build_csr_from_triplets
+        from .device import DeviceMatrix
+
+        bounds = row_partition(a.n, world, a.row_start)
+        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+        rs = np.ascontiguousarray(a.row_start, dtype=np.int64)
+        k0, k1 = int(rs[r0]), int(rs[r1])
+        ci = np.ascontiguousarray(a.col_idx[k0:k1], dtype=np.int64)
+        v = np.ascontiguousarray(a.values[k0:k1], dtype=np.float64)
+        ptrA = np.ascontiguousarray(rs[r0:r1 + 1])
+        keep = [ptrA, ci, v]
+        if isinstance(a, SymHalfMatrix):
+            fmt = N.FMT_SCSR
+            lr, lc, lv = a.strict_lower
+            t = build_csr_from_triplets((lc, lr, lv), a.n)  # rows of L^T
+            tb0, tb1 = int(t.row_start[r0]), int(t.row_start[r1])
+            ptrB = np.ascontiguousarray(t.row_start[r0:r1 + 1], dtype=np.int64)
+            ciB = np.ascontiguousarray(t.col_idx[tb0:tb1], dtype=np.int64)
+            vB = np.ascontiguousarray(t.values[tb0:tb1], dtype=np.float64)
+            keep += [ptrB, ciB, vB]
+            b_args = (int(vB.size), ptrB.ctypes.data, ciB.ctypes.data if ciB.size else None,
+                      vB.ctypes.data if vB.size else None)
+        elif isinstance(a, CsrMatrix):
+            fmt = N.FMT_CSR
+            b_args = (0, None, None, None)
+        else:
+            raise TypeError(f"cannot shard {type(a).__name__}")
+        h = ctypes.c_void_p()
+        N.check(N.load().spcg_matrix_create_rows(
+            fmt, a.n, r0, r1, int(v.size), ptrA.ctypes.data, ci.ctypes.data if ci.size else None,
+            v.ctypes.data if v.size else None, *b_args, ctypes.byref(h)), "spcg_matrix_create_rows")
+        dm = DeviceMatrix(h.value, fmt, 0, 0)
+        dm._refresh()
+        return cls._finish(dm, bounds, rank, all_gather_object)
+
+    def spmv_ext(self, x_ext):
+        """y_loc = A_loc x_ext for an extended vector (own + halo values)."""
+        import torch
+
+        y = torch.empty(self.nloc, dtype=torch.float64, device=x_ext.device)
+        N.check(N.load().spcg_spmv(self.dm.handle, x_ext.data_ptr(), y.data_ptr(), N.ACC_PRIVATIZED,
+                                   torch.cuda.current_stream().cuda_stream), "spcg_spmv")
+        return y
+
+
+def dist_cg_solve(sm: ShardedMatrix, comm: Comm, b_loc, x0_loc=None, tol: float = 1e-10,
+                  max_iter: int | None = None, record_history: bool = False,
+                  recompute_final_residual: bool = True):
+    """One rank's part of the sharded solve.  b_loc / x0_loc: CUDA tensors
+    of this rank's rows.  Returns (x_loc, CgResultC, history or None)."""
+    import torch
+
+    p = sm.plan
+    mi = max_iter if max_iter else max(1, sm.n_global)
+    x = torch.empty(sm.nloc, dtype=torch.float64, device=b_loc.device)
+    hist = torch.empty(mi if record_history else 1, dtype=torch.float64, device=b_loc.device)
+    o = N.CgOptionsC(tol=float(tol), max_iter=int(mi), record_history=int(record_history),
+                     recompute_final_residual=int(recompute_final_residual),
+                     accumulation=N.ACC_PRIVATIZED, engine=2)
+    res = N.CgResultC()
+
+    def ptr(a):
+        return a.ctypes.data if a.size else None
+
+    rc = N.load().spcg_dist_cg_solve(
+        sm.dm.handle, comm.handle, p.npeers, ptr(p.peers), ptr(p.recv_off), ptr(p.send_off),
+        ptr(p.send_idx), b_loc.data_ptr(), x0_loc.data_ptr() if x0_loc is not None else None,
+        x.data_ptr(), hist.data_ptr() if record_history else None, o, res,
+        torch.cuda.current_stream().cuda_stream)
+    from .solver import _BREAKDOWN
+
+    if rc in _BREAKDOWN:
+        raise _BREAKDOWN[rc](int(res.fail_iteration))
+    N.check(rc, "spcg_dist_cg_solve")
+    h = hist[: res.iterations].cpu().numpy() if record_history else None
+    return x, res, h
