@@ -528,6 +528,69 @@ def secondary(peak):
     return out
 
 
+def run_table1(args):
+    """Table I of the paper on the 30880 FEM-shaped matrix: device op rows
+    (CUDA events) next to the reference's compiled kernels on host cores."""
+    import statistics
+
+    from oracle import oracle as O
+    from paper_1010_4639_b200.genprob import fem_mesh, rhs_for
+    from paper_1010_4639_b200.table1 import run_table1 as gpu_rows
+
+    F = fem_mesh()
+    b, _ = rhs_for(F, seed=1)
+    rep = gpu_rows(F, b, reps=15)
+    # reference CPU rows (workers = host cores), median of 15 after a warm-up
+    cores = O.host_cores()
+    K = O.RefKernels(workers=cores, accumulation="atomic")
+    Kp = O.RefKernels(workers=cores, accumulation="privatized")
+    rng = np.random.default_rng(0)
+    u, v = rng.standard_normal(F.n), rng.standard_normal(F.n)
+    from paper_1010_4639_b200.core import extract_lower
+
+    S = extract_lower(F)
+    rows_s = np.repeat(np.arange(S.n, dtype=np.int64), np.diff(S.row_start))
+    mk = S.col_idx < rows_s
+    strict = (np.ascontiguousarray(rows_s[mk]), np.ascontiguousarray(S.col_idx[mk]),
+              np.ascontiguousarray(S.values[mk]))
+    rsF, ciF, vF = (np.ascontiguousarray(a) for a in (F.row_start, F.col_idx, F.values))
+    rsS, ciS, vS = (np.ascontiguousarray(a) for a in (S.row_start, S.col_idx, S.values))
+    cpu_ops = {
+        "dotProd": lambda: K.dot(u, v),
+        "AXPY": lambda: K.axpy(1.5, u, v),
+        "SpMV": lambda: K.spmv_full(rsF, ciF, vF, u),
+        "SpMV(sym)/atomic": lambda: K.spmv_sym(rsS, ciS, vS, strict, u),
+        "SpMV(sym)/privatized": lambda: Kp.spmv_sym(rsS, ciS, vS, strict, u),
+    }
+
+    def med(fn, reps=15):
+        fn()
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            ts.append((time.perf_counter() - t0) * 1e3)
+        return statistics.median(ts)
+
+    for row in rep["ops"]:
+        if row["op"] in cpu_ops:
+            row["cpu_ms"] = med(cpu_ops[row["op"]])
+            row["speedup"] = row["cpu_ms"] / row["median_ms"]
+    for row in rep["cg"]:
+        if row["storage"] in ("full", "sym"):
+            kind = "csr" if row["storage"] == "full" else "sym"
+            arrs = (rsF, ciF, vF) if kind == "csr" else (rsS, ciS, vS)
+            O.cg_solve_ref(kind, *arrs, b, workers=cores, accumulation="atomic")
+            t0 = time.perf_counter()
+            r = O.cg_solve_ref(kind, *arrs, b, workers=cores, accumulation="atomic")
+            row["cpu_ms"] = (time.perf_counter() - t0) * 1e3
+            row["cpu_iterations"] = r.iterations
+            row["speedup"] = row["cpu_ms"] / row["time_ms"]
+    rep["meta"]["cpu_cores"] = cores
+    rep["meta"]["cpu_kind"] = "reference _ckernels (oracle/_ref)"
+    print(json.dumps(rep), flush=True)
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -566,12 +629,16 @@ def main():
     ap.add_argument("--max-iter", type=int, default=0, help="cap iterations (profiling only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--table1", action="store_true",
+                    help="paper Table-I per-op rows (F matrix) on GPU vs the reference CPU path")
     ap.add_argument("--engine", choices=("auto", "sharded"), default="auto",
                     help="sharded: run the row-sharded engine even on one GPU")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours" and args.max_iter == 0:
         print("note: contract requires warmup >= 3", file=sys.stderr)
-    if args.impl == "reference":
+    if args.table1:
+        run_table1(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -152,8 +152,10 @@ __device__ __forceinline__ void run_tiles(Pipe& P, Smem& sm, const MatView& M, c
         mbar_wait(&sm.full[j], 0);
         bool active = false;
         int line = -1;
-        const LineOut o =
-            tile_line<FMT, GATHER_CSC>(sm, j, M, src, y, active, line, res_prod(sm, j));
+        // resident (latency-bound) tiles: thread-per-row beats the two-phase
+        // stream body (one fewer CTA barrier on the critical path)
+        const LineOut o = tile_line<FMT, GATHER_CSC, Src, false>(sm, j, M, src, y, active, line,
+                                                                 res_prod(sm, j));
         if (active) fn(j, line, o);
       }
     }

@@ -166,14 +166,17 @@ struct LineOut {
 // Tiles averaging more than this many entries per line use the two-phase
 // CSR-stream body; shorter rows (e.g. the 7-point stencil) keep one thread
 // per row, which already has all of its gathers in flight.
-constexpr int kStreamMinPerLine = 8;
+#ifndef SPCG_STREAM_MIN
+#define SPCG_STREAM_MIN 8
+#endif
+constexpr int kStreamMinPerLine = SPCG_STREAM_MIN;
 
 // Computes line i (the tid-th line of staged tile s).  For FMT in
 // {SCSR_ATOMIC, CSC} the scatter goes to y (must be zeroed beforehand) and
 // the line's own gather is returned in q; for CSR / SCSR_PRIV the caller
 // stores q.  `active` = this thread owns a line.  Long tiles: every thread
 // must call (CTA-wide reductions); the line's result is valid in thread 0.
-template <int FMT, bool GATHER_CSC, class Src>
+template <int FMT, bool GATHER_CSC, class Src, bool ALLOW_STREAM = true>
 __device__ __forceinline__ LineOut tile_line(Smem& sm, int s, const MatView& M, const Src& src,
                                              double* y, bool& active, int& line, double* prod,
                                              const double* xpre = nullptr) {
@@ -183,7 +186,7 @@ __device__ __forceinline__ LineOut tile_line(Smem& sm, int s, const MatView& M, 
     const int i = mt.row0 + (int)threadIdx.x;
     active = i < mt.row1;
     line = i;
-    const bool stream = (FMT == K_CSR || FMT == K_SCSR_PRIV) &&
+    const bool stream = ALLOW_STREAM && (FMT == K_CSR || FMT == K_SCSR_PRIV) &&
                         mt.cnt > kStreamMinPerLine * (mt.row1 - mt.row0);
     const double* v = sm.val[s];
     const int* ix = sm.idx[s];

@@ -131,6 +131,62 @@ __global__ void stencil_fill_kernel(int kind, int part, long long row0, long lon
   }
 }
 
+// Per-tile column extent (max, min over both segments), one CTA per tile.
+__global__ void tile_colext_kernel(const int4* tdesc, const int2* tdescB, int ntiles,
+                                   const int* idxA, const int* idxB, int* colmax, int* colmin) {
+  __shared__ int smax[32], smin[32];
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int4 d = tdesc[t];
+    int mx = -1, mn = 0x7fffffff;
+    for (int k = d.z + threadIdx.x; k < d.w; k += blockDim.x) {
+      const int c = idxA[k];
+      mx = max(mx, c);
+      mn = min(mn, c);
+    }
+    if (tdescB) {
+      const int2 e = tdescB[t];
+      for (int k = e.x + threadIdx.x; k < e.y; k += blockDim.x) {
+        const int c = idxB[k];
+        mx = max(mx, c);
+        mn = min(mn, c);
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) {
+      smax[w] = mx;
+      smin[w] = mn;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+        mx = max(mx, smax[i]);
+        mn = min(mn, smin[i]);
+      }
+      colmax[t] = mx;
+      colmin[t] = mn;
+    }
+  }
+}
+
+// Leading-edge window of tile t: the columns beyond everything tile t-1
+// touched (banded / stencil matrices: ~one tile's worth of new columns);
+// empty when the tile brings nothing new or the window exceeds `cap`.
+__global__ void tile_window_kernel(int ntiles, const int* colmax, const int* colmin, int cap,
+                                   int2* twin) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntiles) return;
+  const int hi = colmax[t];
+  int lo = colmin[t];
+  if (t > 0) lo = max(lo, colmax[t - 1] + 1);
+  if (hi < 0 || hi - lo + 1 > cap) lo = hi + 1;
+  twin[t] = make_int2(lo, hi);
+}
+
 // int64 -> int32 narrowing on the device (upload path).
 __global__ void narrow_i64_kernel(long long n, const long long* src, int* dst) {
   const long long stride = (long long)gridDim.x * blockDim.x;

@@ -63,6 +63,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// L2 prefetch of a contiguous global range (bulk, no registers, no completion).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // ---- global memory ----------------------------------------------------------
 // fp64 reduction without return (SASS: RED.E.ADD.F64).
 __device__ __forceinline__ void red_add_f64(double* addr, double v) {

@@ -119,6 +119,7 @@ struct Seg {
 struct Tiles {
   int4* desc = nullptr;
   int2* descB = nullptr;
+  int2* win = nullptr;  // leading-edge prefetch windows
   int ntiles = 0;
 };
 
@@ -321,6 +322,24 @@ void transpose_strict_lower(int n, const std::vector<int>& ptr, const int* idx, 
     }
 }
 
+// (Re)compute the per-tile leading-edge windows from the device indices.
+int compute_windows(Tiles& t, const Seg& A, const Seg* B, long long* acct) {
+  if (t.ntiles == 0) return SPCG_OK;
+  int rc;
+  if (!t.win && (rc = dmalloc((void**)&t.win, sizeof(int2) * (size_t)t.ntiles, acct))) return rc;
+  int *cmax = nullptr, *cmin = nullptr;
+  if ((rc = dmalloc((void**)&cmax, sizeof(int) * (size_t)t.ntiles, nullptr))) return rc;
+  if ((rc = dmalloc((void**)&cmin, sizeof(int) * (size_t)t.ntiles, nullptr))) return rc;
+  tile_colext_kernel<<<std::min(t.ntiles, 148 * 16), 256>>>(t.desc, B ? t.descB : nullptr, t.ntiles,
+                                                           A.idx, B ? B->idx : nullptr, cmax, cmin);
+  tile_window_kernel<<<(t.ntiles + 255) / 256, 256>>>(t.ntiles, cmax, cmin, 4 * kTileLines, t.win);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaDeviceSynchronize());
+  cudaFree(cmax);
+  cudaFree(cmin);
+  return SPCG_OK;
+}
+
 int target_tiles() {
   DevInfo* d = nullptr;
   if (dev_info(&d)) return 148;
@@ -356,13 +375,21 @@ int finish_transpose(spcg_matrix_s* m, const std::vector<int>& ptr, const std::v
   return SPCG_OK;
 }
 
+// Windows for both tile tables (after the indices are final / localized).
+int refresh_windows(spcg_matrix_s* m) {
+  int rc;
+  if ((rc = compute_windows(m->t1, m->A, nullptr, &m->bytes))) return rc;
+  if (m->hasB && (rc = compute_windows(m->t2, m->A, &m->B, &m->bytes))) return rc;
+  return SPCG_OK;
+}
+
 void free_matrix(spcg_matrix_s* m) {
   auto F = [](void* p) {
     if (p) cudaFree(p);
   };
   F(m->A.ptr); F(m->A.idx); F(m->A.val);
   F(m->B.ptr); F(m->B.idx); F(m->B.val);
-  F(m->t1.desc); F(m->t1.descB); F(m->t2.desc); F(m->t2.descB);
+  F(m->t1.desc); F(m->t1.descB); F(m->t2.desc); F(m->t2.descB); F(m->t1.win); F(m->t2.win);
   Workspace& w = m->ws;
   F(w.r); F(w.p0); F(w.p1); F(w.q); F(w.part); F(w.slots); F(w.res);
   F(w.b); F(w.x); F(w.x0); F(w.hist);
@@ -390,6 +417,7 @@ MatView view(const spcg_matrix_s* m, bool priv) {
   v.ptrB = m->B.ptr;
   v.idxB = m->B.idx;
   v.valB = m->B.val;
+  v.twin = t.win;
   return v;
 }
 
@@ -625,6 +653,11 @@ int create_from_host(int fmt, int64_t n, int64_t nnz, const PT* hp, const IT* hi
       return rc;
     }
   }
+  if ((rc = refresh_windows(m))) {
+    free_matrix(m);
+    delete m;
+    return rc;
+  }
   *out = m;
   return SPCG_OK;
 }
@@ -781,7 +814,7 @@ int localize(spcg_matrix_s* m) {
                           cudaMemcpyHostToDevice));
   }
   m->localized = true;
-  return SPCG_OK;
+  return refresh_windows(m);
 }
 
 int ensure_dist_ws(spcg_matrix_s* m, long long send_total) {
@@ -1072,6 +1105,11 @@ int spcg_matrix_generate(int kind, int fmt, int64_t d0, int64_t d1, int64_t d2,
       return rc;
     }
   }
+  if ((rc = refresh_windows(m))) {
+    free_matrix(m);
+    delete m;
+    return rc;
+  }
   *out = m;
   return SPCG_OK;
 }
@@ -1290,6 +1328,11 @@ int spcg_matrix_create_rows(int fmt, int64_t n_global, int64_t row0, int64_t row
     delete m;
     return rc;
   }
+  if ((rc = refresh_windows(m))) {
+    free_matrix(m);
+    delete m;
+    return rc;
+  }
   *out = m;
   return SPCG_OK;
 }
@@ -1331,6 +1374,11 @@ int spcg_matrix_generate_rows(int kind, int fmt, int64_t d0, int64_t d1, int64_t
       delete m;
       return rc;
     }
+  }
+  if ((rc = refresh_windows(m))) {
+    free_matrix(m);
+    delete m;
+    return rc;
   }
   *out = m;
   return SPCG_OK;

@@ -50,6 +50,7 @@ struct MatView {
   const int* ptrB;       // CSR of L^T (K_SCSR_PRIV only)
   const int* idxB;
   const double* valB;
+  const int2* twin;      // per tile: new gathered columns [lo,hi] vs the previous tile
 };
 
 struct StageMeta {
@@ -77,17 +78,51 @@ __device__ __forceinline__ int my_tile_count(int ntiles) {
   return (ntiles > (int)blockIdx.x) ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 }
 
-// Thread 0 only: stage tile `t` into ring slot `s`.
+// Tile descriptor(s), fetched ahead of the issue so thread 0 never waits on
+// a global load between a tile's barrier and the next bulk copy.
+struct TileDesc {
+  int4 a;   // {row0,row1,k0,k1}
+  int2 b;   // {k0B,k1B}
+  int2 w;   // leading-edge column window to prefetch (lo > hi: none)
+};
 template <bool TWO>
-__device__ __forceinline__ void issue_tile(Smem& sm, const MatView& M, int t, int s) {
-  const int4 d = M.tdesc[t];
-  const int row0 = d.x, row1 = d.y, kA0 = d.z, kA1 = d.w;
-  int kB0 = 0, kB1 = 0;
-  if (TWO) {
-    const int2 e = M.tdescB[t];
-    kB0 = e.x;
-    kB1 = e.y;
+__device__ __forceinline__ TileDesc load_desc(const MatView& M, int t) {
+  TileDesc d;
+  d.a = M.tdesc[t];
+  d.b = TWO ? M.tdescB[t] : make_int2(0, 0);
+  d.w = M.twin ? M.twin[t] : make_int2(1, 0);
+  return d;
+}
+
+// Vectors a pass may ask to be pulled into L2 (leading-edge window of each
+// tile, issued with the tile's staging copies kStages tiles ahead).  Measured
+// neutral-to-negative on the stencil workloads (profiles/r01/), so the
+// passes leave it unset; kept for matrices with poor gather locality.
+struct Prefetch {
+  const double* v0 = nullptr;  // gathered vectors: leading-edge window
+  const double* v1 = nullptr;
+  const double* own = nullptr; // read at the tile's own rows
+};
+
+__device__ __forceinline__ void prefetch_window(const double* v, int2 w) {
+  if (v == nullptr || w.x > w.y) return;
+  const int lo = w.x & ~1;             // 16-byte aligned
+  const int hi = (w.y + 2) & ~1;       // exclusive, even
+  bulk_prefetch_l2(v + lo, (uint32_t)(hi - lo) * 8u);
+}
+
+// Thread 0 only: stage the tile described by `dd` into ring slot `s`.
+template <bool TWO>
+__device__ __forceinline__ void issue_tile_desc(Smem& sm, const MatView& M, const TileDesc& dd,
+                                                int s, const Prefetch* pf = nullptr) {
+  if (pf) {
+    prefetch_window(pf->v0, dd.w);
+    prefetch_window(pf->v1, dd.w);
+    prefetch_window(pf->own, make_int2(dd.a.x, dd.a.y - 1));
   }
+  const int4 d = dd.a;
+  const int row0 = d.x, row1 = d.y, kA0 = d.z, kA1 = d.w;
+  const int kB0 = TWO ? dd.b.x : 0, kB1 = TWO ? dd.b.y : 0;
   StageMeta& mt = sm.meta[s];
   mt.row0 = row0;
   mt.row1 = row1;
@@ -122,6 +157,11 @@ __device__ __forceinline__ void issue_tile(Smem& sm, const MatView& M, int t, in
   }
 }
 
+template <bool TWO>
+__device__ __forceinline__ void issue_tile(Smem& sm, const MatView& M, int t, int s) {
+  issue_tile_desc<TWO>(sm, M, load_desc<TWO>(M, t), s);
+}
+
 // Ring of kStages stages over this CTA's tile list (t = blockIdx.x + j*gridDim.x).
 // If the CTA owns <= kStages tiles they are loaded once and stay resident in
 // shared memory for the whole kernel (the 30880-row matrix fits this way);
@@ -130,7 +170,9 @@ __device__ __forceinline__ void issue_tile(Smem& sm, const MatView& M, int t, in
 struct Pipe {
   int m;
   bool resident;
-  long long c;  // tiles consumed (streaming mode)
+  long long c;    // tiles consumed (streaming mode)
+  TileDesc next;  // thread 0: descriptor of the next tile to issue
+  Prefetch pf;    // gathered vectors of the pass that will consume issued tiles
 };
 
 // allow_resident=false forces cyclic streaming even for <= kStages tiles
@@ -145,6 +187,7 @@ __device__ __forceinline__ void pipe_start(Pipe& P, Smem& sm, const MatView& M,
   if (threadIdx.x == 0 && P.m > 0) {
     const int pre = P.resident ? P.m : kStages;
     for (int j = 0; j < pre; ++j) issue_tile<TWO>(sm, M, my_tile(j % P.m), j);
+    if (!P.resident) P.next = load_desc<TWO>(M, my_tile(kStages % P.m));
   }
 }
 
@@ -164,7 +207,10 @@ template <bool TWO>
 __device__ __forceinline__ void pipe_release(Pipe& P, Smem& sm, const MatView& M, int s) {
   if (P.resident) return;
   __syncthreads();
-  if (threadIdx.x == 0) issue_tile<TWO>(sm, M, my_tile((int)((P.c + kStages) % P.m)), s);
+  if (threadIdx.x == 0) {
+    issue_tile_desc<TWO>(sm, M, P.next, s, &P.pf);
+    P.next = load_desc<TWO>(M, my_tile((int)((P.c + kStages + 1) % P.m)));
+  }
   P.c++;
 }
 

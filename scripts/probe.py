@@ -93,7 +93,8 @@ def main():
     big = {"P2": ("poisson2d", (4096, 4096), "csr", 1),
            "P3": ("poisson3d", (400, 400, 400), "csr", 1),
            "Q27": ("stencil27", (256, 256, 256), "scsr", 0),
-           "Q27P": ("stencil27", (256, 256, 256), "scsr", 1)}
+           "Q27P": ("stencil27", (256, 256, 256), "scsr", 1),
+           "Q27F": ("stencil27", (256, 256, 256), "csr", 1)}
     for c in cfgs:
         if c not in big:
             continue
