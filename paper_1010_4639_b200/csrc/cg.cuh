@@ -314,6 +314,7 @@ __global__ void __launch_bounds__(kBlock, RES ? 1 : kStreamMinBlocks) cg_kernel(
   double* p_cur = nullptr;
 
   unsigned long long tr[4] = {0, 0, 0, 0};
+  P.trace = A.trace != nullptr;
   unsigned long long tlast = A.trace ? globaltimer_ns() : 0;
   auto mark = [&](int ph) {
     if (A.trace && threadIdx.x == 0) {
@@ -453,7 +454,8 @@ __global__ void __launch_bounds__(kBlock, RES ? 1 : kStreamMinBlocks) cg_kernel(
 
   if (A.trace && threadIdx.x == 0) {
 #pragma unroll
-    for (int ph = 0; ph < 4; ++ph) A.trace[blockIdx.x * 4 + ph] = tr[ph];
+    for (int ph = 0; ph < 4; ++ph) A.trace[blockIdx.x * 5 + ph] = tr[ph];
+    A.trace[blockIdx.x * 5 + 4] = P.wait_ns;
   }
   if (status != ST_OK) {
     if (leader) {

@@ -57,8 +57,11 @@ __device__ __forceinline__ void last_block_sum(double v, SM& sm, double* part, S
 }
 
 // pass A: p_k = fold, q = A p_k, x += alpha_{k-1} p_{k-1}, red = p.q partial
+#ifndef SPCG_DIST_MINB
+#define SPCG_DIST_MINB 2
+#endif
 template <int FMT>
-__global__ void __launch_bounds__(kBlock, 1)
+__global__ void __launch_bounds__(kBlock, SPCG_DIST_MINB)
     dist_pass_a(const MatView M, StepState* S, const double* r_ext, const double* p_old,
                 double* p_new, double* x, double* q, double* part) {
   extern __shared__ __align__(128) unsigned char smem_raw[];

@@ -530,8 +530,8 @@ int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double
   unsigned long long* trace = nullptr;
   static const bool tracing = getenv("SPCG_TRACE") != nullptr;
   if (tracing) {
-    CUDA_TRY(cudaMalloc((void**)&trace, sizeof(unsigned long long) * 4 * (size_t)grid));
-    CUDA_TRY(cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * 4 * (size_t)grid, st));
+    CUDA_TRY(cudaMalloc((void**)&trace, sizeof(unsigned long long) * 5 * (size_t)grid));
+    CUDA_TRY(cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * 5 * (size_t)grid, st));
   }
   a.trace = trace;
   a.res = w.res;
@@ -554,23 +554,23 @@ int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double
   CUDA_TRY(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
   const CgDevResult& r = *w.h_res;
   if (trace) {
-    std::vector<unsigned long long> tv(4 * (size_t)grid);
+    std::vector<unsigned long long> tv(5 * (size_t)grid);
     CUDA_TRY(cudaMemcpy(tv.data(), trace, sizeof(unsigned long long) * tv.size(),
                         cudaMemcpyDeviceToHost));
     cudaFree(trace);
-    double mean[4] = {0, 0, 0, 0}, mx[4] = {0, 0, 0, 0};
+    double mean[5] = {0, 0, 0, 0, 0}, mx[5] = {0, 0, 0, 0, 0};
     for (int b = 0; b < grid; ++b)
-      for (int ph = 0; ph < 4; ++ph) {
-        mean[ph] += (double)tv[4 * b + ph] / grid;
-        mx[ph] = std::max(mx[ph], (double)tv[4 * b + ph]);
+      for (int ph = 0; ph < 5; ++ph) {
+        mean[ph] += (double)tv[5 * b + ph] / grid;
+        mx[ph] = std::max(mx[ph], (double)tv[5 * b + ph]);
       }
     const double it = (double)std::max<long long>(1, r.iterations);
     fprintf(stderr,
             "[spcg trace] grid=%d res=%d iters=%lld us/iter mean(max): passA %.3f(%.3f) "
-            "reduce1 %.3f(%.3f) passB %.3f(%.3f) reduce2 %.3f(%.3f)\n",
+            "reduce1 %.3f(%.3f) passB %.3f(%.3f) reduce2 %.3f(%.3f) tilewait %.3f(%.3f)\n",
             grid, (int)res, r.iterations, mean[0] / it / 1e3, mx[0] / it / 1e3, mean[1] / it / 1e3,
             mx[1] / it / 1e3, mean[2] / it / 1e3, mx[2] / it / 1e3, mean[3] / it / 1e3,
-            mx[3] / it / 1e3);
+            mx[3] / it / 1e3, mean[4] / it / 1e3, mx[4] / it / 1e3);
   }
   out->iterations = r.iterations;
   out->converged = r.converged;

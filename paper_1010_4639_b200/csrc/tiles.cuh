@@ -173,6 +173,8 @@ struct Pipe {
   long long c;    // tiles consumed (streaming mode)
   TileDesc next;  // thread 0: descriptor of the next tile to issue
   Prefetch pf;    // gathered vectors of the pass that will consume issued tiles
+  unsigned long long wait_ns;  // thread 0: time blocked on tile data (tracing)
+  bool trace;
 };
 
 // allow_resident=false forces cyclic streaming even for <= kStages tiles
@@ -184,6 +186,8 @@ __device__ __forceinline__ void pipe_start(Pipe& P, Smem& sm, const MatView& M,
   P.m = my_tile_count(M.ntiles);
   P.resident = allow_resident && P.m <= kStages;
   P.c = 0;
+  P.wait_ns = 0;
+  P.trace = false;
   if (threadIdx.x == 0 && P.m > 0) {
     const int pre = P.resident ? P.m : kStages;
     for (int j = 0; j < pre; ++j) issue_tile<TWO>(sm, M, my_tile(j % P.m), j);
@@ -198,7 +202,13 @@ __device__ __forceinline__ int pipe_acquire(Pipe& P, Smem& sm, int j) {
     return j;
   }
   const int s = (int)(P.c % kStages);
-  mbar_wait(&sm.full[s], (uint32_t)((P.c / kStages) & 1));
+  if (P.trace && threadIdx.x == 0) {
+    const unsigned long long t0 = globaltimer_ns();
+    mbar_wait(&sm.full[s], (uint32_t)((P.c / kStages) & 1));
+    P.wait_ns += globaltimer_ns() - t0;
+  } else {
+    mbar_wait(&sm.full[s], (uint32_t)((P.c / kStages) & 1));
+  }
   return s;
 }
 

@@ -54,9 +54,9 @@ def spmv_time(dm, acc, n, reps=20):
     return e0.elapsed_time(e1) / reps
 
 
-def report(name, dm, n, nnz_stored, b_t, acc=1, max_iter=0):
+def report(name, dm, n, nnz_stored, b_t, acc=1, max_iter=0, engine=0):
     t0 = time.time()
-    res, x = solve(dm, b_t, acc=acc, max_iter=max_iter)
+    res, x = solve(dm, b_t, acc=acc, max_iter=max_iter, engine=engine)
     ms, its, fr = res[-1]
     best = min(r[0] for r in res)
     it_bytes = 12 * nnz_stored + 4 * (n + 1) + 88 * n
@@ -111,7 +111,7 @@ def main():
         if full is not dm:
             full.close()
         print(json.dumps({"gen_s": gen_s, "cfg": c}), flush=True)
-        report(c, dm, n, dm.nnz, bt, acc=acc, max_iter=int(sys.argv[-1]) if False else 0)
+        report(c, dm, n, dm.nnz, bt, acc=acc, engine=int(__import__("os").environ.get("ENGINE", "0")))
         dm.close()
 
 
