@@ -122,8 +122,12 @@ typedef struct {
   int32_t record_history;        /* write rel residual per iteration to hist   */
   int32_t recompute_final_residual; /* default 1 (solver.py:159-162)           */
   int32_t accumulation;          /* spcg_accumulation, SCSR only               */
-  int32_t engine;                /* 0 = auto, 1 = persistent cooperative grid,
-                                    2 = per-pass kernels (multi-launch)        */
+  int32_t engine;                /* 0 = auto (3 when the system is resident
+                                    in shared memory, else 1),
+                                    1 = persistent kernel, two-reduction CG,
+                                    2 = per-pass kernels (the sharded engine),
+                                    3 = persistent single-reduction CG
+                                        (Chronopoulos-Gear, resident only)   */
 } spcg_cg_options;
 
 typedef struct {

@@ -128,7 +128,10 @@ def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
                 f"{p} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`"
             )
         lib = ctypes.CDLL(str(p))
+        lenient = os.environ.get("SPCG_LIB_LENIENT") == "1"  # dev: older library builds
         for name, (res, args) in SIGNATURES.items():
+            if lenient and not hasattr(lib, name):
+                continue
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

@@ -70,8 +70,15 @@ enum : int {
 // l reads slots l, l+32, ...), then fences once for the CTA.
 // The total is summed in the same fixed order in every CTA (bitwise equal).
 constexpr int kSlotWords = 32;  // 256 bytes per CTA slot
-constexpr int kPollWarps = (kBlock / 32) < 8 ? (kBlock / 32) : 8;  // warps polling the slots
-constexpr int kPollPer = 3;  // slots per polling lane: grids up to 32*kPollWarps*3 CTAs
+#ifndef SPCG_POLL_WARPS
+#define SPCG_POLL_WARPS 8
+#endif
+#ifndef SPCG_POLL_NS
+#define SPCG_POLL_NS 200
+#endif
+constexpr int kPollWarps = (kBlock / 32) < SPCG_POLL_WARPS ? (kBlock / 32) : SPCG_POLL_WARPS;
+constexpr int kPollPer = (384 + 32 * kPollWarps - 1) / (32 * kPollWarps);  // grids <= 384 CTAs
+constexpr unsigned kPollSleepNs = SPCG_POLL_NS;  // back-off between polling rounds
 
 __device__ __forceinline__ double grid_allreduce(double v, Smem& sm, unsigned long long* slots,
                                                  uint32_t& epoch) {
@@ -113,6 +120,7 @@ __device__ __forceinline__ double grid_allreduce(double v, Smem& sm, unsigned lo
           any |= pend[u];
         }
       if (++spins > kSpinLimit) asm volatile("trap;");
+      if (kPollSleepNs && any) __nanosleep(kPollSleepNs);
     }
     double s = 0.0;
 #pragma unroll
@@ -313,6 +321,7 @@ __global__ void __launch_bounds__(kBlock, RES ? 1 : kStreamMinBlocks) cg_kernel(
   double* p_new = A.p0;
   double* p_cur = nullptr;
 
+#if SPCG_TRACE
   unsigned long long tr[4] = {0, 0, 0, 0};
   P.trace = A.trace != nullptr;
   unsigned long long tlast = A.trace ? globaltimer_ns() : 0;
@@ -323,6 +332,9 @@ __global__ void __launch_bounds__(kBlock, RES ? 1 : kStreamMinBlocks) cg_kernel(
       tlast = t;
     }
   };
+#else
+  auto mark = [](int) {};
+#endif
   for (long long k = 1; k <= max_it; ++k) {
     // pass A
     double pq = 0.0;
@@ -332,7 +344,7 @@ __global__ void __launch_bounds__(kBlock, RES ? 1 : kStreamMinBlocks) cg_kernel(
         pg[j] = o.xi;
         if (!ATOM) qg[j] = o.q;
       } else {
-        if (k > 1) A.x[i] = mul_add_rn(o.xo, alpha, p_old[i]);
+        if (k > 1) A.x[i] = mul_add_rn(SPCG_NO_XPRE ? A.x[i] : o.xo, alpha, p_old[i]);
         if (!ATOM) A.q[i] = o.q;
       }
       p_new[i] = o.xi;
@@ -452,11 +464,13 @@ __global__ void __launch_bounds__(kBlock, RES ? 1 : kStreamMinBlocks) cg_kernel(
     p_new = t;
   }
 
+#if SPCG_TRACE
   if (A.trace && threadIdx.x == 0) {
 #pragma unroll
     for (int ph = 0; ph < 4; ++ph) A.trace[blockIdx.x * 5 + ph] = tr[ph];
     A.trace[blockIdx.x * 5 + 4] = P.wait_ns;
   }
+#endif
   if (status != ST_OK) {
     if (leader) {
       A.res->iterations = iterations;

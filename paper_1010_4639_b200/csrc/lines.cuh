@@ -186,6 +186,10 @@ __device__ __forceinline__ LineOut tile_line(Smem& sm, int s, const MatView& M, 
     const int i = mt.row0 + (int)threadIdx.x;
     active = i < mt.row1;
     line = i;
+#ifndef SPCG_NO_XPRE
+#define SPCG_NO_XPRE 0
+#endif
+    if (SPCG_NO_XPRE) xpre = nullptr;
     const bool stream = ALLOW_STREAM && (FMT == K_CSR || FMT == K_SCSR_PRIV) &&
                         mt.cnt > kStreamMinPerLine * (mt.row1 - mt.row0);
     const double* v = sm.val[s];

@@ -17,6 +17,7 @@
 
 #include "../../include/spcg_b200.h"
 #include "cg.cuh"
+#include "cg1.cuh"
 #include "dist.cuh"
 #include "ops.cuh"
 
@@ -85,6 +86,14 @@ int dev_info(DevInfo** out) {
     br = std::min(br, t);
     if ((rc = occupancy(cg_kernel<K_CSC, true>, &t, kSmemRes))) return rc;
     br = std::min(br, t);
+    if ((rc = occupancy(cg1_kernel<K_CSR>, &t, kSmemRes))) return rc;
+    br = std::min(br, t);
+    if ((rc = occupancy(cg1_kernel<K_SCSR_ATOMIC>, &t, kSmemRes))) return rc;
+    br = std::min(br, t);
+    if ((rc = occupancy(cg1_kernel<K_SCSR_PRIV>, &t, kSmemRes))) return rc;
+    br = std::min(br, t);
+    if ((rc = occupancy(cg1_kernel<K_CSC>, &t, kSmemRes))) return rc;
+    br = std::min(br, t);
     if ((rc = occupancy(cg_kernel<K_SCSR_ATOMIC, false>, &t))) return rc;
     bs = std::min(bs, t);
     if ((rc = occupancy(cg_kernel<K_SCSR_PRIV, false>, &t))) return rc;
@@ -134,6 +143,7 @@ struct Workspace {
   unsigned long long* slots = nullptr;
   CgDevResult* res = nullptr;
   CgDevResult* h_res = nullptr;  // pinned
+  double* cg1 = nullptr;         // single-reduction engine: R[2], S[2], W[3]
   // host-API staging
   double* b = nullptr;
   double* x = nullptr;
@@ -392,7 +402,7 @@ void free_matrix(spcg_matrix_s* m) {
   F(m->t1.desc); F(m->t1.descB); F(m->t2.desc); F(m->t2.descB); F(m->t1.win); F(m->t2.win);
   Workspace& w = m->ws;
   F(w.r); F(w.p0); F(w.p1); F(w.q); F(w.part); F(w.slots); F(w.res);
-  F(w.b); F(w.x); F(w.x0); F(w.hist);
+  F(w.b); F(w.x); F(w.x0); F(w.hist); F(w.cg1);
   if (w.h_res) cudaFreeHost(w.h_res);
   if (w.ev0) cudaEventDestroy(w.ev0);
   if (w.ev1) cudaEventDestroy(w.ev1);
@@ -458,6 +468,14 @@ int launch_cg(const CgArgs& a, bool res, int grid, cudaStream_t st) {
   const void* fn = res ? (const void*)cg_kernel<FMT, true> : (const void*)cg_kernel<FMT, false>;
   CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBlock), args,
                                        res ? kSmemRes : sizeof(Smem), st));
+  return SPCG_OK;
+}
+
+template <int FMT>
+int launch_cg1(const Cg1Args& a, int grid, cudaStream_t st) {
+  void* args[] = {(void*)&a};
+  const void* fn = (const void*)cg1_kernel<FMT>;
+  CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBlock), args, kSmemRes, st));
   return SPCG_OK;
 }
 
@@ -539,12 +557,34 @@ int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double
   a.max_iter = max_iter;
   a.record_history = o->record_history;
   a.recompute = o->recompute_final_residual;
+  // engine 3 (or auto on resident systems): single-reduction CG, one grid
+  // barrier per iteration; engine 1 forces the two-reduction form
+  const bool single = res && (o->engine == 3 || o->engine == 0);
+  Cg1Args g{};
+  if (single) {
+    const size_t vb = sizeof(double) * (size_t)std::max(1, m->n);
+    if (!w.cg1 && (rc = dmalloc((void**)&w.cg1, 7 * vb, nullptr))) return rc;
+    CUDA_TRY(cudaMemsetAsync(w.cg1, 0, 7 * vb, st));
+    g.base = a;
+    for (int k = 0; k < 2; ++k) g.R[k] = w.cg1 + (size_t)k * std::max(1, m->n);
+    for (int k = 0; k < 2; ++k) g.S[k] = w.cg1 + (size_t)(2 + k) * std::max(1, m->n);
+    for (int k = 0; k < 3; ++k) g.W[k] = w.cg1 + (size_t)(4 + k) * std::max(1, m->n);
+  }
   CUDA_TRY(cudaEventRecord(w.ev0, st));
-  switch (kf) {
-    case K_CSR: rc = launch_cg<K_CSR>(a, res, grid, st); break;
-    case K_SCSR_ATOMIC: rc = launch_cg<K_SCSR_ATOMIC>(a, res, grid, st); break;
-    case K_SCSR_PRIV: rc = launch_cg<K_SCSR_PRIV>(a, res, grid, st); break;
-    default: rc = launch_cg<K_CSC>(a, res, grid, st); break;
+  if (single) {
+    switch (kf) {
+      case K_CSR: rc = launch_cg1<K_CSR>(g, grid, st); break;
+      case K_SCSR_ATOMIC: rc = launch_cg1<K_SCSR_ATOMIC>(g, grid, st); break;
+      case K_SCSR_PRIV: rc = launch_cg1<K_SCSR_PRIV>(g, grid, st); break;
+      default: rc = launch_cg1<K_CSC>(g, grid, st); break;
+    }
+  } else {
+    switch (kf) {
+      case K_CSR: rc = launch_cg<K_CSR>(a, res, grid, st); break;
+      case K_SCSR_ATOMIC: rc = launch_cg<K_SCSR_ATOMIC>(a, res, grid, st); break;
+      case K_SCSR_PRIV: rc = launch_cg<K_SCSR_PRIV>(a, res, grid, st); break;
+      default: rc = launch_cg<K_CSC>(a, res, grid, st); break;
+    }
   }
   if (rc) return rc;
   CUDA_TRY(cudaEventRecord(w.ev1, st));

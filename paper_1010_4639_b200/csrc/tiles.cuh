@@ -19,6 +19,11 @@
 
 namespace spcg {
 
+// SPCG_TRACE=1 builds per-phase timing into the CG kernels (dev builds only:
+// even runtime-disabled, the hooks cost registers in the hot loops).
+#ifndef SPCG_TRACE
+#define SPCG_TRACE 0
+#endif
 #ifndef SPCG_BLOCK
 #define SPCG_BLOCK 512
 #endif
@@ -173,8 +178,10 @@ struct Pipe {
   long long c;    // tiles consumed (streaming mode)
   TileDesc next;  // thread 0: descriptor of the next tile to issue
   Prefetch pf;    // gathered vectors of the pass that will consume issued tiles
+#if SPCG_TRACE
   unsigned long long wait_ns;  // thread 0: time blocked on tile data (tracing)
   bool trace;
+#endif
 };
 
 // allow_resident=false forces cyclic streaming even for <= kStages tiles
@@ -186,8 +193,10 @@ __device__ __forceinline__ void pipe_start(Pipe& P, Smem& sm, const MatView& M,
   P.m = my_tile_count(M.ntiles);
   P.resident = allow_resident && P.m <= kStages;
   P.c = 0;
+#if SPCG_TRACE
   P.wait_ns = 0;
   P.trace = false;
+#endif
   if (threadIdx.x == 0 && P.m > 0) {
     const int pre = P.resident ? P.m : kStages;
     for (int j = 0; j < pre; ++j) issue_tile<TWO>(sm, M, my_tile(j % P.m), j);
@@ -202,13 +211,15 @@ __device__ __forceinline__ int pipe_acquire(Pipe& P, Smem& sm, int j) {
     return j;
   }
   const int s = (int)(P.c % kStages);
+#if SPCG_TRACE
   if (P.trace && threadIdx.x == 0) {
     const unsigned long long t0 = globaltimer_ns();
     mbar_wait(&sm.full[s], (uint32_t)((P.c / kStages) & 1));
     P.wait_ns += globaltimer_ns() - t0;
-  } else {
-    mbar_wait(&sm.full[s], (uint32_t)((P.c / kStages) & 1));
+    return s;
   }
+#endif
+  mbar_wait(&sm.full[s], (uint32_t)((P.c / kStages) & 1));
   return s;
 }
 
