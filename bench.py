@@ -304,6 +304,13 @@ def run_ours(args):
     sp_gbs = spmv_bytes(n, nnz) / (sp_ms / 1e3) / 1e9
 
     err_gen = float(np.max(np.abs(x_check - xg)) / max(1.0, np.max(np.abs(xg))))
+    traffic = None
+    tfile = ROOT / "profiles" / "r01" / "p3_traffic.json"
+    if args.workload == "p3" and tfile.exists():
+        # DRAM bytes per iteration measured by ncu on a full-solve launch of the
+        # same kernel, scaled to this launch's iteration count
+        tj = json.loads(tfile.read_text())
+        traffic = int(tj["dram_bytes_per_iteration"] * it_per)
     _, _, _, _, desc = WORKLOADS[args.workload]
     line = {
         "metric": "fp64 CG iterations/sec (and SpMV HBM GB/s, % of roofline)",
@@ -327,7 +334,9 @@ def run_ours(args):
                 "path": "spcg_cg_solve_host (C-ABI, pinned host b -> x), matrix handle resident"},
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "traffic_source": "profiles/r01/p3_traffic.json (ncu dram__bytes, full solve)"
+                     if traffic else None,
                      "peak_source": peak_src,
                      "kernel": "cg_kernel (persistent cooperative CG solve)",
                      "algorithmic_bytes_per_launch": alg, "kernel_ms": kern_ms,
