@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kBlock, SPCG_DIST_MINB)
 
 // y = A x_ext (plain gather; initial / true residual)
 template <int FMT>
-__global__ void __launch_bounds__(kBlock, 1)
+__global__ void __launch_bounds__(kBlock, 2)
     dist_spmv(const MatView M, const double* x_ext, double* y) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);

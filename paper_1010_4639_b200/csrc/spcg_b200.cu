@@ -18,6 +18,7 @@
 #include "../../include/spcg_b200.h"
 #include "cg.cuh"
 #include "cg1.cuh"
+#include "cgs.cuh"
 #include "dist.cuh"
 #include "ops.cuh"
 
@@ -104,6 +105,10 @@ int dev_info(DevInfo** out) {
     if ((rc = occupancy(spmv_kernel<K_SCSR_ATOMIC>, &t))) return rc;
     if ((rc = occupancy(spmv_kernel<K_SCSR_PRIV>, &t))) return rc;
     if ((rc = occupancy(spmv_kernel<K_CSC>, &t))) return rc;
+    if ((rc = occupancy(cgs_kernel<K_CSR>, &t))) return rc;
+    bs = std::min(bs, t);
+    if ((rc = occupancy(cgs_kernel<K_SCSR_PRIV>, &t))) return rc;
+    bs = std::min(bs, t);
     if ((rc = occupancy(dist_pass_a<K_CSR>, &t))) return rc;
     if ((rc = occupancy(dist_pass_a<K_SCSR_PRIV>, &t))) return rc;
     if ((rc = occupancy(dist_spmv<K_CSR>, &t))) return rc;
@@ -144,6 +149,7 @@ struct Workspace {
   CgDevResult* res = nullptr;
   CgDevResult* h_res = nullptr;  // pinned
   double* cg1 = nullptr;         // single-reduction engine: R[2], S[2], W[3]
+  double2* rp = nullptr;         // streaming engine: RP[2] interleaved (r, p) pairs
   // host-API staging
   double* b = nullptr;
   double* x = nullptr;
@@ -402,7 +408,7 @@ void free_matrix(spcg_matrix_s* m) {
   F(m->t1.desc); F(m->t1.descB); F(m->t2.desc); F(m->t2.descB); F(m->t1.win); F(m->t2.win);
   Workspace& w = m->ws;
   F(w.r); F(w.p0); F(w.p1); F(w.q); F(w.part); F(w.slots); F(w.res);
-  F(w.b); F(w.x); F(w.x0); F(w.hist); F(w.cg1);
+  F(w.b); F(w.x); F(w.x0); F(w.hist); F(w.cg1); F(w.rp);
   if (w.h_res) cudaFreeHost(w.h_res);
   if (w.ev0) cudaEventDestroy(w.ev0);
   if (w.ev1) cudaEventDestroy(w.ev1);
@@ -463,11 +469,21 @@ int ensure_ws(spcg_matrix_s* m, int grid) {
 }
 
 template <int FMT>
-int launch_cg(const CgArgs& a, bool res, int grid, cudaStream_t st) {
-  void* args[] = {(void*)&a};
-  const void* fn = res ? (const void*)cg_kernel<FMT, true> : (const void*)cg_kernel<FMT, false>;
-  CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBlock), args,
-                                       res ? kSmemRes : sizeof(Smem), st));
+int launch_cg(const CgArgs& a, bool res, int grid, cudaStream_t st, double2* rp, int n) {
+  if (res || rp == nullptr) {
+    void* args[] = {(void*)&a};
+    const void* fn = res ? (const void*)cg_kernel<FMT, true> : (const void*)cg_kernel<FMT, false>;
+    CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBlock), args,
+                                         res ? kSmemRes : sizeof(Smem), st));
+    return SPCG_OK;
+  }
+  CgsArgs g{};
+  g.base = a;
+  g.RP[0] = rp;
+  g.RP[1] = rp + std::max(1, n);
+  void* args[] = {(void*)&g};
+  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)cgs_kernel<FMT>, dim3(grid), dim3(kBlock), args,
+                                       sizeof(Smem), st));
   return SPCG_OK;
 }
 
@@ -579,11 +595,21 @@ int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double
       default: rc = launch_cg1<K_CSC>(g, grid, st); break;
     }
   } else {
+    // streaming systems: interleaved (r, p) pairs pay off for the gather-only
+    // formats with long rows (27-point class: 20% on full CSR); short rows
+    // (5/7-point) and the atomic scatters keep separate r and p arrays
+    const double per_line = (double)(m->nnz + (kf == K_SCSR_PRIV ? m->B.nnz : 0)) /
+                            std::max(1, m->n);
+    const bool pairs = !res && (kf == K_CSR || kf == K_SCSR_PRIV) && per_line > 8.0;
+    if (pairs && !w.rp &&
+        (rc = dmalloc((void**)&w.rp, sizeof(double2) * 2 * (size_t)std::max(1, m->n), nullptr)))
+      return rc;
+    double2* rp = pairs ? w.rp : nullptr;
     switch (kf) {
-      case K_CSR: rc = launch_cg<K_CSR>(a, res, grid, st); break;
-      case K_SCSR_ATOMIC: rc = launch_cg<K_SCSR_ATOMIC>(a, res, grid, st); break;
-      case K_SCSR_PRIV: rc = launch_cg<K_SCSR_PRIV>(a, res, grid, st); break;
-      default: rc = launch_cg<K_CSC>(a, res, grid, st); break;
+      case K_CSR: rc = launch_cg<K_CSR>(a, res, grid, st, rp, m->n); break;
+      case K_SCSR_ATOMIC: rc = launch_cg<K_SCSR_ATOMIC>(a, res, grid, st, rp, m->n); break;
+      case K_SCSR_PRIV: rc = launch_cg<K_SCSR_PRIV>(a, res, grid, st, rp, m->n); break;
+      default: rc = launch_cg<K_CSC>(a, res, grid, st, rp, m->n); break;
     }
   }
   if (rc) return rc;
