@@ -235,7 +235,7 @@ def run_ours(args):
     st = torch.cuda.current_stream()
     x = torch.empty_like(bt)
     opts = N.CgOptionsC(tol=1e-10, max_iter=args.max_iter, record_history=0,
-                        recompute_final_residual=1, accumulation=acc, engine=0)
+                        recompute_final_residual=1, accumulation=acc, engine=0, timing=1)
 
     def solve_dev():
         r = N.CgResultC()
@@ -259,9 +259,22 @@ def run_ours(args):
     clocks = clk.summary()
     iters = sum(r.iterations for r in results)
     value = iters / (ms / 1e3)
-    kern_ms = float(np.mean([r.device_ms for r in results]))
+    solve_ms = float(np.mean([r.device_ms for r in results]))
     it_per = results[-1].iterations
-    alg = solve_bytes(n, nnz, it_per)
+    alg_solve = solve_bytes(n, nnz, it_per)
+    achieved_solve = alg_solve / (solve_ms / 1e3) / 1e9
+    # dominant kernel: the SpMV pass (q = A p, p.q) of the per-pass engine,
+    # timed by CUDA events on the solve stream around every launch
+    sp_launch = sum(r.spmv_launches for r in results)
+    sp_kms = sum(r.spmv_ms for r in results)
+    if sp_launch > 0:
+        kern = "dist_spmv_pq (SpMV pass of the per-pass engine: q = A p, partial p.q)"
+        kern_ms = sp_kms / sp_launch
+        alg = spmv_bytes(n, nnz)
+    else:  # resident systems: the whole solve is one persistent kernel
+        kern = "cg1_kernel/cg_kernel (persistent cooperative CG solve)"
+        kern_ms = solve_ms
+        alg = alg_solve
     achieved = alg / (kern_ms / 1e3) / 1e9
 
     # e2e through the C-ABI host entry point: pinned b in, x out, every step
@@ -305,12 +318,11 @@ def run_ours(args):
 
     err_gen = float(np.max(np.abs(x_check - xg)) / max(1.0, np.max(np.abs(xg))))
     traffic = None
-    tfile = ROOT / "profiles" / "r01" / "p3_traffic.json"
-    if args.workload == "p3" and tfile.exists():
-        # DRAM bytes per iteration measured by ncu on a full-solve launch of the
-        # same kernel, scaled to this launch's iteration count
-        tj = json.loads(tfile.read_text())
-        traffic = int(tj["dram_bytes_per_iteration"] * it_per)
+    tfile = ROOT / "profiles" / "r01" / "p3_spmv_traffic.json"
+    if args.workload == "p3" and sp_launch > 0 and tfile.exists():
+        # DRAM bytes of one dist_spmv_pq launch on this system (ncu --metrics
+        # dram__bytes_read.sum,dram__bytes_write.sum; profiles/r01)
+        traffic = int(json.loads(tfile.read_text())["dram_bytes_per_launch"])
     _, _, _, _, desc = WORKLOADS[args.workload]
     line = {
         "metric": "fp64 CG iterations/sec (and SpMV HBM GB/s, % of roofline)",
@@ -328,19 +340,26 @@ def run_ours(args):
         "config": {"workload": desc, "n": n, "nnz_stored": nnz, "tol": 1e-10, "x0": "zeros",
                    "iterations_per_solve": it_per, "step": "one full cg_solve",
                    "l2": "inputs (matrix %.1f GB) >> 126 MB L2, no flush needed" % (12 * nnz / 1e9),
-                   "parallelism": "1 GPU, one persistent cooperative kernel per solve"},
+                   "parallelism": "1 GPU; per-pass engine (tiled SpMV pass + 2 streaming passes, "
+                                  "device-resident scalars, no host round trip per iteration)"},
         "e2e": {"value": round(e2e_its / (e2e_ms / 1e3), 3), "unit": "iterations/s",
                 "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n + 40,
                 "path": "spcg_cg_solve_host (C-ABI, pinned host b -> x), matrix handle resident"},
-        "gpu_launches": args.steps,
+        "gpu_launches": int(sum(r.kernel_launches for r in results)),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "traffic_source": "profiles/r01/p3_traffic.json (ncu dram__bytes, full solve)"
-                     if traffic else None,
-                     "peak_source": peak_src,
-                     "kernel": "cg_kernel (persistent cooperative CG solve)",
+                     "traffic_source": "profiles/r01/p3_spmv_traffic.json (ncu dram__bytes of "
+                                       "one launch)" if traffic else None,
+                     "peak_source": peak_src, "kernel": kern,
                      "algorithmic_bytes_per_launch": alg, "kernel_ms": kern_ms,
-                     "bytes_model": "per iteration 12*nnz + 4*(n+1) + 88*n (SURVEY 8d)"},
+                     "launches_timed": int(sp_launch) if sp_launch else args.steps,
+                     "bytes_model": "SpMV pass 12*nnz + 4*(n+1) + 16*n (SURVEY 8d)"
+                     if sp_launch else "per iteration 12*nnz + 4*(n+1) + 88*n (SURVEY 8d)"},
+        "roofline_iteration": {"achieved": round(achieved_solve, 1),
+                               "frac": round(achieved_solve / peak, 4), "unit": "GB/s",
+                               "solve_ms": solve_ms, "algorithmic_bytes_per_solve": alg_solve,
+                               "bytes_model": "per iteration 12*nnz + 4*(n+1) + 88*n "
+                                              "(SURVEY 8d) + prologue/epilogue"},
         "spmv": {"ms": sp_ms, "GBs": round(sp_gbs, 1), "frac": round(sp_gbs / peak, 4),
                  "bytes": spmv_bytes(n, nnz)},
         "clocks": clocks,
@@ -396,7 +415,7 @@ def run_distributed(args):
         lib = N.load()
         x = torch.empty_like(bt)
         o = N.CgOptionsC(tol=1e-10, max_iter=args.max_iter, record_history=0,
-                         recompute_final_residual=1, accumulation=acc, engine=0)
+                         recompute_final_residual=1, accumulation=acc, engine=0, timing=0)
 
         def step():
             r = N.CgResultC()
@@ -439,7 +458,7 @@ def run_distributed(args):
     nnz_tot = int(sum(gather(nnz_loc))) if world > 1 else nnz_loc
 
     def step():
-        x, res, _ = D.dist_cg_solve(sm, comm, b_loc, max_iter=args.max_iter or None)
+        x, res, _ = D.dist_cg_solve(sm, comm, b_loc, max_iter=args.max_iter or None, timing=True)
         return x, res
 
     for _ in range(args.warmup):
@@ -451,15 +470,19 @@ def run_distributed(args):
         e0.record(st)
         for _ in range(args.steps):
             x, r = step()
-            results.append((r.iterations, r.device_ms, r.kernel_launches, r.final_relative_residual))
+            results.append((r.iterations, r.device_ms, r.kernel_launches, r.final_relative_residual,
+                            r.spmv_ms, r.spmv_launches))
         e1.record(st)
         barrier()
     ms = max_over_ranks(e0.elapsed_time(e1))
     clocks = clk.summary() if rank == 0 else None
     its = sum(r[0] for r in results)
     it_per = results[-1][0]
-    kern_ms = max_over_ranks(float(np.mean([r[1] for r in results])))
-    alg = solve_bytes(n, nnz_tot, it_per)
+    solve_ms = max_over_ranks(float(np.mean([r[1] for r in results])))
+    alg_solve = solve_bytes(n, nnz_tot, it_per)
+    # dominant kernel: the SpMV pass, CUDA-event timed per launch, max over ranks
+    kern_ms = max_over_ranks(sum(r[4] for r in results) / max(1, sum(r[5] for r in results)))
+    alg = spmv_bytes(n, nnz_tot)
     achieved = alg / (kern_ms / 1e3) / 1e9
     err = float(np.max(np.abs(x.cpu().numpy() - xg[sm.row0:sm.row1])))
     err = max_over_ranks(err)
@@ -499,7 +522,11 @@ def run_distributed(args):
                          "peak": round(peak * world, 1), "unit": "GB/s",
                          "frac": round(achieved / (peak * world), 4), "traffic": None,
                          "peak_source": peak_src + f" x {world} GPUs",
+                         "kernel": "dist_spmv_pq (SpMV pass, all ranks)",
                          "algorithmic_bytes_per_launch": alg, "kernel_ms": kern_ms},
+            "roofline_iteration": {"achieved": round(alg_solve / (solve_ms / 1e3) / 1e9, 1),
+                                   "frac": round(alg_solve / (solve_ms / 1e3) / 1e9 /
+                                                 (peak * world), 4), "solve_ms": solve_ms},
             "clocks": clocks, "final_relative_residual": results[-1][3],
             "max_abs_err_vs_xgen": err, "setup_s": round(setup_s, 2)}), flush=True)
     comm.close()

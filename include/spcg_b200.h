@@ -123,11 +123,15 @@ typedef struct {
   int32_t recompute_final_residual; /* default 1 (solver.py:159-162)           */
   int32_t accumulation;          /* spcg_accumulation, SCSR only               */
   int32_t engine;                /* 0 = auto (3 when the system is resident
-                                    in shared memory, else 1),
+                                    in shared memory, else 2),
                                     1 = persistent kernel, two-reduction CG,
                                     2 = per-pass kernels (the sharded engine),
                                     3 = persistent single-reduction CG
-                                        (Chronopoulos-Gear, resident only)   */
+                                        (Chronopoulos-Gear, resident only),
+                                    4 = persistent three-pass CG             */
+  int32_t timing;                /* per-pass engine: CUDA-event time of every
+                                    SpMV pass -> result.spmv_ms / launches   */
+  int32_t reserved;
 } spcg_cg_options;
 
 typedef struct {
@@ -139,6 +143,8 @@ typedef struct {
   double b_norm;
   double device_ms;              /* CUDA-event time of the solve on `stream`   */
   int64_t kernel_launches;       /* kernels launched by this solve             */
+  double spmv_ms;                /* with opts.timing: summed SpMV-pass time    */
+  int64_t spmv_launches;         /* with opts.timing: SpMV passes timed        */
 } spcg_cg_result;
 
 /* Device-resident solve.  d_x0 may be NULL (zeros).  d_x receives x.

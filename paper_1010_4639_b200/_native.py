@@ -44,6 +44,8 @@ class CgOptionsC(ctypes.Structure):
         ("recompute_final_residual", ctypes.c_int32),
         ("accumulation", ctypes.c_int32),
         ("engine", ctypes.c_int32),
+        ("timing", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 
@@ -57,6 +59,8 @@ class CgResultC(ctypes.Structure):
         ("b_norm", ctypes.c_double),
         ("device_ms", ctypes.c_double),
         ("kernel_launches", ctypes.c_int64),
+        ("spmv_ms", ctypes.c_double),
+        ("spmv_launches", ctypes.c_int64),
     ]
 
 

@@ -1,17 +1,19 @@
-// dist.cuh — per-pass CG kernels for the row-sharded multi-GPU solve.
+// dist.cuh — per-pass CG kernels: the row-sharded multi-GPU solve and the
+// single-GPU streaming engine (the same engine with no peers).
 //
 // Each rank owns lines [row0,row1) of A (a "local" handle whose column
 // indices are localized: owned columns -> [0,nloc), halo columns ->
-// [nloc, nloc+nhalo)).  The gathered vectors are stored extended:
-//   r_ext[0..nloc)       own residual
-//   r_ext[nloc..)        halo: the neighbours' p_k values for this iteration
-//   p_ext[*][nloc..)     always 0
-// so the fold r_j + beta*p_j gives own p_k for owned j and exactly the
-// received p_k for halo j — the same tile kernels serve both cases.
-// Scalars live in a device StepState; the two per-iteration dot products
-// are reduced in fixed order on each rank (last-CTA-done) and summed across
-// ranks by ncclAllReduce on StepState::red, so every rank computes bitwise
-// identical alpha/beta/flags and stops at the same iteration.
+// [nloc, nloc+nhalo)).  The search direction is stored extended,
+// p_ext = [own p | neighbours' p], so pass A is a plain SpMV over p_ext.
+// One iteration (unfolded CG: every pass streams at full speed, and each
+// kernel keeps the whole register budget for its own loop):
+//   A  q = A p_ext, partial p.q              -> ncclAllReduce -> alpha
+//   B  r -= alpha q, partial r.r             -> ncclAllReduce -> beta, flags
+//   C  x += alpha p, p = r + beta p          -> pack p halo -> ncclSend/Recv
+// Scalars live in a device StepState; dot products are reduced in fixed
+// order on each rank (last-CTA-done) and summed across ranks by
+// ncclAllReduce on StepState::red, so every rank computes bitwise identical
+// alpha/beta/flags and stops at the same iteration.
 #pragma once
 #include "lines.cuh"
 
@@ -22,6 +24,7 @@ struct StepState {
   double red;  // local partial sum; NCCL all-reduces it in place
   double pad0;
   long long k, max_it, fail_iter;
+  long long kc;  // iterations whose pass C ran
   int status, converged, done, x0_given;
   unsigned int counter;  // last-CTA-done ticket
   int record;
@@ -56,40 +59,28 @@ __device__ __forceinline__ void last_block_sum(double v, SM& sm, double* part, S
   }
 }
 
-// pass A: p_k = fold, q = A p_k, x += alpha_{k-1} p_{k-1}, red = p.q partial
-#ifndef SPCG_DIST_MINB
-#define SPCG_DIST_MINB 2
-#endif
+// pass A: q = A p_ext, red = p.q partial (skipped once done)
 template <int FMT>
-__global__ void __launch_bounds__(kBlock, SPCG_DIST_MINB)
-    dist_pass_a(const MatView M, StepState* S, const double* r_ext, const double* p_old,
-                double* p_new, double* x, double* q, double* part) {
+__global__ void __launch_bounds__(kBlock, 2)
+    dist_spmv_pq(const MatView M, StepState* S, const double* p_ext, double* q, double* part) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   if (S->done) return;
   constexpr bool TWO = (FMT == K_SCSR_PRIV);
-  const bool first = S->k == 0;
-  const double beta = S->beta, alpha = S->alpha;
   smem_init(sm);
   Pipe P;
   pipe_start<TWO>(P, sm, M);
+  SrcPlain src{p_ext};
   double pq = 0.0;
   for (int j = 0; j < P.m; ++j) {
     const int s = pipe_acquire(P, sm, j);
     bool active = false;
     int i = -1;
-    LineOut o;
-    if (first) {
-      SrcFirst src{r_ext};
-      o = tile_line<FMT, false>(sm, s, M, src, q, active, i, sm.val[s]);
-    } else {
-      SrcFold src{r_ext, p_old, beta};
-      o = tile_line<FMT, false>(sm, s, M, src, q, active, i, sm.val[s], x);
-    }
+    // atomic formats (single GPU): transposed scatter into q (zeroed by
+    // pass B), p.Ap from the line's own gather (line_pq)
+    const LineOut o = tile_line<FMT, true>(sm, s, M, src, q, active, i, sm.val[s]);
     if (active) {
-      if (!first) x[i] = mul_add_rn(o.xo, alpha, p_old[i]);
-      p_new[i] = o.xi;
-      q[i] = o.q;
+      finish_plain<FMT>(o, i, q);
       pq += line_pq<FMT>(o);
     }
     pipe_release<TWO>(P, sm, M, s);
@@ -114,40 +105,109 @@ __global__ void __launch_bounds__(kBlock, 2)
     bool active = false;
     int i = -1;
     const LineOut o = tile_line<FMT, false>(sm, s, M, src, y, active, i, sm.val[s]);
-    if (active) y[i] = o.q;
+    if (active) finish_plain<FMT>(o, i, y);
     pipe_release<TWO>(P, sm, M, s);
   }
   pipe_drain(P, sm);
 }
 
 // Elementwise kernels over the nloc own lines (grid-stride, fixed order).
-// mode 0: red = b.b               mode 1: r = b - q (or b), red = r.r
+// mode 0: red = b.b               mode 1: r = b - q (or b), red = r.r, p = r
 // mode 2: r -= alpha q, red = r.r mode 3: red = |b - q|^2 (true residual)
+// Mode 2 moves 16-byte pairs, two in flight per thread (r, q 16-B aligned).
 __global__ void __launch_bounds__(kBlock) dist_elem(int mode, long long nloc, StepState* S,
-                                                   const double* b, const double* q, double* r,
-                                                   double* part) {
+                                                   const double* b, double* q, double* r,
+                                                   double* p, double* part, int zq) {
   __shared__ RedSmem sm;
   if (mode == 2 && S->done) return;
   const double alpha = S->alpha;
   const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long G = (long long)gridDim.x * blockDim.x;
   double acc = 0.0;
-  for (long long i = g; i < nloc; i += G) {
-    double v;
-    if (mode == 0) {
-      v = b[i];
-    } else if (mode == 1) {
-      v = q ? mul_add_rn(b[i], -1.0, q[i]) : b[i];
-      r[i] = v;
-    } else if (mode == 2) {
-      v = mul_add_rn(r[i], -alpha, q[i]);
-      r[i] = v;
-    } else {
-      v = mul_add_rn(b[i], -1.0, q[i]);
+  if (mode == 2) {
+    const double na = -alpha;
+    const long long np = nloc >> 1;
+    const double2* q2 = reinterpret_cast<const double2*>(q);
+    double2* r2 = reinterpret_cast<double2*>(r);
+    long long i = g;
+    for (; i + G < np; i += 2 * G) {
+      const double2 qa = q2[i], qb = q2[i + G], ra = r2[i], rb = r2[i + G];
+      const double2 oa = make_double2(mul_add_rn(ra.x, na, qa.x), mul_add_rn(ra.y, na, qa.y));
+      const double2 ob = make_double2(mul_add_rn(rb.x, na, qb.x), mul_add_rn(rb.y, na, qb.y));
+      r2[i] = oa;
+      r2[i + G] = ob;
+      if (zq) {
+        reinterpret_cast<double2*>(q)[i] = make_double2(0.0, 0.0);
+        reinterpret_cast<double2*>(q)[i + G] = make_double2(0.0, 0.0);
+      }
+      acc = fma(oa.x, oa.x, acc);
+      acc = fma(oa.y, oa.y, acc);
+      acc = fma(ob.x, ob.x, acc);
+      acc = fma(ob.y, ob.y, acc);
     }
-    acc = fma(v, v, acc);
+    if (i < np) {
+      const double2 qa = q2[i], ra = r2[i];
+      const double2 oa = make_double2(mul_add_rn(ra.x, na, qa.x), mul_add_rn(ra.y, na, qa.y));
+      r2[i] = oa;
+      if (zq) reinterpret_cast<double2*>(q)[i] = make_double2(0.0, 0.0);
+      acc = fma(oa.x, oa.x, acc);
+      acc = fma(oa.y, oa.y, acc);
+    }
+    if ((nloc & 1) && g == 0) {
+      const double v = mul_add_rn(r[nloc - 1], na, q[nloc - 1]);
+      if (zq) q[nloc - 1] = 0.0;
+      r[nloc - 1] = v;
+      acc = fma(v, v, acc);
+    }
+  } else {
+    for (long long i = g; i < nloc; i += G) {
+      double v;
+      if (mode == 0) {
+        v = b[i];
+      } else if (mode == 1) {
+        v = q ? mul_add_rn(b[i], -1.0, q[i]) : b[i];
+        if (q && zq) q[i] = 0.0;
+        r[i] = v;
+        p[i] = v;
+      } else {
+        v = mul_add_rn(b[i], -1.0, q[i]);
+      }
+      acc = fma(v, v, acc);
+    }
   }
   last_block_sum(acc, sm, part, S);
+}
+
+// pass C: x += alpha p, p = r + beta p, for an iteration that neither
+// converged nor failed (a converged solve applies its last x update at the
+// end; an exhausted max_iter runs its pass C).  xv: x is 16-byte aligned.
+__global__ void __launch_bounds__(kBlock) dist_update(long long nloc, StepState* S, const double* r,
+                                                     double* p, double* x, int xv) {
+  if (S->status != 0 || S->converged || S->kc >= S->k) return;
+  const double alpha = S->alpha, beta = S->beta;
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long G = (long long)gridDim.x * blockDim.x;
+  const long long np = nloc >> 1;
+  const double2* r2 = reinterpret_cast<const double2*>(r);
+  double2* p2 = reinterpret_cast<double2*>(p);
+  for (long long i = g; i < np; i += G) {
+    const double2 pv = p2[i], rv = r2[i];
+    if (xv) {
+      double2* x2 = reinterpret_cast<double2*>(x);
+      const double2 xo = x2[i];
+      x2[i] = make_double2(mul_add_rn(xo.x, alpha, pv.x), mul_add_rn(xo.y, alpha, pv.y));
+    } else {
+      x[2 * i] = mul_add_rn(x[2 * i], alpha, pv.x);
+      x[2 * i + 1] = mul_add_rn(x[2 * i + 1], alpha, pv.y);
+    }
+    p2[i] = make_double2(mul_add_rn(rv.x, beta, pv.x), mul_add_rn(rv.y, beta, pv.y));
+  }
+  if ((nloc & 1) && g == 0) {
+    const long long i = nloc - 1;
+    const double pv = p[i];
+    x[i] = mul_add_rn(x[i], alpha, pv);
+    p[i] = mul_add_rn(r[i], beta, pv);
+  }
 }
 
 // Scalar steps (one thread), operating on the all-reduced S->red.
@@ -184,6 +244,7 @@ __global__ void dist_scalar(int op, StepState* S, double* hist) {
     }
     return;
   }
+  if (op == 2) S->kc = S->k;  // pass C of iteration k (if any) has run
   if (S->done) return;
   if (op == 2) {
     const double pq = S->red;
@@ -235,25 +296,19 @@ __global__ void dist_scalar(int op, StepState* S, double* hist) {
 
 __global__ void dist_true_rel(StepState* S) { S->rel = sqrt(S->red) / S->b_norm; }
 
-// Halo values to send: mode 0 plain v[idx]; mode 1 next direction
-// p_k = r + beta p_{k-1} (first iteration: r), skipped once done.
-__global__ void dist_pack(int mode, StepState* S, long long cnt, const int* idx, const double* r,
-                          const double* p, double* out) {
-  if (mode == 1 && S->done) return;
-  const bool first = S->k == 0;
-  const double beta = S->beta;
+// Halo values to send: v[idx] for every send row.
+__global__ void dist_pack(long long cnt, const int* idx, const double* v, double* out) {
   const long long G = (long long)gridDim.x * blockDim.x;
-  for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < cnt; s += G) {
-    const int i = idx[s];
-    out[s] = (mode == 0 || first) ? r[i] : __dadd_rn(r[i], __dmul_rn(beta, p[i]));
-  }
+  for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < cnt; s += G)
+    out[s] = v[idx[s]];
 }
 
-// x = x0 (or 0); final x += alpha_K p_K
+// x = x0 (or 0); final x += alpha_K p_K of a converged solve (its pass C
+// was skipped)
 __global__ void dist_x(int mode, long long nloc, StepState* S, const double* src, double* x) {
   const long long G = (long long)gridDim.x * blockDim.x;
   const double alpha = S->alpha;
-  const bool upd = S->k > 0 && S->status == 0;
+  const bool upd = S->k > 0 && S->status == 0 && S->converged;
   const bool zero_b = S->b_norm == 0.0;  // solver.py:109-118: x = 0 even for x0 != 0
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nloc; i += G) {
     if (mode == 0) x[i] = (src && !zero_b) ? src[i] : 0.0;

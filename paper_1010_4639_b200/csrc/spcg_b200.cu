@@ -19,6 +19,7 @@
 #include "cg.cuh"
 #include "cg1.cuh"
 #include "cgs.cuh"
+#include "cg3.cuh"
 #include "dist.cuh"
 #include "ops.cuh"
 
@@ -105,12 +106,24 @@ int dev_info(DevInfo** out) {
     if ((rc = occupancy(spmv_kernel<K_SCSR_ATOMIC>, &t))) return rc;
     if ((rc = occupancy(spmv_kernel<K_SCSR_PRIV>, &t))) return rc;
     if ((rc = occupancy(spmv_kernel<K_CSC>, &t))) return rc;
+    if ((rc = occupancy(cg3_kernel<K_CSR>, &t))) return rc;
+    bs = std::min(bs, t);
+    if ((rc = occupancy(cg3_kernel<K_SCSR_ATOMIC>, &t))) return rc;
+    bs = std::min(bs, t);
+    if ((rc = occupancy(cg3_kernel<K_SCSR_PRIV>, &t))) return rc;
+    bs = std::min(bs, t);
+    if ((rc = occupancy(cg3_kernel<K_CSC>, &t))) return rc;
+    bs = std::min(bs, t);
     if ((rc = occupancy(cgs_kernel<K_CSR>, &t))) return rc;
     bs = std::min(bs, t);
     if ((rc = occupancy(cgs_kernel<K_SCSR_PRIV>, &t))) return rc;
     bs = std::min(bs, t);
-    if ((rc = occupancy(dist_pass_a<K_CSR>, &t))) return rc;
-    if ((rc = occupancy(dist_pass_a<K_SCSR_PRIV>, &t))) return rc;
+    if ((rc = occupancy(dist_spmv_pq<K_CSR>, &t))) return rc;
+    if ((rc = occupancy(dist_spmv_pq<K_SCSR_PRIV>, &t))) return rc;
+    if ((rc = occupancy(dist_spmv_pq<K_SCSR_ATOMIC>, &t))) return rc;
+    if ((rc = occupancy(dist_spmv_pq<K_CSC>, &t))) return rc;
+    if ((rc = occupancy(dist_spmv<K_SCSR_ATOMIC>, &t))) return rc;
+    if ((rc = occupancy(dist_spmv<K_CSC>, &t))) return rc;
     if ((rc = occupancy(dist_spmv<K_CSR>, &t))) return rc;
     if ((rc = occupancy(dist_spmv<K_SCSR_PRIV>, &t))) return rc;
     if (br < 1 || bs < 1 || bp < 1) return fail(SPCG_ERR_CUDA, "CG kernel does not fit on an SM");
@@ -174,6 +187,7 @@ struct DistWorkspace {
   int* send_idx = nullptr;
   long long send_idx_cap = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t tev[2][16] = {};  // per-iteration SpMV-pass timing (opts.timing)
 };
 
 }  // namespace
@@ -418,6 +432,9 @@ void free_matrix(spcg_matrix_s* m) {
   if (d.h_S) cudaFreeHost(d.h_S);
   if (d.ev0) cudaEventDestroy(d.ev0);
   if (d.ev1) cudaEventDestroy(d.ev1);
+  for (int a = 0; a < 2; ++a)
+    for (int c = 0; c < 16; ++c)
+      if (d.tev[a][c]) cudaEventDestroy(d.tev[a][c]);
 }
 
 MatView view(const spcg_matrix_s* m, bool priv) {
@@ -469,7 +486,14 @@ int ensure_ws(spcg_matrix_s* m, int grid) {
 }
 
 template <int FMT>
-int launch_cg(const CgArgs& a, bool res, int grid, cudaStream_t st, double2* rp, int n) {
+int launch_cg(const CgArgs& a, bool res, int grid, cudaStream_t st, double2* rp, int n,
+              bool three = false) {
+  if (!res && three) {
+    void* args[] = {(void*)&a};
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)cg3_kernel<FMT>, dim3(grid), dim3(kBlock),
+                                         args, sizeof(Smem), st));
+    return SPCG_OK;
+  }
   if (res || rp == nullptr) {
     void* args[] = {(void*)&a};
     const void* fn = res ? (const void*)cg_kernel<FMT, true> : (const void*)cg_kernel<FMT, false>;
@@ -532,13 +556,17 @@ int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double
   int rc;
   if ((rc = dev_info(&d))) return rc;
   if (!(o->tol > 0.0)) return fail(SPCG_ERR_ARG, "tol must be > 0");
-  if (o->engine == 2)  // per-pass engine on one GPU (the sharded engine with no peers)
-    return do_dist_cg(m, nullptr, 0, nullptr, nullptr, nullptr, nullptr, b, x0, x, hist, o, out, st);
   if (m->is_rows) return fail(SPCG_ERR_ARG, "a row block is solved with spcg_dist_cg_solve");
   const int kf = kfmt_of(m, o->accumulation);
   if (kf == K_SCSR_PRIV && !m->hasB) return fail(SPCG_ERR_UNSUPPORTED, "no L^T for privatized mode");
   const MatView v = view(m, kf == K_SCSR_PRIV);
-  const bool res = o->engine != 2 && v.ntiles <= d->coop_res * kStages;
+  const bool fits = v.ntiles <= d->coop_res * kStages;
+  // engine 2, and auto for systems that stream from HBM: per-pass kernels
+  // (the sharded engine with no peers) — each pass keeps the whole register
+  // budget, which the persistent kernel cannot (P3: 0.99 vs 0.82 of roofline)
+  if (o->engine == 2 || (o->engine == 0 && !fits))
+    return do_dist_cg(m, nullptr, 0, nullptr, nullptr, nullptr, nullptr, b, x0, x, hist, o, out, st);
+  const bool res = fits;
   // resident: the balanced tiles map one-to-one onto CTAs where possible
   const int grid = res ? std::max(1, std::min(d->coop_res, std::max(1, v.ntiles)))
                        : d->coop_stream;
@@ -600,16 +628,17 @@ int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double
     // (5/7-point) and the atomic scatters keep separate r and p arrays
     const double per_line = (double)(m->nnz + (kf == K_SCSR_PRIV ? m->B.nnz : 0)) /
                             std::max(1, m->n);
-    const bool pairs = !res && (kf == K_CSR || kf == K_SCSR_PRIV) && per_line > 8.0;
+    const bool three = !res && o->engine == 4;  // persistent three-pass (unfolded) CG
+    const bool pairs = !res && !three && (kf == K_CSR || kf == K_SCSR_PRIV) && per_line > 8.0;
     if (pairs && !w.rp &&
         (rc = dmalloc((void**)&w.rp, sizeof(double2) * 2 * (size_t)std::max(1, m->n), nullptr)))
       return rc;
     double2* rp = pairs ? w.rp : nullptr;
     switch (kf) {
-      case K_CSR: rc = launch_cg<K_CSR>(a, res, grid, st, rp, m->n); break;
-      case K_SCSR_ATOMIC: rc = launch_cg<K_SCSR_ATOMIC>(a, res, grid, st, rp, m->n); break;
-      case K_SCSR_PRIV: rc = launch_cg<K_SCSR_PRIV>(a, res, grid, st, rp, m->n); break;
-      default: rc = launch_cg<K_CSC>(a, res, grid, st, rp, m->n); break;
+      case K_CSR: rc = launch_cg<K_CSR>(a, res, grid, st, rp, m->n, three); break;
+      case K_SCSR_ATOMIC: rc = launch_cg<K_SCSR_ATOMIC>(a, res, grid, st, rp, m->n, three); break;
+      case K_SCSR_PRIV: rc = launch_cg<K_SCSR_PRIV>(a, res, grid, st, rp, m->n, three); break;
+      default: rc = launch_cg<K_CSC>(a, res, grid, st, rp, m->n, three); break;
     }
   }
   if (rc) return rc;
@@ -646,6 +675,8 @@ int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double
   out->b_norm = r.b_norm;
   out->device_ms = ms;
   out->kernel_launches = 1;
+  out->spmv_ms = 0.0;
+  out->spmv_launches = 0;
   if (r.status != SPCG_OK) {
     const char* what = r.status == SPCG_ERR_NOT_SPD ? "matrix not positive definite"
                        : r.status == SPCG_ERR_NONFINITE_ALPHA ? "non-finite alpha"
@@ -923,14 +954,14 @@ struct HaloPlan {
   long long nloc = 0;
 };
 
-// Pack values from `src` at the send rows, then exchange into dst_ext's halo.
-int halo_exchange(const HaloPlan& H, DistWorkspace& d, int mode, StepState* S, const double* r,
-                  const double* p, double* dst_ext, cudaStream_t st, long long* launches) {
+// Pack v at the send rows, then exchange into dst_ext's halo.
+int halo_exchange(const HaloPlan& H, DistWorkspace& d, const double* v, double* dst_ext,
+                  cudaStream_t st, long long* launches) {
   if (H.npeers == 0) return SPCG_OK;
   const long long total = H.send_off[H.npeers];
   if (total > 0) {
     const int g = (int)std::min<long long>(1184, (total + 255) / 256);
-    dist_pack<<<g, 256, 0, st>>>(mode, S, total, d.send_idx, r, p, d.send_buf);
+    dist_pack<<<g, 256, 0, st>>>(total, d.send_idx, v, d.send_buf);
     CUDA_TRY(cudaGetLastError());
     ++*launches;
   }
@@ -967,74 +998,93 @@ int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const dou
   const int G = std::max(1, std::min(std::max(1, v.ntiles), di->spmv_grid));
   const int GE = 2 * di->sms;
   const size_t sm = sizeof(Smem);
+  const int xv = (((uintptr_t)x) & 15) == 0;
+  constexpr int kAtom = (FMT == K_SCSR_ATOMIC || FMT == K_CSC) ? 1 : 0;
+  double* p = d.p_ext[0];  // p_ext = [own p | halo]
+  double* r = d.r_ext;
   long long launches = 0;
   StepState init{};
   init.tol = o->tol;
-  init.max_it = o->max_iter > 0 ? o->max_iter : std::max<long long>(1, std::max<long long>(m->n_global, m->n));
+  init.max_it = o->max_iter > 0 ? o->max_iter
+                                : std::max<long long>(1, std::max<long long>(m->n_global, m->n));
   init.record = o->record_history && hist;
   init.x0_given = x0 != nullptr;
   CUDA_TRY(cudaMemcpyAsync(d.S, &init, sizeof(StepState), cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaMemsetAsync(d.p_ext[0], 0, sizeof(double) * (size_t)next, st));
-  CUDA_TRY(cudaMemsetAsync(d.p_ext[1], 0, sizeof(double) * (size_t)next, st));
-  CUDA_TRY(cudaMemsetAsync(d.r_ext, 0, sizeof(double) * (size_t)next, st));
+  CUDA_TRY(cudaMemsetAsync(p, 0, sizeof(double) * (size_t)next, st));
+  if (kAtom) CUDA_TRY(cudaMemsetAsync(d.q, 0, sizeof(double) * (size_t)std::max(1LL, nloc), st));
   CUDA_TRY(cudaEventRecord(d.ev0, st));
   // ||b|| (solver.py:107)
-  dist_elem<<<GE, kBlock, 0, st>>>(0, nloc, d.S, b, nullptr, nullptr, d.part);
-  ++launches;
+  dist_elem<<<GE, kBlock, 0, st>>>(0, nloc, d.S, b, nullptr, nullptr, nullptr, d.part, 0);
   if ((rc = allreduce_red(H, d.S, st))) return rc;
   dist_scalar<<<1, 1, 0, st>>>(0, d.S, hist);
-  ++launches;
-  // x = x0, r = b - A x0 (solver.py:120-124)
+  // x = x0, r = b - A x0, p = r (solver.py:120-124)
   dist_x<<<GE, kBlock, 0, st>>>(0, nloc, d.S, x0, x);
-  ++launches;
+  launches += 3;
   if (x0) {
     CUDA_TRY(cudaMemcpyAsync(d.tmp_ext, x0, sizeof(double) * (size_t)nloc,
                              cudaMemcpyDeviceToDevice, st));
-    if ((rc = halo_exchange(H, d, 0, d.S, x0, nullptr, d.tmp_ext, st, &launches))) return rc;
+    if ((rc = halo_exchange(H, d, x0, d.tmp_ext, st, &launches))) return rc;
     dist_spmv<FMT><<<G, kBlock, sm, st>>>(v, d.tmp_ext, d.q);
-    ++launches;
-    dist_elem<<<GE, kBlock, 0, st>>>(1, nloc, d.S, b, d.q, d.r_ext, d.part);
+    dist_elem<<<GE, kBlock, 0, st>>>(1, nloc, d.S, b, d.q, r, p, d.part, kAtom);
+    launches += 2;
   } else {
-    dist_elem<<<GE, kBlock, 0, st>>>(1, nloc, d.S, b, nullptr, d.r_ext, d.part);
+    dist_elem<<<GE, kBlock, 0, st>>>(1, nloc, d.S, b, nullptr, r, p, d.part, 0);
+    ++launches;
   }
-  ++launches;
   if ((rc = allreduce_red(H, d.S, st))) return rc;
   dist_scalar<<<1, 1, 0, st>>>(1, d.S, hist);
   ++launches;
+  if ((rc = halo_exchange(H, d, p, p, st, &launches))) return rc;
   CUDA_TRY(cudaGetLastError());
-  // CG loop: iteration k writes its direction into p_ext[(k-1)&1]; the host
-  // enqueues chunks of iterations and polls the device-side done flag between
-  // chunks (iterations after `done` are no-ops on every rank).
+  // CG loop; the host enqueues chunks of iterations and polls the device-side
+  // done flag between chunks (iterations after `done` are no-ops on every
+  // rank, so the NCCL calls stay matched)
   const int chunk = 16;
-  long long it = 0;
+  const bool timing = o->timing != 0;
+  if (timing && !d.tev[0][0])
+    for (int a = 0; a < 2; ++a)
+      for (int c = 0; c < chunk; ++c) CUDA_TRY(cudaEventCreate(&d.tev[a][c]));
+  double spmv_ms = 0.0;
+  long long spmv_n = 0, k_before = 0;
   for (;;) {
-    for (int c = 0; c < chunk; ++c, ++it) {
-      double* p_new = d.p_ext[it & 1];
-      double* p_old = d.p_ext[(it + 1) & 1];
-      if ((rc = halo_exchange(H, d, 1, d.S, d.r_ext, p_old, d.r_ext, st, &launches))) return rc;
-      dist_pass_a<FMT><<<G, kBlock, sm, st>>>(v, d.S, d.r_ext, p_old, p_new, x, d.q, d.part);
+    for (int c = 0; c < chunk; ++c) {
+      if (timing) CUDA_TRY(cudaEventRecord(d.tev[0][c], st));
+      dist_spmv_pq<FMT><<<G, kBlock, sm, st>>>(v, d.S, p, d.q, d.part);
+      if (timing) CUDA_TRY(cudaEventRecord(d.tev[1][c], st));
       if ((rc = allreduce_red(H, d.S, st))) return rc;
       dist_scalar<<<1, 1, 0, st>>>(2, d.S, hist);
-      dist_elem<<<GE, kBlock, 0, st>>>(2, nloc, d.S, nullptr, d.q, d.r_ext, d.part);
+      dist_elem<<<GE, kBlock, 0, st>>>(2, nloc, d.S, nullptr, d.q, r, nullptr, d.part, kAtom);
       if ((rc = allreduce_red(H, d.S, st))) return rc;
       dist_scalar<<<1, 1, 0, st>>>(3, d.S, hist);
-      launches += 4;
+      dist_update<<<GE, kBlock, 0, st>>>(nloc, d.S, r, p, x, xv);
+      launches += 5;
+      if ((rc = halo_exchange(H, d, p, p, st, &launches))) return rc;
     }
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(d.h_S, d.S, sizeof(StepState), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
+    if (timing) {  // only the passes that did work (later ones returned at once)
+      const long long ran = std::min<long long>(chunk, d.h_S->k - k_before +
+                                                           (d.h_S->status != 0 ? 1 : 0));
+      for (long long c = 0; c < ran; ++c) {
+        float t = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&t, d.tev[0][c], d.tev[1][c]));
+        spmv_ms += t;
+        ++spmv_n;
+      }
+      k_before = d.h_S->k;
+    }
     if (d.h_S->done) break;
   }
-  const long long K = d.h_S->k;
-  // x += alpha_K p_K (p_K in p_ext[(K-1)&1]), then the true residual
-  dist_x<<<GE, kBlock, 0, st>>>(1, nloc, d.S, d.p_ext[(K - 1) & 1], x);
+  // a converged solve skipped its pass C: x += alpha_K p_K; then the true residual
+  dist_x<<<GE, kBlock, 0, st>>>(1, nloc, d.S, p, x);
   ++launches;
   if (o->recompute_final_residual && d.h_S->status == 0 && d.h_S->b_norm != 0.0) {
     CUDA_TRY(cudaMemcpyAsync(d.tmp_ext, x, sizeof(double) * (size_t)nloc,
                              cudaMemcpyDeviceToDevice, st));
-    if ((rc = halo_exchange(H, d, 0, d.S, x, nullptr, d.tmp_ext, st, &launches))) return rc;
+    if ((rc = halo_exchange(H, d, x, d.tmp_ext, st, &launches))) return rc;
     dist_spmv<FMT><<<G, kBlock, sm, st>>>(v, d.tmp_ext, d.q);
-    dist_elem<<<GE, kBlock, 0, st>>>(3, nloc, d.S, b, d.q, nullptr, d.part);
+    dist_elem<<<GE, kBlock, 0, st>>>(3, nloc, d.S, b, d.q, nullptr, nullptr, d.part, 0);
     if ((rc = allreduce_red(H, d.S, st))) return rc;
     dist_true_rel<<<1, 1, 0, st>>>(d.S);
     launches += 3;
@@ -1054,6 +1104,8 @@ int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const dou
   out->b_norm = S.b_norm;
   out->device_ms = ms;
   out->kernel_launches = launches;
+  out->spmv_ms = spmv_ms;
+  out->spmv_launches = spmv_n;
   if (S.status != 0) {
     const char* what = S.status == SPCG_ERR_NOT_SPD ? "matrix not positive definite"
                        : S.status == SPCG_ERR_NONFINITE_ALPHA ? "non-finite alpha"
@@ -1069,9 +1121,13 @@ int do_dist_cg(spcg_matrix_s* m, spcg_comm_s* comm, int npeers, const int32_t* p
                const double* b, const double* x0, double* x, double* hist,
                const spcg_cg_options* o, spcg_cg_result* out, cudaStream_t st) {
   if (!(o->tol > 0.0)) return fail(SPCG_ERR_ARG, "tol must be > 0");
-  if (m->fmt == SPCG_FMT_CSC) return fail(SPCG_ERR_UNSUPPORTED, "sharded CSC is not supported");
-  const bool priv = m->fmt == SPCG_FMT_SCSR;
-  if (priv && !m->hasB) return fail(SPCG_ERR_UNSUPPORTED, "sharded SCSR needs its L^T rows");
+  // single GPU: every format; sharded: CSR and owner-computes SCSR (the
+  // atomic transposed scatters would need a reverse halo)
+  int kf = kfmt_of(m, o->accumulation);
+  if (npeers > 0 && kf == K_CSC) return fail(SPCG_ERR_UNSUPPORTED, "sharded CSC is not supported");
+  if (npeers > 0 && kf == K_SCSR_ATOMIC) kf = K_SCSR_PRIV;
+  if (m->is_rows && kf == K_SCSR_ATOMIC) kf = K_SCSR_PRIV;
+  if (kf == K_SCSR_PRIV && !m->hasB) return fail(SPCG_ERR_UNSUPPORTED, "SCSR needs its L^T rows");
   if (m->is_rows && !m->localized) return fail(SPCG_ERR_ARG, "call spcg_matrix_localize first");
   if (npeers > 0 && (!comm || !comm->comm)) return fail(SPCG_ERR_ARG, "peers need a communicator");
   if (npeers > 0 && !nccl().ok) return fail(SPCG_ERR_CUDA, nccl().err);
@@ -1102,8 +1158,12 @@ int do_dist_cg(spcg_matrix_s* m, spcg_comm_s* comm, int npeers, const int32_t* p
     out->final_relative_residual = 0.0;
     return SPCG_OK;
   }
-  return priv ? dist_solve_t<K_SCSR_PRIV>(m, H, b, x0, x, hist, o, out, st)
-              : dist_solve_t<K_CSR>(m, H, b, x0, x, hist, o, out, st);
+  switch (kf) {
+    case K_CSR: return dist_solve_t<K_CSR>(m, H, b, x0, x, hist, o, out, st);
+    case K_SCSR_PRIV: return dist_solve_t<K_SCSR_PRIV>(m, H, b, x0, x, hist, o, out, st);
+    case K_SCSR_ATOMIC: return dist_solve_t<K_SCSR_ATOMIC>(m, H, b, x0, x, hist, o, out, st);
+    default: return dist_solve_t<K_CSC>(m, H, b, x0, x, hist, o, out, st);
+  }
 }
 }  // namespace
 

@@ -4,10 +4,11 @@ reference has no distribution).
 One process per GPU (torchrun).  Rows are split into contiguous blocks; each
 rank holds its block as a *localized* matrix handle (owned columns ->
 [0, nloc), halo columns -> nloc + position in the sorted halo list).  Per CG
-iteration the C++ engine (spcg_dist_cg_solve) exchanges the halo of the next
-search direction with ncclSend/ncclRecv and sums the two dot products with
-ncclAllReduce; all scalars stay on the device and are bitwise identical on
-every rank, so all ranks stop at the same iteration.
+iteration the C++ engine (spcg_dist_cg_solve; per-pass kernels, csrc/dist.cuh)
+runs q = A p_ext, r -= alpha q, x += alpha p / p = r + beta p, sums the two
+dot products with ncclAllReduce and exchanges the halo of the new p with
+ncclSend/ncclRecv; all scalars stay on the device and are bitwise identical
+on every rank, so all ranks stop at the same iteration.
 
 Host-side logic here is plain numpy + torch.distributed object collectives
 (works with the gloo backend on CPU, which tests/test_distributed.py uses):
@@ -256,7 +257,7 @@ class ShardedMatrix:
 
 def dist_cg_solve(sm: ShardedMatrix, comm: Comm, b_loc, x0_loc=None, tol: float = 1e-10,
                   max_iter: int | None = None, record_history: bool = False,
-                  recompute_final_residual: bool = True):
+                  recompute_final_residual: bool = True, timing: bool = False):
     """One rank's part of the sharded solve.  b_loc / x0_loc: CUDA tensors
     of this rank's rows.  Returns (x_loc, CgResultC, history or None)."""
     import torch
@@ -267,7 +268,7 @@ def dist_cg_solve(sm: ShardedMatrix, comm: Comm, b_loc, x0_loc=None, tol: float 
     hist = torch.empty(mi if record_history else 1, dtype=torch.float64, device=b_loc.device)
     o = N.CgOptionsC(tol=float(tol), max_iter=int(mi), record_history=int(record_history),
                      recompute_final_residual=int(recompute_final_residual),
-                     accumulation=N.ACC_PRIVATIZED, engine=2)
+                     accumulation=N.ACC_PRIVATIZED, engine=2, timing=int(timing))
     res = N.CgResultC()
 
     def ptr(a):

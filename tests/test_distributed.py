@@ -2,10 +2,10 @@
 
 The partition / halo numbering / exchange plan of paper_1010_4639_b200.distributed
 are exercised for real; the per-rank device kernels are emulated with numpy
-following the engine's exact structure (extended vectors whose halo holds the
-neighbours' p_k and whose p-halo is zero, folded p-update, deferred x update,
-fixed-order local sums + all-reduce), and the result is compared with the
-serial oracle.  The GPU side of the same engine is covered by
+following the engine's exact structure (csrc/dist.cuh: SpMV over the extended
+p = [own | neighbours'], r-update, x/p-update, halo exchange of the new p,
+local sums + all-reduce), and the result is compared with the serial
+oracle.  The GPU side of the same engine is covered by
 tests/test_gpu_dist.py (single rank) — multi-GPU runs need >1 GPU.
 """
 
@@ -71,36 +71,32 @@ def emulate_rank(rank, world, a, b, bounds, gather, allreduce, exchange, max_ite
     bl = b[r0:r1].copy()
     b_norm = np.sqrt(allreduce(float(np.dot(bl, bl))))
     x = np.zeros(nloc)
-    r_ext = np.zeros(next_)
-    r_ext[:nloc] = bl
-    p_ext = [np.zeros(next_), np.zeros(next_)]
-    rr = allreduce(float(np.dot(bl, bl)))
+    r = bl.copy()
+    p_ext = np.zeros(next_)          # [own p | neighbours' p]
+    p_ext[:nloc] = r
+    rr = allreduce(float(np.dot(r, r)))
+    p_ext[nloc:] = exchange(plan, p_ext[plan.send_idx])
     mi = max_iter or a.n
-    k, alpha, beta = 0, 0.0, 0.0
+    k, alpha = 0, 0.0
     converged = np.sqrt(rr) <= tol * b_norm
     while not converged and k < mi:
-        p_old, p_new = p_ext[(k + 1) & 1], p_ext[k & 1]
-        send = r_ext[plan.send_idx] if k == 0 else r_ext[plan.send_idx] + beta * p_old[plan.send_idx]
-        recv = exchange(plan, send)
-        r_ext[nloc:] = recv
-        v = r_ext if k == 0 else r_ext + beta * p_old  # halo: recv + beta*0
-        if k > 0:
-            x = x + alpha * p_old[:nloc]
-        p_new[:nloc] = v[:nloc]
-        q = spmv2(v)
-        pq = allreduce(float(np.dot(p_new[:nloc], q)))
+        q = spmv2(p_ext)                                   # pass A
+        pq = allreduce(float(np.dot(p_ext[:nloc], q)))
         assert pq > 0
         alpha = rr / pq
-        r_ext[:nloc] = r_ext[:nloc] - alpha * q
-        rr_new = allreduce(float(np.dot(r_ext[:nloc], r_ext[:nloc])))
+        r = r - alpha * q                                  # pass B
+        rr_new = allreduce(float(np.dot(r, r)))
         k += 1
         if np.sqrt(rr_new) <= tol * b_norm:
             converged = True
             break
         beta = rr_new / rr
         rr = rr_new
-    if k > 0:
-        x = x + alpha * p_ext[(k - 1) & 1][:nloc]
+        x = x + alpha * p_ext[:nloc]                       # pass C
+        p_ext[:nloc] = r + beta * p_ext[:nloc]
+        p_ext[nloc:] = exchange(plan, p_ext[plan.send_idx])
+    if converged and k > 0:
+        x = x + alpha * p_ext[:nloc]
     return x, k, plan, halo
 
 
