@@ -211,8 +211,7 @@ __global__ void __launch_bounds__(kBlock, RES ? 1 : kStreamMinBlocks) cg_kernel(
       if (u < P.m) {
         mbar_wait(&sm.full[u], 0);
         const StageMeta& mt = sm.meta[u];
-        const int i = mt.is_long ? (threadIdx.x == 0 ? mt.row0 : -1) : mt.row0 + (int)threadIdx.x;
-        li[u] = (i >= 0 && i < mt.row1) ? i : -1;
+        li[u] = owned_line<FMT>(mt);
       }
     }
   }

@@ -149,8 +149,7 @@ __global__ void __launch_bounds__(kBlock, 1) cg1_kernel(const Cg1Args G) {
     if (u < P.m) {
       mbar_wait(&sm.full[u], 0);
       const StageMeta& mt = sm.meta[u];
-      const int i = mt.is_long ? (threadIdx.x == 0 ? mt.row0 : -1) : mt.row0 + (int)threadIdx.x;
-      li[u] = (i >= 0 && i < mt.row1) ? i : -1;
+      li[u] = owned_line<FMT>(mt);
     }
   }
   // ||b||

@@ -95,22 +95,19 @@ __device__ __forceinline__ double sym_row_atomic(const double* v, const int* ix,
   double acc = 0.0;
   for (int k = ks; k < ke; k += kUnroll) {
     double pr[kUnroll];
-    int jj[kUnroll];
-    double vv[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      const bool ok = k + u < ke;
-      jj[u] = ok ? ix[k + u] : i;
-      vv[u] = ok ? v[k + u] : 0.0;
-      pr[u] = ok ? __dmul_rn(vv[u], src.get(jj[u])) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      if (k + u < ke) {
-        acc = __dadd_rn(acc, pr[u]);
-        if (jj[u] != i) red_add_f64(y + jj[u], __dmul_rn(vv[u], xi));
+      pr[u] = 0.0;
+      if (k + u < ke) {  // scatter issued at load time: only pr[] stays live
+        const int j = ix[k + u];
+        const double a = v[k + u];
+        pr[u] = __dmul_rn(a, src.get(j));
+        if (j != i) red_add_f64(y + j, __dmul_rn(a, xi));
       }
     }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (k + u < ke) acc = __dadd_rn(acc, pr[u]);
   }
   return acc;
 }
@@ -171,6 +168,26 @@ struct LineOut {
 #endif
 constexpr int kStreamMinPerLine = SPCG_STREAM_MIN;
 
+// Scatter formats give each line of a short tile 2^lg adjacent lanes when
+// the tile has at most kBlock/2 (kBlock/4) lines (see scatter_line_cap).
+template <int FMT>
+__device__ __forceinline__ int split_lg(const StageMeta& mt) {
+  if (FMT != K_SCSR_ATOMIC && FMT != K_CSC) return 0;
+  const int rows = mt.row1 - mt.row0;
+  return (rows * 4 <= kBlock) ? 2 : (rows * 2 <= kBlock ? 1 : 0);
+}
+
+// The line this thread reports for staged tile mt (-1: none); matches
+// tile_line's `active` / `line` outputs.
+template <int FMT>
+__device__ __forceinline__ int owned_line(const StageMeta& mt) {
+  if (mt.is_long) return threadIdx.x == 0 ? mt.row0 : -1;
+  const int lg = split_lg<FMT>(mt);
+  if ((int)threadIdx.x & ((1 << lg) - 1)) return -1;
+  const int i = mt.row0 + ((int)threadIdx.x >> lg);
+  return i < mt.row1 ? i : -1;
+}
+
 // Computes line i (the tid-th line of staged tile s).  For FMT in
 // {SCSR_ATOMIC, CSC} the scatter goes to y (must be zeroed beforehand) and
 // the line's own gather is returned in q; for CSR / SCSR_PRIV the caller
@@ -190,6 +207,44 @@ __device__ __forceinline__ LineOut tile_line(Smem& sm, int s, const MatView& M, 
 #define SPCG_NO_XPRE 0
 #endif
     if (SPCG_NO_XPRE) xpre = nullptr;
+    if (FMT == K_SCSR_ATOMIC || FMT == K_CSC) {
+      // split lines: tiles of <= 256 (128) lines give each line 2 (4)
+      // adjacent lanes (512-line tiles: one lane per line); lane g takes the g-th contiguous segment of the
+      // line's entries (gather partial + its scatters), and the partials
+      // combine in fixed order (s0+s1)+(s2+s3), so the gather half stays
+      // deterministic.  Warp-uniform: every lane reaches the shuffles.
+      const int lg = split_lg<FMT>(mt);
+      {
+        const int tpl = 1 << lg;
+        const int g = (int)threadIdx.x & (tpl - 1);
+        const int li = mt.row0 + ((int)threadIdx.x >> lg);
+        const bool has = li < mt.row1;
+        double acc = 0.0;
+        if (has) {
+          const int l = li - mt.r0a;
+          const int a0 = sm.rpA[s][l] - mt.kA0a;
+          const int a1 = sm.rpA[s][l + 1] - mt.kA0a;
+          const int c = (a1 - a0 + tpl - 1) >> lg;
+          const int ks = min(a1, a0 + g * c);
+          const int ke = min(a1, ks + c);
+          o.xi = src.get(li);
+          if (xpre) o.xo = xpre[li];
+          if (FMT == K_SCSR_ATOMIC) {
+            acc = sym_row_atomic(sm.val[s], sm.idx[s], ks, ke, li, o.xi, src, y);
+            o.dg = (a1 > a0) ? sm.val[s][a1 - 1] : 0.0;
+          } else {
+            acc = csc_col<GATHER_CSC>(sm.val[s], sm.idx[s], ks, ke, o.xi, src, y);
+          }
+        }
+        double t = acc;
+        if (lg >= 1) t = __dadd_rn(t, __shfl_down_sync(0xffffffffu, t, 1));
+        if (lg == 2) t = __dadd_rn(t, __shfl_down_sync(0xffffffffu, t, 2));
+        o.q = t;
+        active = has && g == 0;
+        line = li;
+        return o;
+      }
+    }
     const bool stream = ALLOW_STREAM && (FMT == K_CSR || FMT == K_SCSR_PRIV) &&
                         mt.cnt > kStreamMinPerLine * (mt.row1 - mt.row0);
     const double* v = sm.val[s];

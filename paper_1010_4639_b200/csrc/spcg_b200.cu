@@ -253,7 +253,7 @@ int upload_seg(Seg& s, int n, const std::vector<int>& ptr, const int* idx, const
 // caps (kTileLines lines, kTileNnz entries) is split greedily; a single line
 // over kTileNnz becomes a "long" one-line tile.
 void build_tiles(int n, const std::vector<int>& pA, const std::vector<int>* pB, int target,
-                 std::vector<int4>& desc, std::vector<int2>* descB) {
+                 std::vector<int4>& desc, std::vector<int2>* descB, int line_cap = kTileLines) {
   desc.clear();
   if (descB) descB->clear();
   if (n == 0) return;
@@ -266,7 +266,7 @@ void build_tiles(int n, const std::vector<int>& pA, const std::vector<int>* pB, 
   const long long tot = W(n);
   const long long nzt = nz(0, n);
   long long T = std::max<long long>(target, (nzt + kTileNnz - 1) / kTileNnz);
-  T = std::max<long long>(T, ((long long)n + kTileLines - 1) / kTileLines);
+  T = std::max<long long>(T, ((long long)n + line_cap - 1) / line_cap);
   T = std::max<long long>(1, std::min<long long>(T, n));
   auto push = [&](int s, int e) {
     desc.push_back(make_int4(s, e, pA[s], pA[e]));
@@ -291,7 +291,7 @@ void build_tiles(int n, const std::vector<int>& pA, const std::vector<int>* pB, 
     // enforce caps
     int a = s;
     while (a < e) {
-      int lim = std::min(e, a + kTileLines);
+      int lim = std::min(e, a + line_cap);
       int lo = a + 1, hi = lim;  // largest b in [a+1, lim] with nz(a,b) <= cap
       if (nz(a, a + 1) > kTileNnz) {
         push(a, a + 1);
@@ -376,6 +376,17 @@ int target_tiles() {
   return d->sms;
 }
 
+// Scatter formats (SCSR single pass, CSC) split a line over 2 or 4 lanes
+// when a full 512-line tile would not fit kTileNnz (tile_line): cap their
+// tiles at 256 / 128 lines so every thread of the CTA has a segment.
+int scatter_line_cap(int fmt, int n, const std::vector<int>& ptr) {
+  if (fmt == SPCG_FMT_CSR || n == 0) return kTileLines;
+  const double avg = (double)ptr[n] / (double)n;
+  if (avg * kTileLines <= kTileNnz) return kTileLines;
+  if (avg * (kTileLines / 2) <= kTileNnz) return kTileLines / 2;
+  return kTileLines / 4;
+}
+
 // Finish a handle from host int32 arrays (ptrA, idxA, valA).
 int finish_matrix(spcg_matrix_s* m, const std::vector<int>& ptr, const int* idx, const double* val,
                   bool device_arrays_ready) {
@@ -385,7 +396,7 @@ int finish_matrix(spcg_matrix_s* m, const std::vector<int>& ptr, const int* idx,
   }
   const int target = target_tiles();
   std::vector<int4> desc;
-  build_tiles(m->n, ptr, nullptr, target, desc, nullptr);
+  build_tiles(m->n, ptr, nullptr, target, desc, nullptr, scatter_line_cap(m->fmt, m->n, ptr));
   if ((rc = upload_tiles(m->t1, desc, nullptr, &m->bytes))) return rc;
   return SPCG_OK;
 }

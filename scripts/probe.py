@@ -27,14 +27,14 @@ def solve(dm, b_t, acc=1, tol=1e-10, max_iter=0, engine=0, reps=3):
     lib = N.load()
     x = torch.empty_like(b_t)
     o = N.CgOptionsC(tol=tol, max_iter=max_iter, record_history=0, recompute_final_residual=1,
-                     accumulation=acc, engine=engine)
+                     accumulation=acc, engine=engine, timing=1)
     out = []
     for _ in range(reps):
         r = N.CgResultC()
         rc = lib.spcg_cg_solve(dm.handle, b_t.data_ptr(), None, x.data_ptr(), None, o, r,
                                torch.cuda.current_stream().cuda_stream)
         N.check(rc, "solve")
-        out.append((r.device_ms, r.iterations, r.final_relative_residual))
+        out.append((r.device_ms, r.iterations, r.final_relative_residual, r.spmv_ms / max(r.spmv_launches, 1)))
     return out, x
 
 
@@ -57,7 +57,7 @@ def spmv_time(dm, acc, n, reps=20):
 def report(name, dm, n, nnz_stored, b_t, acc=1, max_iter=0, engine=0):
     t0 = time.time()
     res, x = solve(dm, b_t, acc=acc, max_iter=max_iter, engine=engine)
-    ms, its, fr = res[-1]
+    ms, its, fr, pq_ms = res[-1]
     best = min(r[0] for r in res)
     it_bytes = 12 * nnz_stored + 4 * (n + 1) + 88 * n
     sp_bytes = 12 * nnz_stored + 4 * (n + 1) + 16 * n
@@ -66,7 +66,7 @@ def report(name, dm, n, nnz_stored, b_t, acc=1, max_iter=0, engine=0):
     d = dict(cfg=name, n=n, nnz=nnz_stored, iterations=its, final_rel=fr, solve_ms=best,
              us_per_it=us_it, it_per_s=its / (best / 1e3),
              it_GBs=it_bytes / (us_it * 1e-6) / 1e9, it_frac=it_bytes / (us_it * 1e-6) / 1e9 / PEAK,
-             spmv_ms=spms, spmv_GBs=sp_bytes / (spms * 1e-3) / 1e9,
+             spmv_ms=spms, pass_a_ms=pq_ms, pass_a_frac=sp_bytes / (pq_ms * 1e-3) / 1e9 / PEAK if pq_ms else None, spmv_GBs=sp_bytes / (spms * 1e-3) / 1e9,
              spmv_frac=sp_bytes / (spms * 1e-3) / 1e9 / PEAK, wall_s=time.time() - t0,
              all_ms=[r[0] for r in res])
     print(json.dumps(d), flush=True)
