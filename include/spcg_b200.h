@@ -122,13 +122,16 @@ typedef struct {
   int32_t record_history;        /* write rel residual per iteration to hist   */
   int32_t recompute_final_residual; /* default 1 (solver.py:159-162)           */
   int32_t accumulation;          /* spcg_accumulation, SCSR only               */
-  int32_t engine;                /* 0 = auto (3 when the system is resident
-                                    in shared memory, else 2),
+  int32_t engine;                /* 0 = auto (5 for CSR / CSC systems that
+                                    fit one thread-block cluster, else 3 when
+                                    the system is resident on chip, else 2),
                                     1 = persistent kernel, two-reduction CG,
                                     2 = per-pass kernels (the sharded engine),
                                     3 = persistent single-reduction CG
                                         (Chronopoulos-Gear, resident only),
-                                    4 = persistent three-pass CG             */
+                                    4 = persistent three-pass CG,
+                                    5 = cluster-resident single-reduction CG
+                                        (<= 16 CTAs, banded systems)         */
   int32_t timing;                /* per-pass engine: CUDA-event time of every
                                     SpMV pass -> result.spmv_ms / launches   */
   int32_t reserved;

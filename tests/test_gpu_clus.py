@@ -1,5 +1,7 @@
-"""Single-reduction (Chronopoulos-Gear) resident engine vs the reference's
-own CG output, and the two-reduction resident engine kept selectable."""
+"""Cluster-resident engine (engine 5, csrc/clus.cuh) vs the reference's own
+CG output: the paper-size FEM matrix in all four storages (16-CTA cluster,
+SELL slices partly streamed from L2, DSMEM halo exchange), the solver.py
+semantics (x0, max_iter, b = 0, history) and breakdown attribution."""
 
 import numpy as np
 import pytest
@@ -22,15 +24,14 @@ def as_storage(a, kind):
                                           else "atomic")
 
 
-@pytest.mark.parametrize("engine", [1, 3])
 @pytest.mark.parametrize("kind", STORAGES)
-def test_fem_mesh_both_resident_engines(golden, kind, engine):
+def test_fem_mesh_cluster_engine(golden, kind):
     from paper_1010_4639_b200 import CgOptions, cg_solve
     from paper_1010_4639_b200.genprob import fem_mesh
 
     g = golden("fem")
     m, cfg = as_storage(fem_mesh(), kind)
-    r = cg_solve(m, g["F_b"], opts=CgOptions(record_history=True), cfg=cfg, engine=engine)
+    r = cg_solve(m, g["F_b"], opts=CgOptions(record_history=True), cfg=cfg, engine=5)
     assert abs(r.iterations - int(g["F_full_it"])) <= 3
     xr = g["F_full_x"]
     assert np.linalg.norm(r.x - xr) / np.linalg.norm(xr) <= 1e-8
@@ -39,7 +40,7 @@ def test_fem_mesh_both_resident_engines(golden, kind, engine):
 
 
 @pytest.mark.parametrize("kind", STORAGES)
-def test_single_reduction_semantics(golden, kind):
+def test_cluster_semantics(golden, kind):
     from paper_1010_4639_b200 import CgOptions, cg_solve
     from paper_1010_4639_b200.genprob import poisson3d
 
@@ -47,41 +48,70 @@ def test_single_reduction_semantics(golden, kind):
     a = poisson3d(12, 12, 12)
     m, cfg = as_storage(a, kind)
     r = cg_solve(m, g["p3_b"], x0=g["p3_x0"], opts=CgOptions(tol=1e-9, record_history=True),
-                 cfg=cfg, engine=3)
+                 cfg=cfg, engine=5)
     assert abs(r.iterations - int(g["p3_it"])) <= 1
     assert np.linalg.norm(r.x - g["p3_x"]) / np.linalg.norm(g["p3_x"]) <= 1e-8
     assert len(r.residual_history) == r.iterations
     t = cg_solve(m, g["p3_b"], x0=g["p3_x0"], opts=CgOptions(max_iter=7, record_history=True,
                                                              recompute_final_residual=False),
-                 cfg=cfg, engine=3)
+                 cfg=cfg, engine=5)
     assert t.iterations == 7 and not t.converged and len(t.residual_history) == 7
     assert abs(t.final_relative_residual - float(g["p3t_final"])) <= 1e-9 * float(g["p3t_final"])
-    z = cg_solve(m, np.zeros(a.n), x0=g["p3_x0"], cfg=cfg, engine=3)
+    z = cg_solve(m, np.zeros(a.n), x0=g["p3_x0"], cfg=cfg, engine=5)
     assert z.iterations == 0 and (z.x == 0).all()
 
 
-def test_single_reduction_breakdowns():
+def test_cluster_unbanded_random_spd():
+    """Random SPD (windows span the whole matrix): every CTA's halo is every
+    other CTA's rows; the result must still match the reference CG."""
+    from paper_1010_4639_b200 import CgOptions, cg_solve
+    from paper_1010_4639_b200.genprob import random_spd
+
+    a = random_spd(3000, 0.004, seed=5)
+    rng = np.random.default_rng(3)
+    b = rng.standard_normal(a.n)
+    ref = O.cg_solve("csr", a.row_start, a.col_idx, a.values, b, tol=1e-10)
+    r = cg_solve(a, b, opts=CgOptions(tol=1e-10), engine=5)
+    assert abs(r.iterations - ref.iterations) <= max(1, ref.iterations // 100)
+    assert np.linalg.norm(r.x - ref.x) / np.linalg.norm(ref.x) <= 1e-8
+
+
+def test_cluster_breakdowns():
     from paper_1010_4639_b200 import NotPositiveDefiniteError, build_csr_from_triplets, cg_solve
 
     a = build_csr_from_triplets([(0, 0, 1.0), (1, 1, -1.0)], 2)
     with pytest.raises(NotPositiveDefiniteError, match="not positive definite"):
-        cg_solve(a, np.array([1.0, 2.0]), engine=3)
-    # indefinite but p0.Ap0 > 0: the breakdown appears at a later iteration,
-    # which must be the iteration the reference reports
+        cg_solve(a, np.array([1.0, 2.0]), engine=5)
     d = build_csr_from_triplets([(0, 0, 4.0), (1, 1, 3.0), (2, 2, -0.5)], 3)
     b = np.array([1.0, 1.0, 0.1])
-    with pytest.raises(NotPositiveDefiniteError):
-        cg_solve(d, b, engine=3)
     ref = O.cg_solve("csr", d.row_start, d.col_idx, d.values, b)
     assert ref.status == 3
+    with pytest.raises(NotPositiveDefiniteError):
+        cg_solve(d, b, engine=5)
+    # the iteration the breakdown is attributed to (C-ABI) is the reference's
+    from paper_1010_4639_b200 import _native as N
+    import torch
+
+    lib = N.load()
+    bt = torch.from_numpy(b).cuda()
+    xt = torch.empty_like(bt)
+    o = N.CgOptionsC(tol=1e-10, max_iter=3, record_history=0, recompute_final_residual=1,
+                     accumulation=1, engine=5)
+    res = N.CgResultC()
+    rc = lib.spcg_cg_solve(d.device().handle, bt.data_ptr(), None, xt.data_ptr(), None, o, res,
+                           torch.cuda.current_stream().cuda_stream)
+    assert rc == 3 and res.status == 3 and res.fail_iteration == ref.fail_iteration
 
 
-def test_engine3_is_deterministic():
+def test_auto_engine_is_cluster_for_small_systems():
     from paper_1010_4639_b200 import cg_solve
     from paper_1010_4639_b200.genprob import fem_mesh, rhs_for
 
     F = fem_mesh()
     b, _ = rhs_for(F, seed=1)
-    r1 = cg_solve(F, b, engine=3)
-    r2 = cg_solve(F, b, engine=3)
-    assert r1.iterations == r2.iterations and (r1.x == r2.x).all()
+    r0 = cg_solve(F, b)            # auto
+    r5 = cg_solve(F, b, engine=5)
+    assert r0.iterations == r5.iterations and (r0.x == r5.x).all()  # deterministic
+    r3 = cg_solve(F, b, engine=3)  # grid-resident single reduction: same method
+    assert r3.iterations == r5.iterations
+    assert np.linalg.norm(r3.x - r5.x) / np.linalg.norm(r5.x) <= 1e-10
