@@ -17,7 +17,7 @@ NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC", "-shared",
-    "-Xptxas", "-v",
+    "-Xptxas", "-v", "-diag-suppress", "128",
 ]
 
 

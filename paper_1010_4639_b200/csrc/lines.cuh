@@ -168,13 +168,51 @@ struct LineOut {
 #endif
 constexpr int kStreamMinPerLine = SPCG_STREAM_MIN;
 
-// Scatter formats give each line of a short tile 2^lg adjacent lanes when
-// the tile has at most kBlock/2 (kBlock/4) lines (see scatter_line_cap).
-template <int FMT>
+// A line of a short tile gets 2^lg adjacent lanes when the tile has at most
+// kBlock/2 (kBlock/4) lines (long-row matrices: see tile_line_cap).
+// Gather formats (CSR, SCSR privatized) split only in the streaming passes:
+// in the latency-bound resident kernels the shuffle chain costs more than
+// the idle lanes (S: 8.6 vs 9.5 us per iteration).
+template <int FMT, bool STREAMING>
 __device__ __forceinline__ int split_lg(const StageMeta& mt) {
-  if (FMT != K_SCSR_ATOMIC && FMT != K_CSC) return 0;
+  if (!STREAMING && (FMT == K_CSR || FMT == K_SCSR_PRIV)) return 0;
   const int rows = mt.row1 - mt.row0;
   return (rows * 4 <= kBlock) ? 2 : (rows * 2 <= kBlock ? 1 : 0);
+}
+
+// Sequential (storage-order) sum of one line segment [ks, ke) of a staged
+// tile, computed by the line's 2^lg adjacent lanes: lane g gathers entries
+// u = g, g + T, g + 2T, ... (up to 8 per round, so each lane keeps 8 gathers
+// in flight) and every lane of the group then adds all products in entry
+// order, taking them by shuffles.  Bitwise the reference's row sum, with no
+// product round trip through shared memory.  Warp-uniform: all 32 lanes
+// call it (lanes without a line pass ks == ke).
+template <class Src>
+__device__ __forceinline__ double lane_seq_sum(const double* v, const int* ix, int ks, int ke,
+                                               int lg, const Src& src) {
+  const int T = 1 << lg;
+  const int lane = (int)threadIdx.x & 31;
+  const int g = lane & (T - 1), owner = lane & ~(T - 1);
+  const int L = ke - ks;
+  const int Lmax = __reduce_max_sync(0xffffffffu, L);
+  double acc = 0.0;
+  for (int base = 0; base < Lmax; base += 8 * T) {
+    double p[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int u = base + t * T + g;
+      p[t] = (u < L) ? __dmul_rn(v[ks + u], src.get(ix[ks + u])) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+#pragma unroll
+      for (int gg = 0; gg < 4; ++gg)
+        if (gg < T) {
+          const double q = __shfl_sync(0xffffffffu, p[t], owner + gg);
+          if (base + t * T + gg < L) acc = __dadd_rn(acc, q);
+        }
+  }
+  return acc;
 }
 
 // The line this thread reports for staged tile mt (-1: none); matches
@@ -182,10 +220,72 @@ __device__ __forceinline__ int split_lg(const StageMeta& mt) {
 template <int FMT>
 __device__ __forceinline__ int owned_line(const StageMeta& mt) {
   if (mt.is_long) return threadIdx.x == 0 ? mt.row0 : -1;
-  const int lg = split_lg<FMT>(mt);
+  const int lg = split_lg<FMT, false>(mt);  // resident kernels
   if ((int)threadIdx.x & ((1 << lg) - 1)) return -1;
   const int i = mt.row0 + ((int)threadIdx.x >> lg);
   return i < mt.row1 ? i : -1;
+}
+
+// Two segments (SCSR privatized: L+D then L^T) in the same rounds, so the
+// gathers of both are in flight together; sums kept separate (g, t).
+template <class Src>
+__device__ __forceinline__ void lane_seq_sum2(const double* v, const int* ix, int ka, int kae,
+                                              int kb, int kbe, int lg, const Src& src,
+                                              double& ga, double& gb) {
+  const int T = 1 << lg;
+  const int lane = (int)threadIdx.x & 31;
+  const int g = lane & (T - 1), owner = lane & ~(T - 1);
+  const int LA = kae - ka, LB = kbe - kb;
+  const int Lmax = __reduce_max_sync(0xffffffffu, max(LA, LB));
+  double acc = 0.0, acc2 = 0.0;
+  for (int base = 0; base < Lmax; base += 4 * T) {
+    double p[4], q[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int u = base + t * T + g;
+      p[t] = (u < LA) ? __dmul_rn(v[ka + u], src.get(ix[ka + u])) : 0.0;
+      q[t] = (u < LB) ? __dmul_rn(v[kb + u], src.get(ix[kb + u])) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int gg = 0; gg < 4; ++gg)
+        if (gg < T) {
+          const int u = base + t * T + gg;
+          const double a = __shfl_sync(0xffffffffu, p[t], owner + gg);
+          const double b = __shfl_sync(0xffffffffu, q[t], owner + gg);
+          if (u < LA) acc = __dadd_rn(acc, a);
+          if (u < LB) acc2 = __dadd_rn(acc2, b);
+        }
+  }
+  ga = acc;
+  gb = acc2;
+}
+
+// Same sums through the tile's product buffer: lane g writes the products
+// of its entries u = g, g+T, ... (8 gathers in flight per round) to prod[k]
+// (prod may alias the staged values: the stage is not read again this pass),
+// then after a warp-level sync the line's first lane adds prod[ks..ke) in
+// order.  The line's lanes are in one warp, so no CTA barrier is needed.
+template <class Src>
+__device__ __forceinline__ void lane_products(const double* v, const int* ix, int ks, int ke,
+                                              int lg, const Src& src, double* prod) {
+  const int T = 1 << lg;
+  const int g = (int)threadIdx.x & (T - 1);
+  const int L = ke - ks;
+  for (int base = 0; base < L; base += 8 * T) {
+    double p[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int u = base + t * T + g;
+      p[t] = (u < L) ? __dmul_rn(v[ks + u], src.get(ix[ks + u])) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int u = base + t * T + g;
+      if (u < L) prod[ks + u] = p[t];
+    }
+  }
 }
 
 // Computes line i (the tid-th line of staged tile s).  For FMT in
@@ -213,7 +313,7 @@ __device__ __forceinline__ LineOut tile_line(Smem& sm, int s, const MatView& M, 
       // line's entries (gather partial + its scatters), and the partials
       // combine in fixed order (s0+s1)+(s2+s3), so the gather half stays
       // deterministic.  Warp-uniform: every lane reaches the shuffles.
-      const int lg = split_lg<FMT>(mt);
+      const int lg = split_lg<FMT, ALLOW_STREAM>(mt);
       {
         const int tpl = 1 << lg;
         const int g = (int)threadIdx.x & (tpl - 1);
@@ -240,6 +340,54 @@ __device__ __forceinline__ LineOut tile_line(Smem& sm, int s, const MatView& M, 
         if (lg >= 1) t = __dadd_rn(t, __shfl_down_sync(0xffffffffu, t, 1));
         if (lg == 2) t = __dadd_rn(t, __shfl_down_sync(0xffffffffu, t, 2));
         o.q = t;
+        active = has && g == 0;
+        line = li;
+        return o;
+      }
+    }
+    if (FMT == K_CSR || FMT == K_SCSR_PRIV) {
+      // long-row tiles capped at <= 256 (128) lines: split lines, every
+      // lane of the group gets the line's sequential sum(s)
+      const int lg = split_lg<FMT, ALLOW_STREAM>(mt);
+      if (lg > 0) {
+        const int g = (int)threadIdx.x & ((1 << lg) - 1);
+        const int li = mt.row0 + ((int)threadIdx.x >> lg);
+        const bool has = li < mt.row1;
+        int ks = 0, ke = 0, kb = 0, kbe = 0;
+        if (has) {
+          const int l = li - mt.r0a;
+          ks = sm.rpA[s][l] - mt.kA0a;
+          ke = sm.rpA[s][l + 1] - mt.kA0a;
+          if (FMT == K_SCSR_PRIV) {
+            kb = sm.rpB[s][l] - mt.kB0a + mt.offB;
+            kbe = sm.rpB[s][l + 1] - mt.kB0a + mt.offB;
+          }
+          if (g == 0) {
+            o.xi = src.get(li);
+            if (xpre) o.xo = xpre[li];
+          }
+        }
+#ifndef SPCG_SPLIT_SHFL
+#define SPCG_SPLIT_SHFL 1  // 0: products through shared memory (slower)
+#endif
+        if (SPCG_SPLIT_SHFL) {
+          if (FMT == K_SCSR_PRIV) {
+            double ga, gb;
+            lane_seq_sum2(sm.val[s], sm.idx[s], ks, ke, kb, kbe, lg, src, ga, gb);
+            o.q = __dadd_rn(ga, gb);
+          } else {
+            o.q = lane_seq_sum(sm.val[s], sm.idx[s], ks, ke, lg, src);
+          }
+        } else {
+          lane_products(sm.val[s], sm.idx[s], ks, ke, lg, src, prod);
+          if (FMT == K_SCSR_PRIV) lane_products(sm.val[s], sm.idx[s], kb, kbe, lg, src, prod);
+          __syncwarp();
+          if (has && g == 0) {
+            o.q = seq_sum(prod, ks, ke);
+            if (FMT == K_SCSR_PRIV) o.q = __dadd_rn(o.q, seq_sum(prod, kb, kbe));
+          }
+          __syncwarp();  // prod (may alias a resident tile's buffer) reused next line
+        }
         active = has && g == 0;
         line = li;
         return o;

@@ -396,15 +396,17 @@ int target_tiles() {
   return d->sms;
 }
 
-// Scatter formats (SCSR single pass, CSC) split a line over 2 or 4 lanes
-// when a full 512-line tile would not fit kTileNnz (tile_line): cap their
-// tiles at 256 / 128 lines so every thread of the CTA has a segment.
-int scatter_line_cap(int fmt, int n, const std::vector<int>& ptr) {
-  if (fmt == SPCG_FMT_CSR || n == 0) return kTileLines;
-  const double avg = (double)ptr[n] / (double)n;
+// Long-row matrices split a line over 2 or 4 lanes when a full 512-line
+// tile would not fit kTileNnz (tile_line): cap their tiles at 256 / 128
+// lines so every thread of the CTA has a segment.  Rows averaging more than
+// 32 entries keep 512-line tiles (CSR-stream body for the gather formats).
+int tile_line_cap(long long entries, int n) {
+  if (n == 0) return kTileLines;
+  const double avg = (double)entries / (double)n;
   if (avg * kTileLines <= kTileNnz) return kTileLines;
   if (avg * (kTileLines / 2) <= kTileNnz) return kTileLines / 2;
-  return kTileLines / 4;
+  if (avg * (kTileLines / 4) <= kTileNnz) return kTileLines / 4;
+  return kTileLines;
 }
 
 // Finish a handle from host int32 arrays (ptrA, idxA, valA).
@@ -416,7 +418,7 @@ int finish_matrix(spcg_matrix_s* m, const std::vector<int>& ptr, const int* idx,
   }
   const int target = target_tiles();
   std::vector<int4> desc;
-  build_tiles(m->n, ptr, nullptr, target, desc, nullptr, scatter_line_cap(m->fmt, m->n, ptr));
+  build_tiles(m->n, ptr, nullptr, target, desc, nullptr, tile_line_cap(m->n ? ptr[m->n] : 0, m->n));
   if ((rc = upload_tiles(m->t1, desc, nullptr, &m->bytes))) return rc;
   return SPCG_OK;
 }
@@ -430,7 +432,8 @@ int finish_transpose(spcg_matrix_s* m, const std::vector<int>& ptr, const std::v
   }
   std::vector<int4> desc;
   std::vector<int2> descB;
-  build_tiles(m->n, ptr, &tptr, target_tiles(), desc, &descB);
+  build_tiles(m->n, ptr, &tptr, target_tiles(), desc, &descB,
+              tile_line_cap(m->n ? (long long)ptr[m->n] + tptr[m->n] : 0, m->n));
   if ((rc = upload_tiles(m->t2, desc, &descB, &m->bytes))) return rc;
   m->hasB = true;
   return SPCG_OK;

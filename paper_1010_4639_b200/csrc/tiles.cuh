@@ -33,7 +33,10 @@ namespace spcg {
 constexpr int kBlock = SPCG_BLOCK;     // threads per CTA == lines per tile
 constexpr int kTileLines = kBlock;
 constexpr int kTileNnz = SPCG_TILE_NNZ;  // stored entries per tile (both segments)
-constexpr int kStages = 2;
+#ifndef SPCG_STAGES
+#define SPCG_STAGES 2
+#endif
+constexpr int kStages = SPCG_STAGES;  // TMA ring depth (tiles in flight + 1)
 #ifndef SPCG_STREAM_MINB
 #define SPCG_STREAM_MINB (1024 / SPCG_BLOCK)
 #endif
