@@ -1,7 +1,7 @@
 """Benchmark: fp64 CG iterations/s (and SpMV HBM GB/s, % of roofline) on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload p3|p2|q27|f|s|csc] [--max-iter M]
+                    [--workload p3|p2|q27|q27p|f|s|csc] [--max-iter M]
 
 Workload (BASELINE.json configs[3]; the largest single-GPU config and the one
 the metric's 1/2/4/8-GPU scaling is quoted on): 3-D 7-point Poisson 400^3
@@ -44,6 +44,9 @@ WORKLOADS = {
     "p2": ("poisson2d", (4096, 4096), "csr", 1, "2D 5-point Poisson 4096^2, CSR fp64 CG"),
     "q27": ("stencil27", (256, 256, 256), "scsr", 0,
             "3D 27-point stencil 256^3, symmetric CSR (L+D, atomic scatter) fp64 CG"),
+    "q27p": ("stencil27", (256, 256, 256), "scsr", 1,
+             "3D 27-point stencil 256^3, symmetric CSR (L+D and L^T rows, privatized: "
+             "deterministic, the reference's default accumulation) fp64 CG"),
     "f": ("fem", None, "csr", 1, "FEM-shaped 30880x30880 / 449,798 nnz, full CSR fp64 CG"),
     "s": ("fem", None, "scsr", 1, "FEM-shaped 30880, symmetric CSR (L+D) fp64 CG"),
     "csc": ("fem", None, "csc", 1, "FEM-shaped 30880, CSC fp64 CG"),
@@ -457,8 +460,11 @@ def run_distributed(args):
     nnz_loc = sm.dm.nnz
     nnz_tot = int(sum(gather(nnz_loc))) if world > 1 else nnz_loc
 
+    accum = "atomic" if acc == 0 else "privatized"  # SCSR shards: reverse halo vs stored L^T
+
     def step():
-        x, res, _ = D.dist_cg_solve(sm, comm, b_loc, max_iter=args.max_iter or None, timing=True)
+        x, res, _ = D.dist_cg_solve(sm, comm, b_loc, max_iter=args.max_iter or None, timing=True,
+                                    accumulation=accum)
         return x, res
 
     for _ in range(args.warmup):
@@ -496,7 +502,8 @@ def run_distributed(args):
     e2e_its = 0
     for _ in range(args.steps):
         bd = bh.to("cuda", non_blocking=True)
-        xd, r, _ = D.dist_cg_solve(sm, comm, bd, max_iter=args.max_iter or None)
+        xd, r, _ = D.dist_cg_solve(sm, comm, bd, max_iter=args.max_iter or None,
+                                   accumulation=accum)
         xh.copy_(xd, non_blocking=True)
         e2e_its += r.iterations
     e3.record(st)

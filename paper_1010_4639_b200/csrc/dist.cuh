@@ -89,6 +89,18 @@ __global__ void __launch_bounds__(kBlock, 2)
   last_block_sum(pq, sm, part, S);
 }
 
+// Reverse halo of the single-pass symmetric SpMV: partial sums of the
+// transposed scatters that landed in this rank's ghost slots (halo columns
+// owned by lower ranks) arrive in buf, aligned with the send list; add them
+// into q at those rows.  Atomic adds: a row can be in several peers' halos,
+// and this format's summation order is unspecified anyway.
+__global__ void __launch_bounds__(256) dist_unpack_add(long long total, const int* idx,
+                                                       const double* buf, double* q) {
+  const long long G = (long long)gridDim.x * blockDim.x;
+  for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < total; s += G)
+    red_add_f64(q + idx[s], buf[s]);
+}
+
 // y = A x_ext (plain gather; initial / true residual)
 template <int FMT>
 __global__ void __launch_bounds__(kBlock, 2)

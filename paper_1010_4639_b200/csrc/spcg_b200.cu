@@ -1356,13 +1356,20 @@ int ensure_dist_ws(spcg_matrix_s* m, long long send_total) {
   int rc;
   const long long next = (long long)m->n + (long long)m->halo.size();
   if (d.next != next) {
+    for (double* q : {d.r_ext, d.p_ext[0], d.p_ext[1], d.tmp_ext, d.q, d.part})
+      if (q) cudaFree(q);
+    if (d.S) cudaFree(d.S);
+    if (d.h_S) cudaFreeHost(d.h_S);
+    if (d.ev0) cudaEventDestroy(d.ev0);
+    if (d.ev1) cudaEventDestroy(d.ev1);
     const size_t eb = sizeof(double) * (size_t)std::max<long long>(1, next);
     if ((rc = dmalloc((void**)&d.r_ext, eb, nullptr))) return rc;
     if ((rc = dmalloc((void**)&d.p_ext[0], eb, nullptr))) return rc;
     if ((rc = dmalloc((void**)&d.p_ext[1], eb, nullptr))) return rc;
     if ((rc = dmalloc((void**)&d.tmp_ext, eb, nullptr))) return rc;
-    if ((rc = dmalloc((void**)&d.q, sizeof(double) * (size_t)std::max(1, m->n), nullptr)))
-      return rc;
+    // q is extended too: the single-pass SCSR scatter puts the transposed
+    // contributions of halo columns in q[nloc ..] (reverse halo)
+    if ((rc = dmalloc((void**)&d.q, eb, nullptr))) return rc;
     if ((rc = dmalloc((void**)&d.part, sizeof(double) * 4096, nullptr))) return rc;
     if ((rc = dmalloc((void**)&d.S, sizeof(StepState), nullptr))) return rc;
     CUDA_TRY(cudaMallocHost((void**)&d.h_S, sizeof(StepState)));
@@ -1417,6 +1424,34 @@ int halo_exchange(const HaloPlan& H, DistWorkspace& d, const double* v, double* 
   return SPCG_OK;
 }
 
+// Reverse halo: ghost partial sums q[nloc + recv_off[k] ..] go back to
+// their owner k, which adds them at its send rows; ghosts are then zeroed
+// for the next scatter.
+int reverse_halo(const HaloPlan& H, DistWorkspace& d, double* q, long long nhalo,
+                 cudaStream_t st, long long* launches) {
+  if (H.npeers == 0) return SPCG_OK;
+  NcclApi& N = nccl();
+  NCCL_TRY(N.GroupStart());
+  for (int k = 0; k < H.npeers; ++k) {
+    const long long sc = H.send_off[k + 1] - H.send_off[k];
+    const long long rc = H.recv_off[k + 1] - H.recv_off[k];
+    if (rc > 0)
+      NCCL_TRY(N.Send(q + H.nloc + H.recv_off[k], (size_t)rc, ncclDouble, H.peers[k], H.comm, st));
+    if (sc > 0)
+      NCCL_TRY(N.Recv(d.send_buf + H.send_off[k], (size_t)sc, ncclDouble, H.peers[k], H.comm, st));
+  }
+  NCCL_TRY(N.GroupEnd());
+  const long long total = H.send_off[H.npeers];
+  if (total > 0) {
+    const int g = (int)std::min<long long>(1184, (total + 255) / 256);
+    dist_unpack_add<<<g, 256, 0, st>>>(total, d.send_idx, d.send_buf, q);
+    CUDA_TRY(cudaGetLastError());
+    ++*launches;
+  }
+  if (nhalo > 0) CUDA_TRY(cudaMemsetAsync(q + H.nloc, 0, sizeof(double) * (size_t)nhalo, st));
+  return SPCG_OK;
+}
+
 int allreduce_red(const HaloPlan& H, StepState* S, cudaStream_t st) {
   if (!H.comm) return SPCG_OK;
   NCCL_TRY(nccl().AllReduce(&S->red, &S->red, 1, ncclDouble, ncclSum, H.comm, st));
@@ -1448,7 +1483,9 @@ int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const dou
   init.x0_given = x0 != nullptr;
   CUDA_TRY(cudaMemcpyAsync(d.S, &init, sizeof(StepState), cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaMemsetAsync(p, 0, sizeof(double) * (size_t)next, st));
-  if (kAtom) CUDA_TRY(cudaMemsetAsync(d.q, 0, sizeof(double) * (size_t)std::max(1LL, nloc), st));
+  if (kAtom) CUDA_TRY(cudaMemsetAsync(d.q, 0, sizeof(double) * (size_t)std::max(1LL, next), st));
+  const long long nhalo = next - nloc;
+  constexpr bool kRev = (FMT == K_SCSR_ATOMIC);  // transposed scatters reach halo rows
   CUDA_TRY(cudaEventRecord(d.ev0, st));
   // ||b|| (solver.py:107)
   dist_elem<<<GE, kBlock, 0, st>>>(0, nloc, d.S, b, nullptr, nullptr, nullptr, d.part, 0);
@@ -1462,6 +1499,7 @@ int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const dou
                              cudaMemcpyDeviceToDevice, st));
     if ((rc = halo_exchange(H, d, x0, d.tmp_ext, st, &launches))) return rc;
     dist_spmv<FMT><<<G, kBlock, sm, st>>>(v, d.tmp_ext, d.q);
+    if (kRev && (rc = reverse_halo(H, d, d.q, nhalo, st, &launches))) return rc;
     dist_elem<<<GE, kBlock, 0, st>>>(1, nloc, d.S, b, d.q, r, p, d.part, kAtom);
     launches += 2;
   } else {
@@ -1489,6 +1527,7 @@ int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const dou
       dist_spmv_pq<FMT><<<G, kBlock, sm, st>>>(v, d.S, p, d.q, d.part);
       if (timing) CUDA_TRY(cudaEventRecord(d.tev[1][c], st));
       if ((rc = allreduce_red(H, d.S, st))) return rc;
+      if (kRev && (rc = reverse_halo(H, d, d.q, nhalo, st, &launches))) return rc;
       dist_scalar<<<1, 1, 0, st>>>(2, d.S, hist);
       dist_elem<<<GE, kBlock, 0, st>>>(2, nloc, d.S, nullptr, d.q, r, nullptr, d.part, kAtom);
       if ((rc = allreduce_red(H, d.S, st))) return rc;
@@ -1521,6 +1560,7 @@ int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const dou
                              cudaMemcpyDeviceToDevice, st));
     if ((rc = halo_exchange(H, d, x, d.tmp_ext, st, &launches))) return rc;
     dist_spmv<FMT><<<G, kBlock, sm, st>>>(v, d.tmp_ext, d.q);
+    if (kRev && (rc = reverse_halo(H, d, d.q, nhalo, st, &launches))) return rc;
     dist_elem<<<GE, kBlock, 0, st>>>(3, nloc, d.S, b, d.q, nullptr, nullptr, d.part, 0);
     if ((rc = allreduce_red(H, d.S, st))) return rc;
     dist_true_rel<<<1, 1, 0, st>>>(d.S);
@@ -1558,12 +1598,11 @@ int do_dist_cg(spcg_matrix_s* m, spcg_comm_s* comm, int npeers, const int32_t* p
                const double* b, const double* x0, double* x, double* hist,
                const spcg_cg_options* o, spcg_cg_result* out, cudaStream_t st) {
   if (!(o->tol > 0.0)) return fail(SPCG_ERR_ARG, "tol must be > 0");
-  // single GPU: every format; sharded: CSR and owner-computes SCSR (the
-  // atomic transposed scatters would need a reverse halo)
-  int kf = kfmt_of(m, o->accumulation);
+  // single GPU: every format; sharded: CSR, owner-computes SCSR, and the
+  // single-pass SCSR whose transposed scatters into halo rows travel back to
+  // their owners (reverse halo)
+  const int kf = kfmt_of(m, o->accumulation);
   if (npeers > 0 && kf == K_CSC) return fail(SPCG_ERR_UNSUPPORTED, "sharded CSC is not supported");
-  if (npeers > 0 && kf == K_SCSR_ATOMIC) kf = K_SCSR_PRIV;
-  if (m->is_rows && kf == K_SCSR_ATOMIC) kf = K_SCSR_PRIV;
   if (kf == K_SCSR_PRIV && !m->hasB) return fail(SPCG_ERR_UNSUPPORTED, "SCSR needs its L^T rows");
   if (m->is_rows && !m->localized) return fail(SPCG_ERR_ARG, "call spcg_matrix_localize first");
   if (npeers > 0 && (!comm || !comm->comm)) return fail(SPCG_ERR_ARG, "peers need a communicator");

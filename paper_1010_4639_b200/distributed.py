@@ -257,9 +257,13 @@ class ShardedMatrix:
 
 def dist_cg_solve(sm: ShardedMatrix, comm: Comm, b_loc, x0_loc=None, tol: float = 1e-10,
                   max_iter: int | None = None, record_history: bool = False,
-                  recompute_final_residual: bool = True, timing: bool = False):
+                  recompute_final_residual: bool = True, timing: bool = False,
+                  accumulation: str = "privatized"):
     """One rank's part of the sharded solve.  b_loc / x0_loc: CUDA tensors
-    of this rank's rows.  Returns (x_loc, CgResultC, history or None)."""
+    of this rank's rows.  accumulation (symmetric-half shards): "privatized"
+    (owner-computes with the stored L^T rows, deterministic) or "atomic"
+    (one pass over L+D; transposed contributions to other ranks' rows go back
+    through a reverse halo).  Returns (x_loc, CgResultC, history or None)."""
     import torch
 
     p = sm.plan
@@ -268,7 +272,8 @@ def dist_cg_solve(sm: ShardedMatrix, comm: Comm, b_loc, x0_loc=None, tol: float 
     hist = torch.empty(mi if record_history else 1, dtype=torch.float64, device=b_loc.device)
     o = N.CgOptionsC(tol=float(tol), max_iter=int(mi), record_history=int(record_history),
                      recompute_final_residual=int(recompute_final_residual),
-                     accumulation=N.ACC_PRIVATIZED, engine=2, timing=int(timing))
+                     accumulation=N.ACC_ATOMIC if accumulation == "atomic" else N.ACC_PRIVATIZED,
+                     engine=2, timing=int(timing))
     res = N.CgResultC()
 
     def ptr(a):

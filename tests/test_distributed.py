@@ -36,8 +36,11 @@ def _sym_rows(a, r0, r1):
     return t
 
 
-def emulate_rank(rank, world, a, b, bounds, gather, allreduce, exchange, max_iter=None, tol=1e-10):
-    """One rank of the sharded CG in numpy (mirrors dist.cuh)."""
+def emulate_rank(rank, world, a, b, bounds, gather, allreduce, exchange, max_iter=None, tol=1e-10,
+                 atomic=False, reverse=None):
+    """One rank of the sharded CG in numpy (mirrors dist.cuh).  atomic: the
+    single-pass symmetric SpMV over L+D only, its transposed scatters into
+    halo rows sent back to their owners (reverse halo)."""
     from paper_1010_4639_b200.core import SymHalfMatrix
     from paper_1010_4639_b200.distributed import halo_plan, localize_columns
 
@@ -45,7 +48,7 @@ def emulate_rank(rank, world, a, b, bounds, gather, allreduce, exchange, max_ite
     nloc = r1 - r0
     rs = a.row_start
     segs = [(rs[r0:r1 + 1] - rs[r0], a.col_idx[rs[r0]:rs[r1]], a.values[rs[r0]:rs[r1]])]
-    if isinstance(a, SymHalfMatrix):
+    if isinstance(a, SymHalfMatrix) and not atomic:
         t = _sym_rows(a, r0, r1)
         segs.append((t.row_start[r0:r1 + 1] - t.row_start[r0],
                      t.col_idx[t.row_start[r0]:t.row_start[r1]],
@@ -68,6 +71,28 @@ def emulate_rank(rank, world, a, b, bounds, gather, allreduce, exchange, max_ite
             outs.append(part)
         return outs[0] if len(outs) == 1 else outs[0] + outs[1]
 
+    def spmv_atomic(v_ext):
+        """(q, p.Ap partial): gather over L+D, scatter of the transpose into
+        q_ext (ghost slots for halo columns), reverse halo, local p.Ap."""
+        ptr, _, val = segs[0]
+        ci = loc[0]
+        q_ext = np.zeros(next_)
+        pq = 0.0
+        for i in range(nloc):
+            g = 0.0
+            dg = 0.0
+            for k in range(ptr[i], ptr[i + 1]):
+                g = g + val[k] * v_ext[ci[k]]
+                if ci[k] != i:
+                    q_ext[ci[k]] += val[k] * v_ext[i]
+                else:
+                    dg = val[k]
+            q_ext[i] += g
+            pq += v_ext[i] * (2.0 * g - dg * v_ext[i])
+        back = reverse(plan, q_ext[nloc:])
+        np.add.at(q_ext, plan.send_idx, back)
+        return q_ext[:nloc], pq
+
     bl = b[r0:r1].copy()
     b_norm = np.sqrt(allreduce(float(np.dot(bl, bl))))
     x = np.zeros(nloc)
@@ -80,8 +105,12 @@ def emulate_rank(rank, world, a, b, bounds, gather, allreduce, exchange, max_ite
     k, alpha = 0, 0.0
     converged = np.sqrt(rr) <= tol * b_norm
     while not converged and k < mi:
-        q = spmv2(p_ext)                                   # pass A
-        pq = allreduce(float(np.dot(p_ext[:nloc], q)))
+        if atomic:                                         # pass A
+            q, pq_loc = spmv_atomic(p_ext)
+            pq = allreduce(float(pq_loc))
+        else:
+            q = spmv2(p_ext)
+            pq = allreduce(float(np.dot(p_ext[:nloc], q)))
         assert pq > 0
         alpha = rr / pq
         r = r - alpha * q                                  # pass B
@@ -114,7 +143,7 @@ def _worker(rank, world, port, kind, q):
         gather, _ = torch_collectives()
         if kind == "p3":
             a = poisson3d(7, 6, 5)
-        elif kind == "sym":
+        elif kind in ("sym", "sym_atomic"):
             a = extract_lower(poisson3d(6, 5, 6))
         else:
             a = random_spd(90, 0.08, 5)
@@ -145,7 +174,29 @@ def _worker(rank, world, port, kind, q):
                 out[r0_:r1_] = t.numpy()
             return out
 
-        x, k, plan, halo = emulate_rank(rank, world, a, b, bounds, gather, allreduce, exchange)
+        def reverse(plan, ghosts):
+            """Ghost partial sums -> their owners; returns the received values
+            aligned with this rank's send list (dist_unpack_add's input)."""
+            reqs, bufs = [], []
+            out = np.zeros(int(plan.send_off[-1]))
+            for k, peer in enumerate(plan.peers):
+                s0, s1 = plan.send_off[k], plan.send_off[k + 1]
+                r0_, r1_ = plan.recv_off[k], plan.recv_off[k + 1]
+                if r1_ > r0_:
+                    reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(ghosts[r0_:r1_])),
+                                           int(peer)))
+                if s1 > s0:
+                    t = torch.empty(int(s1 - s0), dtype=torch.float64)
+                    bufs.append((s0, s1, t))
+                    reqs.append(dist.irecv(t, int(peer)))
+            for rq in reqs:
+                rq.wait()
+            for s0, s1, t in bufs:
+                out[s0:s1] = t.numpy()
+            return out
+
+        x, k, plan, halo = emulate_rank(rank, world, a, b, bounds, gather, allreduce, exchange,
+                                        atomic=kind == "sym_atomic", reverse=reverse)
         xs = [None] * world
         dist.all_gather_object(xs, (rank, x, k, plan.npeers, halo.size))
         if rank == 0:
@@ -154,7 +205,7 @@ def _worker(rank, world, port, kind, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind", ["p3", "sym", "rand"])
+@pytest.mark.parametrize("kind", ["p3", "sym", "sym_atomic", "rand"])
 def test_sharded_cg_world2_matches_serial(kind):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -170,7 +221,7 @@ def test_sharded_cg_world2_matches_serial(kind):
     x = np.concatenate([t[1] for t in xs])
     its = {t[2] for t in xs}
     assert len(its) == 1, its  # every rank stops at the same iteration
-    if kind == "sym":
+    if kind in ("sym", "sym_atomic"):
         from paper_1010_4639_b200.core import expand_symmetric
 
         full = expand_symmetric(a)

@@ -137,3 +137,26 @@ def test_sharded_world1_solve():
     assert res.iterations == o.iterations
     assert np.linalg.norm(x.cpu().numpy() - o.x) / np.linalg.norm(o.x) <= 1e-8
     assert len(hist) == res.iterations
+
+
+@pytest.mark.parametrize("accumulation", ["privatized", "atomic"])
+def test_sharded_world1_symmetric_rows(accumulation):
+    """Symmetric-half row blocks (generated 27-point stencil, L+D and L^T
+    rows) through the sharded engine at world 1, both accumulation modes
+    (atomic: reverse-halo path with no peers)."""
+    import torch
+
+    from paper_1010_4639_b200.distributed import Comm, ShardedMatrix, dist_cg_solve
+    from paper_1010_4639_b200.genprob import rhs_for, stencil27
+
+    a = stencil27(12, 10, 9)  # full matrix (the shards generate L+D / L^T rows)
+    b, _ = rhs_for(a, seed=2)
+    sm = ShardedMatrix.from_stencil("stencil27", (12, 10, 9), "scsr", 0, 1, lambda o: [o])
+    comm = Comm(0, 1)
+    x0 = np.random.default_rng(4).standard_normal(a.n)
+    x, res, _ = dist_cg_solve(sm, comm, torch.from_numpy(b).cuda(), torch.from_numpy(x0).cuda(),
+                              accumulation=accumulation)
+    o = O.cg_solve("csr", a.row_start, a.col_idx, a.values, b, x0=x0)
+    assert abs(res.iterations - o.iterations) <= 1
+    assert np.linalg.norm(x.cpu().numpy() - o.x) / np.linalg.norm(o.x) <= 1e-8
+    assert res.final_relative_residual <= 1e-10
