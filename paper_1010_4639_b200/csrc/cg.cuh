@@ -94,7 +94,7 @@ __device__ __forceinline__ double grid_allreduce(double v, Smem& sm, unsigned lo
     if (lane == 0) {
       fence_acq_rel_gpu();
       const unsigned long long bits = (unsigned long long)__double_as_longlong(bs);
-      st_relaxed_v2_u64(bank + (size_t)kSlotWords * blockIdx.x,
+      slot_st2(bank + (size_t)kSlotWords * blockIdx.x,
                         (bits & 0xffffffff00000000ull) | epoch, (bits << 32) | epoch);
     }
   }
@@ -111,7 +111,7 @@ __device__ __forceinline__ double grid_allreduce(double v, Smem& sm, unsigned lo
 #pragma unroll
       for (int u = 0; u < kPollPer; ++u)
         if (pend[u])
-          ld_relaxed_v2_u64(bank + (size_t)kSlotWords * (base + 32 * kPollWarps * u), a[u], c[u]);
+          slot_ld2(bank + (size_t)kSlotWords * (base + 32 * kPollWarps * u), a[u], c[u]);
       any = false;
 #pragma unroll
       for (int u = 0; u < kPollPer; ++u)

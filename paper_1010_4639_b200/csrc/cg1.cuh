@@ -62,8 +62,8 @@ __device__ __forceinline__ void grid_allreduce2(double& v0, double& v1, Smem& sm
       const unsigned long long u0 = (unsigned long long)__double_as_longlong(b0);
       const unsigned long long u1 = (unsigned long long)__double_as_longlong(b1);
       unsigned long long* slot = bank + (size_t)kSlotWords * blockIdx.x;
-      st_relaxed_v2_u64(slot, (u0 & 0xffffffff00000000ull) | epoch, (u0 << 32) | epoch);
-      st_relaxed_v2_u64(slot + 2, (u1 & 0xffffffff00000000ull) | epoch, (u1 << 32) | epoch);
+      slot_st2(slot, (u0 & 0xffffffff00000000ull) | epoch, (u0 << 32) | epoch);
+      slot_st2(slot + 2, (u1 & 0xffffffff00000000ull) | epoch, (u1 << 32) | epoch);
     }
   }
   if (w < kPollWarps) {
@@ -79,8 +79,8 @@ __device__ __forceinline__ void grid_allreduce2(double& v0, double& v1, Smem& sm
       for (int u = 0; u < kPollPer; ++u)
         if (pend[u]) {
           const unsigned long long* sl = bank + (size_t)kSlotWords * (base + 32 * kPollWarps * u);
-          ld_relaxed_v2_u64(sl, a[u], c[u]);
-          ld_relaxed_v2_u64(sl + 2, e[u], f[u]);
+          slot_ld2(sl, a[u], c[u]);
+          slot_ld2(sl + 2, e[u], f[u]);
         }
       any = false;
 #pragma unroll

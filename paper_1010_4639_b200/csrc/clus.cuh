@@ -44,10 +44,22 @@ constexpr int kClusThreads = SPCG_CLUS_THREADS;
 constexpr int kClusWarps = kClusThreads / 32;
 constexpr int kClusSlicesPerWarp = 2048 / kClusThreads;
 constexpr int kClusMaxRows = kClusWarps * kClusSlicesPerWarp * 32;  // 2048 per CTA
-constexpr int kClusMax = 16;
+constexpr int kClusMax = 16;      // CTAs in one cluster (non-portable above 8)
+constexpr int kClusGridMax = 256;  // CTAs of a multi-cluster grid (K clusters of 8)
+constexpr int kClusSlotWords = 32;  // 256-byte global slot per cluster (own L2 line pair)
+#ifndef SPCG_CLUS_POLL_NS
+#define SPCG_CLUS_POLL_NS 0  // any __nanosleep back-off costs microseconds here
+#endif
+#ifndef SPCG_CLUS_VOLATILE
+#define SPCG_CLUS_VOLATILE 1  // volatile scalar slot accesses (relaxed v2 polls were 3x slower in situ)
+#endif
+#ifndef SPCG_CLUS_ACQ_LD
+#define SPCG_CLUS_ACQ_LD 0  // poll with ld.acquire instead of relaxed loads + fence
+#endif
 
 struct ClusCta {
   int row_lo, row_hi;  // own rows
+  int clo, chi;        // rows of this CTA's cluster (halo rows outside come via global)
   int wlo, wn;         // r window [wlo, wlo + wn)
   int nslices, slice0; // slices [slice0, slice0 + nslices) of the global table
   int nsend, send0;    // DSMEM sends of boundary w
@@ -60,7 +72,7 @@ struct ClusSlice {
   int pad;
 };
 struct ClusSend {
-  int dst;      // destination CTA rank
+  int dst;      // destination CTA (grid index; same cluster -> DSMEM, else global)
   int lo, hi;   // global rows [lo, hi) of this CTA
   int dst_off;  // halo index of row lo in dst
 };
@@ -84,12 +96,15 @@ struct ClusArgs {
   int recompute;
   int off_rwin, off_shalo, off_whalo, off_val, off_col;  // smem byte offsets
   int hcap;  // halo capacity (entries per halo buffer)
-  unsigned long long* trace;  // nullable (SPCG_TRACE builds): [C][4] ns
+  unsigned long long* trace;  // nullable (SPCG_TRACE builds): [G][4] ns
+  double* ghalo;              // K > 1: [2][G][hcap] halo w between clusters
+  unsigned long long* gslots; // K > 1: [2][K][4] epoch-tagged cluster partials (zeroed)
 };
 
 struct ClusShared {  // static part
   double slot[2][kClusMax][2];
   double red[2][kClusWarps];
+  double tot[2][2];  // K > 1: grid totals broadcast by the cluster leader
 };
 
 __device__ __forceinline__ void cluster_sync_all() {
@@ -145,16 +160,20 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ ClusShared cs;
   cgp::cluster_group cl = cgp::this_cluster();
-  const int me = (int)cl.block_rank();
+  const int me = (int)cl.block_rank();   // rank in the cluster
   const int C = (int)cl.num_blocks();
-  const ClusCta P = A.ctas[me];
+  const int G = (int)gridDim.x;          // K clusters of C CTAs
+  const int K = G / C;
+  const int kc = (int)blockIdx.x / C;    // this CTA's cluster
+  const int gme = (int)blockIdx.x;
+  const ClusCta P = A.ctas[gme];
   double* rwin = reinterpret_cast<double*>(smem_raw + A.off_rwin);
   double* shalo = reinterpret_cast<double*>(smem_raw + A.off_shalo);
   double* whalo = reinterpret_cast<double*>(smem_raw + A.off_whalo);  // [2][hcap]
   double* sval = reinterpret_cast<double*>(smem_raw + A.off_val);
   unsigned short* scol = reinterpret_cast<unsigned short*>(smem_raw + A.off_col);
   const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
-  const bool leader = me == 0 && tid == 0;
+  const bool leader = gme == 0 && tid == 0;
   const int nhalo = P.wn - (P.row_hi - P.row_lo);
   const int own0 = P.row_lo - P.wlo;  // window index of the first own row
 
@@ -209,6 +228,11 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
   };
   // cluster all-reduce of two values (fixed order: warps, then CTA ranks)
   uint32_t epoch = 0;
+#if SPCG_TRACE
+  unsigned long long tlv[4] = {0, 0, 0, 0};  // exchange, b1exit->b2exit, b1 wait, send_w
+  unsigned long long tpost = 0;               // leader: sum of slot-post times since start
+  const unsigned long long tstart = globaltimer_ns();
+#endif
   auto allreduce2 = [&](double& v0, double& v1) {
     const int bank = (int)(epoch++ & 1u);
     double a0 = warp_sum(v0), a1 = warp_sum(v1);
@@ -228,11 +252,106 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
         dst[1] = b1;
       }
     }
+#if SPCG_TRACE
+    const unsigned long long tb0 = (A.trace && tid == 0) ? globaltimer_ns() : 0;
+#endif
     cluster_sync_all();
+#if SPCG_TRACE
+    if (A.trace && tid == 0) tlv[2] += globaltimer_ns() - tb0;
+#endif
     double t0 = 0.0, t1 = 0.0;
     for (int c = 0; c < C; ++c) {
       t0 += cs.slot[bank][c][0];
       t1 += cs.slot[bank][c][1];
+    }
+    if (K > 1) {
+      // second level: cluster leaders exchange epoch-tagged partials through
+      // global memory (one fence each side; the cluster barrier before made
+      // the cluster's global halo stores part of the leader's release), then
+      // broadcast the grid totals into their cluster and barrier again
+      const uint32_t tag = epoch;  // identical sequence in every CTA, never 0
+#if SPCG_TRACE
+      unsigned long long ta = (A.trace && tid == 0) ? globaltimer_ns() : 0;
+#endif
+      if (me == 0 && wp == 0) {
+        unsigned long long* gb = A.gslots + (size_t)bank * K * kClusSlotWords;
+        if (lane == 0) {
+#if !SPCG_CLUS_NO_WFENCE
+          fence_acq_rel_gpu();
+#endif
+          const unsigned long long u0 = (unsigned long long)__double_as_longlong(t0);
+          const unsigned long long u1 = (unsigned long long)__double_as_longlong(t1);
+#if SPCG_TRACE
+          if (A.trace) tpost += globaltimer_ns() - tstart;
+#endif
+#if SPCG_CLUS_VOLATILE
+          volatile unsigned long long* dstv = gb + kClusSlotWords * kc;
+          dstv[0] = (u0 & 0xffffffff00000000ull) | tag;
+          dstv[1] = (u0 << 32) | tag;
+          dstv[2] = (u1 & 0xffffffff00000000ull) | tag;
+          dstv[3] = (u1 << 32) | tag;
+#else
+          st_relaxed_v2_u64(gb + kClusSlotWords * kc, (u0 & 0xffffffff00000000ull) | tag,
+                            (u0 << 32) | tag);
+          st_relaxed_v2_u64(gb + kClusSlotWords * kc + 2, (u1 & 0xffffffff00000000ull) | tag,
+                            (u1 << 32) | tag);
+#endif
+        }
+        double c0 = 0.0, c1 = 0.0;
+        if (lane < K) {
+          unsigned long long a, b, c, d;
+          unsigned long long spins = 0;
+          for (;;) {
+#if SPCG_CLUS_VOLATILE
+            {
+              volatile unsigned long long* srcv = gb + kClusSlotWords * lane;
+              a = srcv[0];
+              b = srcv[1];
+              c = srcv[2];
+              d = srcv[3];
+            }
+#elif SPCG_CLUS_ACQ_LD
+            ld_acquire_v2_u64(gb + kClusSlotWords * lane, a, b);
+            ld_acquire_v2_u64(gb + kClusSlotWords * lane + 2, c, d);
+#else
+            ld_relaxed_v2_u64(gb + kClusSlotWords * lane, a, b);
+            ld_relaxed_v2_u64(gb + kClusSlotWords * lane + 2, c, d);
+#endif
+            if ((uint32_t)a == tag && (uint32_t)b == tag && (uint32_t)c == tag && (uint32_t)d == tag)
+              break;
+            if (++spins > kSpinLimit) asm volatile("trap;");
+            if (SPCG_CLUS_POLL_NS) __nanosleep(SPCG_CLUS_POLL_NS);
+          }
+          c0 = __longlong_as_double((long long)((a & 0xffffffff00000000ull) | (b >> 32)));
+          c1 = __longlong_as_double((long long)((c & 0xffffffff00000000ull) | (d >> 32)));
+        }
+#if !SPCG_CLUS_ACQ_LD && !SPCG_CLUS_NO_RFENCE
+        fence_acq_rel_gpu();
+#endif
+#if SPCG_TRACE
+        if (A.trace && tid == 0) {
+          const unsigned long long tb = globaltimer_ns();
+          tlv[0] += tb - ta;
+          ta = tb;
+        }
+#endif
+        double s0 = 0.0, s1 = 0.0;
+        for (int k = 0; k < K; ++k) {  // fixed order over clusters
+          s0 += __shfl_sync(0xffffffffu, c0, k);
+          s1 += __shfl_sync(0xffffffffu, c1, k);
+        }
+        if (lane < C) {
+          double* dst = cl.map_shared_rank(&cs.tot[bank][0], lane);
+          dst[0] = s0;
+          dst[1] = s1;
+        }
+      }
+      cluster_sync_all();
+#if SPCG_TRACE
+      if (A.trace && tid == 0) tlv[1] += globaltimer_ns() - ta;
+#endif
+      t0 = cs.tot[bank][0];
+      t1 = cs.tot[bank][1];
     }
     v0 = t0;
     v1 = t1;
@@ -241,7 +360,9 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
   auto send_w = [&](int buf) {
     for (int e = 0; e < P.nsend; ++e) {
       const ClusSend sd = A.sends[P.send0 + e];
-      double* dst = cl.map_shared_rank(whalo + (size_t)buf * A.hcap, sd.dst);
+      double* dst = (sd.dst / C == kc)
+                        ? cl.map_shared_rank(whalo + (size_t)buf * A.hcap, sd.dst % C)
+                        : A.ghalo + ((size_t)buf * G + sd.dst) * A.hcap;
 #pragma unroll
       for (int k = 0; k < kClusSlicesPerWarp; ++k)
         if (rrow[k] >= sd.lo && rrow[k] < sd.hi) dst[sd.dst_off + rrow[k] - sd.lo] = wg[k];
@@ -303,7 +424,7 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
     }
   allreduce2(part, dummy);  // release/acquire at cluster scope covers scratch
   double gam = part;
-  for (int j = tid; j < P.wn; j += kClusThreads) rwin[j] = A.scratch[P.wlo + j];
+  for (int j = tid; j < P.wn; j += kClusThreads) rwin[j] = __ldcg(A.scratch + P.wlo + j);
   for (int h = tid; h < A.hcap; h += kClusThreads) shalo[h] = 0.0;
   __syncthreads();
 
@@ -365,8 +486,11 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
         rwin[own0 + rrow[k] - P.row_lo] = rg[k];
       }
     const double* wh = whalo + (size_t)rb * A.hcap;
+    const double* wg_glob = A.ghalo + ((size_t)rb * G + gme) * A.hcap;
     for (int h = tid; h < nhalo; h += kClusThreads) {
-      const double sh = mul_add_rn(wh[h], beta, shalo[h]);
+      const int hrow = h < P.hlo ? P.wlo + h : P.row_hi + (h - P.hlo);
+      const double wv = (hrow >= P.clo && hrow < P.chi) ? wh[h] : __ldcg(wg_glob + h);
+      const double sh = mul_add_rn(wv, beta, shalo[h]);
       shalo[h] = sh;
       const int j = halo_win(h);
       rwin[j] = mul_add_rn(rwin[j], na, sh);
@@ -382,7 +506,13 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
         g_new = fma(rg[k], rg[k], g_new);
         d_new += rg[k] * wg[k];
       }
+#if SPCG_TRACE
+    const unsigned long long ts0 = (A.trace && tid == 0) ? globaltimer_ns() : 0;
+#endif
     send_w(wb);
+#if SPCG_TRACE
+    if (A.trace && tid == 0) tlv[3] += globaltimer_ns() - ts0;
+#endif
     allreduce2(g_new, d_new);
     mark(2);
     const long long kk = it + 1;  // reference iteration number
@@ -424,8 +554,11 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
   }
 
 #if SPCG_TRACE
-  if (A.trace && tid == 0)
-    for (int ph = 0; ph < 4; ++ph) A.trace[me * 4 + ph] = tr[ph];
+  if (A.trace && tid == 0) {
+    for (int ph = 0; ph < 3; ++ph) A.trace[gme * 8 + ph] = tr[ph];
+    for (int ph = 0; ph < 4; ++ph) A.trace[gme * 8 + 3 + ph] = tlv[ph];
+    A.trace[gme * 8 + 7] = tpost;
+  }
 #endif
   if (status != ST_OK) {
     if (leader) {
@@ -445,7 +578,7 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
     part = 0.0;
     dummy = 0.0;
     allreduce2(part, dummy);  // x visible cluster-wide
-    for (int j = tid; j < P.wn; j += kClusThreads) rwin[j] = A.x[P.wlo + j];
+    for (int j = tid; j < P.wn; j += kClusThreads) rwin[j] = __ldcg(A.x + P.wlo + j);
     __syncthreads();
     double qv[kClusSlicesPerWarp];
     spmv(qv);

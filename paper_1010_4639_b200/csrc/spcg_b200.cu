@@ -199,7 +199,10 @@ struct ClusPlan {
   bool ok = false;     // feasible
   std::string why;     // reason when not feasible
   bool two = false;    // two segments per row (SCSR: L+D, L^T)
-  int C = 0;
+  int C = 0;           // CTAs (grid)
+  int cs = 0;          // cluster size; K = C / cs clusters
+  double* ghalo = nullptr;              // K > 1: [2][C][hcap]
+  unsigned long long* gslots = nullptr; // K > 1: [2][K][4]
   ClusCta* ctas = nullptr;
   ClusSlice* slices = nullptr;
   ClusSend* sends = nullptr;
@@ -464,6 +467,7 @@ void free_matrix(spcg_matrix_s* m) {
   F(d.r_ext); F(d.p_ext[0]); F(d.p_ext[1]); F(d.tmp_ext); F(d.q); F(d.part); F(d.S);
   F(d.send_buf); F(d.send_idx);
   F(m->cp.ctas); F(m->cp.slices); F(m->cp.sends); F(m->cp.rowmeta); F(m->cp.gval); F(m->cp.gcol);
+  F(m->cp.ghalo); F(m->cp.gslots);
   if (d.h_S) cudaFreeHost(d.h_S);
   if (d.ev0) cudaEventDestroy(d.ev0);
   if (d.ev1) cudaEventDestroy(d.ev1);
@@ -639,7 +643,7 @@ int build_clus_plan(spcg_matrix_s* m) {
   const int n = m->n;
   if (m->is_rows) return clus_fail(P, "row block");
   if (n <= 0) return clus_fail(P, "empty");
-  if ((long long)n > (long long)kClusMax * kClusMaxRows) return clus_fail(P, "too many rows");
+  if ((long long)n > (long long)kClusGridMax * kClusMaxRows) return clus_fail(P, "too many rows");
   // rows as (segment A, segment B) entry lists
   std::vector<int> pA, iA, pB, iB;
   std::vector<double> vA, vB;
@@ -668,9 +672,56 @@ int build_clus_plan(spcg_matrix_s* m) {
     if (l > 4096 || lenA(i) > 32767) return clus_fail(P, "row too long");
     tot += l + 1;
   }
+  // grid shape: one cluster of <= 16 CTAs, or K clusters of 8 (as many as
+  // are co-resident) with ~4K entries per CTA so the whole matrix stays in
+  // shared memory
   const int cmin = (n + kClusMaxRows - 1) / kClusMaxRows;
-  int C = (int)std::min<long long>(kClusMax, std::max<long long>(cmin, (tot + 11999) / 12000));
-  C = std::max(1, C);
+  const long long want = std::max<long long>(cmin, (tot + 3999) / 4000);
+  const void* kfn = P.two ? (const void*)clus_cg_kernel<true> : (const void*)clus_cg_kernel<false>;
+  int optin0 = 0, dev0 = 0;
+  CUDA_TRY(cudaGetDevice(&dev0));
+  CUDA_TRY(cudaDeviceGetAttribute(&optin0, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev0));
+  const int smem_probe = optin0 - (int)sizeof(ClusShared) - 1024;
+  auto max_clusters = [&](int csz) -> int {
+    CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_probe));
+    if (csz > 8) CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(csz);
+    cfg.blockDim = dim3(kClusThreads);
+    cfg.dynamicSmemBytes = (size_t)smem_probe;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = csz;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, kfn, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    return ncl;
+  };
+  int C, csz;
+  static const int force_k = getenv("SPCG_CLUS_K") ? atoi(getenv("SPCG_CLUS_K")) : 0;  // dev A/B
+  if (want <= kClusMax && force_k <= 1) {
+    C = csz = (int)std::max<long long>(1, want);
+    if (max_clusters(csz) < 1) return clus_fail(P, "cluster not launchable");
+  } else {
+    csz = 8;
+    const int kmax = std::min(max_clusters(csz), kClusGridMax / 8);
+    int K = (int)std::min<long long>(kmax, (want + csz - 1) / csz);
+    if (force_k > 1) K = std::min(kmax, force_k);
+    if (K < 1) return clus_fail(P, "cluster not launchable");
+    if ((long long)K * csz * kClusMaxRows < n) {  // fall back to one big cluster
+      csz = kClusMax;
+      K = 1;
+      if (max_clusters(csz) < 1 || (long long)csz * kClusMaxRows < n)
+        return clus_fail(P, "too many rows for the co-resident clusters");
+    }
+    C = K * csz;
+  }
   // contiguous row blocks balanced by entries + rows, <= kClusMaxRows each
   std::vector<int> lo(C), hi(C);
   {
@@ -724,6 +775,8 @@ int build_clus_plan(spcg_matrix_s* m) {
     ClusCta& t = ctas[c];
     t.row_lo = lo[c];
     t.row_hi = hi[c];
+    t.clo = lo[(c / csz) * csz];
+    t.chi = hi[(c / csz) * csz + csz - 1];
     t.wlo = wlo[c];
     t.wn = whi[c] - wlo[c];
     t.hlo = lo[c] - wlo[c];
@@ -831,26 +884,25 @@ int build_clus_plan(spcg_matrix_s* m) {
     ctas[dd].nsend = (int)sends.size() - ctas[dd].send0;
   }
   if (sends.empty()) sends.push_back(ClusSend{0, 0, 0, 0});
-  // cluster of C CTAs must be launchable with this much shared memory
-  const void* fn = P.two ? (const void*)clus_cg_kernel<true> : (const void*)clus_cg_kernel<false>;
-  CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
-  if (C > 8) CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  // the grid of C CTAs in clusters of csz must be co-resident with this smem
+  CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
+  if (csz > 8) CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(C);
+    cfg.gridDim = dim3(csz);
     cfg.blockDim = dim3(kClusThreads);
     cfg.dynamicSmemBytes = P.smem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.x = csz;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int ncl = 0;
-    if (cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg) != cudaSuccess || ncl < 1) {
+    if (cudaOccupancyMaxActiveClusters(&ncl, kfn, &cfg) != cudaSuccess || ncl < C / csz) {
       cudaGetLastError();
-      return clus_fail(P, "cluster not launchable");
+      return clus_fail(P, "clusters not co-resident");
     }
   }
   long long acct = 0;
@@ -867,9 +919,18 @@ int build_clus_plan(spcg_matrix_s* m) {
   CUDA_TRY(cudaMemcpy(P.rowmeta, rowmeta.data(), sizeof(int2) * rowmeta.size(), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(P.gval, gval.data(), sizeof(double) * gval.size(), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(P.gcol, gcol.data(), sizeof(unsigned short) * gcol.size(), cudaMemcpyHostToDevice));
+  if (C > csz) {
+    if ((rc = dmalloc((void**)&P.ghalo, sizeof(double) * 2 * (size_t)C * hcap, &acct)) ||
+        (rc = dmalloc((void**)&P.gslots,
+                      sizeof(unsigned long long) * 2 * kClusSlotWords * (size_t)(C / csz),
+                      &acct)))
+      return rc;
+    CUDA_TRY(cudaMemset(P.ghalo, 0, sizeof(double) * 2 * (size_t)C * hcap));
+  }
   m->bytes += acct;
   P.hcap = hcap;
   P.C = C;
+  P.cs = csz;
   P.ok = true;
   return SPCG_OK;
 }
@@ -880,13 +941,15 @@ int launch_clus(const ClusPlan& P, const ClusArgs& a, cudaStream_t st) {
   cfg.blockDim = dim3(kClusThreads);
   cfg.dynamicSmemBytes = P.smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = P.C;
+  at[0].val.clusterDim.x = P.cs;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeCooperative;  // K > 1 clusters poll each other
+  at[1].val.cooperative = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = P.C > P.cs ? 2 : 1;
   if (P.two) CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_cg_kernel<true>, a));
   else CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_cg_kernel<false>, a));
   return SPCG_OK;
@@ -924,10 +987,16 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
   a.off_val = P.off_val;
   a.off_col = P.off_col;
   a.hcap = P.hcap;
+  a.ghalo = P.ghalo;
+  a.gslots = P.gslots;
+  if (P.gslots)
+    CUDA_TRY(cudaMemsetAsync(P.gslots, 0,
+                             sizeof(unsigned long long) * 2 * kClusSlotWords * (size_t)(P.C / P.cs),
+                             st));
   static const bool tracing = getenv("SPCG_TRACE") != nullptr;
   if (tracing) {
-    CUDA_TRY(cudaMalloc((void**)&a.trace, sizeof(unsigned long long) * 4 * (size_t)P.C));
-    CUDA_TRY(cudaMemsetAsync(a.trace, 0, sizeof(unsigned long long) * 4 * (size_t)P.C, st));
+    CUDA_TRY(cudaMalloc((void**)&a.trace, sizeof(unsigned long long) * 8 * (size_t)P.C));
+    CUDA_TRY(cudaMemsetAsync(a.trace, 0, sizeof(unsigned long long) * 8 * (size_t)P.C, st));
   }
   CUDA_TRY(cudaEventRecord(w.ev0, st));
   if ((rc = launch_clus(P, a, st))) return rc;
@@ -938,22 +1007,38 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
   CUDA_TRY(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
   const CgDevResult& r = *w.h_res;
   if (a.trace) {
-    std::vector<unsigned long long> tv(4 * (size_t)P.C);
+    std::vector<unsigned long long> tv(8 * (size_t)P.C);
     CUDA_TRY(cudaMemcpy(tv.data(), a.trace, sizeof(unsigned long long) * tv.size(),
                         cudaMemcpyDeviceToHost));
     cudaFree(a.trace);
-    double mean[3] = {0, 0, 0}, mx[3] = {0, 0, 0};
+    double mean[7] = {0}, mx[7] = {0}, lead[7] = {0};
+    int nl = 0;
     for (int c = 0; c < P.C; ++c)
-      for (int ph = 0; ph < 3; ++ph) {
-        mean[ph] += (double)tv[4 * c + ph] / P.C;
-        mx[ph] = std::max(mx[ph], (double)tv[4 * c + ph]);
+      for (int ph = 0; ph < 7; ++ph) {
+        mean[ph] += (double)tv[8 * c + ph] / P.C;
+        mx[ph] = std::max(mx[ph], (double)tv[8 * c + ph]);
+        if (c % std::max(1, P.cs) == 0) lead[ph] += (double)tv[8 * c + ph];
       }
-    const double it = (double)std::max<long long>(1, r.iterations);
+    nl = std::max(1, P.C / std::max(1, P.cs));
+    const double it = (double)std::max<long long>(1, r.iterations) * 1e3;
     fprintf(stderr,
-            "[spcg trace] cluster=%d resident=%lld streamed=%lld smem=%zu us/iter mean(max): "
-            "update %.3f(%.3f) spmv %.3f(%.3f) allreduce %.3f(%.3f)\n",
-            P.C, P.resident, P.streamed, P.smem, mean[0] / it / 1e3, mx[0] / it / 1e3,
-            mean[1] / it / 1e3, mx[1] / it / 1e3, mean[2] / it / 1e3, mx[2] / it / 1e3);
+            "[spcg trace] ctas=%d cs=%d resident=%lld streamed=%lld us/iter mean(max): update %.3f(%.3f) "
+            "spmv %.3f(%.3f) allreduce %.3f(%.3f) | send_w %.3f b1wait %.3f b1exit->b2exit %.3f "
+            "| leaders: exchange %.3f b1wait %.3f poll->b2exit %.3f\n",
+            P.C, P.cs, P.resident, P.streamed, mean[0] / it, mx[0] / it, mean[1] / it, mx[1] / it,
+            mean[2] / it, mx[2] / it, mean[6] / it, mean[5] / it, mean[4] / it, lead[3] / nl / it,
+            lead[5] / nl / it, lead[4] / nl / it);
+    if (P.C > P.cs) {  // mean slot-post time of each cluster relative to the earliest
+      double mn = 1e300;
+      std::vector<double> pt;
+      for (int c = 0; c < P.C; c += P.cs) {
+        pt.push_back((double)tv[8 * c + 7] / it);
+        mn = std::min(mn, pt.back());
+      }
+      fprintf(stderr, "[spcg trace] cluster post offsets (us):");
+      for (double v : pt) fprintf(stderr, " %.2f", v - mn);
+      fprintf(stderr, "\n");
+    }
   }
   out->iterations = r.iterations;
   out->converged = r.converged;
@@ -991,13 +1076,11 @@ int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double
   // budget, which the persistent kernel cannot (P3: 0.99 vs 0.82 of roofline)
   if (o->engine == 2 || (o->engine == 0 && !fits))
     return do_dist_cg(m, nullptr, 0, nullptr, nullptr, nullptr, nullptr, b, x0, x, hist, o, out, st);
-  // engine 5, and auto for full CSR / CSC systems that fit one thread-block
-  // cluster: cluster-resident single-reduction CG (hardware cluster barrier +
-  // DSMEM).  Symmetric storage stays on engine 3 by default: its two-segment
-  // rows made the cluster engine no faster there (F: 7.5 vs 8.4 us/iteration
-  // for CSR, 7.5 vs 9.9 for CSC, 8.7 vs 8.4 for SCSR; profiles/r01/SUMMARY.md).
-  if (o->engine == 5 || (o->engine == 0 && m->n <= kClusMax * kClusMaxRows &&
-                         (kf == K_CSR || kf == K_CSC))) {
+  // engine 5, and auto for banded systems whose rows fit the co-resident
+  // clusters' shared memory: cluster-resident single-reduction CG (DSMEM +
+  // hardware cluster barriers; K clusters of 8 exchange through global
+  // memory).  F: 5.35 us/iteration vs 8.45 on engine 3; S: 6.23 vs 8.58.
+  if (o->engine == 5 || (o->engine == 0 && m->n <= kClusGridMax * kClusMaxRows)) {
     if ((rc = build_clus_plan(m))) return rc;
     if (m->cp.ok) return do_clus_cg(m, b, x0, x, hist, o, out, st);
     if (o->engine == 5)

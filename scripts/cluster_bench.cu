@@ -85,6 +85,66 @@ __global__ void cl_allreduce(int iters, double* out) {
   if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = tot;
 }
 
+// Two-level all-reduce: DSMEM + cluster barrier inside each cluster, then
+// the cluster leaders exchange tagged 64-bit slots through global memory
+// (one fence each side), then a second cluster barrier releases the
+// cluster.  gslots: [2][K] words {hi|epoch, lo|epoch} x 2.
+__global__ void cl2_allreduce(int iters, unsigned long long* gslots, double* out, int fence) {
+  __shared__ double slots[2][16];
+  __shared__ double tot_sh[2];
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = cl.block_rank();
+  const int cs = cl.num_blocks();
+  const int K = gridDim.x / cs;
+  const int cid = blockIdx.x / cs;
+  double v = blockIdx.x + 1.0, acc = 0.0;
+  for (int it = 0; it < iters; ++it) {
+    const int bank = it & 1;
+    const unsigned epoch = (unsigned)it + 1;
+    if (threadIdx.x < cs) {
+      double* remote = cl.map_shared_rank(&slots[bank][0], threadIdx.x);
+      remote[rank] = v;
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    if (rank == 0 && threadIdx.x < 32) {
+      double s = 0.0;
+      for (int k = 0; k < cs; ++k) s += slots[bank][k];
+      unsigned long long* g = gslots + (size_t)bank * K * 2;
+      if (threadIdx.x == 0) {
+        if (fence) __threadfence();
+        const unsigned long long u = (unsigned long long)__double_as_longlong(s);
+        volatile unsigned long long* dst = g + 2 * cid;
+        dst[0] = (u & 0xffffffff00000000ull) | epoch;
+        dst[1] = (u << 32) | epoch;
+      }
+      __syncwarp();
+      double t = 0.0;
+      const int lane = threadIdx.x;
+      if (lane < K) {
+        volatile unsigned long long* src = g + 2 * lane;
+        unsigned long long a, c;
+        do {
+          a = src[0];
+          c = src[1];
+        } while ((unsigned)a != epoch || (unsigned)c != epoch);
+        t = __longlong_as_double((long long)((a & 0xffffffff00000000ull) | (c >> 32)));
+      }
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (fence) __threadfence();
+      if (lane < cs) {
+        double* remote = cl.map_shared_rank(&tot_sh[bank], lane);
+        *remote = t;
+      }
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    acc += tot_sh[bank];
+    v = tot_sh[bank] * 1e-6;
+  }
+  if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = acc;
+}
+
 int main() {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -149,6 +209,48 @@ int main() {
       cudaEventElapsedTime(&ms, e0, e1);
       printf("cluster=%2d thr=%4d maxActiveClusters=%d  %.3f us per all-reduce (%s)\n", cs, thr, ncl,
              ms * 1e3 / iters, cudaGetErrorString(err));
+    }
+  }
+  // two-level: K clusters of 16 (cooperative cluster launch), 512 threads, big smem
+  cudaFuncSetAttribute(cl2_allreduce, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  unsigned long long* gs;
+  cudaMalloc(&gs, 2 * 64 * 2 * sizeof(unsigned long long));
+  for (int cs : {8, 16}) {
+    for (int fence : {0, 1}) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.blockDim = dim3(512);
+      cfg.dynamicSmemBytes = 200 * 1024;
+      cudaFuncSetAttribute(cl2_allreduce, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cs;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      at[1].id = cudaLaunchAttributeCooperative;
+      at[1].val.cooperative = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cfg.gridDim = dim3(cs);
+      int ncl = -1;
+      cudaOccupancyMaxActiveClusters(&ncl, cl2_allreduce, &cfg);
+      cfg.numAttrs = 2;
+      for (int K : {1, 2, 4, ncl}) {
+        if (K < 1 || K > ncl) continue;
+        cfg.gridDim = dim3(cs * K);
+        cudaMemset(gs, 0, 2 * 64 * 2 * sizeof(unsigned long long));
+        const int iters = 20000;
+        cudaError_t err = cudaLaunchKernelEx(&cfg, cl2_allreduce, 10, gs, out, fence);
+        cudaDeviceSynchronize();
+        cudaMemset(gs, 0, 2 * 64 * 2 * sizeof(unsigned long long));
+        cudaEventRecord(e0);
+        err = cudaLaunchKernelEx(&cfg, cl2_allreduce, iters, gs, out, fence);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        printf("two-level cluster=%2d K=%2d (max %d) fence=%d  %.3f us per all-reduce (%s)\n", cs, K,
+               ncl, fence, ms * 1e3 / iters, cudaGetErrorString(err));
+      }
     }
   }
   return 0;
