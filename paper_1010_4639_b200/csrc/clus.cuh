@@ -47,14 +47,8 @@ constexpr int kClusMaxRows = kClusWarps * kClusSlicesPerWarp * 32;  // 2048 per 
 constexpr int kClusMax = 16;      // CTAs in one cluster (non-portable above 8)
 constexpr int kClusGridMax = 256;  // CTAs of a multi-cluster grid (K clusters of 8)
 constexpr int kClusSlotWords = 32;  // 256-byte global slot per cluster (own L2 line pair)
-#ifndef SPCG_CLUS_POLL_NS
-#define SPCG_CLUS_POLL_NS 0  // any __nanosleep back-off costs microseconds here
-#endif
-#ifndef SPCG_CLUS_VOLATILE
-#define SPCG_CLUS_VOLATILE 1  // volatile scalar slot accesses (relaxed v2 polls were 3x slower in situ)
-#endif
-#ifndef SPCG_CLUS_ACQ_LD
-#define SPCG_CLUS_ACQ_LD 0  // poll with ld.acquire instead of relaxed loads + fence
+#ifndef SPCG_CLUS_ALLPOLL
+#define SPCG_CLUS_ALLPOLL 0  // 1: every CTA polls the cluster slots (2.3x slower: contention)
 #endif
 
 struct ClusCta {
@@ -101,10 +95,13 @@ struct ClusArgs {
   unsigned long long* gslots; // K > 1: [2][K][4] epoch-tagged cluster partials (zeroed)
 };
 
+constexpr int kClusSendCache = 8;  // send descriptors staged in shared memory
+
 struct ClusShared {  // static part
   double slot[2][kClusMax][2];
   double red[2][kClusWarps];
   double tot[2][2];  // K > 1: grid totals broadcast by the cluster leader
+  ClusSend send[kClusSendCache];
 };
 
 __device__ __forceinline__ void cluster_sync_all() {
@@ -187,6 +184,7 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
       scol[sd.soff + e] = A.gcol[sd.goff + e];
     }
   }
+  if (tid < min(P.nsend, kClusSendCache)) cs.send[tid] = A.sends[P.send0 + tid];
   // this thread's row slots
   int rrow[kClusSlicesPerWarp], rlen[kClusSlicesPerWarp], rlenA[kClusSlicesPerWarp];
   int swidth[kClusSlicesPerWarp], sbase[kClusSlicesPerWarp];
@@ -265,69 +263,49 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
       t1 += cs.slot[bank][c][1];
     }
     if (K > 1) {
-      // second level: cluster leaders exchange epoch-tagged partials through
-      // global memory (one fence each side; the cluster barrier before made
-      // the cluster's global halo stores part of the leader's release), then
-      // broadcast the grid totals into their cluster and barrier again
+      // second level through global memory: the cluster leader posts the
+      // cluster's partials in its own 256-byte slot as epoch-tagged 64-bit
+      // words (volatile scalar accesses; one fence before the post — the
+      // cluster barrier above made the cluster's global halo stores part of
+      // it — and one after the poll).  ALLPOLL: every CTA polls the K slots
+      // itself; otherwise the leader polls and broadcasts over DSMEM behind a
+      // second cluster barrier.  Sums run in cluster order in every CTA.
       const uint32_t tag = epoch;  // identical sequence in every CTA, never 0
+      unsigned long long* gb = A.gslots + (size_t)bank * K * kClusSlotWords;
 #if SPCG_TRACE
       unsigned long long ta = (A.trace && tid == 0) ? globaltimer_ns() : 0;
 #endif
-      if (me == 0 && wp == 0) {
-        unsigned long long* gb = A.gslots + (size_t)bank * K * kClusSlotWords;
-        if (lane == 0) {
-#if !SPCG_CLUS_NO_WFENCE
-          fence_acq_rel_gpu();
-#endif
-          const unsigned long long u0 = (unsigned long long)__double_as_longlong(t0);
-          const unsigned long long u1 = (unsigned long long)__double_as_longlong(t1);
+      if (me == 0 && tid == 0) {
+        fence_acq_rel_gpu();
+        const unsigned long long u0 = (unsigned long long)__double_as_longlong(t0);
+        const unsigned long long u1 = (unsigned long long)__double_as_longlong(t1);
 #if SPCG_TRACE
-          if (A.trace) tpost += globaltimer_ns() - tstart;
+        if (A.trace) tpost += globaltimer_ns() - tstart;
 #endif
-#if SPCG_CLUS_VOLATILE
-          volatile unsigned long long* dstv = gb + kClusSlotWords * kc;
-          dstv[0] = (u0 & 0xffffffff00000000ull) | tag;
-          dstv[1] = (u0 << 32) | tag;
-          dstv[2] = (u1 & 0xffffffff00000000ull) | tag;
-          dstv[3] = (u1 << 32) | tag;
-#else
-          st_relaxed_v2_u64(gb + kClusSlotWords * kc, (u0 & 0xffffffff00000000ull) | tag,
-                            (u0 << 32) | tag);
-          st_relaxed_v2_u64(gb + kClusSlotWords * kc + 2, (u1 & 0xffffffff00000000ull) | tag,
-                            (u1 << 32) | tag);
-#endif
-        }
+        volatile unsigned long long* dst = gb + kClusSlotWords * kc;
+        dst[0] = (u0 & 0xffffffff00000000ull) | tag;
+        dst[1] = (u0 << 32) | tag;
+        dst[2] = (u1 & 0xffffffff00000000ull) | tag;
+        dst[3] = (u1 << 32) | tag;
+      }
+      if ((SPCG_CLUS_ALLPOLL || me == 0) && wp == 0) {
         double c0 = 0.0, c1 = 0.0;
         if (lane < K) {
-          unsigned long long a, b, c, d;
-          unsigned long long spins = 0;
+          const volatile unsigned long long* src = gb + kClusSlotWords * lane;
+          unsigned long long a, b, c, d, spins = 0;
           for (;;) {
-#if SPCG_CLUS_VOLATILE
-            {
-              volatile unsigned long long* srcv = gb + kClusSlotWords * lane;
-              a = srcv[0];
-              b = srcv[1];
-              c = srcv[2];
-              d = srcv[3];
-            }
-#elif SPCG_CLUS_ACQ_LD
-            ld_acquire_v2_u64(gb + kClusSlotWords * lane, a, b);
-            ld_acquire_v2_u64(gb + kClusSlotWords * lane + 2, c, d);
-#else
-            ld_relaxed_v2_u64(gb + kClusSlotWords * lane, a, b);
-            ld_relaxed_v2_u64(gb + kClusSlotWords * lane + 2, c, d);
-#endif
+            a = src[0];
+            b = src[1];
+            c = src[2];
+            d = src[3];
             if ((uint32_t)a == tag && (uint32_t)b == tag && (uint32_t)c == tag && (uint32_t)d == tag)
               break;
             if (++spins > kSpinLimit) asm volatile("trap;");
-            if (SPCG_CLUS_POLL_NS) __nanosleep(SPCG_CLUS_POLL_NS);
           }
           c0 = __longlong_as_double((long long)((a & 0xffffffff00000000ull) | (b >> 32)));
           c1 = __longlong_as_double((long long)((c & 0xffffffff00000000ull) | (d >> 32)));
         }
-#if !SPCG_CLUS_ACQ_LD && !SPCG_CLUS_NO_RFENCE
         fence_acq_rel_gpu();
-#endif
 #if SPCG_TRACE
         if (A.trace && tid == 0) {
           const unsigned long long tb = globaltimer_ns();
@@ -340,13 +318,19 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
           s0 += __shfl_sync(0xffffffffu, c0, k);
           s1 += __shfl_sync(0xffffffffu, c1, k);
         }
-        if (lane < C) {
-          double* dst = cl.map_shared_rank(&cs.tot[bank][0], lane);
-          dst[0] = s0;
-          dst[1] = s1;
+        if (SPCG_CLUS_ALLPOLL) {
+          if (lane == 0) {
+            cs.tot[bank][0] = s0;
+            cs.tot[bank][1] = s1;
+          }
+        } else if (lane < C) {
+          double* d2 = cl.map_shared_rank(&cs.tot[bank][0], lane);
+          d2[0] = s0;
+          d2[1] = s1;
         }
       }
-      cluster_sync_all();
+      if (SPCG_CLUS_ALLPOLL) __syncthreads();
+      else cluster_sync_all();
 #if SPCG_TRACE
       if (A.trace && tid == 0) tlv[1] += globaltimer_ns() - ta;
 #endif
@@ -359,7 +343,7 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
   // boundary w of this CTA -> the halo buffers of the CTAs that gather it
   auto send_w = [&](int buf) {
     for (int e = 0; e < P.nsend; ++e) {
-      const ClusSend sd = A.sends[P.send0 + e];
+      const ClusSend sd = e < kClusSendCache ? cs.send[e] : A.sends[P.send0 + e];
       double* dst = (sd.dst / C == kc)
                         ? cl.map_shared_rank(whalo + (size_t)buf * A.hcap, sd.dst % C)
                         : A.ghalo + ((size_t)buf * G + sd.dst) * A.hcap;
@@ -370,6 +354,14 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
   };
   // window index of halo index h
   auto halo_win = [&](int h) { return h < P.hlo ? h : own0 + (P.row_hi - P.row_lo) + (h - P.hlo); };
+  // w of halo index h from buffer buf: DSMEM-delivered (same cluster) or
+  // global (other cluster, L2 only)
+  auto halo_w = [&](int buf, int h) {
+    const int hrow = h < P.hlo ? P.wlo + h : P.row_hi + (h - P.hlo);
+    return (hrow >= P.clo && hrow < P.chi) ? whalo[(size_t)buf * A.hcap + h]
+                                           : __ldcg(A.ghalo + ((size_t)buf * G + gme) * A.hcap + h);
+  };
+  double wpre = 0.0;  // halo w of h = tid for the next update, loaded right after the barrier
 
   // ||b||
   double part = 0.0, dummy = 0.0;
@@ -446,6 +438,7 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
       if (rrow[k] >= 0) part += rg[k] * wg[k];
     send_w(0);
     allreduce2(part, dummy);
+    if (tid < nhalo) wpre = halo_w(0, tid);
     const double d0 = part;
     if (d0 <= 0.0) {
       status = ST_NOT_SPD;
@@ -485,11 +478,8 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
         rg[k] = mul_add_rn(rg[k], na, sg[k]);
         rwin[own0 + rrow[k] - P.row_lo] = rg[k];
       }
-    const double* wh = whalo + (size_t)rb * A.hcap;
-    const double* wg_glob = A.ghalo + ((size_t)rb * G + gme) * A.hcap;
     for (int h = tid; h < nhalo; h += kClusThreads) {
-      const int hrow = h < P.hlo ? P.wlo + h : P.row_hi + (h - P.hlo);
-      const double wv = (hrow >= P.clo && hrow < P.chi) ? wh[h] : __ldcg(wg_glob + h);
+      const double wv = h == tid ? wpre : halo_w(rb, h);
       const double sh = mul_add_rn(wv, beta, shalo[h]);
       shalo[h] = sh;
       const int j = halo_win(h);
@@ -514,6 +504,7 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
     if (A.trace && tid == 0) tlv[3] += globaltimer_ns() - ts0;
 #endif
     allreduce2(g_new, d_new);
+    if (tid < nhalo) wpre = halo_w(wb, tid);  // in flight during the scalar updates
     mark(2);
     const long long kk = it + 1;  // reference iteration number
     rel = sqrt(g_new) / b_norm;
