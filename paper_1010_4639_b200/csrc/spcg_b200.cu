@@ -1082,7 +1082,10 @@ int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double
   // memory).  F: 5.35 us/iteration vs 8.45 on engine 3; S: 6.23 vs 8.58.
   if (o->engine == 5 || (o->engine == 0 && m->n <= kClusGridMax * kClusMaxRows)) {
     if ((rc = build_clus_plan(m))) return rc;
-    if (m->cp.ok) return do_clus_cg(m, b, x0, x, hist, o, out, st);
+    // auto only when (nearly) everything stays in shared memory: streamed
+    // slices are re-read from L2 every iteration at L2 latency
+    const bool resident = m->cp.streamed * 9 <= m->cp.resident;
+    if (m->cp.ok && (o->engine == 5 || resident)) return do_clus_cg(m, b, x0, x, hist, o, out, st);
     if (o->engine == 5)
       return fail(SPCG_ERR_UNSUPPORTED, "cluster engine not applicable: " + m->cp.why);
   }
