@@ -54,7 +54,8 @@ enum : int {
   ST_NOT_SPD = 3,
   ST_NF_ALPHA = 4,
   ST_NF_RES = 5,
-  ST_NF_BETA = 6
+  ST_NF_BETA = 6,
+  ST_BAD_LAUNCH = 100  // cluster engine launched with another cluster shape
 };
 
 // Grid-wide all-reduce + barrier.  Each CTA publishes its fixed-order block

@@ -47,6 +47,9 @@ constexpr int kClusMaxRows = kClusWarps * kClusSlicesPerWarp * 32;  // 2048 per 
 constexpr int kClusMax = 16;      // CTAs in one cluster (non-portable above 8)
 constexpr int kClusGridMax = 256;  // CTAs of a multi-cluster grid (K clusters of 8)
 constexpr int kClusSlotWords = 32;  // 256-byte global slot per cluster (own L2 line pair)
+#ifndef SPCG_CLUS_WRITER_FENCE
+#define SPCG_CLUS_WRITER_FENCE 0  // 1: writers fence their own inter-cluster stores (+0.5 us)
+#endif
 #ifndef SPCG_CLUS_ALLPOLL
 #define SPCG_CLUS_ALLPOLL 0  // 1: every CTA polls the cluster slots (2.3x slower: contention)
 #endif
@@ -93,6 +96,7 @@ struct ClusArgs {
   unsigned long long* trace;  // nullable (SPCG_TRACE builds): [G][4] ns
   double* ghalo;              // K > 1: [2][G][hcap] halo w between clusters
   unsigned long long* gslots; // K > 1: [2][K][4] epoch-tagged cluster partials (zeroed)
+  int cluster_size;           // the plan's cluster size (checked against the launch)
 };
 
 constexpr int kClusSendCache = 8;  // send descriptors staged in shared memory
@@ -163,6 +167,17 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
   const int K = G / C;
   const int kc = (int)blockIdx.x / C;    // this CTA's cluster
   const int gme = (int)blockIdx.x;
+  if (C != A.cluster_size) {  // launched without the plan's cluster shape: refuse
+    if (gme == 0 && threadIdx.x == 0) {
+      A.res->iterations = 0;
+      A.res->fail_iter = 0;
+      A.res->converged = 0;
+      A.res->status = ST_BAD_LAUNCH;
+      A.res->final_rel = 0.0;
+      A.res->b_norm = 0.0;
+    }
+    return;
+  }
   const ClusCta P = A.ctas[gme];
   double* rwin = reinterpret_cast<double*>(smem_raw + A.off_rwin);
   double* shalo = reinterpret_cast<double*>(smem_raw + A.off_shalo);
@@ -342,15 +357,24 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
   };
   // boundary w of this CTA -> the halo buffers of the CTAs that gather it
   auto send_w = [&](int buf) {
+    bool global = false;
     for (int e = 0; e < P.nsend; ++e) {
       const ClusSend sd = e < kClusSendCache ? cs.send[e] : A.sends[P.send0 + e];
-      double* dst = (sd.dst / C == kc)
-                        ? cl.map_shared_rank(whalo + (size_t)buf * A.hcap, sd.dst % C)
-                        : A.ghalo + ((size_t)buf * G + sd.dst) * A.hcap;
+      const bool remote_cluster = sd.dst / C != kc;
+      double* dst = remote_cluster ? A.ghalo + ((size_t)buf * G + sd.dst) * A.hcap
+                                   : cl.map_shared_rank(whalo + (size_t)buf * A.hcap, sd.dst % C);
 #pragma unroll
       for (int k = 0; k < kClusSlicesPerWarp; ++k)
-        if (rrow[k] >= sd.lo && rrow[k] < sd.hi) dst[sd.dst_off + rrow[k] - sd.lo] = wg[k];
+        if (rrow[k] >= sd.lo && rrow[k] < sd.hi) {
+          dst[sd.dst_off + rrow[k] - sd.lo] = wg[k];
+          global |= remote_cluster;
+        }
     }
+#if SPCG_CLUS_WRITER_FENCE
+    // the writer's own gpu-scope fence: inter-cluster halo values must not
+    // rely on the cluster barrier's release being cumulative at gpu scope
+    if (global) fence_acq_rel_gpu();
+#endif
   };
   // window index of halo index h
   auto halo_win = [&](int h) { return h < P.hlo ? h : own0 + (P.row_hi - P.row_lo) + (h - P.hlo); };
@@ -414,6 +438,7 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
       A.scratch[rrow[k]] = rg[k];
       part = fma(rg[k], rg[k], part);
     }
+  if (SPCG_CLUS_WRITER_FENCE && K > 1) fence_acq_rel_gpu();
   allreduce2(part, dummy);  // release/acquire at cluster scope covers scratch
   double gam = part;
   for (int j = tid; j < P.wn; j += kClusThreads) rwin[j] = __ldcg(A.scratch + P.wlo + j);
@@ -565,6 +590,7 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
 #pragma unroll
   for (int k = 0; k < kClusSlicesPerWarp; ++k)
     if (rrow[k] >= 0) A.x[rrow[k]] = xr[k];
+  if (SPCG_CLUS_WRITER_FENCE && K > 1) fence_acq_rel_gpu();
   if (A.recompute) {  // true residual ||b - A x|| / ||b||
     part = 0.0;
     dummy = 0.0;

@@ -705,8 +705,8 @@ int build_clus_plan(spcg_matrix_s* m) {
   };
   int C, csz;
   static const int force_k = getenv("SPCG_CLUS_K") ? atoi(getenv("SPCG_CLUS_K")) : 0;  // dev A/B
-  if (want <= kClusMax && force_k <= 1) {
-    C = csz = (int)std::max<long long>(1, want);
+  if ((want <= kClusMax && force_k <= 1) || force_k == 1) {
+    C = csz = (int)std::min<long long>(kClusMax, std::max<long long>(1, want));
     if (max_clusters(csz) < 1) return clus_fail(P, "cluster not launchable");
   } else {
     csz = 8;
@@ -949,7 +949,11 @@ int launch_clus(const ClusPlan& P, const ClusArgs& a, cudaStream_t st) {
   at[1].id = cudaLaunchAttributeCooperative;  // K > 1 clusters poll each other
   at[1].val.cooperative = 1;
   cfg.attrs = at;
-  cfg.numAttrs = P.C > P.cs ? 2 : 1;
+  // SPCG_CLUS_NONCOOP=1 (profiling only): ncu drops the cluster shape of a
+  // cooperative cluster launch; the K clusters still fit on the device at
+  // once, and the kernel refuses a launch whose cluster size is not the plan's
+  static const bool noncoop = getenv("SPCG_CLUS_NONCOOP") != nullptr;
+  cfg.numAttrs = (P.C > P.cs && !noncoop) ? 2 : 1;
   if (P.two) CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_cg_kernel<true>, a));
   else CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_cg_kernel<false>, a));
   return SPCG_OK;
@@ -989,6 +993,7 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
   a.hcap = P.hcap;
   a.ghalo = P.ghalo;
   a.gslots = P.gslots;
+  a.cluster_size = P.cs;
   if (P.gslots)
     CUDA_TRY(cudaMemsetAsync(P.gslots, 0,
                              sizeof(unsigned long long) * 2 * kClusSlotWords * (size_t)(P.C / P.cs),
@@ -1006,6 +1011,9 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
   float ms = 0.f;
   CUDA_TRY(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
   const CgDevResult& r = *w.h_res;
+  if (r.status == ST_BAD_LAUNCH)
+    return fail(SPCG_ERR_CUDA, "cluster engine: kernel ran with a different cluster shape than "
+                               "planned (cluster launch attribute not honoured)");
   if (a.trace) {
     std::vector<unsigned long long> tv(8 * (size_t)P.C);
     CUDA_TRY(cudaMemcpy(tv.data(), a.trace, sizeof(unsigned long long) * tv.size(),
