@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kBlock, 2)
 // Mode 2 moves 16-byte pairs, two in flight per thread (r, q 16-B aligned).
 __global__ void __launch_bounds__(kBlock) dist_elem(int mode, long long nloc, StepState* S,
                                                    const double* b, double* q, double* r,
-                                                   double* p, double* part, int zq) {
+                                                   double* p, double* part, int zq, int rev = 0) {
   __shared__ RedSmem sm;
   if (mode == 2 && S->done) return;
   const double alpha = S->alpha;
@@ -143,14 +143,15 @@ __global__ void __launch_bounds__(kBlock) dist_elem(int mode, long long nloc, St
     double2* r2 = reinterpret_cast<double2*>(r);
     long long i = g;
     for (; i + G < np; i += 2 * G) {
-      const double2 qa = q2[i], qb = q2[i + G], ra = r2[i], rb = r2[i + G];
+      const long long ia = rev ? np - 1 - i : i, ib = rev ? np - 1 - (i + G) : i + G;
+      const double2 qa = q2[ia], qb = q2[ib], ra = r2[ia], rb = r2[ib];
       const double2 oa = make_double2(mul_add_rn(ra.x, na, qa.x), mul_add_rn(ra.y, na, qa.y));
       const double2 ob = make_double2(mul_add_rn(rb.x, na, qb.x), mul_add_rn(rb.y, na, qb.y));
-      r2[i] = oa;
-      r2[i + G] = ob;
+      r2[ia] = oa;
+      r2[ib] = ob;
       if (zq) {
-        reinterpret_cast<double2*>(q)[i] = make_double2(0.0, 0.0);
-        reinterpret_cast<double2*>(q)[i + G] = make_double2(0.0, 0.0);
+        reinterpret_cast<double2*>(q)[ia] = make_double2(0.0, 0.0);
+        reinterpret_cast<double2*>(q)[ib] = make_double2(0.0, 0.0);
       }
       acc = fma(oa.x, oa.x, acc);
       acc = fma(oa.y, oa.y, acc);
@@ -158,10 +159,11 @@ __global__ void __launch_bounds__(kBlock) dist_elem(int mode, long long nloc, St
       acc = fma(ob.y, ob.y, acc);
     }
     if (i < np) {
-      const double2 qa = q2[i], ra = r2[i];
+      const long long ia = rev ? np - 1 - i : i;
+      const double2 qa = q2[ia], ra = r2[ia];
       const double2 oa = make_double2(mul_add_rn(ra.x, na, qa.x), mul_add_rn(ra.y, na, qa.y));
-      r2[i] = oa;
-      if (zq) reinterpret_cast<double2*>(q)[i] = make_double2(0.0, 0.0);
+      r2[ia] = oa;
+      if (zq) reinterpret_cast<double2*>(q)[ia] = make_double2(0.0, 0.0);
       acc = fma(oa.x, oa.x, acc);
       acc = fma(oa.y, oa.y, acc);
     }
@@ -194,7 +196,7 @@ __global__ void __launch_bounds__(kBlock) dist_elem(int mode, long long nloc, St
 // converged nor failed (a converged solve applies its last x update at the
 // end; an exhausted max_iter runs its pass C).  xv: x is 16-byte aligned.
 __global__ void __launch_bounds__(kBlock) dist_update(long long nloc, StepState* S, const double* r,
-                                                     double* p, double* x, int xv) {
+                                                     double* p, double* x, int xv, int rev = 0) {
   if (S->status != 0 || S->converged || S->kc >= S->k) return;
   const double alpha = S->alpha, beta = S->beta;
   const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -202,7 +204,8 @@ __global__ void __launch_bounds__(kBlock) dist_update(long long nloc, StepState*
   const long long np = nloc >> 1;
   const double2* r2 = reinterpret_cast<const double2*>(r);
   double2* p2 = reinterpret_cast<double2*>(p);
-  for (long long i = g; i < np; i += G) {
+  for (long long j = g; j < np; j += G) {
+    const long long i = rev ? np - 1 - j : j;
     const double2 pv = p2[i], rv = r2[i];
     if (xv) {
       double2* x2 = reinterpret_cast<double2*>(x);

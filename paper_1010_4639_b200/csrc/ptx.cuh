@@ -63,6 +63,26 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Same with an L2 evict-first policy: streamed matrix bytes should not push
+// the (reused) vectors out of L2.
+#ifndef SPCG_MAT_EVICT_FIRST
+#define SPCG_MAT_EVICT_FIRST 1
+#endif
+__device__ __forceinline__ void bulk_g2s_stream(void* dst, const void* src, uint32_t bytes,
+                                                uint64_t* bar) {
+#if SPCG_MAT_EVICT_FIRST
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
+      "%2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+#else
+  bulk_g2s(dst, src, bytes, bar);
+#endif
+}
+
 // L2 prefetch of a contiguous global range (bulk, no registers, no completion).
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");

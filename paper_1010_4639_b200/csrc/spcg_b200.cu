@@ -1614,19 +1614,30 @@ int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const dou
     for (int a = 0; a < 2; ++a)
       for (int c = 0; c < chunk; ++c) CUDA_TRY(cudaEventCreate(&d.tev[a][c]));
   double spmv_ms = 0.0;
-  long long spmv_n = 0, k_before = 0;
+  long long spmv_n = 0, k_before = 0, iter_enq = 0;
+#ifndef SPCG_ALTERNATE
+#define SPCG_ALTERNATE 1
+#endif
+  constexpr bool kAlternate = SPCG_ALTERNATE != 0;
   for (;;) {
     for (int c = 0; c < chunk; ++c) {
       if (timing) CUDA_TRY(cudaEventRecord(d.tev[0][c], st));
-      dist_spmv_pq<FMT><<<G, kBlock, sm, st>>>(v, d.S, p, d.q, d.part);
+      // alternate traversal directions pass to pass (A, B, C, A, ...): each
+      // pass starts on the lines the previous one wrote last (still in L2)
+      const int dirA = kAlternate ? (int)((iter_enq & 1) == 0) : 0;
+      MatView va = v;
+      va.rev = dirA;
+      dist_spmv_pq<FMT><<<G, kBlock, sm, st>>>(va, d.S, p, d.q, d.part);
       if (timing) CUDA_TRY(cudaEventRecord(d.tev[1][c], st));
       if ((rc = allreduce_red(H, d.S, st))) return rc;
       if (kRev && (rc = reverse_halo(H, d, d.q, nhalo, st, &launches))) return rc;
       dist_scalar<<<1, 1, 0, st>>>(2, d.S, hist);
-      dist_elem<<<GE, kBlock, 0, st>>>(2, nloc, d.S, nullptr, d.q, r, nullptr, d.part, kAtom);
+      dist_elem<<<GE, kBlock, 0, st>>>(2, nloc, d.S, nullptr, d.q, r, nullptr, d.part, kAtom,
+                                       kAlternate ? 1 - dirA : 0);
       if ((rc = allreduce_red(H, d.S, st))) return rc;
       dist_scalar<<<1, 1, 0, st>>>(3, d.S, hist);
-      dist_update<<<GE, kBlock, 0, st>>>(nloc, d.S, r, p, x, xv);
+      dist_update<<<GE, kBlock, 0, st>>>(nloc, d.S, r, p, x, xv, dirA);
+      ++iter_enq;
       launches += 5;
       if ((rc = halo_exchange(H, d, p, p, st, &launches))) return rc;
     }

@@ -59,6 +59,8 @@ struct MatView {
   const int* idxB;
   const double* valB;
   const int2* twin;      // per tile: new gathered columns [lo,hi] vs the previous tile
+  int rev;               // visit tiles last-to-first (per-pass engine: alternate passes
+                         // start where the previous one ended, on its L2-resident lines)
 };
 
 struct StageMeta {
@@ -81,7 +83,10 @@ struct __align__(16) Smem {
   double bcast;
 };
 
-__device__ __forceinline__ int my_tile(int j) { return blockIdx.x + j * gridDim.x; }
+__device__ __forceinline__ int my_tile(const MatView& M, int j) {
+  const int t = blockIdx.x + j * gridDim.x;
+  return M.rev ? M.ntiles - 1 - t : t;
+}
 __device__ __forceinline__ int my_tile_count(int ntiles) {
   return (ntiles > (int)blockIdx.x) ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 }
@@ -156,12 +161,12 @@ __device__ __forceinline__ void issue_tile_desc(Smem& sm, const MatView& M, cons
   bulk_g2s(sm.rpA[s], M.ptrA + r0a, (uint32_t)rcnt * 4u, &sm.full[s]);
   if (TWO) bulk_g2s(sm.rpB[s], M.ptrB + r0a, (uint32_t)rcnt * 4u, &sm.full[s]);
   if (cA > 0) {
-    bulk_g2s(sm.idx[s], M.idxA + kA0a, (uint32_t)cA * 4u, &sm.full[s]);
-    bulk_g2s(sm.val[s], M.valA + kA0a, (uint32_t)cA * 8u, &sm.full[s]);
+    bulk_g2s_stream(sm.idx[s], M.idxA + kA0a, (uint32_t)cA * 4u, &sm.full[s]);
+    bulk_g2s_stream(sm.val[s], M.valA + kA0a, (uint32_t)cA * 8u, &sm.full[s]);
   }
   if (TWO && cB > 0) {
-    bulk_g2s(sm.idx[s] + cA, M.idxB + kB0a, (uint32_t)cB * 4u, &sm.full[s]);
-    bulk_g2s(sm.val[s] + cA, M.valB + kB0a, (uint32_t)cB * 8u, &sm.full[s]);
+    bulk_g2s_stream(sm.idx[s] + cA, M.idxB + kB0a, (uint32_t)cB * 4u, &sm.full[s]);
+    bulk_g2s_stream(sm.val[s] + cA, M.valB + kB0a, (uint32_t)cB * 8u, &sm.full[s]);
   }
 }
 
@@ -202,8 +207,8 @@ __device__ __forceinline__ void pipe_start(Pipe& P, Smem& sm, const MatView& M,
 #endif
   if (threadIdx.x == 0 && P.m > 0) {
     const int pre = P.resident ? P.m : kStages;
-    for (int j = 0; j < pre; ++j) issue_tile<TWO>(sm, M, my_tile(j % P.m), j);
-    if (!P.resident) P.next = load_desc<TWO>(M, my_tile(kStages % P.m));
+    for (int j = 0; j < pre; ++j) issue_tile<TWO>(sm, M, my_tile(M, j % P.m), j);
+    if (!P.resident) P.next = load_desc<TWO>(M, my_tile(M, kStages % P.m));
   }
 }
 
@@ -233,7 +238,7 @@ __device__ __forceinline__ void pipe_release(Pipe& P, Smem& sm, const MatView& M
   __syncthreads();
   if (threadIdx.x == 0) {
     issue_tile_desc<TWO>(sm, M, P.next, s, &P.pf);
-    P.next = load_desc<TWO>(M, my_tile((int)((P.c + kStages + 1) % P.m)));
+    P.next = load_desc<TWO>(M, my_tile(M, (int)((P.c + kStages + 1) % P.m)));
   }
   P.c++;
 }
