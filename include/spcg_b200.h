@@ -174,6 +174,21 @@ int spcg_comm_unique_id(unsigned char* out_id);
 int spcg_comm_create(int nranks, int rank, const unsigned char* id, spcg_comm_t* out);
 int spcg_comm_destroy(spcg_comm_t comm);
 
+/* Host-callback communicator (no NCCL): the engine stages its collectives
+ * through host memory and calls back into the host framework -- the same
+ * sharded kernels over another transport (tests run two ranks as two
+ * processes on ONE GPU over torch.distributed/gloo this way).  allreduce:
+ * in-place sum of n doubles over all ranks.  sendrecv: for peer k send
+ * send[send_off[k] .. send_off[k+1]) and receive recv[recv_off[k] ..
+ * recv_off[k+1]).  Callbacks return 0 on success; they run on the calling
+ * thread, after the stream has been synchronised. */
+typedef int (*spcg_host_allreduce_fn)(double* buf, int64_t n, void* user);
+typedef int (*spcg_host_sendrecv_fn)(int npeers, const int32_t* peers, const double* send,
+                                     const int64_t* send_off, double* recv,
+                                     const int64_t* recv_off, void* user);
+int spcg_comm_create_host(int nranks, int rank, spcg_host_allreduce_fn allreduce,
+                          spcg_host_sendrecv_fn sendrecv, void* user, spcg_comm_t* out);
+
 /* Rows [row0,row1) of an n_global-row matrix, GLOBAL column ids (int64 host
  * arrays; ptr may be a slice of a global offsets array).  SCSR: A = the L+D
  * rows, B = the same rows of L^T (strict upper), needed for sharded solves. */

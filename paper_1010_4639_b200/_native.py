@@ -95,6 +95,7 @@ SIGNATURES = {
     "spcg_comm_unique_id": (_i32, [_vp]),
     "spcg_comm_create": (_i32, [_i32, _i32, _vp, ctypes.POINTER(_vp)]),
     "spcg_comm_destroy": (_i32, [_vp]),
+    "spcg_comm_create_host": (_i32, [_i32, _i32, _vp, _vp, _vp, ctypes.POINTER(_vp)]),
     "spcg_matrix_create_rows": (
         _i32,
         [_i32, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, ctypes.POINTER(_vp)],
@@ -179,3 +180,12 @@ def current_stream() -> int:
     except Exception:  # pragma: no cover - torch is plumbing only
         pass
     return 0
+
+
+# Host-callback communicator (spcg_comm_create_host)
+HOST_ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.POINTER(ctypes.c_double), ctypes.c_int64,
+                                     ctypes.c_void_p)
+HOST_SENDRECV_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+                                    ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64),
+                                    ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64),
+                                    ctypes.c_void_p)

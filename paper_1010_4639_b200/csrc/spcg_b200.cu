@@ -237,6 +237,11 @@ struct spcg_matrix_s {
 struct spcg_comm_s {
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
+  // host-callback transport (spcg_comm_create_host): data staged through
+  // host memory, collectives done by the caller's framework
+  spcg_host_allreduce_fn host_ar = nullptr;
+  spcg_host_sendrecv_fn host_sr = nullptr;
+  void* host_user = nullptr;
 };
 
 namespace {
@@ -1485,6 +1490,7 @@ int ensure_dist_ws(spcg_matrix_s* m, long long send_total) {
 
 struct HaloPlan {
   ncclComm_t comm = nullptr;
+  const spcg_comm_s* hc = nullptr;  // host-callback transport when set
   int npeers = 0;
   const int32_t* peers = nullptr;
   const int64_t* recv_off = nullptr;
@@ -1493,6 +1499,20 @@ struct HaloPlan {
 };
 
 // Pack v at the send rows, then exchange into dst_ext's halo.
+// Host-callback transport: stage the send buffer, exchange through the
+// caller's sendrecv, upload the received halo.  Synchronous (bring-up/tests).
+int host_sendrecv(const HaloPlan& H, const double* d_send, double* d_recv, const int64_t* soff,
+                  const int64_t* roff, cudaStream_t st) {
+  const long long sn = soff[H.npeers], rn = roff[H.npeers];
+  std::vector<double> hs((size_t)std::max(1LL, sn)), hr((size_t)std::max(1LL, rn));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (sn) CUDA_TRY(cudaMemcpy(hs.data(), d_send, sizeof(double) * (size_t)sn, cudaMemcpyDeviceToHost));
+  if (H.hc->host_sr(H.npeers, H.peers, hs.data(), soff, hr.data(), roff, H.hc->host_user) != 0)
+    return fail(SPCG_ERR_CUDA, "host sendrecv callback failed");
+  if (rn) CUDA_TRY(cudaMemcpy(d_recv, hr.data(), sizeof(double) * (size_t)rn, cudaMemcpyHostToDevice));
+  return SPCG_OK;
+}
+
 int halo_exchange(const HaloPlan& H, DistWorkspace& d, const double* v, double* dst_ext,
                   cudaStream_t st, long long* launches) {
   if (H.npeers == 0) return SPCG_OK;
@@ -1503,6 +1523,7 @@ int halo_exchange(const HaloPlan& H, DistWorkspace& d, const double* v, double* 
     CUDA_TRY(cudaGetLastError());
     ++*launches;
   }
+  if (H.hc) return host_sendrecv(H, d.send_buf, dst_ext + H.nloc, H.send_off, H.recv_off, st);
   NcclApi& N = nccl();
   NCCL_TRY(N.GroupStart());
   for (int k = 0; k < H.npeers; ++k) {
@@ -1524,17 +1545,22 @@ int halo_exchange(const HaloPlan& H, DistWorkspace& d, const double* v, double* 
 int reverse_halo(const HaloPlan& H, DistWorkspace& d, double* q, long long nhalo,
                  cudaStream_t st, long long* launches) {
   if (H.npeers == 0) return SPCG_OK;
-  NcclApi& N = nccl();
-  NCCL_TRY(N.GroupStart());
-  for (int k = 0; k < H.npeers; ++k) {
-    const long long sc = H.send_off[k + 1] - H.send_off[k];
-    const long long rc = H.recv_off[k + 1] - H.recv_off[k];
-    if (rc > 0)
-      NCCL_TRY(N.Send(q + H.nloc + H.recv_off[k], (size_t)rc, ncclDouble, H.peers[k], H.comm, st));
-    if (sc > 0)
-      NCCL_TRY(N.Recv(d.send_buf + H.send_off[k], (size_t)sc, ncclDouble, H.peers[k], H.comm, st));
+  if (H.hc) {  // roles swapped: ghosts (halo order) out, owner rows (send order) in
+    int rc;
+    if ((rc = host_sendrecv(H, q + H.nloc, d.send_buf, H.recv_off, H.send_off, st))) return rc;
+  } else {
+    NcclApi& N = nccl();
+    NCCL_TRY(N.GroupStart());
+    for (int k = 0; k < H.npeers; ++k) {
+      const long long sc = H.send_off[k + 1] - H.send_off[k];
+      const long long rc = H.recv_off[k + 1] - H.recv_off[k];
+      if (rc > 0)
+        NCCL_TRY(N.Send(q + H.nloc + H.recv_off[k], (size_t)rc, ncclDouble, H.peers[k], H.comm, st));
+      if (sc > 0)
+        NCCL_TRY(N.Recv(d.send_buf + H.send_off[k], (size_t)sc, ncclDouble, H.peers[k], H.comm, st));
+    }
+    NCCL_TRY(N.GroupEnd());
   }
-  NCCL_TRY(N.GroupEnd());
   const long long total = H.send_off[H.npeers];
   if (total > 0) {
     const int g = (int)std::min<long long>(1184, (total + 255) / 256);
@@ -1547,6 +1573,15 @@ int reverse_halo(const HaloPlan& H, DistWorkspace& d, double* q, long long nhalo
 }
 
 int allreduce_red(const HaloPlan& H, StepState* S, cudaStream_t st) {
+  if (H.hc) {
+    double v = 0.0;
+    CUDA_TRY(cudaStreamSynchronize(st));
+    CUDA_TRY(cudaMemcpy(&v, &S->red, sizeof(double), cudaMemcpyDeviceToHost));
+    if (H.hc->host_ar(&v, 1, H.hc->host_user) != 0)
+      return fail(SPCG_ERR_CUDA, "host allreduce callback failed");
+    CUDA_TRY(cudaMemcpy(&S->red, &v, sizeof(double), cudaMemcpyHostToDevice));
+    return SPCG_OK;
+  }
   if (!H.comm) return SPCG_OK;
   NCCL_TRY(nccl().AllReduce(&S->red, &S->red, 1, ncclDouble, ncclSum, H.comm, st));
   return SPCG_OK;
@@ -1710,11 +1745,14 @@ int do_dist_cg(spcg_matrix_s* m, spcg_comm_s* comm, int npeers, const int32_t* p
   if (npeers > 0 && kf == K_CSC) return fail(SPCG_ERR_UNSUPPORTED, "sharded CSC is not supported");
   if (kf == K_SCSR_PRIV && !m->hasB) return fail(SPCG_ERR_UNSUPPORTED, "SCSR needs its L^T rows");
   if (m->is_rows && !m->localized) return fail(SPCG_ERR_ARG, "call spcg_matrix_localize first");
-  if (npeers > 0 && (!comm || !comm->comm)) return fail(SPCG_ERR_ARG, "peers need a communicator");
-  if (npeers > 0 && !nccl().ok) return fail(SPCG_ERR_CUDA, nccl().err);
+  const bool host_comm = comm && comm->host_ar;
+  if (npeers > 0 && (!comm || (!comm->comm && !host_comm)))
+    return fail(SPCG_ERR_ARG, "peers need a communicator");
+  if (npeers > 0 && !host_comm && !nccl().ok) return fail(SPCG_ERR_CUDA, nccl().err);
   if (o->record_history && !hist) return fail(SPCG_ERR_ARG, "record_history needs a history buffer");
   HaloPlan H;
   H.comm = comm ? comm->comm : nullptr;
+  H.hc = (comm && comm->host_ar) ? comm : nullptr;
   H.npeers = npeers;
   H.peers = peers;
   H.recv_off = recv_off;
@@ -1993,6 +2031,20 @@ int spcg_comm_create(int nranks, int rank, const unsigned char* id_bytes, spcg_c
       return fail(SPCG_ERR_CUDA, std::string("ncclCommInitRank: ") + N.GetErrorString(r));
     }
   }
+  *out = c;
+  return SPCG_OK;
+}
+
+int spcg_comm_create_host(int nranks, int rank, spcg_host_allreduce_fn allreduce,
+                          spcg_host_sendrecv_fn sendrecv, void* user, spcg_comm_t* out) {
+  if (!out || nranks < 1 || rank < 0 || rank >= nranks || !allreduce || !sendrecv)
+    return fail(SPCG_ERR_ARG, "bad host comm args");
+  spcg_comm_s* c = new spcg_comm_s();
+  c->nranks = nranks;
+  c->rank = rank;
+  c->host_ar = allreduce;
+  c->host_sr = sendrecv;
+  c->host_user = user;
   *out = c;
   return SPCG_OK;
 }

@@ -128,6 +128,52 @@ class Comm:
             N.check(lib.spcg_comm_create(1, 0, None, ctypes.byref(h)), "spcg_comm_create")
         self._h = h
 
+    @classmethod
+    def host(cls, rank: int, world: int, allreduce, sendrecv) -> "Comm":
+        """Communicator over the caller's own transport (spcg_comm_create_host):
+        allreduce(np.ndarray) sums in place over all ranks; sendrecv(peers,
+        send, send_off, recv_off) -> recv exchanges per-peer slices.  The
+        engine stages data through host memory, so this is for bring-up and
+        tests (e.g. several ranks on one GPU over gloo), not for speed."""
+        import numpy as _np
+
+        def _ar(buf, n, _user):
+            try:
+                a = _np.ctypeslib.as_array(buf, shape=(n,))
+                a[:] = allreduce(a.copy())
+                return 0
+            except Exception:  # noqa: BLE001 - reported to the C side as failure
+                import traceback
+
+                traceback.print_exc()
+                return 1
+
+        def _sr(npeers, peers, send, soff, recv, roff, _user):
+            try:
+                pe = _np.ctypeslib.as_array(peers, shape=(npeers,)).copy()
+                so = _np.ctypeslib.as_array(soff, shape=(npeers + 1,)).copy()
+                ro = _np.ctypeslib.as_array(roff, shape=(npeers + 1,)).copy()
+                sv = _np.ctypeslib.as_array(send, shape=(max(1, int(so[-1])),))[: int(so[-1])].copy()
+                out = sendrecv(pe, sv, so, ro)
+                if int(ro[-1]):
+                    _np.ctypeslib.as_array(recv, shape=(int(ro[-1]),))[:] = out
+                return 0
+            except Exception:  # noqa: BLE001
+                import traceback
+
+                traceback.print_exc()
+                return 1
+
+        self = cls.__new__(cls)
+        self.rank, self.world = rank, world
+        self._cb = (N.HOST_ALLREDUCE_FN(_ar), N.HOST_SENDRECV_FN(_sr))  # keep alive
+        h = ctypes.c_void_p()
+        N.check(N.load().spcg_comm_create_host(world, rank, ctypes.cast(self._cb[0], ctypes.c_void_p),
+                                               ctypes.cast(self._cb[1], ctypes.c_void_p), None,
+                                               ctypes.byref(h)), "spcg_comm_create_host")
+        self._h = h
+        return self
+
     @property
     def handle(self):
         return self._h
@@ -142,6 +188,37 @@ class Comm:
             self.close()
         except Exception:
             pass
+
+
+def torch_host_transport():
+    """(allreduce, sendrecv) callables for Comm.host over the default
+    torch.distributed process group (any backend, e.g. gloo on CPU tensors)."""
+    import torch
+    import torch.distributed as dist
+
+    def allreduce(a):
+        t = torch.from_numpy(np.ascontiguousarray(a))
+        dist.all_reduce(t)
+        return t.numpy()
+
+    def sendrecv(peers, send, soff, roff):
+        reqs, bufs = [], []
+        out = np.zeros(int(roff[-1]))
+        for k, peer in enumerate(peers):
+            s0, s1, r0, r1 = int(soff[k]), int(soff[k + 1]), int(roff[k]), int(roff[k + 1])
+            if s1 > s0:
+                reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(send[s0:s1])), int(peer)))
+            if r1 > r0:
+                t = torch.empty(r1 - r0, dtype=torch.float64)
+                bufs.append((r0, r1, t))
+                reqs.append(dist.irecv(t, int(peer)))
+        for rq in reqs:
+            rq.wait()
+        for r0, r1, t in bufs:
+            out[r0:r1] = t.numpy()
+        return out
+
+    return allreduce, sendrecv
 
 
 def torch_collectives():
