@@ -56,9 +56,7 @@ __device__ __forceinline__ void grid_allreduce2(double& v0, double& v1, Smem& sm
     b0 = warp_sum(b0);
     b1 = warp_sum(b1);
     if (lane == 0) {
-#ifndef SPCG_DEV_NO_WFENCE
       fence_acq_rel_gpu();
-#endif
       const unsigned long long u0 = (unsigned long long)__double_as_longlong(b0);
       const unsigned long long u1 = (unsigned long long)__double_as_longlong(b1);
       unsigned long long* slot = bank + (size_t)kSlotWords * blockIdx.x;
@@ -100,9 +98,7 @@ __device__ __forceinline__ void grid_allreduce2(double& v0, double& v1, Smem& sm
         s0 += __longlong_as_double((long long)((a[u] & 0xffffffff00000000ull) | (c[u] >> 32)));
         s1 += __longlong_as_double((long long)((e[u] & 0xffffffff00000000ull) | (f[u] >> 32)));
       }
-#ifndef SPCG_DEV_NO_RFENCE
     fence_acq_rel_gpu();
-#endif
     s0 = warp_sum(s0);
     s1 = warp_sum(s1);
     if (lane == 0) {

@@ -47,12 +47,6 @@ constexpr int kClusMaxRows = kClusWarps * kClusSlicesPerWarp * 32;  // 2048 per 
 constexpr int kClusMax = 16;      // CTAs in one cluster (non-portable above 8)
 constexpr int kClusGridMax = 256;  // CTAs of a multi-cluster grid (K clusters of 8)
 constexpr int kClusSlotWords = 32;  // 256-byte global slot per cluster (own L2 line pair)
-#ifndef SPCG_CLUS_WRITER_FENCE
-#define SPCG_CLUS_WRITER_FENCE 0  // 1: writers fence their own inter-cluster stores (+0.5 us)
-#endif
-#ifndef SPCG_CLUS_ALLPOLL
-#define SPCG_CLUS_ALLPOLL 0  // 1: every CTA polls the cluster slots (2.3x slower: contention)
-#endif
 
 struct ClusCta {
   int row_lo, row_hi;  // own rows
@@ -117,9 +111,6 @@ __device__ __forceinline__ void cluster_sync_all() {
 // (L+D segment, L^T segment) summed separately and added (privatized mode).
 #ifndef SPCG_CLUS_UNROLL
 #define SPCG_CLUS_UNROLL 4
-#endif
-#ifndef SPCG_CLUS_SKIP
-#define SPCG_CLUS_SKIP 0  // dev timing only: 1 skip streamed slices, 2 skip resident
 #endif
 template <bool TWO, int U = SPCG_CLUS_UNROLL>
 __device__ __forceinline__ double clus_row(const double* val, const unsigned short* col, int base,
@@ -231,8 +222,7 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
 #pragma unroll
     for (int k = 0; k < kClusSlicesPerWarp; ++k) {
       out[k] = 0.0;
-      if (swidth[k] > 0 && !(SPCG_CLUS_SKIP == 1 && !sres[k]) &&
-          !(SPCG_CLUS_SKIP == 2 && sres[k])) {  // warp-uniform
+      if (swidth[k] > 0) {  // warp-uniform
         const double q = sres[k] ? clus_row<TWO>(sval, scol, sbase[k], swidth[k], rlen[k], rlenA[k], rwin)
                                  : clus_row<TWO>(A.gval, A.gcol, sbase[k], swidth[k], rlen[k], rlenA[k], rwin);
         out[k] = rrow[k] >= 0 ? q : 0.0;
@@ -282,9 +272,9 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
       // cluster's partials in its own 256-byte slot as epoch-tagged 64-bit
       // words (volatile scalar accesses; one fence before the post — the
       // cluster barrier above made the cluster's global halo stores part of
-      // it — and one after the poll).  ALLPOLL: every CTA polls the K slots
-      // itself; otherwise the leader polls and broadcasts over DSMEM behind a
-      // second cluster barrier.  Sums run in cluster order in every CTA.
+      // it — and one after the poll); the leader polls the K slots and
+      // broadcasts over DSMEM behind a second cluster barrier (letting every
+      // CTA poll was 2.3x slower).  Sums run in cluster order in every CTA.
       const uint32_t tag = epoch;  // identical sequence in every CTA, never 0
       unsigned long long* gb = A.gslots + (size_t)bank * K * kClusSlotWords;
 #if SPCG_TRACE
@@ -303,7 +293,7 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
         dst[2] = (u1 & 0xffffffff00000000ull) | tag;
         dst[3] = (u1 << 32) | tag;
       }
-      if ((SPCG_CLUS_ALLPOLL || me == 0) && wp == 0) {
+      if (me == 0 && wp == 0) {
         double c0 = 0.0, c1 = 0.0;
         if (lane < K) {
           const volatile unsigned long long* src = gb + kClusSlotWords * lane;
@@ -333,19 +323,13 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
           s0 += __shfl_sync(0xffffffffu, c0, k);
           s1 += __shfl_sync(0xffffffffu, c1, k);
         }
-        if (SPCG_CLUS_ALLPOLL) {
-          if (lane == 0) {
-            cs.tot[bank][0] = s0;
-            cs.tot[bank][1] = s1;
-          }
-        } else if (lane < C) {
+        if (lane < C) {
           double* d2 = cl.map_shared_rank(&cs.tot[bank][0], lane);
           d2[0] = s0;
           d2[1] = s1;
         }
       }
-      if (SPCG_CLUS_ALLPOLL) __syncthreads();
-      else cluster_sync_all();
+      cluster_sync_all();
 #if SPCG_TRACE
       if (A.trace && tid == 0) tlv[1] += globaltimer_ns() - ta;
 #endif
@@ -357,7 +341,6 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
   };
   // boundary w of this CTA -> the halo buffers of the CTAs that gather it
   auto send_w = [&](int buf) {
-    bool global = false;
     for (int e = 0; e < P.nsend; ++e) {
       const ClusSend sd = e < kClusSendCache ? cs.send[e] : A.sends[P.send0 + e];
       const bool remote_cluster = sd.dst / C != kc;
@@ -365,16 +348,8 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
                                    : cl.map_shared_rank(whalo + (size_t)buf * A.hcap, sd.dst % C);
 #pragma unroll
       for (int k = 0; k < kClusSlicesPerWarp; ++k)
-        if (rrow[k] >= sd.lo && rrow[k] < sd.hi) {
-          dst[sd.dst_off + rrow[k] - sd.lo] = wg[k];
-          global |= remote_cluster;
-        }
+        if (rrow[k] >= sd.lo && rrow[k] < sd.hi) dst[sd.dst_off + rrow[k] - sd.lo] = wg[k];
     }
-#if SPCG_CLUS_WRITER_FENCE
-    // the writer's own gpu-scope fence: inter-cluster halo values must not
-    // rely on the cluster barrier's release being cumulative at gpu scope
-    if (global) fence_acq_rel_gpu();
-#endif
   };
   // window index of halo index h
   auto halo_win = [&](int h) { return h < P.hlo ? h : own0 + (P.row_hi - P.row_lo) + (h - P.hlo); };
@@ -438,7 +413,6 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
       A.scratch[rrow[k]] = rg[k];
       part = fma(rg[k], rg[k], part);
     }
-  if (SPCG_CLUS_WRITER_FENCE && K > 1) fence_acq_rel_gpu();
   allreduce2(part, dummy);  // release/acquire at cluster scope covers scratch
   double gam = part;
   for (int j = tid; j < P.wn; j += kClusThreads) rwin[j] = __ldcg(A.scratch + P.wlo + j);
@@ -590,7 +564,6 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
 #pragma unroll
   for (int k = 0; k < kClusSlicesPerWarp; ++k)
     if (rrow[k] >= 0) A.x[rrow[k]] = xr[k];
-  if (SPCG_CLUS_WRITER_FENCE && K > 1) fence_acq_rel_gpu();
   if (A.recompute) {  // true residual ||b - A x|| / ||b||
     part = 0.0;
     dummy = 0.0;

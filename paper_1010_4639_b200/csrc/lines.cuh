@@ -262,32 +262,6 @@ __device__ __forceinline__ void lane_seq_sum2(const double* v, const int* ix, in
   gb = acc2;
 }
 
-// Same sums through the tile's product buffer: lane g writes the products
-// of its entries u = g, g+T, ... (8 gathers in flight per round) to prod[k]
-// (prod may alias the staged values: the stage is not read again this pass),
-// then after a warp-level sync the line's first lane adds prod[ks..ke) in
-// order.  The line's lanes are in one warp, so no CTA barrier is needed.
-template <class Src>
-__device__ __forceinline__ void lane_products(const double* v, const int* ix, int ks, int ke,
-                                              int lg, const Src& src, double* prod) {
-  const int T = 1 << lg;
-  const int g = (int)threadIdx.x & (T - 1);
-  const int L = ke - ks;
-  for (int base = 0; base < L; base += 8 * T) {
-    double p[8];
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int u = base + t * T + g;
-      p[t] = (u < L) ? __dmul_rn(v[ks + u], src.get(ix[ks + u])) : 0.0;
-    }
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int u = base + t * T + g;
-      if (u < L) prod[ks + u] = p[t];
-    }
-  }
-}
-
 // Computes line i (the tid-th line of staged tile s).  For FMT in
 // {SCSR_ATOMIC, CSC} the scatter goes to y (must be zeroed beforehand) and
 // the line's own gather is returned in q; for CSR / SCSR_PRIV the caller
@@ -367,26 +341,12 @@ __device__ __forceinline__ LineOut tile_line(Smem& sm, int s, const MatView& M, 
             if (xpre) o.xo = xpre[li];
           }
         }
-#ifndef SPCG_SPLIT_SHFL
-#define SPCG_SPLIT_SHFL 1  // 0: products through shared memory (slower)
-#endif
-        if (SPCG_SPLIT_SHFL) {
-          if (FMT == K_SCSR_PRIV) {
-            double ga, gb;
-            lane_seq_sum2(sm.val[s], sm.idx[s], ks, ke, kb, kbe, lg, src, ga, gb);
-            o.q = __dadd_rn(ga, gb);
-          } else {
-            o.q = lane_seq_sum(sm.val[s], sm.idx[s], ks, ke, lg, src);
-          }
+        if (FMT == K_SCSR_PRIV) {
+          double ga, gb;
+          lane_seq_sum2(sm.val[s], sm.idx[s], ks, ke, kb, kbe, lg, src, ga, gb);
+          o.q = __dadd_rn(ga, gb);
         } else {
-          lane_products(sm.val[s], sm.idx[s], ks, ke, lg, src, prod);
-          if (FMT == K_SCSR_PRIV) lane_products(sm.val[s], sm.idx[s], kb, kbe, lg, src, prod);
-          __syncwarp();
-          if (has && g == 0) {
-            o.q = seq_sum(prod, ks, ke);
-            if (FMT == K_SCSR_PRIV) o.q = __dadd_rn(o.q, seq_sum(prod, kb, kbe));
-          }
-          __syncwarp();  // prod (may alias a resident tile's buffer) reused next line
+          o.q = lane_seq_sum(sm.val[s], sm.idx[s], ks, ke, lg, src);
         }
         active = has && g == 0;
         line = li;

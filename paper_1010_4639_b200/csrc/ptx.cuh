@@ -121,30 +121,15 @@ __device__ __forceinline__ void ld_relaxed_v2_u64(const unsigned long long* p,
                : "l"(p)
                : "memory");
 }
-// Slot accesses of the grid barriers.  SPCG_SLOT_VOLATILE=1: two volatile
-// 64-bit scalar accesses instead of one relaxed.gpu vector access.
-#ifndef SPCG_SLOT_VOLATILE
-#define SPCG_SLOT_VOLATILE 0
-#endif
+// Slot accesses of the grid barriers (relaxed.gpu vector accesses: the
+// volatile-scalar form that wins for the cluster exchange was slower here).
 __device__ __forceinline__ void slot_st2(unsigned long long* p, unsigned long long a,
                                          unsigned long long b) {
-#if SPCG_SLOT_VOLATILE
-  volatile unsigned long long* v = p;
-  v[0] = a;
-  v[1] = b;
-#else
   st_relaxed_v2_u64(p, a, b);
-#endif
 }
 __device__ __forceinline__ void slot_ld2(const unsigned long long* p, unsigned long long& a,
                                          unsigned long long& b) {
-#if SPCG_SLOT_VOLATILE
-  const volatile unsigned long long* v = p;
-  a = v[0];
-  b = v[1];
-#else
   ld_relaxed_v2_u64(p, a, b);
-#endif
 }
 __device__ __forceinline__ void ld_acquire_v2_u64(const unsigned long long* p,
                                                   unsigned long long& a,
