@@ -299,12 +299,15 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
           const volatile unsigned long long* src = gb + kClusSlotWords * lane;
           unsigned long long a, b, c, d, spins = 0;
           for (;;) {
-            a = src[0];
-            b = src[1];
-            c = src[2];
+            // spin on the last-written word only (one load per round keeps
+            // the pollers' pressure on the slot lines low), then validate all
             d = src[3];
-            if ((uint32_t)a == tag && (uint32_t)b == tag && (uint32_t)c == tag && (uint32_t)d == tag)
-              break;
+            if ((uint32_t)d == tag) {
+              a = src[0];
+              b = src[1];
+              c = src[2];
+              if ((uint32_t)a == tag && (uint32_t)b == tag && (uint32_t)c == tag) break;
+            }
             if (++spins > kSpinLimit) asm volatile("trap;");
           }
           c0 = __longlong_as_double((long long)((a & 0xffffffff00000000ull) | (b >> 32)));
