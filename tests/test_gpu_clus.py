@@ -131,3 +131,29 @@ def test_auto_engine_is_cluster_for_small_systems():
     r3 = cg_solve(F, b, engine=3)  # grid-resident single reduction: same method
     assert r3.iterations == r5.iterations
     assert np.linalg.norm(r3.x - r5.x) / np.linalg.norm(r5.x) <= 1e-10
+
+
+def test_multi_cluster_x0_truncation_and_zero_rhs():
+    """The paper-size matrix on the K-cluster grid with the solver.py edge
+    semantics: x0 (the initial residual goes through the global scratch
+    window), max_iter truncation (history and final residual), b = 0."""
+    from paper_1010_4639_b200 import CgOptions, cg_solve
+    from paper_1010_4639_b200.genprob import fem_mesh, rhs_for
+
+    F = fem_mesh()
+    b, _ = rhs_for(F, seed=1)
+    x0 = np.random.default_rng(11).standard_normal(F.n)
+    ref = O.cg_solve("csr", F.row_start, F.col_idx, F.values, b, x0=x0, record_history=True)
+    r = cg_solve(F, b, x0=x0, opts=CgOptions(record_history=True), engine=5)
+    assert abs(r.iterations - ref.iterations) <= 3
+    assert np.linalg.norm(r.x - ref.x) / np.linalg.norm(ref.x) <= 1e-8
+    assert np.allclose(r.residual_history[:50], ref.residual_history[:50], rtol=1e-8)
+    t = cg_solve(F, b, x0=x0, opts=CgOptions(max_iter=25, record_history=True,
+                                             recompute_final_residual=False), engine=5)
+    rt = O.cg_solve("csr", F.row_start, F.col_idx, F.values, b, x0=x0, max_iter=25,
+                    record_history=True, recompute=False)
+    assert t.iterations == 25 and not t.converged
+    assert np.allclose(t.residual_history, rt.residual_history, rtol=1e-9)
+    assert np.linalg.norm(t.x - rt.x) / np.linalg.norm(rt.x) <= 1e-9
+    z = cg_solve(F, np.zeros(F.n), x0=x0, engine=5)
+    assert z.iterations == 0 and (z.x == 0).all()
