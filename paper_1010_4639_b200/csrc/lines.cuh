@@ -141,14 +141,28 @@ __device__ __forceinline__ double csc_col(const double* v, const int* ix, int ks
 }
 
 // ---- long lines: one line with > kTileNnz entries, read from global by the
-// whole CTA (strided partial sums + fixed-order block reduction).
+// whole CTA.  Scatter formats (order unspecified anyway) use strided partial
+// sums + a fixed-order block reduction (tile_line).
+// Long line of a gather format, bitwise the reference's sequential row sum:
+// chunk by chunk all threads form the products (coalesced loads, every
+// gather in flight) into `prod` (>= kTileNnz doubles: the stage's unused
+// value buffer), then thread 0 adds them in storage order.  The dependent
+// add chain costs ~17 us per 4096 entries -- fine for the rare rows longer
+// than a tile.  Result valid in thread 0.
 template <class Src>
-__device__ __forceinline__ double long_gather(const double* val, const int* idx, int k0, int k1,
-                                              const Src& src, Smem& sm) {
-  double part = 0.0;
-  for (int k = k0 + (int)threadIdx.x; k < k1; k += blockDim.x)
-    part = __dadd_rn(part, __dmul_rn(ld_stream_f64(val + k), src.get(ld_stream_s32(idx + k))));
-  return block_sum(part, sm);
+__device__ __forceinline__ double long_gather_seq(const double* val, const int* idx, int k0, int k1,
+                                                  const Src& src, double* prod) {
+  double acc = 0.0;
+  for (int base = k0; base < k1; base += kTileNnz) {
+    const int cnt = min(kTileNnz, k1 - base);
+    for (int e = (int)threadIdx.x; e < cnt; e += blockDim.x)
+      prod[e] = __dmul_rn(ld_stream_f64(val + base + e), src.get(ld_stream_s32(idx + base + e)));
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int e = 0; e < cnt; ++e) acc = __dadd_rn(acc, prod[e]);
+    __syncthreads();  // prod is rewritten by the next chunk
+  }
+  return acc;
 }
 
 // Result of one line of a tile pass: the line's output value and the line's
@@ -407,11 +421,11 @@ __device__ __forceinline__ LineOut tile_line(Smem& sm, int s, const MatView& M, 
   if (xpre) o.xo = xpre[i];
   const int k0 = M.ptrA[i], k1 = M.ptrA[i + 1];
   if (FMT == K_CSR) {
-    o.q = long_gather(M.valA, M.idxA, k0, k1, src, sm);
+    o.q = long_gather_seq(M.valA, M.idxA, k0, k1, src, prod);
     o.xi = src.get(i);
   } else if (FMT == K_SCSR_PRIV) {
-    const double g = long_gather(M.valA, M.idxA, k0, k1, src, sm);
-    const double t = long_gather(M.valB, M.idxB, M.ptrB[i], M.ptrB[i + 1], src, sm);
+    const double g = long_gather_seq(M.valA, M.idxA, k0, k1, src, prod);
+    const double t = long_gather_seq(M.valB, M.idxB, M.ptrB[i], M.ptrB[i + 1], src, prod);
     o.q = __dadd_rn(g, t);
     o.xi = src.get(i);
   } else if (FMT == K_SCSR_ATOMIC) {
