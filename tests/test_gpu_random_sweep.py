@@ -73,17 +73,49 @@ def test_random_spmv_all_storages(n, kind):
     assert np.abs(ysa - ys_ref).max() <= 1e-12 * sc * max(1, np.diff(s_full.row_start).max())
 
 
+def _storage(a, kind):
+    from paper_1010_4639_b200 import KernelConfig, extract_lower
+
+    if kind == "csr":
+        return a, KernelConfig()
+    if kind == "csc":
+        return a.to_csc(), KernelConfig()
+    return extract_lower(a), KernelConfig(accumulation="privatized" if kind == "sym_priv"
+                                          else "atomic")
+
+
+def _arrow(n):
+    """SPD arrow matrix: dense first row/column (a line longer than a tile),
+    tridiagonal body, diagonally dominant."""
+    from paper_1010_4639_b200.core import build_csr_from_triplets
+
+    rng = np.random.default_rng(n)
+    i = np.arange(1, n)
+    w = -rng.uniform(0.1, 1.0, n - 1) / n
+    t = -rng.uniform(0.1, 0.5, n - 2)
+    rows = np.concatenate([np.zeros(n - 1, int), i, i[:-1], i[1:]])
+    cols = np.concatenate([i, np.zeros(n - 1, int), i[1:], i[:-1]])
+    vals = np.concatenate([w, w, t, t])
+    diag = np.bincount(rows, weights=np.abs(vals), minlength=n) + 0.5
+    return build_csr_from_triplets((np.concatenate([rows, np.arange(n)]),
+                                    np.concatenate([cols, np.arange(n)]),
+                                    np.concatenate([vals, diag])), n)
+
+
 @pytest.mark.parametrize("engine", [0, 2, 3, 5])
-@pytest.mark.parametrize("n,density,seed", [(300, 0.05, 1), (2500, 0.004, 2), (12000, 0.0008, 3)])
-def test_random_spd_all_engines(engine, n, density, seed):
+@pytest.mark.parametrize("storage", ["csr", "sym_priv", "sym_atomic", "csc"])
+@pytest.mark.parametrize("n,density,seed", [(300, 0.05, 1), (2500, 0.004, 2), (12000, 0.0008, 3),
+                                            (6000, -1.0, 4)])
+def test_random_spd_all_engines(engine, storage, n, density, seed):
     from paper_1010_4639_b200 import CgOptions, cg_solve
     from paper_1010_4639_b200.genprob import random_spd
 
-    a = random_spd(n, density, seed)
+    a = random_spd(n, density, seed) if density > 0 else _arrow(n)
     b = np.random.default_rng(seed).standard_normal(n)
     ref = O.cg_solve("csr", a.row_start, a.col_idx, a.values, b)
+    m, cfg = _storage(a, storage)
     try:
-        r = cg_solve(a, b, opts=CgOptions(record_history=True), engine=engine)
+        r = cg_solve(m, b, opts=CgOptions(record_history=True), cfg=cfg, engine=engine)
     except Exception as e:  # engine 5 may decline unbanded systems; auto never does
         assert engine == 5 and "not applicable" in str(e), e
         return
