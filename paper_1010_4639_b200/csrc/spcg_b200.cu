@@ -1080,6 +1080,11 @@ int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double
   if ((rc = dev_info(&d))) return rc;
   if (!(o->tol > 0.0)) return fail(SPCG_ERR_ARG, "tol must be > 0");
   if (m->is_rows) return fail(SPCG_ERR_ARG, "a row block is solved with spcg_dist_cg_solve");
+  if (m->n == 0) {  // ||b|| = 0: x = [] converged in 0 iterations, any engine (solver.py:109-118)
+    *out = spcg_cg_result{};
+    out->converged = 1;
+    return SPCG_OK;
+  }
   const int kf = kfmt_of(m, o->accumulation);
   if (kf == K_SCSR_PRIV && !m->hasB) return fail(SPCG_ERR_UNSUPPORTED, "no L^T for privatized mode");
   const MatView v = view(m, kf == K_SCSR_PRIV);

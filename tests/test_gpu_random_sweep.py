@@ -122,3 +122,23 @@ def test_random_spd_all_engines(engine, storage, n, density, seed):
     assert abs(r.iterations - ref.iterations) <= max(1, ref.iterations // 100)
     assert np.linalg.norm(r.x - ref.x) / np.linalg.norm(ref.x) <= 1e-8
     assert r.final_relative_residual <= 1e-10
+
+
+@pytest.mark.parametrize("engine", [0, 2, 3, 5])
+def test_degenerate_sizes(engine):
+    """n = 0 (empty system: b = 0 -> x = [] converged, as solver.py:109-118)
+    and n = 1 through every engine and storage."""
+    from paper_1010_4639_b200 import CgOptions, cg_solve, spmv_full
+    from paper_1010_4639_b200.core import build_csr_from_triplets
+
+    e = np.empty(0, dtype=np.int64)
+    a0 = build_csr_from_triplets((e, e, np.empty(0)), 0)
+    r0 = cg_solve(a0, np.empty(0), engine=engine)
+    assert r0.iterations == 0 and r0.converged and r0.x.shape == (0,)
+    assert spmv_full(a0, np.empty(0)).shape == (0,)
+    a1 = build_csr_from_triplets((np.array([0]), np.array([0]), np.array([4.0])), 1)
+    for kind in ("csr", "sym_priv", "sym_atomic", "csc"):
+        m, cfg = _storage(a1, kind)
+        r1 = cg_solve(m, np.array([2.0]), opts=CgOptions(record_history=True), cfg=cfg,
+                      engine=engine)
+        assert r1.iterations == 1 and r1.converged and r1.x[0] == 0.5, (kind, r1)
