@@ -84,6 +84,17 @@ def get_backend() -> str:
     return _active
 
 
+class _CudaBackend:
+    """Backend module interface of the reference (_compiled.py:10-57: name,
+    spmv_full, spmv_sym, dot, axpy); filled in below."""
+
+    name = "cuda"
+
+
+# The reference's backend registry (kernels/__init__.py:21-50), with the one
+# backend this library has; code that looks backends up by name keeps working.
+BACKENDS = {"cuda": _CudaBackend}
+
 # SPCG_BACKEND (kernels/__init__.py:50) may name a reference backend; the
 # only implementation here is the device one.
 set_backend("auto")
@@ -221,7 +232,11 @@ def pairwise_merge(partials) -> float:
     return float(arr[0])
 
 
+for _n in ("spmv_full", "spmv_sym", "dot", "axpy"):
+    setattr(_CudaBackend, _n, staticmethod(globals()[_n]))
+del _n
+
 __all__ = [
     "KernelConfig", "ACCUMULATION_MODES", "pairwise_merge", "spmv_full", "spmv_sym", "spmv_csc",
-    "dot", "axpy", "norm2", "set_backend", "get_backend", "available_backends",
+    "dot", "axpy", "norm2", "set_backend", "get_backend", "available_backends", "BACKENDS",
 ]
