@@ -134,7 +134,14 @@ typedef struct {
                                         (<= 16 CTAs, banded systems)         */
   int32_t timing;                /* per-pass engine: CUDA-event time of every
                                     SpMV pass -> result.spmv_ms / launches   */
-  int32_t reserved;
+  int32_t row_sums;              /* 0 = auto: in the streaming CG passes, lines
+                                    split over 2-4 lanes sum per-lane partials
+                                    + a fixed shuffle tree (deterministic,
+                                    fp64-reassociated like the reference's
+                                    parallel modes); 1 = every row sum in
+                                    storage order (bitwise the reference's
+                                    sequential sums).  SpMV entry points are
+                                    always in storage order.                  */
 } spcg_cg_options;
 
 typedef struct {

@@ -45,7 +45,7 @@ class CgOptionsC(ctypes.Structure):
         ("accumulation", ctypes.c_int32),
         ("engine", ctypes.c_int32),
         ("timing", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("row_sums", ctypes.c_int32),
     ]
 
 

@@ -240,6 +240,69 @@ __device__ __forceinline__ int owned_line(const StageMeta& mt) {
   return i < mt.row1 ? i : -1;
 }
 
+// Reassociated (but deterministic) variant for the CG passes: lane g sums
+// its entries u = g, g+T, ... in order, then the partials combine by a fixed
+// shuffle tree ((s0+s1)+(s2+s3)); valid in the group's first lane.  No
+// per-product shuffles: the long-row bodies run at streaming speed.
+template <class Src>
+__device__ __forceinline__ double lane_tree_sum(const double* v, const int* ix, int ks, int ke,
+                                                int lg, const Src& src) {
+  const int T = 1 << lg;
+  const int g = (int)threadIdx.x & (T - 1);
+  const int L = ke - ks;
+  double acc = 0.0;
+  for (int base = 0; base < L; base += 8 * T) {
+    double p[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int u = base + t * T + g;
+      p[t] = (u < L) ? __dmul_rn(v[ks + u], src.get(ix[ks + u])) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+      if (base + t * T + g < L) acc = __dadd_rn(acc, p[t]);
+  }
+  if (lg >= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, 1));
+  if (lg == 2) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, 2));
+  return acc;
+}
+
+// Both segments of a privatized SCSR line in the same rounds (the gathers
+// of L+D and L^T in flight together), each reduced by its own fixed tree.
+template <class Src>
+__device__ __forceinline__ double lane_tree_sum2(const double* v, const int* ix, int ka, int kae,
+                                                 int kb, int kbe, int lg, const Src& src) {
+  const int T = 1 << lg;
+  const int g = (int)threadIdx.x & (T - 1);
+  const int LA = kae - ka, LB = kbe - kb;
+  const int L = max(LA, LB);
+  double acc = 0.0, acc2 = 0.0;
+  for (int base = 0; base < L; base += 4 * T) {
+    double p[4], q[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int u = base + t * T + g;
+      p[t] = (u < LA) ? __dmul_rn(v[ka + u], src.get(ix[ka + u])) : 0.0;
+      q[t] = (u < LB) ? __dmul_rn(v[kb + u], src.get(ix[kb + u])) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int u = base + t * T + g;
+      if (u < LA) acc = __dadd_rn(acc, p[t]);
+      if (u < LB) acc2 = __dadd_rn(acc2, q[t]);
+    }
+  }
+  if (lg >= 1) {
+    acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, 1));
+    acc2 = __dadd_rn(acc2, __shfl_down_sync(0xffffffffu, acc2, 1));
+  }
+  if (lg == 2) {
+    acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, 2));
+    acc2 = __dadd_rn(acc2, __shfl_down_sync(0xffffffffu, acc2, 2));
+  }
+  return __dadd_rn(acc, acc2);
+}
+
 // Two segments (SCSR privatized: L+D then L^T) in the same rounds, so the
 // gathers of both are in flight together; sums kept separate (g, t).
 template <class Src>
@@ -355,7 +418,11 @@ __device__ __forceinline__ LineOut tile_line(Smem& sm, int s, const MatView& M, 
             if (xpre) o.xo = xpre[li];
           }
         }
-        if (FMT == K_SCSR_PRIV) {
+        if (M.tree) {  // warp-uniform
+          o.q = FMT == K_SCSR_PRIV
+                    ? lane_tree_sum2(sm.val[s], sm.idx[s], ks, ke, kb, kbe, lg, src)
+                    : lane_tree_sum(sm.val[s], sm.idx[s], ks, ke, lg, src);
+        } else if (FMT == K_SCSR_PRIV) {
           double ga, gb;
           lane_seq_sum2(sm.val[s], sm.idx[s], ks, ke, kb, kbe, lg, src, ga, gb);
           o.q = __dadd_rn(ga, gb);

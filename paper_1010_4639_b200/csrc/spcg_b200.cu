@@ -1667,6 +1667,7 @@ int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const dou
       const int dirA = kAlternate ? (int)((iter_enq & 1) == 0) : 0;
       MatView va = v;
       va.rev = dirA;
+      va.tree = o->row_sums == 0;  // auto: reassociated long-row sums in pass A
       dist_spmv_pq<FMT><<<G, kBlock, sm, st>>>(va, d.S, p, d.q, d.part);
       if (timing) CUDA_TRY(cudaEventRecord(d.tev[1][c], st));
       if ((rc = allreduce_red(H, d.S, st))) return rc;

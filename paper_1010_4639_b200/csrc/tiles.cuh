@@ -61,6 +61,8 @@ struct MatView {
   const int2* twin;      // per tile: new gathered columns [lo,hi] vs the previous tile
   int rev;               // visit tiles last-to-first (per-pass engine: alternate passes
                          // start where the previous one ended, on its L2-resident lines)
+  int tree;              // split long lines: per-lane partial sums + a fixed shuffle tree
+                         // (reassociated, deterministic) instead of the in-order sum
 };
 
 struct StageMeta {

@@ -34,11 +34,15 @@ ACCUMULATION_MODES = ("atomic", "privatized")
 class KernelConfig:
     """Execution contract (config.py:13-40).  On the GPU `workers`/`chunk`
     have no meaning (the grid is sized to the SM count) but are validated;
-    `accumulation` selects the symmetric scatter mode."""
+    `accumulation` selects the symmetric scatter mode.  `row_sums` (new):
+    "auto" lets the streaming CG passes sum long rows as per-lane partials +
+    a fixed tree (deterministic, fp64-reassociated); "sequential" keeps every
+    row sum in storage order (bitwise the reference's sequential sums)."""
 
     workers: int = 1
     chunk: int | None = None
     accumulation: str = "privatized"
+    row_sums: str = "auto"
 
     def __post_init__(self):
         if self.workers < 1:
@@ -47,6 +51,8 @@ class KernelConfig:
             raise ValueError("chunk must be >= 1")
         if self.accumulation not in ACCUMULATION_MODES:
             raise ValueError(f"accumulation must be one of {ACCUMULATION_MODES}")
+        if self.row_sums not in ("auto", "sequential"):
+            raise ValueError("row_sums must be 'auto' or 'sequential'")
 
     def resolve_chunk(self, work_items: int) -> int:
         if self.chunk is not None:

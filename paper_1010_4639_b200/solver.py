@@ -127,7 +127,8 @@ def cg_solve(a, b, x0=None, opts: CgOptions | None = None, cfg: KernelConfig | N
     o = N.CgOptionsC(tol=float(opts.tol), max_iter=int(max_iter),
                      record_history=int(bool(opts.record_history)),
                      recompute_final_residual=int(bool(opts.recompute_final_residual)),
-                     accumulation=_acc_code(cfg), engine=int(engine))
+                     accumulation=_acc_code(cfg), engine=int(engine),
+                     row_sums=1 if cfg.row_sums == "sequential" else 0)
     res = N.CgResultC()
     if device_io:
         import torch

@@ -142,3 +142,26 @@ def test_degenerate_sizes(engine):
         r1 = cg_solve(m, np.array([2.0]), opts=CgOptions(record_history=True), cfg=cfg,
                       engine=engine)
         assert r1.iterations == 1 and r1.converged and r1.x[0] == 0.5, (kind, r1)
+
+
+@pytest.mark.parametrize("storage", ["csr", "sym_priv"])
+def test_row_sums_modes_long_rows(storage):
+    """27-point rows (split-line tiles) in the per-pass engine: the default
+    reassociated long-row sums and KernelConfig(row_sums="sequential") both
+    follow the reference CG; each is deterministic run to run."""
+    from paper_1010_4639_b200 import CgOptions, KernelConfig, cg_solve, extract_lower
+    from paper_1010_4639_b200.genprob import rhs_for, stencil27
+
+    a = stencil27(20, 18, 16)
+    b, _ = rhs_for(a, seed=4)
+    ref = O.cg_solve("csr", a.row_start, a.col_idx, a.values, b)
+    m = a if storage == "csr" else extract_lower(a)
+    for mode in ("auto", "sequential"):
+        cfg = KernelConfig(accumulation="privatized", row_sums=mode)
+        r1 = cg_solve(m, b, opts=CgOptions(record_history=True), cfg=cfg, engine=2)
+        r2 = cg_solve(m, b, opts=CgOptions(record_history=True), cfg=cfg, engine=2)
+        assert r1.iterations == r2.iterations and (r1.x == r2.x).all()
+        assert abs(r1.iterations - ref.iterations) <= max(1, ref.iterations // 100)
+        assert np.linalg.norm(r1.x - ref.x) / np.linalg.norm(ref.x) <= 1e-8
+    with pytest.raises(ValueError):
+        KernelConfig(row_sums="fast")
