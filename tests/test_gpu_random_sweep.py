@@ -165,3 +165,23 @@ def test_row_sums_modes_long_rows(storage):
         assert np.linalg.norm(r1.x - ref.x) / np.linalg.norm(ref.x) <= 1e-8
     with pytest.raises(ValueError):
         KernelConfig(row_sums="fast")
+
+
+@pytest.mark.parametrize("engine", [1, 2, 4])
+@pytest.mark.parametrize("storage", ["csr", "sym_priv", "sym_atomic", "csc"])
+def test_streaming_engines_all_storages(engine, storage):
+    """A system too large for the resident kernels (so engines 1 and 4 run
+    their streaming persistent bodies: folded / paired and three-pass) in
+    every storage, against the reference CG."""
+    from paper_1010_4639_b200 import CgOptions, cg_solve
+    from paper_1010_4639_b200.genprob import poisson3d, rhs_for
+
+    a = poisson3d(48, 48, 64)
+    b, _ = rhs_for(a, seed=6)
+    ref = O.cg_solve("csr", a.row_start, a.col_idx, a.values, b)
+    m, cfg = _storage(a, storage)
+    assert m.device().info()["ntiles"] > 2 * 148
+    r = cg_solve(m, b, opts=CgOptions(record_history=True), cfg=cfg, engine=engine)
+    assert abs(r.iterations - ref.iterations) <= max(1, ref.iterations // 100)
+    assert np.linalg.norm(r.x - ref.x) / np.linalg.norm(ref.x) <= 1e-8
+    assert r.final_relative_residual <= 1e-10
