@@ -1,0 +1,483 @@
+// host_cluster.cuh — host side of spcg_b200.cu: cluster-resident engine (engine 5): plan builder, launch, solve.
+// Included exactly once, by spcg_b200.cu inside its anonymous namespace
+// (one translation unit: the kernels' templates are instantiated there).
+#pragma once
+
+// ---- cluster-resident engine (engine 5, clus.cuh) ---------------------------
+
+int clus_fail(ClusPlan& P, const char* why) {
+  P.ok = false;
+  P.why = why;
+  return SPCG_OK;
+}
+
+int download_seg(const Seg& sg, int n, std::vector<int>& ptr, std::vector<int>& idx,
+                 std::vector<double>& val) {
+  ptr.resize((size_t)n + 1);
+  CUDA_TRY(cudaMemcpy(ptr.data(), sg.ptr, sizeof(int) * ((size_t)n + 1), cudaMemcpyDeviceToHost));
+  const size_t nz = (size_t)ptr[n];
+  idx.resize(nz);
+  val.resize(nz);
+  if (nz) {
+    CUDA_TRY(cudaMemcpy(idx.data(), sg.idx, sizeof(int) * nz, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(val.data(), sg.val, sizeof(double) * nz, cudaMemcpyDeviceToHost));
+  }
+  return SPCG_OK;
+}
+
+// Host CSR transpose (entries of each output row in ascending source-row
+// order: the reference's privatized / sequential-scatter order).
+void host_transpose(int n, const std::vector<int>& ptr, const std::vector<int>& idx,
+                    const std::vector<double>& val, bool strict_lower, std::vector<int>& tp,
+                    std::vector<int>& ti, std::vector<double>& tv) {
+  tp.assign((size_t)n + 1, 0);
+  for (int i = 0; i < n; ++i)
+    for (int k = ptr[i]; k < ptr[i + 1]; ++k)
+      if (!strict_lower || idx[k] < i) ++tp[(size_t)idx[k] + 1];
+  for (int i = 0; i < n; ++i) tp[(size_t)i + 1] += tp[i];
+  ti.resize((size_t)tp[n]);
+  tv.resize((size_t)tp[n]);
+  std::vector<int> pos(tp.begin(), tp.end() - 1);
+  for (int i = 0; i < n; ++i)
+    for (int k = ptr[i]; k < ptr[i + 1]; ++k)
+      if (!strict_lower || idx[k] < i) {
+        const int j = idx[k];
+        ti[(size_t)pos[j]] = i;
+        tv[(size_t)pos[j]++] = val[k];
+      }
+}
+
+// Builds the cluster plan: row blocks, windows, SELL-32 slices (rows sorted
+// by length), resident/streamed split, halo sends.  Infeasible systems keep
+// P.ok = false (the caller falls back to the grid engines).
+int build_clus_plan(spcg_matrix_s* m) {
+  ClusPlan& P = m->cp;
+  if (P.built) return SPCG_OK;
+  P.built = true;
+  const int n = m->n;
+  if (m->is_rows) return clus_fail(P, "row block");
+  if (n <= 0) return clus_fail(P, "empty");
+  if ((long long)n > (long long)kClusGridMax * kClusMaxRows) return clus_fail(P, "too many rows");
+  // rows as (segment A, segment B) entry lists
+  std::vector<int> pA, iA, pB, iB;
+  std::vector<double> vA, vB;
+  int rc;
+  if ((rc = download_seg(m->A, n, pA, iA, vA))) return rc;
+  P.two = m->fmt == SPCG_FMT_SCSR;
+  if (m->fmt == SPCG_FMT_CSC) {  // rows of A = transpose of the column store
+    std::vector<int> tp, ti;
+    std::vector<double> tv;
+    host_transpose(n, pA, iA, vA, false, tp, ti, tv);
+    pA.swap(tp);
+    iA.swap(ti);
+    vA.swap(tv);
+  } else if (P.two) {
+    if (m->hasB) {
+      if ((rc = download_seg(m->B, n, pB, iB, vB))) return rc;
+    } else {
+      host_transpose(n, pA, iA, vA, true, pB, iB, vB);
+    }
+  }
+  auto lenA = [&](int i) { return pA[(size_t)i + 1] - pA[i]; };
+  auto lenB = [&](int i) { return P.two ? pB[(size_t)i + 1] - pB[i] : 0; };
+  long long tot = 0;
+  for (int i = 0; i < n; ++i) {
+    const int l = lenA(i) + lenB(i);
+    if (l > 4096 || lenA(i) > 32767) return clus_fail(P, "row too long");
+    tot += l + 1;
+  }
+  // grid shape: one cluster of <= 16 CTAs, or K clusters of 8 (as many as
+  // are co-resident) with ~4K entries per CTA so the whole matrix stays in
+  // shared memory
+  const int cmin = (n + kClusMaxRows - 1) / kClusMaxRows;
+  const long long want = std::max<long long>(cmin, (tot + 3999) / 4000);
+  const void* kfn = P.two ? (const void*)clus_cg_kernel<true> : (const void*)clus_cg_kernel<false>;
+  int optin0 = 0, dev0 = 0;
+  CUDA_TRY(cudaGetDevice(&dev0));
+  CUDA_TRY(cudaDeviceGetAttribute(&optin0, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev0));
+  const int smem_probe = optin0 - (int)sizeof(ClusShared) - 1024;
+  auto max_clusters = [&](int csz) -> int {
+    CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_probe));
+    if (csz > 8) CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(csz);
+    cfg.blockDim = dim3(kClusThreads);
+    cfg.dynamicSmemBytes = (size_t)smem_probe;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = csz;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, kfn, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    return ncl;
+  };
+  int C, csz;
+  static const int force_k = getenv("SPCG_CLUS_K") ? atoi(getenv("SPCG_CLUS_K")) : 0;  // dev A/B
+  if ((want <= kClusMax && force_k <= 1) || force_k == 1) {
+    C = csz = (int)std::min<long long>(kClusMax, std::max<long long>(1, want));
+    if (max_clusters(csz) < 1) return clus_fail(P, "cluster not launchable");
+  } else {
+    csz = 8;
+    const int kmax = std::min(max_clusters(csz), kClusGridMax / 8);
+    int K = (int)std::min<long long>(kmax, (want + csz - 1) / csz);
+    if (force_k > 1) K = std::min(kmax, force_k);
+    if (K < 1) return clus_fail(P, "cluster not launchable");
+    if ((long long)K * csz * kClusMaxRows < n) {  // fall back to one big cluster
+      csz = kClusMax;
+      K = 1;
+      if (max_clusters(csz) < 1 || (long long)csz * kClusMaxRows < n)
+        return clus_fail(P, "too many rows for the co-resident clusters");
+    }
+    C = K * csz;
+  }
+  // contiguous row blocks balanced by entries + rows, <= kClusMaxRows each
+  std::vector<int> lo(C), hi(C);
+  {
+    int r = 0;
+    long long acc = 0;
+    for (int c = 0; c < C; ++c) {
+      lo[c] = r;
+      const long long goal = tot * (c + 1) / C;
+      while (r < n && (r - lo[c]) < kClusMaxRows && (acc < goal || c == C - 1)) {
+        acc += lenA(r) + lenB(r) + 1;
+        ++r;
+      }
+      hi[c] = r;
+    }
+    if (r < n) return clus_fail(P, "row blocks exceed the cluster");
+  }
+  // windows
+  std::vector<int> wlo(C), whi(C);
+  for (int c = 0; c < C; ++c) {
+    int a = lo[c], z = hi[c];
+    for (int i = lo[c]; i < hi[c]; ++i) {
+      for (int k = pA[i]; k < pA[(size_t)i + 1]; ++k) {
+        a = std::min(a, iA[k]);
+        z = std::max(z, iA[k] + 1);
+      }
+      if (P.two)
+        for (int k = pB[i]; k < pB[(size_t)i + 1]; ++k) {
+          a = std::min(a, iB[k]);
+          z = std::max(z, iB[k] + 1);
+        }
+    }
+    wlo[c] = a;
+    whi[c] = z;
+    if (z - a > 8192) return clus_fail(P, "gather window too wide (not banded)");
+  }
+  int wmax = 1, hcap = 1;
+  for (int c = 0; c < C; ++c) {
+    wmax = std::max(wmax, whi[c] - wlo[c]);
+    hcap = std::max(hcap, (whi[c] - wlo[c]) - (hi[c] - lo[c]));
+  }
+  // slices: rows of a block sorted by length (descending, stable)
+  std::vector<ClusCta> ctas(C);
+  std::vector<ClusSlice> slices;
+  std::vector<int2> rowmeta;
+  std::vector<std::vector<int>> order(C);
+  for (int c = 0; c < C; ++c) {
+    std::vector<int>& o = order[c];
+    for (int i = lo[c]; i < hi[c]; ++i) o.push_back(i);
+    std::stable_sort(o.begin(), o.end(),
+                     [&](int a, int b2) { return lenA(a) + lenB(a) > lenA(b2) + lenB(b2); });
+    ClusCta& t = ctas[c];
+    t.row_lo = lo[c];
+    t.row_hi = hi[c];
+    t.clo = lo[(c / csz) * csz];
+    t.chi = hi[(c / csz) * csz + csz - 1];
+    t.wlo = wlo[c];
+    t.wn = whi[c] - wlo[c];
+    t.hlo = lo[c] - wlo[c];
+    t.slice0 = (int)slices.size();
+    t.nslices = ((int)o.size() + 31) / 32;
+    for (int s = 0; s < t.nslices; ++s) {
+      ClusSlice sd{};
+      int wdt = 0;
+      for (int l = 0; l < 32; ++l) {
+        const int q = 32 * s + l;
+        if (q < (int)o.size()) wdt = std::max(wdt, lenA(o[q]) + lenB(o[q]));
+      }
+      sd.width = wdt;
+      sd.soff = -1;
+      slices.push_back(sd);
+      for (int l = 0; l < 32; ++l) {
+        const int q = 32 * s + l;
+        if (q < (int)o.size()) {
+          const int i = o[q];
+          rowmeta.push_back(make_int2(i, (lenA(i) << 16) | (lenA(i) + lenB(i))));
+        } else {
+          rowmeta.push_back(make_int2(-1, 0));
+        }
+      }
+    }
+  }
+  // shared-memory layout and the resident budget
+  DevInfo* d;
+  if ((rc = dev_info(&d))) return rc;
+  int optin = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, d->device));
+  auto al = [](size_t v) { return (v + 127) & ~(size_t)127; };
+  size_t off = 0;
+  P.off_rwin = (int)off;
+  off = al(off + sizeof(double) * (size_t)wmax);
+  P.off_shalo = (int)off;
+  off = al(off + sizeof(double) * (size_t)hcap);
+  P.off_whalo = (int)off;
+  off = al(off + sizeof(double) * 2 * (size_t)hcap);
+  P.off_val = (int)off;
+  const long long budget = (long long)optin - (long long)sizeof(ClusShared) - (long long)off - 1024;
+  if (budget < 0) return clus_fail(P, "window does not fit shared memory");
+  const long long E = budget / 10;  // 8 B value + 2 B column per resident entry
+  long long goff = 0;
+  for (int c = 0; c < C; ++c) {
+    long long used = 0;
+    const ClusCta& t = ctas[c];
+    for (int k = 0; k < kClusSlicesPerWarp; ++k)
+      for (int w = 0; w < kClusWarps; ++w) {
+        const int s = w + kClusWarps * k;
+        if (s >= t.nslices) continue;
+        ClusSlice& sd = slices[(size_t)t.slice0 + s];
+        const long long cnt = 32LL * sd.width;
+        if (used + cnt <= E) {
+          sd.soff = (int)used;
+          used += cnt;
+          P.resident += cnt;
+        } else {
+          P.streamed += cnt;
+        }
+      }
+    for (int s = 0; s < t.nslices; ++s) {
+      slices[(size_t)t.slice0 + s].goff = (int)goff;
+      goff += 32LL * slices[(size_t)t.slice0 + s].width;
+    }
+  }
+  if (goff >= (1LL << 31)) return clus_fail(P, "too many entries");
+  P.off_col = (int)(P.off_val + 8 * E);
+  P.smem = (size_t)P.off_col + 2 * (size_t)E;
+  // SELL values / window-relative columns
+  std::vector<double> gval((size_t)goff + 8, 0.0);
+  std::vector<unsigned short> gcol((size_t)goff + 8, 0);
+  for (int c = 0; c < C; ++c) {
+    const ClusCta& t = ctas[c];
+    for (int s = 0; s < t.nslices; ++s) {
+      const ClusSlice& sd = slices[(size_t)t.slice0 + s];
+      for (int l = 0; l < 32; ++l) {
+        const int2 rm = rowmeta[((size_t)t.slice0 + s) * 32 + l];
+        if (rm.x < 0) continue;
+        const int i = rm.x;
+        int u = 0;
+        for (int k = pA[i]; k < pA[(size_t)i + 1]; ++k, ++u) {
+          gval[(size_t)sd.goff + (size_t)u * 32 + l] = vA[k];
+          gcol[(size_t)sd.goff + (size_t)u * 32 + l] = (unsigned short)(iA[k] - t.wlo);
+        }
+        if (P.two)
+          for (int k = pB[i]; k < pB[(size_t)i + 1]; ++k, ++u) {
+            gval[(size_t)sd.goff + (size_t)u * 32 + l] = vB[k];
+            gcol[(size_t)sd.goff + (size_t)u * 32 + l] = (unsigned short)(iB[k] - t.wlo);
+          }
+      }
+    }
+  }
+  // halo sends: owner d -> every CTA c whose window holds d's rows
+  std::vector<ClusSend> sends;
+  for (int dd = 0; dd < C; ++dd) {
+    ctas[dd].send0 = (int)sends.size();
+    for (int c = 0; c < C; ++c) {
+      if (c == dd) continue;
+      const int a1 = std::max(wlo[c], lo[dd]), z1 = std::min(lo[c], hi[dd]);  // lower halo
+      if (a1 < z1) sends.push_back(ClusSend{c, a1, z1, a1 - wlo[c]});
+      const int a2 = std::max(hi[c], lo[dd]), z2 = std::min(whi[c], hi[dd]);  // upper halo
+      if (a2 < z2) sends.push_back(ClusSend{c, a2, z2, ctas[c].hlo + (a2 - hi[c])});
+    }
+    ctas[dd].nsend = (int)sends.size() - ctas[dd].send0;
+  }
+  if (sends.empty()) sends.push_back(ClusSend{0, 0, 0, 0});
+  // the grid of C CTAs in clusters of csz must be co-resident with this smem
+  CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
+  if (csz > 8) CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(csz);
+    cfg.blockDim = dim3(kClusThreads);
+    cfg.dynamicSmemBytes = P.smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = csz;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, kfn, &cfg) != cudaSuccess || ncl < C / csz) {
+      cudaGetLastError();
+      return clus_fail(P, "clusters not co-resident");
+    }
+  }
+  long long acct = 0;
+  if ((rc = dmalloc((void**)&P.ctas, sizeof(ClusCta) * ctas.size(), &acct)) ||
+      (rc = dmalloc((void**)&P.slices, sizeof(ClusSlice) * slices.size(), &acct)) ||
+      (rc = dmalloc((void**)&P.sends, sizeof(ClusSend) * sends.size(), &acct)) ||
+      (rc = dmalloc((void**)&P.rowmeta, sizeof(int2) * rowmeta.size(), &acct)) ||
+      (rc = dmalloc((void**)&P.gval, sizeof(double) * gval.size(), &acct)) ||
+      (rc = dmalloc((void**)&P.gcol, sizeof(unsigned short) * gcol.size(), &acct)))
+    return rc;
+  CUDA_TRY(cudaMemcpy(P.ctas, ctas.data(), sizeof(ClusCta) * ctas.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(P.slices, slices.data(), sizeof(ClusSlice) * slices.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(P.sends, sends.data(), sizeof(ClusSend) * sends.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(P.rowmeta, rowmeta.data(), sizeof(int2) * rowmeta.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(P.gval, gval.data(), sizeof(double) * gval.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(P.gcol, gcol.data(), sizeof(unsigned short) * gcol.size(), cudaMemcpyHostToDevice));
+  if (C > csz) {
+    if ((rc = dmalloc((void**)&P.ghalo, sizeof(double) * 2 * (size_t)C * hcap, &acct)) ||
+        (rc = dmalloc((void**)&P.gslots,
+                      sizeof(unsigned long long) * 2 * kClusSlotWords * (size_t)(C / csz),
+                      &acct)))
+      return rc;
+    CUDA_TRY(cudaMemset(P.ghalo, 0, sizeof(double) * 2 * (size_t)C * hcap));
+  }
+  m->bytes += acct;
+  P.hcap = hcap;
+  P.C = C;
+  P.cs = csz;
+  P.ok = true;
+  return SPCG_OK;
+}
+
+int launch_clus(const ClusPlan& P, const ClusArgs& a, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(P.C);
+  cfg.blockDim = dim3(kClusThreads);
+  cfg.dynamicSmemBytes = P.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = P.cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeCooperative;  // K > 1 clusters poll each other
+  at[1].val.cooperative = 1;
+  cfg.attrs = at;
+  // SPCG_CLUS_NONCOOP=1 (profiling only): ncu drops the cluster shape of a
+  // cooperative cluster launch; the K clusters still fit on the device at
+  // once, and the kernel refuses a launch whose cluster size is not the plan's
+  static const bool noncoop = getenv("SPCG_CLUS_NONCOOP") != nullptr;
+  cfg.numAttrs = (P.C > P.cs && !noncoop) ? 2 : 1;
+  if (P.two) CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_cg_kernel<true>, a));
+  else CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_cg_kernel<false>, a));
+  return SPCG_OK;
+}
+
+int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double* hist,
+               const spcg_cg_options* o, spcg_cg_result* out, cudaStream_t st) {
+  int rc;
+  const ClusPlan& P = m->cp;
+  if ((rc = ensure_ws(m, 1))) return rc;
+  Workspace& w = m->ws;
+  const long long max_iter = o->max_iter > 0 ? o->max_iter : std::max(1, m->n);
+  if (o->record_history && hist == nullptr)
+    return fail(SPCG_ERR_ARG, "record_history needs a history buffer");
+  ClusArgs a{};
+  a.ctas = P.ctas;
+  a.slices = P.slices;
+  a.sends = P.sends;
+  a.rowmeta = P.rowmeta;
+  a.gval = P.gval;
+  a.gcol = P.gcol;
+  a.b = b;
+  a.x0 = x0;
+  a.x = x;
+  a.scratch = w.q;
+  a.hist = hist;
+  a.res = w.res;
+  a.tol = o->tol;
+  a.max_iter = max_iter;
+  a.record_history = o->record_history;
+  a.recompute = o->recompute_final_residual;
+  a.off_rwin = P.off_rwin;
+  a.off_shalo = P.off_shalo;
+  a.off_whalo = P.off_whalo;
+  a.off_val = P.off_val;
+  a.off_col = P.off_col;
+  a.hcap = P.hcap;
+  a.ghalo = P.ghalo;
+  a.gslots = P.gslots;
+  a.cluster_size = P.cs;
+  if (P.gslots)
+    CUDA_TRY(cudaMemsetAsync(P.gslots, 0,
+                             sizeof(unsigned long long) * 2 * kClusSlotWords * (size_t)(P.C / P.cs),
+                             st));
+  static const bool tracing = getenv("SPCG_TRACE") != nullptr;
+  if (tracing) {
+    CUDA_TRY(cudaMalloc((void**)&a.trace, sizeof(unsigned long long) * 8 * (size_t)P.C));
+    CUDA_TRY(cudaMemsetAsync(a.trace, 0, sizeof(unsigned long long) * 8 * (size_t)P.C, st));
+  }
+  CUDA_TRY(cudaEventRecord(w.ev0, st));
+  if ((rc = launch_clus(P, a, st))) return rc;
+  CUDA_TRY(cudaEventRecord(w.ev1, st));
+  CUDA_TRY(cudaMemcpyAsync(w.h_res, w.res, sizeof(CgDevResult), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
+  const CgDevResult& r = *w.h_res;
+  if (r.status == ST_BAD_LAUNCH)
+    return fail(SPCG_ERR_CUDA, "cluster engine: kernel ran with a different cluster shape than "
+                               "planned (cluster launch attribute not honoured)");
+  if (a.trace) {
+    std::vector<unsigned long long> tv(8 * (size_t)P.C);
+    CUDA_TRY(cudaMemcpy(tv.data(), a.trace, sizeof(unsigned long long) * tv.size(),
+                        cudaMemcpyDeviceToHost));
+    cudaFree(a.trace);
+    double mean[7] = {0}, mx[7] = {0}, lead[7] = {0};
+    int nl = 0;
+    for (int c = 0; c < P.C; ++c)
+      for (int ph = 0; ph < 7; ++ph) {
+        mean[ph] += (double)tv[8 * c + ph] / P.C;
+        mx[ph] = std::max(mx[ph], (double)tv[8 * c + ph]);
+        if (c % std::max(1, P.cs) == 0) lead[ph] += (double)tv[8 * c + ph];
+      }
+    nl = std::max(1, P.C / std::max(1, P.cs));
+    const double it = (double)std::max<long long>(1, r.iterations) * 1e3;
+    fprintf(stderr,
+            "[spcg trace] ctas=%d cs=%d resident=%lld streamed=%lld us/iter mean(max): update %.3f(%.3f) "
+            "spmv %.3f(%.3f) allreduce %.3f(%.3f) | send_w %.3f b1wait %.3f b1exit->b2exit %.3f "
+            "| leaders: exchange %.3f b1wait %.3f poll->b2exit %.3f\n",
+            P.C, P.cs, P.resident, P.streamed, mean[0] / it, mx[0] / it, mean[1] / it, mx[1] / it,
+            mean[2] / it, mx[2] / it, mean[6] / it, mean[5] / it, mean[4] / it, lead[3] / nl / it,
+            lead[5] / nl / it, lead[4] / nl / it);
+    if (P.C > P.cs) {  // mean slot-post time of each cluster relative to the earliest
+      double mn = 1e300;
+      std::vector<double> pt;
+      for (int c = 0; c < P.C; c += P.cs) {
+        pt.push_back((double)tv[8 * c + 7] / it);
+        mn = std::min(mn, pt.back());
+      }
+      fprintf(stderr, "[spcg trace] cluster post offsets (us):");
+      for (double v : pt) fprintf(stderr, " %.2f", v - mn);
+      fprintf(stderr, "\n");
+    }
+  }
+  out->iterations = r.iterations;
+  out->converged = r.converged;
+  out->status = r.status;
+  out->fail_iteration = r.fail_iter;
+  out->final_relative_residual = r.final_rel;
+  out->b_norm = r.b_norm;
+  out->device_ms = ms;
+  out->kernel_launches = 1;
+  out->spmv_ms = 0.0;
+  out->spmv_launches = 0;
+  if (r.status != SPCG_OK) {
+    const char* what = r.status == SPCG_ERR_NOT_SPD ? "matrix not positive definite"
+                       : r.status == SPCG_ERR_NONFINITE_ALPHA ? "non-finite alpha"
+                       : r.status == SPCG_ERR_NONFINITE_RESIDUAL ? "non-finite residual"
+                                                                  : "non-finite beta";
+    return fail(r.status, std::string(what) + " at iteration " + std::to_string(r.fail_iter));
+  }
+  return SPCG_OK;
+}
