@@ -89,52 +89,56 @@ __device__ __forceinline__ double seq_sum(const double* prod, int ks, int ke) {
 
 // Symmetric L+D row i (diagonal last): g = sum_{j<=i} a_ij x_j, and the
 // transpose contributions a_ij * x_i scattered into y_j (j<i) with fp64 red.
+// Phase order matters: every gather of the round is issued before the first
+// red (a red is an asm statement with a memory clobber, so no load can be
+// hoisted above it, and each red waits for x_i -- the line's own, usually
+// uncached, value).  Interleaving "gather u, red u" serialised the round's
+// gathers behind that x_i load.
 template <class Src>
 __device__ __forceinline__ double sym_row_atomic(const double* v, const int* ix, int ks, int ke,
                                                  int i, double xi, const Src& src, double* y) {
   double acc = 0.0;
   for (int k = ks; k < ke; k += kUnroll) {
-    double pr[kUnroll];
+    int jj[kUnroll];
+    double gx[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      pr[u] = 0.0;
-      if (k + u < ke) {  // scatter issued at load time: only pr[] stays live
-        const int j = ix[k + u];
-        const double a = v[k + u];
-        pr[u] = __dmul_rn(a, src.get(j));
-        if (j != i) red_add_f64(y + j, __dmul_rn(a, xi));
-      }
-    }
+    for (int u = 0; u < kUnroll; ++u) jj[u] = (k + u < ke) ? ix[k + u] : i;
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) gx[u] = (k + u < ke) ? src.get(jj[u]) : 0.0;
+    // values re-read from shared memory (cheaper than keeping 8 live)
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u)
-      if (k + u < ke) acc = __dadd_rn(acc, pr[u]);
+      if (jj[u] != i) red_add_f64(y + jj[u], __dmul_rn(v[k + u], xi));
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (k + u < ke) acc = __dadd_rn(acc, __dmul_rn(v[k + u], gx[u]));
   }
   return acc;
 }
 
 // CSC column j: y[row_k] += a_kj * xj (red), and (if GATHER) the transposed
-// gather g = sum_k a_kj x_{row_k} that makes p.Ap = sum_j p_j g_j.
+// gather g = sum_k a_kj x_{row_k} that makes p.Ap = sum_j p_j g_j.  Gathers
+// of a round go out before its reds (see sym_row_atomic).
 template <bool GATHER, class Src>
 __device__ __forceinline__ double csc_col(const double* v, const int* ix, int ks, int ke,
                                           double xj, const Src& src, double* y) {
   double acc = 0.0;
   for (int k = ks; k < ke; k += kUnroll) {
-    double pr[kUnroll];
+    int rr[kUnroll];
+    double gx[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      if (k + u < ke) {
-        const int row = ix[k + u];
-        const double a = v[k + u];
-        red_add_f64(y + row, __dmul_rn(a, xj));
-        pr[u] = GATHER ? __dmul_rn(a, src.get(row)) : 0.0;
-      } else {
-        pr[u] = 0.0;
-      }
+    for (int u = 0; u < kUnroll; ++u) rr[u] = (k + u < ke) ? ix[k + u] : 0;
+    if (GATHER) {
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) gx[u] = (k + u < ke) ? src.get(rr[u]) : 0.0;
     }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (k + u < ke) red_add_f64(y + rr[u], __dmul_rn(v[k + u], xj));
     if (GATHER) {
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u)
-        if (k + u < ke) acc = __dadd_rn(acc, pr[u]);
+        if (k + u < ke) acc = __dadd_rn(acc, __dmul_rn(v[k + u], gx[u]));
     }
   }
   return acc;
