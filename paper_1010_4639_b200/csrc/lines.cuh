@@ -105,13 +105,15 @@ __device__ __forceinline__ double sym_row_atomic(const double* v, const int* ix,
     for (int u = 0; u < kUnroll; ++u) jj[u] = (k + u < ke) ? ix[k + u] : i;
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) gx[u] = (k + u < ke) ? src.get(jj[u]) : 0.0;
-    // values re-read from shared memory (cheaper than keeping 8 live)
+    // one shared-memory read of each value serves its red and its product
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u)
-      if (jj[u] != i) red_add_f64(y + jj[u], __dmul_rn(v[k + u], xi));
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u)
-      if (k + u < ke) acc = __dadd_rn(acc, __dmul_rn(v[k + u], gx[u]));
+    for (int u = 0; u < kUnroll; ++u) {
+      if (k + u < ke) {
+        const double a = v[k + u];
+        if (jj[u] != i) red_add_f64(y + jj[u], __dmul_rn(a, xi));
+        acc = __dadd_rn(acc, __dmul_rn(a, gx[u]));
+      }
+    }
   }
   return acc;
 }
@@ -133,12 +135,12 @@ __device__ __forceinline__ double csc_col(const double* v, const int* ix, int ks
       for (int u = 0; u < kUnroll; ++u) gx[u] = (k + u < ke) ? src.get(rr[u]) : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u)
-      if (k + u < ke) red_add_f64(y + rr[u], __dmul_rn(v[k + u], xj));
-    if (GATHER) {
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u)
-        if (k + u < ke) acc = __dadd_rn(acc, __dmul_rn(v[k + u], gx[u]));
+    for (int u = 0; u < kUnroll; ++u) {
+      if (k + u < ke) {
+        const double a = v[k + u];
+        red_add_f64(y + rr[u], __dmul_rn(a, xj));
+        if (GATHER) acc = __dadd_rn(acc, __dmul_rn(a, gx[u]));
+      }
     }
   }
   return acc;
