@@ -74,14 +74,27 @@ __global__ void __launch_bounds__(kBlock, 2)
   double pq = 0.0;
   for (int j = 0; j < P.m; ++j) {
     const int s = pipe_acquire(P, sm, j);
-    bool active = false;
-    int i = -1;
-    // atomic formats (single GPU): transposed scatter into q (zeroed by
-    // pass B), p.Ap from the line's own gather (line_pq)
-    const LineOut o = tile_line<FMT, true>(sm, s, M, src, q, active, i, sm.val[s]);
-    if (active) {
-      finish_plain<FMT>(o, i, q);
-      pq += line_pq<FMT>(o);
+    if (wide_tile<FMT>(sm, s)) {
+      LineOut o2[2];
+      bool act[2];
+      int li[2];
+      csr_line_pair(sm, s, src, o2, act, li, nullptr);
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+        if (act[t]) {
+          q[li[t]] = o2[t].q;
+          pq += o2[t].xi * o2[t].q;
+        }
+    } else {
+      bool active = false;
+      int i = -1;
+      // atomic formats (single GPU): transposed scatter into q (zeroed by
+      // pass B), p.Ap from the line's own gather (line_pq)
+      const LineOut o = tile_line<FMT, true>(sm, s, M, src, q, active, i, sm.val[s]);
+      if (active) {
+        finish_plain<FMT>(o, i, q);
+        pq += line_pq<FMT>(o);
+      }
     }
     pipe_release<TWO>(P, sm, M, s);
   }
@@ -114,10 +127,20 @@ __global__ void __launch_bounds__(kBlock, 2)
   SrcPlain src{x_ext};
   for (int j = 0; j < P.m; ++j) {
     const int s = pipe_acquire(P, sm, j);
-    bool active = false;
-    int i = -1;
-    const LineOut o = tile_line<FMT, false>(sm, s, M, src, y, active, i, sm.val[s]);
-    if (active) finish_plain<FMT>(o, i, y);
+    if (wide_tile<FMT>(sm, s)) {
+      LineOut o2[2];
+      bool act[2];
+      int li[2];
+      csr_line_pair(sm, s, src, o2, act, li, nullptr);
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+        if (act[t]) y[li[t]] = o2[t].q;
+    } else {
+      bool active = false;
+      int i = -1;
+      const LineOut o = tile_line<FMT, false>(sm, s, M, src, y, active, i, sm.val[s]);
+      if (active) finish_plain<FMT>(o, i, y);
+    }
     pipe_release<TWO>(P, sm, M, s);
   }
   pipe_drain(P, sm);

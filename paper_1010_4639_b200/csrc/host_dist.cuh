@@ -274,7 +274,7 @@ int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const dou
   int rc;
   if ((rc = dev_info(&di))) return rc;
   DistWorkspace& d = m->dw;
-  const MatView v = view(m, FMT == K_SCSR_PRIV);
+  const MatView v = view_stream(m, FMT == K_SCSR_PRIV);
   const long long nloc = m->n, next = d.next;
   const int G = std::max(1, std::min(std::max(1, v.ntiles), di->spmv_grid));
   const int GE = 2 * di->sms;

@@ -183,8 +183,18 @@ int finish_matrix(spcg_matrix_s* m, const std::vector<int>& ptr, const int* idx,
   }
   const int target = target_tiles();
   std::vector<int4> desc;
-  build_tiles(m->n, ptr, nullptr, target, desc, nullptr, tile_line_cap(m->n ? ptr[m->n] : 0, m->n));
+  const int cap = tile_line_cap(m->n ? ptr[m->n] : 0, m->n);
+  build_tiles(m->n, ptr, nullptr, target, desc, nullptr, cap);
   if ((rc = upload_tiles(m->t1, desc, nullptr, &m->bytes))) return rc;
+  // wide tiles only where their second line slot fills well (>= 3/4 of a
+  // kTileLines tile at the average row length: P2's 5-entry rows, not P3's
+  // 7, where the mostly idle second slot cost 17 % on the 7-point stencil)
+  const long long ent = m->n ? (long long)ptr[m->n] : 0;
+  if (kWideLines > kTileLines && m->fmt == SPCG_FMT_CSR && cap == kTileLines && m->n > 0 &&
+      ent * (long long)(kTileLines + kTileLines / 2) <= (long long)kTileNnz * m->n) {
+    build_tiles(m->n, ptr, nullptr, target, desc, nullptr, kWideLines);
+    if ((rc = upload_tiles(m->t1w, desc, nullptr, &m->bytes))) return rc;
+  }
   return SPCG_OK;
 }
 
@@ -218,7 +228,7 @@ void free_matrix(spcg_matrix_s* m) {
   };
   F(m->A.ptr); F(m->A.idx); F(m->A.val);
   F(m->B.ptr); F(m->B.idx); F(m->B.val);
-  F(m->t1.desc); F(m->t1.descB); F(m->t2.desc); F(m->t2.descB); F(m->t1.win); F(m->t2.win);
+  F(m->t1.desc); F(m->t1.descB); F(m->t1w.desc); F(m->t2.desc); F(m->t2.descB); F(m->t1.win); F(m->t2.win);
   Workspace& w = m->ws;
   F(w.r); F(w.p0); F(w.p1); F(w.q); F(w.part); F(w.slots); F(w.res);
   F(w.b); F(w.x); F(w.x0); F(w.hist); F(w.cg1); F(w.rp);
@@ -252,6 +262,19 @@ MatView view(const spcg_matrix_s* m, bool priv) {
   v.idxB = m->B.idx;
   v.valB = m->B.val;
   v.twin = t.win;
+  return v;
+}
+
+// Tile table of the streaming passes (per-pass engine, standalone SpMV):
+// the wide table when the matrix has one.
+MatView view_stream(const spcg_matrix_s* m, bool priv) {
+  MatView v = view(m, priv);
+  if (!priv && m->t1w.ntiles > 0) {
+    v.ntiles = m->t1w.ntiles;
+    v.tdesc = m->t1w.desc;
+    v.tdescB = nullptr;
+    v.twin = nullptr;
+  }
   return v;
 }
 
@@ -333,7 +356,7 @@ int do_spmv(spcg_matrix_s* m, const double* x, double* y, int accumulation, cuda
   if ((rc = dev_info(&d))) return rc;
   const int kf = kfmt_of(m, accumulation);
   if (kf == K_SCSR_PRIV && !m->hasB) return fail(SPCG_ERR_UNSUPPORTED, "no L^T for privatized mode");
-  const MatView v = view(m, kf == K_SCSR_PRIV);
+  const MatView v = view_stream(m, kf == K_SCSR_PRIV);
   if (m->n == 0) return SPCG_OK;
   if (kf == K_SCSR_ATOMIC || kf == K_CSC)
     CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(double) * (size_t)m->n, st));

@@ -528,6 +528,59 @@ __device__ __forceinline__ LineOut tile_line(Smem& sm, int s, const MatView& M, 
   return o;
 }
 
+// Wide CSR tile (more than kBlock lines, thread-per-row rows): thread t
+// computes lines row0 + t and row0 + t + kBlock with both lines' gathers in
+// flight together; each line is summed sequentially in storage order
+// (bitwise csr_gather).  Warp-uniform control flow.
+template <class Src>
+__device__ __forceinline__ void csr_line_pair(const Smem& sm, int s, const Src& src,
+                                              LineOut (&o)[2], bool (&act)[2], int (&li)[2],
+                                              const double* xpre) {
+  const StageMeta& mt = sm.meta[s];
+  const double* v = sm.val[s];
+  const int* ix = sm.idx[s];
+  int ks[2], len[2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    li[t] = mt.row0 + (int)threadIdx.x + t * kBlock;
+    act[t] = li[t] < mt.row1;
+    o[t] = LineOut{0.0, 0.0, 0.0, 0.0};
+    ks[t] = 0;
+    len[t] = 0;
+    if (act[t]) {
+      const int lr = li[t] - mt.r0a;
+      ks[t] = sm.rpA[s][lr] - mt.kA0a;
+      len[t] = sm.rpA[s][lr + 1] - mt.kA0a - ks[t];
+      o[t].xi = src.get(li[t]);
+      if (xpre) o[t].xo = xpre[li[t]];
+    }
+  }
+  constexpr int U = 8;
+  double acc0 = 0.0, acc1 = 0.0;
+  const int L = max(len[0], len[1]);
+  for (int base = 0; base < L; base += U) {
+    double p0[U], p1[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      p0[u] = (base + u < len[0]) ? __dmul_rn(v[ks[0] + base + u], src.get(ix[ks[0] + base + u])) : 0.0;
+      p1[u] = (base + u < len[1]) ? __dmul_rn(v[ks[1] + base + u], src.get(ix[ks[1] + base + u])) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (base + u < len[0]) acc0 = __dadd_rn(acc0, p0[u]);
+      if (base + u < len[1]) acc1 = __dadd_rn(acc1, p1[u]);
+    }
+  }
+  o[0].q = acc0;
+  o[1].q = acc1;
+}
+
+// True when staged tile s is a wide CSR tile (handled by csr_line_pair).
+template <int FMT>
+__device__ __forceinline__ bool wide_tile(const Smem& sm, int s) {
+  return FMT == K_CSR && !sm.meta[s].is_long && sm.meta[s].row1 - sm.meta[s].row0 > kBlock;
+}
+
 // Finish a line of a plain SpMV y = A x (no CG bookkeeping).
 template <int FMT>
 __device__ __forceinline__ void finish_plain(const LineOut& o, int i, double* y) {

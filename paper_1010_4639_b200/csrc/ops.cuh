@@ -18,10 +18,20 @@ __global__ void __launch_bounds__(kBlock, 2) spmv_kernel(const MatView M, const 
   SrcPlain src{x};
   for (int j = 0; j < P.m; ++j) {
     const int s = pipe_acquire(P, sm, j);
-    bool active = false;
-    int line = -1;
-    const LineOut o = tile_line<FMT, false>(sm, s, M, src, y, active, line, sm.val[s]);
-    if (active) finish_plain<FMT>(o, line, y);
+    if (wide_tile<FMT>(sm, s)) {
+      LineOut o2[2];
+      bool act[2];
+      int li[2];
+      csr_line_pair(sm, s, src, o2, act, li, nullptr);
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+        if (act[t]) y[li[t]] = o2[t].q;
+    } else {
+      bool active = false;
+      int line = -1;
+      const LineOut o = tile_line<FMT, false>(sm, s, M, src, y, active, line, sm.val[s]);
+      if (active) finish_plain<FMT>(o, line, y);
+    }
     pipe_release<TWO>(P, sm, M, s);
   }
   pipe_drain(P, sm);

@@ -222,6 +222,7 @@ struct spcg_matrix_s {
   Seg A, B;
   bool hasB = false;
   Tiles t1, t2;
+  Tiles t1w;  // wide tiles (<= kWideLines lines) for the streaming passes; short-row CSR only
   long long bytes = 0;
   Workspace ws;
   // row block of a sharded matrix (rows [row0,row1) of an n_global system)

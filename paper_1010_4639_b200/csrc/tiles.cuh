@@ -42,6 +42,15 @@ constexpr int kStages = SPCG_STAGES;  // TMA ring depth (tiles in flight + 1)
 #endif
 constexpr int kStreamMinBlocks = SPCG_STREAM_MINB;  // CTAs/SM targeted by streaming kernels
 constexpr int kRpCap = kTileLines + 8;
+// Streaming passes over short-row CSR matrices use "wide" tiles of up to
+// kWideLines lines (two per thread), so a stage carries up to kTileNnz
+// entries instead of 512 x (row length): more bytes in flight per SM
+// (P2's 5-entry rows filled only 2,560 of a stage's 4,096 entries).
+#ifndef SPCG_WIDE
+#define SPCG_WIDE 2
+#endif
+constexpr int kWideLines = SPCG_WIDE * kBlock;
+constexpr int kRpCapA = kWideLines + 8;
 constexpr int kNzCap = kTileNnz + 16;
 
 // Kernel-level storage variants.
@@ -77,7 +86,7 @@ struct StageMeta {
 struct __align__(16) Smem {
   double val[kStages][kNzCap];
   int idx[kStages][kNzCap];
-  int rpA[kStages][kRpCap];
+  int rpA[kStages][kRpCapA];
   int rpB[kStages][kRpCap];
   uint64_t full[kStages];
   StageMeta meta[kStages];

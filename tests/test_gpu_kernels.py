@@ -155,3 +155,48 @@ def test_device_generators_match_host(kind, dims):
         rs, ci, v = O.stencil(kind, dims, part="lower")
         off, idx, val = dm.download()
         assert (off == rs).all() and (idx == ci).all() and (val == v).all()
+
+
+@pytest.mark.parametrize("ragged", [False, True])
+def test_spmv_wide_tiles_bitwise(ragged):
+    """Short-row CSR matrices large enough for wide tiles (two lines per
+    thread in the streaming passes) stay bitwise equal to csr_gather."""
+    from paper_1010_4639_b200 import spmv_full
+    from paper_1010_4639_b200.core import CsrMatrix
+
+    rng = np.random.default_rng(77 + ragged)
+    n = 400_000
+    lens = (rng.choice([0, 1, 2, 3, 4, 5, 6, 9, 17, 24], size=n,
+                       p=[.06, .1, .12, .2, .2, .17, .1, .03, .015, .005])
+            if ragged else np.full(n, 5))
+    rows = np.repeat(np.arange(n), lens)
+    cols = np.clip(rows + rng.integers(-3000, 3000, size=len(rows)), 0, n - 1)
+    order = np.lexsort((cols, rows))
+    rows, cols = rows[order], cols[order]
+    keep = np.ones(len(rows), bool)
+    keep[1:] = (rows[1:] != rows[:-1]) | (cols[1:] != cols[:-1])
+    rows, cols = rows[keep], cols[keep]
+    rs = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(rs, rows + 1, 1)
+    rs = np.cumsum(rs)
+    vals = rng.standard_normal(len(cols))
+    a = CsrMatrix(n=n, row_start=rs, col_idx=cols.astype(np.int64), values=vals)
+    x = rng.standard_normal(n)
+    y = spmv_full(a, x)
+    ref = O.spmv_full(a.row_start, a.col_idx, a.values, x)
+    assert (y == ref).all()
+
+
+def test_cg_wide_tiles_poisson2d_matches_reference():
+    """CG on a 2D Poisson system with wide tiles (640^2 rows) against the
+    reference CG: same iteration count, x within 1e-8."""
+    from paper_1010_4639_b200 import CgOptions, cg_solve
+    from paper_1010_4639_b200.genprob import poisson2d, rhs_for
+
+    a = poisson2d(640, 640)
+    b, _ = rhs_for(a, seed=3)
+    ref = O.cg_solve("csr", a.row_start, a.col_idx, a.values, b, max_iter=5000)
+    r = cg_solve(a, b, opts=CgOptions(max_iter=5000))
+    assert r.converged
+    assert abs(r.iterations - ref.iterations) <= max(1, ref.iterations // 100)
+    assert np.linalg.norm(r.x - ref.x) / np.linalg.norm(ref.x) <= 1e-8
