@@ -139,6 +139,12 @@ int ensure_dist_ws(spcg_matrix_s* m, long long send_total) {
       if (q) cudaFree(q);
     if (d.S) cudaFree(d.S);
     if (d.h_S) cudaFreeHost(d.h_S);
+    for (int c = 0; c < 2; ++c) {
+      if (d.h_Sc[c]) cudaFreeHost(d.h_Sc[c]);
+      if (d.cev[c]) cudaEventDestroy(d.cev[c]);
+      d.h_Sc[c] = nullptr;
+      d.cev[c] = nullptr;
+    }
     if (d.ev0) cudaEventDestroy(d.ev0);
     if (d.ev1) cudaEventDestroy(d.ev1);
     const size_t eb = sizeof(double) * (size_t)std::max<long long>(1, next);
@@ -152,6 +158,10 @@ int ensure_dist_ws(spcg_matrix_s* m, long long send_total) {
     if ((rc = dmalloc((void**)&d.part, sizeof(double) * 4096, nullptr))) return rc;
     if ((rc = dmalloc((void**)&d.S, sizeof(StepState), nullptr))) return rc;
     CUDA_TRY(cudaMallocHost((void**)&d.h_S, sizeof(StepState)));
+    for (int c = 0; c < 2; ++c) {
+      CUDA_TRY(cudaMallocHost((void**)&d.h_Sc[c], sizeof(StepState)));
+      CUDA_TRY(cudaEventCreateWithFlags(&d.cev[c], cudaEventDisableTiming));
+    }
     CUDA_TRY(cudaEventCreate(&d.ev0));
     CUDA_TRY(cudaEventCreate(&d.ev1));
     d.next = next;
@@ -321,22 +331,25 @@ int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const dou
   if ((rc = halo_exchange(H, d, p, p, st, &launches))) return rc;
   CUDA_TRY(cudaGetLastError());
   // CG loop; the host enqueues chunks of iterations and polls the device-side
-  // done flag between chunks (iterations after `done` are no-ops on every
-  // rank, so the NCCL calls stay matched)
+  // done flag of chunk c while chunk c + 1 is already queued (double
+  // buffered), so the GPU never idles while the host enqueues.  Iterations
+  // after `done` are no-ops on every rank, so the NCCL calls stay matched;
+  // the one chunk enqueued past convergence costs only empty launches.
   const int chunk = 16;
   const bool timing = o->timing != 0;
-  if (timing && !d.tev[0][0])
-    for (int a = 0; a < 2; ++a)
-      for (int c = 0; c < chunk; ++c) CUDA_TRY(cudaEventCreate(&d.tev[a][c]));
+  if (timing && !d.tev[0][0][0])
+    for (int bb = 0; bb < 2; ++bb)
+      for (int a = 0; a < 2; ++a)
+        for (int c = 0; c < chunk; ++c) CUDA_TRY(cudaEventCreate(&d.tev[bb][a][c]));
   double spmv_ms = 0.0;
   long long spmv_n = 0, k_before = 0, iter_enq = 0;
 #ifndef SPCG_ALTERNATE
 #define SPCG_ALTERNATE 1
 #endif
   constexpr bool kAlternate = SPCG_ALTERNATE != 0;
-  for (;;) {
+  auto enqueue_chunk = [&](int bb) -> int {
     for (int c = 0; c < chunk; ++c) {
-      if (timing) CUDA_TRY(cudaEventRecord(d.tev[0][c], st));
+      if (timing) CUDA_TRY(cudaEventRecord(d.tev[bb][0][c], st));
       // alternate traversal directions pass to pass (A, B, C, A, ...): each
       // pass starts on the lines the previous one wrote last (still in L2)
       const int dirA = kAlternate ? (int)((iter_enq & 1) == 0) : 0;
@@ -344,34 +357,49 @@ int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const dou
       va.rev = dirA;
       va.tree = o->row_sums == 0;  // auto: reassociated long-row sums in pass A
       dist_spmv_pq<FMT><<<G, kBlock, sm, st>>>(va, d.S, p, d.q, d.part);
-      if (timing) CUDA_TRY(cudaEventRecord(d.tev[1][c], st));
-      if ((rc = allreduce_red(H, d.S, st))) return rc;
-      if (kRev && (rc = reverse_halo(H, d, d.q, nhalo, st, &launches))) return rc;
+      if (timing) CUDA_TRY(cudaEventRecord(d.tev[bb][1][c], st));
+      int rc2;
+      if ((rc2 = allreduce_red(H, d.S, st))) return rc2;
+      if (kRev && (rc2 = reverse_halo(H, d, d.q, nhalo, st, &launches))) return rc2;
       dist_scalar<<<1, 1, 0, st>>>(2, d.S, hist);
       dist_elem<<<GE, kBlock, 0, st>>>(2, nloc, d.S, nullptr, d.q, r, nullptr, d.part, kAtom,
                                        kAlternate ? 1 - dirA : 0);
-      if ((rc = allreduce_red(H, d.S, st))) return rc;
+      if ((rc2 = allreduce_red(H, d.S, st))) return rc2;
       dist_scalar<<<1, 1, 0, st>>>(3, d.S, hist);
       dist_update<<<GE, kBlock, 0, st>>>(nloc, d.S, r, p, x, xv, dirA);
       ++iter_enq;
       launches += 5;
-      if ((rc = halo_exchange(H, d, p, p, st, &launches))) return rc;
+      if ((rc2 = halo_exchange(H, d, p, p, st, &launches))) return rc2;
     }
     CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaMemcpyAsync(d.h_S, d.S, sizeof(StepState), cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
+    CUDA_TRY(cudaMemcpyAsync(d.h_Sc[bb], d.S, sizeof(StepState), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaEventRecord(d.cev[bb], st));
+    return SPCG_OK;
+  };
+  // the host-callback transport synchronises inside every exchange: no
+  // point (and no room) for a second chunk in flight
+  const bool two = H.hc == nullptr;
+  if ((rc = enqueue_chunk(0))) return rc;
+  for (long long ci = 0;; ++ci) {
+    const int bb = (int)(ci & 1);
+    if (two && (rc = enqueue_chunk(bb ^ 1))) return rc;
+    CUDA_TRY(cudaEventSynchronize(d.cev[bb]));
+    const StepState& hs = *d.h_Sc[bb];
     if (timing) {  // only the passes that did work (later ones returned at once)
-      const long long ran = std::min<long long>(chunk, d.h_S->k - k_before +
-                                                           (d.h_S->status != 0 ? 1 : 0));
+      const long long ran = std::min<long long>(chunk, hs.k - k_before + (hs.status != 0 ? 1 : 0));
       for (long long c = 0; c < ran; ++c) {
         float t = 0.f;
-        CUDA_TRY(cudaEventElapsedTime(&t, d.tev[0][c], d.tev[1][c]));
+        CUDA_TRY(cudaEventElapsedTime(&t, d.tev[bb][0][c], d.tev[bb][1][c]));
         spmv_ms += t;
         ++spmv_n;
       }
-      k_before = d.h_S->k;
+      k_before = hs.k;
     }
-    if (d.h_S->done) break;
+    if (hs.done) {
+      *d.h_S = hs;
+      break;
+    }
+    if (!two && (rc = enqueue_chunk(bb ^ 1))) return rc;
   }
   // a converged solve skipped its pass C: x += alpha_K p_K; then the true residual
   dist_x<<<GE, kBlock, 0, st>>>(1, nloc, d.S, p, x);

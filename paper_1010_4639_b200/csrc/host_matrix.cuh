@@ -243,9 +243,13 @@ void free_matrix(spcg_matrix_s* m) {
   if (d.h_S) cudaFreeHost(d.h_S);
   if (d.ev0) cudaEventDestroy(d.ev0);
   if (d.ev1) cudaEventDestroy(d.ev1);
-  for (int a = 0; a < 2; ++a)
-    for (int c = 0; c < 16; ++c)
-      if (d.tev[a][c]) cudaEventDestroy(d.tev[a][c]);
+  for (int bb = 0; bb < 2; ++bb) {
+    if (d.h_Sc[bb]) cudaFreeHost(d.h_Sc[bb]);
+    if (d.cev[bb]) cudaEventDestroy(d.cev[bb]);
+    for (int a = 0; a < 2; ++a)
+      for (int c = 0; c < 16; ++c)
+        if (d.tev[bb][a][c]) cudaEventDestroy(d.tev[bb][a][c]);
+  }
 }
 
 MatView view(const spcg_matrix_s* m, bool priv) {

@@ -183,12 +183,14 @@ struct DistWorkspace {
   double* part = nullptr;
   StepState* S = nullptr;
   StepState* h_S = nullptr;  // pinned
+  StepState* h_Sc[2] = {nullptr, nullptr};  // pinned, per in-flight chunk
+  cudaEvent_t cev[2] = {nullptr, nullptr};  // chunk copies done
   double* send_buf = nullptr;
   long long send_cap = 0;
   int* send_idx = nullptr;
   long long send_idx_cap = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  cudaEvent_t tev[2][16] = {};  // per-iteration SpMV-pass timing (opts.timing)
+  cudaEvent_t tev[2][2][16] = {};  // [chunk buffer][start/end][iteration]: SpMV-pass timing
 };
 
 }  // namespace
