@@ -61,7 +61,7 @@ __device__ __forceinline__ void last_block_sum(double v, SM& sm, double* part, S
 
 // pass A: q = A p_ext, red = p.q partial (skipped once done)
 template <int FMT>
-__global__ void __launch_bounds__(kBlock, 2)
+__global__ void __launch_bounds__(kBlock, kStreamMinBlocks)
     dist_spmv_pq(const MatView M, StepState* S, const double* p_ext, double* q, double* part) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(256) dist_unpack_add(long long total, const in
 
 // y = A x_ext (plain gather; initial / true residual)
 template <int FMT>
-__global__ void __launch_bounds__(kBlock, 2)
+__global__ void __launch_bounds__(kBlock, kStreamMinBlocks)
     dist_spmv(const MatView M, const double* x_ext, double* y) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);

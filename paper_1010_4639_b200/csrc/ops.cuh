@@ -7,7 +7,7 @@ namespace spcg {
 
 // y = A x over the tile table (same staging + line bodies as the CG kernel).
 template <int FMT>
-__global__ void __launch_bounds__(kBlock, 2) spmv_kernel(const MatView M, const double* x,
+__global__ void __launch_bounds__(kBlock, kStreamMinBlocks) spmv_kernel(const MatView M, const double* x,
                                                          double* y) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
