@@ -59,8 +59,10 @@ __device__ __forceinline__ void last_block_sum(double v, SM& sm, double* part, S
   }
 }
 
-// pass A: q = A p_ext, red = p.q partial (skipped once done)
-template <int FMT>
+// pass A: q = A p_ext, red = p.q partial (skipped once done).  WIDE: the
+// view carries wide tiles (short-row CSR); a separate instantiation so the
+// other kernels do not pay the two-line body's registers.
+template <int FMT, bool WIDE = false>
 __global__ void __launch_bounds__(kBlock, kStreamMinBlocks)
     dist_spmv_pq(const MatView M, StepState* S, const double* p_ext, double* q, double* part) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -74,7 +76,7 @@ __global__ void __launch_bounds__(kBlock, kStreamMinBlocks)
   double pq = 0.0;
   for (int j = 0; j < P.m; ++j) {
     const int s = pipe_acquire(P, sm, j);
-    if (wide_tile<FMT>(sm, s)) {
+    if (WIDE && wide_tile<FMT>(sm, s)) {
       LineOut o2[2];
       bool act[2];
       int li[2];
@@ -115,7 +117,7 @@ __global__ void __launch_bounds__(256) dist_unpack_add(long long total, const in
 }
 
 // y = A x_ext (plain gather; initial / true residual)
-template <int FMT>
+template <int FMT, bool WIDE = false>
 __global__ void __launch_bounds__(kBlock, kStreamMinBlocks)
     dist_spmv(const MatView M, const double* x_ext, double* y) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -127,7 +129,7 @@ __global__ void __launch_bounds__(kBlock, kStreamMinBlocks)
   SrcPlain src{x_ext};
   for (int j = 0; j < P.m; ++j) {
     const int s = pipe_acquire(P, sm, j);
-    if (wide_tile<FMT>(sm, s)) {
+    if (WIDE && wide_tile<FMT>(sm, s)) {
       LineOut o2[2];
       bool act[2];
       int li[2];

@@ -317,7 +317,8 @@ int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const dou
     CUDA_TRY(cudaMemcpyAsync(d.tmp_ext, x0, sizeof(double) * (size_t)nloc,
                              cudaMemcpyDeviceToDevice, st));
     if ((rc = halo_exchange(H, d, x0, d.tmp_ext, st, &launches))) return rc;
-    dist_spmv<FMT><<<G, kBlock, sm, st>>>(v, d.tmp_ext, d.q);
+    if (FMT == K_CSR && v.wide) dist_spmv<K_CSR, true><<<G, kBlock, sm, st>>>(v, d.tmp_ext, d.q);
+    else dist_spmv<FMT><<<G, kBlock, sm, st>>>(v, d.tmp_ext, d.q);
     if (kRev && (rc = reverse_halo(H, d, d.q, nhalo, st, &launches))) return rc;
     dist_elem<<<GE, kBlock, 0, st>>>(1, nloc, d.S, b, d.q, r, p, d.part, kAtom);
     launches += 2;
@@ -356,7 +357,10 @@ int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const dou
       MatView va = v;
       va.rev = dirA;
       va.tree = o->row_sums == 0;  // auto: reassociated long-row sums in pass A
-      dist_spmv_pq<FMT><<<G, kBlock, sm, st>>>(va, d.S, p, d.q, d.part);
+      if (FMT == K_CSR && v.wide)
+        dist_spmv_pq<K_CSR, true><<<G, kBlock, sm, st>>>(va, d.S, p, d.q, d.part);
+      else
+        dist_spmv_pq<FMT><<<G, kBlock, sm, st>>>(va, d.S, p, d.q, d.part);
       if (timing) CUDA_TRY(cudaEventRecord(d.tev[bb][1][c], st));
       int rc2;
       if ((rc2 = allreduce_red(H, d.S, st))) return rc2;
@@ -408,7 +412,8 @@ int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const dou
     CUDA_TRY(cudaMemcpyAsync(d.tmp_ext, x, sizeof(double) * (size_t)nloc,
                              cudaMemcpyDeviceToDevice, st));
     if ((rc = halo_exchange(H, d, x, d.tmp_ext, st, &launches))) return rc;
-    dist_spmv<FMT><<<G, kBlock, sm, st>>>(v, d.tmp_ext, d.q);
+    if (FMT == K_CSR && v.wide) dist_spmv<K_CSR, true><<<G, kBlock, sm, st>>>(v, d.tmp_ext, d.q);
+    else dist_spmv<FMT><<<G, kBlock, sm, st>>>(v, d.tmp_ext, d.q);
     if (kRev && (rc = reverse_halo(H, d, d.q, nhalo, st, &launches))) return rc;
     dist_elem<<<GE, kBlock, 0, st>>>(3, nloc, d.S, b, d.q, nullptr, nullptr, d.part, 0);
     if ((rc = allreduce_red(H, d.S, st))) return rc;

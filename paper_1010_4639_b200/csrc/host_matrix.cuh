@@ -278,6 +278,7 @@ MatView view_stream(const spcg_matrix_s* m, bool priv) {
     v.tdesc = m->t1w.desc;
     v.tdescB = nullptr;
     v.twin = nullptr;
+    v.wide = 1;
   }
   return v;
 }
@@ -349,7 +350,8 @@ int launch_cg1(const Cg1Args& a, int grid, cudaStream_t st) {
 
 template <int FMT>
 int launch_spmv(const MatView& v, const double* x, double* y, int grid, cudaStream_t st) {
-  spmv_kernel<FMT><<<grid, kBlock, sizeof(Smem), st>>>(v, x, y);
+  if (FMT == K_CSR && v.wide) spmv_kernel<K_CSR, true><<<grid, kBlock, sizeof(Smem), st>>>(v, x, y);
+  else spmv_kernel<FMT><<<grid, kBlock, sizeof(Smem), st>>>(v, x, y);
   CUDA_TRY(cudaGetLastError());
   return SPCG_OK;
 }

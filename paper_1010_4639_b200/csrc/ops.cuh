@@ -6,7 +6,7 @@
 namespace spcg {
 
 // y = A x over the tile table (same staging + line bodies as the CG kernel).
-template <int FMT>
+template <int FMT, bool WIDE = false>
 __global__ void __launch_bounds__(kBlock, kStreamMinBlocks) spmv_kernel(const MatView M, const double* x,
                                                          double* y) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -18,7 +18,7 @@ __global__ void __launch_bounds__(kBlock, kStreamMinBlocks) spmv_kernel(const Ma
   SrcPlain src{x};
   for (int j = 0; j < P.m; ++j) {
     const int s = pipe_acquire(P, sm, j);
-    if (wide_tile<FMT>(sm, s)) {
+    if (WIDE && wide_tile<FMT>(sm, s)) {
       LineOut o2[2];
       bool act[2];
       int li[2];

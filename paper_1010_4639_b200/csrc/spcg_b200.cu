@@ -119,7 +119,11 @@ int dev_info(DevInfo** out) {
     bs = std::min(bs, t);
     if ((rc = occupancy(cgs_kernel<K_SCSR_PRIV>, &t))) return rc;
     bs = std::min(bs, t);
+    // (these calls also raise each kernel's dynamic shared-memory limit)
     if ((rc = occupancy(dist_spmv_pq<K_CSR>, &t))) return rc;
+    if ((rc = occupancy(dist_spmv_pq<K_CSR, true>, &t))) return rc;
+    if ((rc = occupancy(dist_spmv<K_CSR, true>, &t))) return rc;
+    if ((rc = occupancy(spmv_kernel<K_CSR, true>, &t))) return rc;
     if ((rc = occupancy(dist_spmv_pq<K_SCSR_PRIV>, &t))) return rc;
     if ((rc = occupancy(dist_spmv_pq<K_SCSR_ATOMIC>, &t))) return rc;
     if ((rc = occupancy(dist_spmv_pq<K_CSC>, &t))) return rc;

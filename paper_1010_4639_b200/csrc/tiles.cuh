@@ -72,6 +72,7 @@ struct MatView {
                          // start where the previous one ended, on its L2-resident lines)
   int tree;              // split long lines: per-lane partial sums + a fixed shuffle tree
                          // (reassociated, deterministic) instead of the in-order sum
+  int wide;              // tiles may exceed kBlock lines (launch the WIDE instantiation)
 };
 
 struct StageMeta {
