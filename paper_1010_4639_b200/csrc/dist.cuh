@@ -19,6 +19,10 @@
 
 namespace spcg {
 
+// Block size of the elementwise passes (B, C, x): independent of the tile
+// kernels' kBlock so their grid-stride parallelism does not shrink with it.
+constexpr int kElemBlock = 512;
+
 struct StepState {
   double rr, alpha, beta, b_norm, rel, tol;
   double red;  // local partial sum; NCCL all-reduces it in place
@@ -152,7 +156,7 @@ __global__ void __launch_bounds__(kBlock, kStreamMinBlocks)
 // mode 0: red = b.b               mode 1: r = b - q (or b), red = r.r, p = r
 // mode 2: r -= alpha q, red = r.r mode 3: red = |b - q|^2 (true residual)
 // Mode 2 moves 16-byte pairs, two in flight per thread (r, q 16-B aligned).
-__global__ void __launch_bounds__(kBlock) dist_elem(int mode, long long nloc, StepState* S,
+__global__ void __launch_bounds__(kElemBlock) dist_elem(int mode, long long nloc, StepState* S,
                                                    const double* b, double* q, double* r,
                                                    double* p, double* part, int zq, int rev = 0) {
   __shared__ RedSmem sm;
@@ -220,7 +224,7 @@ __global__ void __launch_bounds__(kBlock) dist_elem(int mode, long long nloc, St
 // pass C: x += alpha p, p = r + beta p, for an iteration that neither
 // converged nor failed (a converged solve applies its last x update at the
 // end; an exhausted max_iter runs its pass C).  xv: x is 16-byte aligned.
-__global__ void __launch_bounds__(kBlock) dist_update(long long nloc, StepState* S, const double* r,
+__global__ void __launch_bounds__(kElemBlock) dist_update(long long nloc, StepState* S, const double* r,
                                                      double* p, double* x, int xv, int rev = 0) {
   if (S->status != 0 || S->converged || S->kc >= S->k) return;
   const double alpha = S->alpha, beta = S->beta;

@@ -307,11 +307,11 @@ int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const dou
   constexpr bool kRev = (FMT == K_SCSR_ATOMIC);  // transposed scatters reach halo rows
   CUDA_TRY(cudaEventRecord(d.ev0, st));
   // ||b|| (solver.py:107)
-  dist_elem<<<GE, kBlock, 0, st>>>(0, nloc, d.S, b, nullptr, nullptr, nullptr, d.part, 0);
+  dist_elem<<<GE, kElemBlock, 0, st>>>(0, nloc, d.S, b, nullptr, nullptr, nullptr, d.part, 0);
   if ((rc = allreduce_red(H, d.S, st))) return rc;
   dist_scalar<<<1, 1, 0, st>>>(0, d.S, hist);
   // x = x0, r = b - A x0, p = r (solver.py:120-124)
-  dist_x<<<GE, kBlock, 0, st>>>(0, nloc, d.S, x0, x);
+  dist_x<<<GE, kElemBlock, 0, st>>>(0, nloc, d.S, x0, x);
   launches += 3;
   if (x0) {
     CUDA_TRY(cudaMemcpyAsync(d.tmp_ext, x0, sizeof(double) * (size_t)nloc,
@@ -320,10 +320,10 @@ int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const dou
     if (FMT == K_CSR && v.wide) dist_spmv<K_CSR, true><<<G, kBlock, sm, st>>>(v, d.tmp_ext, d.q);
     else dist_spmv<FMT><<<G, kBlock, sm, st>>>(v, d.tmp_ext, d.q);
     if (kRev && (rc = reverse_halo(H, d, d.q, nhalo, st, &launches))) return rc;
-    dist_elem<<<GE, kBlock, 0, st>>>(1, nloc, d.S, b, d.q, r, p, d.part, kAtom);
+    dist_elem<<<GE, kElemBlock, 0, st>>>(1, nloc, d.S, b, d.q, r, p, d.part, kAtom);
     launches += 2;
   } else {
-    dist_elem<<<GE, kBlock, 0, st>>>(1, nloc, d.S, b, nullptr, r, p, d.part, 0);
+    dist_elem<<<GE, kElemBlock, 0, st>>>(1, nloc, d.S, b, nullptr, r, p, d.part, 0);
     ++launches;
   }
   if ((rc = allreduce_red(H, d.S, st))) return rc;
@@ -366,11 +366,11 @@ int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const dou
       if ((rc2 = allreduce_red(H, d.S, st))) return rc2;
       if (kRev && (rc2 = reverse_halo(H, d, d.q, nhalo, st, &launches))) return rc2;
       dist_scalar<<<1, 1, 0, st>>>(2, d.S, hist);
-      dist_elem<<<GE, kBlock, 0, st>>>(2, nloc, d.S, nullptr, d.q, r, nullptr, d.part, kAtom,
+      dist_elem<<<GE, kElemBlock, 0, st>>>(2, nloc, d.S, nullptr, d.q, r, nullptr, d.part, kAtom,
                                        kAlternate ? 1 - dirA : 0);
       if ((rc2 = allreduce_red(H, d.S, st))) return rc2;
       dist_scalar<<<1, 1, 0, st>>>(3, d.S, hist);
-      dist_update<<<GE, kBlock, 0, st>>>(nloc, d.S, r, p, x, xv, dirA);
+      dist_update<<<GE, kElemBlock, 0, st>>>(nloc, d.S, r, p, x, xv, dirA);
       ++iter_enq;
       launches += 5;
       if ((rc2 = halo_exchange(H, d, p, p, st, &launches))) return rc2;
@@ -406,7 +406,7 @@ int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const dou
     if (!two && (rc = enqueue_chunk(bb ^ 1))) return rc;
   }
   // a converged solve skipped its pass C: x += alpha_K p_K; then the true residual
-  dist_x<<<GE, kBlock, 0, st>>>(1, nloc, d.S, p, x);
+  dist_x<<<GE, kElemBlock, 0, st>>>(1, nloc, d.S, p, x);
   ++launches;
   if (o->recompute_final_residual && d.h_S->status == 0 && d.h_S->b_norm != 0.0) {
     CUDA_TRY(cudaMemcpyAsync(d.tmp_ext, x, sizeof(double) * (size_t)nloc,
@@ -415,7 +415,7 @@ int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const dou
     if (FMT == K_CSR && v.wide) dist_spmv<K_CSR, true><<<G, kBlock, sm, st>>>(v, d.tmp_ext, d.q);
     else dist_spmv<FMT><<<G, kBlock, sm, st>>>(v, d.tmp_ext, d.q);
     if (kRev && (rc = reverse_halo(H, d, d.q, nhalo, st, &launches))) return rc;
-    dist_elem<<<GE, kBlock, 0, st>>>(3, nloc, d.S, b, d.q, nullptr, nullptr, d.part, 0);
+    dist_elem<<<GE, kElemBlock, 0, st>>>(3, nloc, d.S, b, d.q, nullptr, nullptr, d.part, 0);
     if ((rc = allreduce_red(H, d.S, st))) return rc;
     dist_true_rel<<<1, 1, 0, st>>>(d.S);
     launches += 3;
