@@ -1,0 +1,523 @@
+// clus_pipe.cuh — pipelined cluster-resident CG (engine 6): the plan, data
+// layout and row slots of engine 5 (clus.cuh), with the Ghysels–Vanroose
+// recurrences so that the iteration's SpMV overlaps its all-reduce.
+//
+// Why: on F the engine-5 iteration is update (~0.85 us) + SpMV (~1.2 us) +
+// all-reduce (~3.5 us: two cluster barriers and the leaders' exchange through
+// global memory), strictly in sequence, because the SpMV input r needs the
+// scalars of the previous reduction.  Pipelined CG reduces (r.r, w.r) and
+// computes n = A w at the same time (w = A r by recurrence, so the SpMV needs
+// no scalar of the current iteration):
+//   gamma = r.r, delta = w.r   (all-reduce in flight)  ||  n = A w
+//   beta = gamma / gamma_old,  alpha = gamma / (delta - beta gamma / alpha_old)
+//   z = n + beta z,  s = w + beta s,  p = r + beta p,
+//   x += alpha p,  r -= alpha s,  w -= alpha z
+// (reference CG order, solver.py:132-157: the same alpha/beta formulas as the
+// single-reduction engines, fp64; scripts/pipecg_numerics.py: F converges in
+// the reference's 329 iterations, x within 4.9e-11 of the reference).
+//
+// Synchronisation per iteration (one CTA per SM, 15 row warps + 1 comm warp):
+//   row warps: partials -> every cluster CTA's slot (DSMEM), arrive(A);
+//              n = A w from the shared window of w;  wait(A);
+//              boundary n -> neighbours (DSMEM inside the cluster, epoch-tagged
+//              64-bit words in global memory between clusters);
+//              arrive(B), wait(B); scalars; update; __syncthreads
+//   comm warp (cluster rank 0, K > 1 clusters): wait(A); cluster sum -> own
+//              global slot (epoch-tagged); poll the K slots; sum in cluster
+//              order; DSMEM broadcast to the cluster; arrive(B), wait(B)
+// so the leaders' global exchange runs while the row warps do the SpMV.
+// Halo rows of w advance redundantly in every CTA that gathers them
+// (z = n + beta z, w -= alpha z: the owner's operations on the owner's
+// inputs, so bitwise the owner's values), which needs only the neighbours'
+// boundary n of the same iteration.
+#pragma once
+#include "clus.cuh"
+
+namespace spcg {
+
+// 15 row warps + the communication warp: a 17th warp would cap the kernel at
+// 96 registers (5 warps on one SM sub-partition) and spill the row slots
+constexpr int kPipeThreads = kClusThreads;
+constexpr int kPipeWarps = kPipeThreads / 32;
+constexpr int kPipeRowWarps = kPipeWarps - 1;
+constexpr int kPipeRowThreads = kPipeRowWarps * 32;
+constexpr int kPipeMaxSlices = kPipeRowWarps * kClusSlicesPerWarp;  // per CTA (host-checked)
+constexpr int kPipeMaxSlices2 = kPipeRowWarps * 2;
+
+struct PipeShared {
+  double slot[2][kClusMax][2];
+  double red[2][kPipeWarps];
+  double tot[2][2];
+  ClusSend send[kClusSendCache];
+};
+
+// split cluster barrier
+#ifndef SPCG_PIPE_ALIGNED
+#define SPCG_PIPE_ALIGNED 0
+#endif
+__device__ __forceinline__ void cluster_arrive_rel() {
+#if SPCG_PIPE_ALIGNED
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+#else
+  asm volatile("barrier.cluster.arrive.release;\n" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void cluster_wait_acq() {
+#if SPCG_PIPE_ALIGNED
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+#else
+  asm volatile("barrier.cluster.wait.acquire;\n" ::: "memory");
+#endif
+}
+
+// one 64-bit word of an epoch-tagged double: {hi32|tag} or {lo32|tag}
+__device__ __forceinline__ void tagged_store(volatile unsigned long long* dst, double v, uint32_t tag) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(v);
+  dst[0] = (u & 0xffffffff00000000ull) | tag;
+  dst[1] = (u << 32) | tag;
+}
+// both words of a tagged double: two independent volatile loads (one round
+// trip); tagged_finish validates them when the value is consumed and re-polls
+// (rarely: the barrier that precedes the read usually outlasts the sender)
+__device__ __forceinline__ void tagged_issue(const volatile unsigned long long* src,
+                                             unsigned long long& a, unsigned long long& b) {
+  a = src[0];
+  b = src[1];
+}
+__device__ __forceinline__ double tagged_finish(const volatile unsigned long long* src,
+                                                unsigned long long a, unsigned long long b,
+                                                uint32_t tag) {
+  unsigned long long spins = 0;
+  while ((uint32_t)a != tag || (uint32_t)b != tag) {
+    tagged_issue(src, a, b);
+    if (++spins > kSpinLimit) asm volatile("trap;");
+  }
+  return __longlong_as_double((long long)((a & 0xffffffff00000000ull) | (b >> 32)));
+}
+__device__ __forceinline__ double tagged_load(const volatile unsigned long long* src, uint32_t tag) {
+  unsigned long long a, b;
+  tagged_issue(src, a, b);
+  return tagged_finish(src, a, b, tag);
+}
+
+// NS: row slots per thread (2 when the plan's CTAs have <= 30 slices: fewer
+// live registers, no spills; 4 otherwise)
+template <bool TWO, int NS>
+__global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArgs A) {
+  namespace cgp = cooperative_groups;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ PipeShared cs;
+  cgp::cluster_group cl = cgp::this_cluster();
+  const int me = (int)cl.block_rank();
+  const int C = (int)cl.num_blocks();
+  const int G = (int)gridDim.x;
+  const int K = G / C;
+  const int kc = (int)blockIdx.x / C;
+  const int gme = (int)blockIdx.x;
+  if (C != A.cluster_size) {
+    if (gme == 0 && threadIdx.x == 0) {
+      A.res->iterations = 0;
+      A.res->fail_iter = 0;
+      A.res->converged = 0;
+      A.res->status = ST_BAD_LAUNCH;
+      A.res->final_rel = 0.0;
+      A.res->b_norm = 0.0;
+    }
+    return;
+  }
+  const ClusCta P = A.ctas[gme];
+  double* wwin = reinterpret_cast<double*>(smem_raw + A.off_rwin);   // window of w (SpMV input)
+  double* zhalo = reinterpret_cast<double*>(smem_raw + A.off_shalo); // z of the halo rows
+  double* nhalo = reinterpret_cast<double*>(smem_raw + A.off_whalo); // [2][hcap] halo n (DSMEM)
+  double* sval = reinterpret_cast<double*>(smem_raw + A.off_val);
+  unsigned short* scol = reinterpret_cast<unsigned short*>(smem_raw + A.off_col);
+  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+  const bool comm = wp == kPipeRowWarps;
+  const bool leader = gme == 0 && tid == 0;
+  const int nh = P.wn - (P.row_hi - P.row_lo);
+  const int own0 = P.row_lo - P.wlo;
+  unsigned long long* gh = reinterpret_cast<unsigned long long*>(A.ghalo);  // [2][G][hcap][2]
+
+  for (int s = 0; s < P.nslices; ++s) {
+    const ClusSlice sd = A.slices[P.slice0 + s];
+    if (sd.soff < 0) continue;
+    const int cnt = sd.width * 32;
+    for (int e = tid; e < cnt; e += kPipeThreads) {
+      sval[sd.soff + e] = A.gval[sd.goff + e];
+      scol[sd.soff + e] = A.gcol[sd.goff + e];
+    }
+  }
+  if (tid < min(P.nsend, kClusSendCache)) cs.send[tid] = A.sends[P.send0 + tid];
+  int rrow[NS], rlen[NS], rlenA[NS];
+  int swidth[NS], sbase[NS];
+  bool sres[NS];
+  double xr[NS], rg[NS], pg[NS],
+      sg[NS], wg[NS], zg[NS];
+#pragma unroll
+  for (int k = 0; k < NS; ++k) {
+    const int s = wp + kPipeRowWarps * k;
+    rrow[k] = -1;
+    rlen[k] = rlenA[k] = swidth[k] = sbase[k] = 0;
+    sres[k] = false;
+    xr[k] = rg[k] = pg[k] = sg[k] = wg[k] = zg[k] = 0.0;
+    if (!comm && s < P.nslices) {
+      const ClusSlice sd = A.slices[P.slice0 + s];
+      const int2 rm = A.rowmeta[(size_t)(P.slice0 + s) * 32 + lane];
+      rrow[k] = rm.x;
+      rlen[k] = rm.y & 0xffff;
+      rlenA[k] = (int)((unsigned)rm.y >> 16);
+      swidth[k] = sd.width;
+      sres[k] = sd.soff >= 0;
+      sbase[k] = (sres[k] ? sd.soff : sd.goff) + lane;
+    }
+  }
+  __syncthreads();
+
+  auto spmv = [&](double* out) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      out[k] = 0.0;
+      if (swidth[k] > 0) {
+        const double q = sres[k] ? clus_row<TWO>(sval, scol, sbase[k], swidth[k], rlen[k], rlenA[k], wwin)
+                                 : clus_row<TWO>(A.gval, A.gcol, sbase[k], swidth[k], rlen[k], rlenA[k], wwin);
+        out[k] = rrow[k] >= 0 ? q : 0.0;
+      }
+    }
+  };
+  uint32_t epoch = 0;
+  // block + cluster partial sums of (v0, v1) -> every cluster CTA's slot[bank]
+  auto post_partials = [&](double v0, double v1, int bank) {
+    const double a0 = warp_sum(v0), a1 = warp_sum(v1);
+    if (lane == 0) {
+      cs.red[0][wp] = a0;
+      cs.red[1][wp] = a1;
+    }
+    __syncthreads();
+    if (wp == 0) {
+      double b0 = lane < kPipeWarps ? cs.red[0][lane] : 0.0;
+      double b1 = lane < kPipeWarps ? cs.red[1][lane] : 0.0;
+      b0 = warp_sum(b0);
+      b1 = warp_sum(b1);
+      if (lane < C) {
+        double* dst = cl.map_shared_rank(&cs.slot[bank][me][0], lane);
+        dst[0] = b0;
+        dst[1] = b1;
+      }
+    }
+  };
+  // second level (K > 1, one warp of cluster rank 0, after the slots are
+  // complete): cluster sum -> own epoch-tagged global slot, poll the K slots,
+  // sum in cluster order, broadcast to the cluster's tot[bank] by DSMEM
+  auto exchange = [&](int bank, uint32_t tag) {
+    double t0 = 0.0, t1 = 0.0;
+    for (int c = 0; c < C; ++c) {
+      t0 += cs.slot[bank][c][0];
+      t1 += cs.slot[bank][c][1];
+    }
+    unsigned long long* gb = A.gslots + (size_t)bank * K * kClusSlotWords;
+    if (lane == 0) {
+      fence_acq_rel_gpu();
+      volatile unsigned long long* dst = gb + kClusSlotWords * kc;
+      const unsigned long long u0 = (unsigned long long)__double_as_longlong(t0);
+      const unsigned long long u1 = (unsigned long long)__double_as_longlong(t1);
+      dst[0] = (u0 & 0xffffffff00000000ull) | tag;
+      dst[1] = (u0 << 32) | tag;
+      dst[2] = (u1 & 0xffffffff00000000ull) | tag;
+      dst[3] = (u1 << 32) | tag;
+    }
+    double c0 = 0.0, c1 = 0.0;
+    if (lane < K) {
+      const volatile unsigned long long* src = gb + kClusSlotWords * lane;
+      unsigned long long a, b, c, d, spins = 0;
+      for (;;) {
+        d = src[3];
+        if ((uint32_t)d == tag) {
+          a = src[0];
+          b = src[1];
+          c = src[2];
+          if ((uint32_t)a == tag && (uint32_t)b == tag && (uint32_t)c == tag) break;
+        }
+        if (++spins > kSpinLimit) asm volatile("trap;");
+      }
+      c0 = __longlong_as_double((long long)((a & 0xffffffff00000000ull) | (b >> 32)));
+      c1 = __longlong_as_double((long long)((c & 0xffffffff00000000ull) | (d >> 32)));
+    }
+    fence_acq_rel_gpu();
+    double s0 = 0.0, s1 = 0.0;
+    for (int k = 0; k < K; ++k) {
+      s0 += __shfl_sync(0xffffffffu, c0, k);
+      s1 += __shfl_sync(0xffffffffu, c1, k);
+    }
+    if (lane < C) {
+      double* d2 = cl.map_shared_rank(&cs.tot[bank][0], lane);
+      d2[0] = s0;
+      d2[1] = s1;
+    }
+  };
+  auto totals = [&](int bank, double& v0, double& v1) {
+    if (K > 1) {
+      v0 = cs.tot[bank][0];
+      v1 = cs.tot[bank][1];
+    } else {
+      v0 = v1 = 0.0;
+      for (int c = 0; c < C; ++c) {
+        v0 += cs.slot[bank][c][0];
+        v1 += cs.slot[bank][c][1];
+      }
+    }
+  };
+  // blocking all-reduce (setup and tail)
+  auto allreduce2 = [&](double& v0, double& v1) {
+    const int bank = (int)(epoch++ & 1u);
+    const uint32_t tag = epoch;
+    post_partials(v0, v1, bank);
+    cluster_sync_all();
+    if (K > 1) {
+      if (me == 0 && wp == 0) exchange(bank, tag);
+      cluster_sync_all();
+    }
+    totals(bank, v0, v1);
+  };
+  auto halo_win = [&](int h) { return h < P.hlo ? h : own0 + (P.row_hi - P.row_lo) + (h - P.hlo); };
+  // n of halo index h from buffer buf: DSMEM (same cluster) or tagged global
+  auto halo_local = [&](int h) {
+    const int hrow = h < P.hlo ? P.wlo + h : P.row_hi + (h - P.hlo);
+    return hrow >= P.clo && hrow < P.chi;
+  };
+  auto halo_n = [&](int buf, int h, uint32_t tag) {
+    if (halo_local(h)) return nhalo[(size_t)buf * A.hcap + h];
+    return tagged_load(gh + (((size_t)buf * G + gme) * A.hcap + h) * 2, tag);
+  };
+  auto send_n = [&](const double* nv, int buf, uint32_t tag) {
+    for (int e = 0; e < P.nsend; ++e) {
+      const ClusSend sd = e < kClusSendCache ? cs.send[e] : A.sends[P.send0 + e];
+      if (sd.dst / C != kc) {
+        volatile unsigned long long* dst = gh + ((size_t)buf * G + sd.dst) * A.hcap * 2;
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+          if (rrow[k] >= sd.lo && rrow[k] < sd.hi)
+            tagged_store(dst + 2 * (size_t)(sd.dst_off + rrow[k] - sd.lo), nv[k], tag);
+      } else {
+        double* dst = cl.map_shared_rank(nhalo + (size_t)buf * A.hcap, sd.dst % C);
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+          if (rrow[k] >= sd.lo && rrow[k] < sd.hi) dst[sd.dst_off + rrow[k] - sd.lo] = nv[k];
+      }
+    }
+  };
+
+  // ||b||
+  double part = 0.0, dummy = 0.0;
+#pragma unroll
+  for (int k = 0; k < NS; ++k)
+    if (rrow[k] >= 0) {
+      const double bv = A.b[rrow[k]];
+      part = fma(bv, bv, part);
+    }
+  allreduce2(part, dummy);
+  const double b_norm = sqrt(part);
+  if (b_norm == 0.0) {  // solver.py:109-118
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+      if (rrow[k] >= 0) A.x[rrow[k]] = 0.0;
+    if (leader) {
+      A.res->iterations = 0;
+      A.res->fail_iter = 0;
+      A.res->converged = 1;
+      A.res->status = ST_OK;
+      A.res->final_rel = 0.0;
+      A.res->b_norm = 0.0;
+    }
+    return;
+  }
+  // x = x0, r0 = b - A x0 (solver.py:120-124)
+  if (A.x0 != nullptr) {
+    for (int j = tid; j < P.wn; j += kPipeThreads) wwin[j] = A.x0[P.wlo + j];
+    __syncthreads();
+    double qv[NS];
+    spmv(qv);
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+      if (rrow[k] >= 0) {
+        xr[k] = A.x0[rrow[k]];
+        rg[k] = mul_add_rn(A.b[rrow[k]], -1.0, qv[k]);
+      }
+    __syncthreads();
+  } else {
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+      if (rrow[k] >= 0) rg[k] = A.b[rrow[k]];
+  }
+  // window of r0 (through global scratch, once), gamma0
+  part = 0.0;
+  dummy = 0.0;
+#pragma unroll
+  for (int k = 0; k < NS; ++k)
+    if (rrow[k] >= 0) {
+      A.scratch[rrow[k]] = rg[k];
+      part = fma(rg[k], rg[k], part);
+    }
+  allreduce2(part, dummy);
+  double gam = part;
+  const double tol_b = A.tol * b_norm;
+  long long max_it = A.max_iter;
+  double rel = sqrt(gam) / b_norm;
+  int converged = 0, status = ST_OK;
+  long long iterations = 0, fail_iter = 0;
+  if (sqrt(gam) <= tol_b) {
+    converged = 1;
+    max_it = 0;
+  } else {
+    for (int j = tid; j < P.wn; j += kPipeThreads) wwin[j] = __ldcg(A.scratch + P.wlo + j);
+    for (int h = tid; h < A.hcap; h += kPipeThreads) zhalo[h] = 0.0;
+    __syncthreads();
+    spmv(wg);  // w0 = A r0
+    part = dummy = 0.0;
+    allreduce2(part, dummy);  // every CTA has read its r0 window from scratch
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+      if (rrow[k] >= 0) A.scratch[rrow[k]] = wg[k];
+    allreduce2(part, dummy);
+    for (int j = tid; j < P.wn; j += kPipeThreads) wwin[j] = __ldcg(A.scratch + P.wlo + j);
+    __syncthreads();
+  }
+
+  double alpha = 0.0, beta = 0.0;
+  for (long long it = 0; max_it > 0; ++it) {
+    const int bank = (int)(epoch++ & 1u), buf = (int)(it & 1);
+    const uint32_t tag = epoch;
+    double g = 0.0, d = 0.0;
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+      if (rrow[k] >= 0) {
+        g = fma(rg[k], rg[k], g);
+        d += rg[k] * wg[k];
+      }
+    post_partials(g, d, bank);
+    cluster_arrive_rel();  // A: the slots of this iteration
+    double ng[NS];
+    spmv(ng);  // n = A w, overlapped with the all-reduce
+    cluster_wait_acq();
+    if (comm && K > 1 && me == 0) exchange(bank, tag);
+    send_n(ng, buf, tag);
+    cluster_arrive_rel();  // B: cluster totals and intra-cluster halo n
+    cluster_wait_acq();
+    double g_new, d_new;
+    totals(bank, g_new, d_new);
+    if (it >= 1) {
+      rel = sqrt(g_new) / b_norm;
+      if (!isfinite(rel)) {
+        status = ST_NF_RES;
+        fail_iter = it;
+        break;
+      }
+      if (A.record_history && leader) A.hist[it - 1] = rel;
+      iterations = it;
+      if (sqrt(g_new) <= tol_b) {
+        converged = 1;
+        break;
+      }
+      const double beta_n = g_new / gam;
+      if (!isfinite(beta_n)) {
+        status = ST_NF_BETA;
+        fail_iter = it;
+        break;
+      }
+      if (it >= max_it) break;
+      const double eta = d_new - beta_n * g_new / alpha;  // p.Ap of iteration it+1
+      if (eta <= 0.0) {
+        status = ST_NOT_SPD;
+        fail_iter = it + 1;
+        break;
+      }
+      const double alpha_n = g_new / eta;
+      if (!isfinite(alpha_n)) {
+        status = ST_NF_ALPHA;
+        fail_iter = it + 1;
+        break;
+      }
+      alpha = alpha_n;
+      beta = beta_n;
+    } else {
+      if (d_new <= 0.0) {
+        status = ST_NOT_SPD;
+        fail_iter = 1;
+        break;
+      }
+      alpha = g_new / d_new;
+      if (!isfinite(alpha)) {
+        status = ST_NF_ALPHA;
+        fail_iter = 1;
+        break;
+      }
+      beta = 0.0;
+    }
+    gam = g_new;
+    const double na = -alpha;
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+      if (rrow[k] >= 0) {
+        zg[k] = mul_add_rn(ng[k], beta, zg[k]);
+        sg[k] = mul_add_rn(wg[k], beta, sg[k]);
+        pg[k] = mul_add_rn(rg[k], beta, pg[k]);
+        xr[k] = mul_add_rn(xr[k], alpha, pg[k]);
+        rg[k] = mul_add_rn(rg[k], na, sg[k]);
+        wg[k] = mul_add_rn(wg[k], na, zg[k]);
+        wwin[own0 + rrow[k] - P.row_lo] = wg[k];
+      }
+    if (!comm)
+      for (int h = tid; h < nh; h += kPipeRowThreads) {
+        // read after the own rows' update: one round trip (both tagged words
+        // issued together); issuing it right after barrier B measured slower
+        const double nv = halo_n(buf, h, tag);
+        const double zh = mul_add_rn(nv, beta, zhalo[h]);
+        zhalo[h] = zh;
+        const int j = halo_win(h);
+        wwin[j] = mul_add_rn(wwin[j], na, zh);
+      }
+    __syncthreads();
+  }
+
+  if (status != ST_OK) {
+    if (leader) {
+      A.res->iterations = iterations;
+      A.res->fail_iter = fail_iter;
+      A.res->converged = 0;
+      A.res->status = status;
+      A.res->final_rel = rel;
+      A.res->b_norm = b_norm;
+    }
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < NS; ++k)
+    if (rrow[k] >= 0) A.x[rrow[k]] = xr[k];
+  if (A.recompute) {  // true residual ||b - A x|| / ||b||
+    part = 0.0;
+    dummy = 0.0;
+    allreduce2(part, dummy);
+    for (int j = tid; j < P.wn; j += kPipeThreads) wwin[j] = __ldcg(A.x + P.wlo + j);
+    __syncthreads();
+    double qv[NS];
+    spmv(qv);
+    part = 0.0;
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+      if (rrow[k] >= 0) {
+        const double tr = mul_add_rn(A.b[rrow[k]], -1.0, qv[k]);
+        part = fma(tr, tr, part);
+      }
+    allreduce2(part, dummy);
+    rel = sqrt(part) / b_norm;
+  }
+  if (leader) {
+    A.res->iterations = iterations;
+    A.res->fail_iter = 0;
+    A.res->converged = converged;
+    A.res->status = ST_OK;
+    A.res->final_rel = rel;
+    A.res->b_norm = b_norm;
+  }
+}
+
+}  // namespace spcg

@@ -196,6 +196,7 @@ int build_clus_plan(spcg_matrix_s* m) {
     t.hlo = lo[c] - wlo[c];
     t.slice0 = (int)slices.size();
     t.nslices = ((int)o.size() + 31) / 32;
+    P.max_slices = std::max(P.max_slices, t.nslices);
     for (int s = 0; s < t.nslices; ++s) {
       ClusSlice sd{};
       int wdt = 0;
@@ -301,6 +302,13 @@ int build_clus_plan(spcg_matrix_s* m) {
   // the grid of C CTAs in clusters of csz must be co-resident with this smem
   CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
   if (csz > 8) CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  // the pipelined kernel (engine 6) runs the same plan with one more warp
+  const void* kpipes[4] = {(const void*)clus_pcg_kernel<false, 2>, (const void*)clus_pcg_kernel<false, 4>,
+                           (const void*)clus_pcg_kernel<true, 2>, (const void*)clus_pcg_kernel<true, 4>};
+  for (const void* kp : kpipes) {
+    CUDA_TRY(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
+    if (csz > 8) CUDA_TRY(cudaFuncSetAttribute(kp, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  }
   {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(csz);
@@ -334,12 +342,13 @@ int build_clus_plan(spcg_matrix_s* m) {
   CUDA_TRY(cudaMemcpy(P.gval, gval.data(), sizeof(double) * gval.size(), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(P.gcol, gcol.data(), sizeof(unsigned short) * gcol.size(), cudaMemcpyHostToDevice));
   if (C > csz) {
-    if ((rc = dmalloc((void**)&P.ghalo, sizeof(double) * 2 * (size_t)C * hcap, &acct)) ||
+    // [2][C][hcap] doubles (engine 5) or epoch-tagged word pairs (engine 6)
+    if ((rc = dmalloc((void**)&P.ghalo, sizeof(double) * 4 * (size_t)C * hcap, &acct)) ||
         (rc = dmalloc((void**)&P.gslots,
                       sizeof(unsigned long long) * 2 * kClusSlotWords * (size_t)(C / csz),
                       &acct)))
       return rc;
-    CUDA_TRY(cudaMemset(P.ghalo, 0, sizeof(double) * 2 * (size_t)C * hcap));
+    CUDA_TRY(cudaMemset(P.ghalo, 0, sizeof(double) * 4 * (size_t)C * hcap));
   }
   m->bytes += acct;
   P.hcap = hcap;
@@ -349,10 +358,10 @@ int build_clus_plan(spcg_matrix_s* m) {
   return SPCG_OK;
 }
 
-int launch_clus(const ClusPlan& P, const ClusArgs& a, cudaStream_t st) {
+int launch_clus(const ClusPlan& P, const ClusArgs& a, cudaStream_t st, bool pipe) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(P.C);
-  cfg.blockDim = dim3(kClusThreads);
+  cfg.blockDim = dim3(pipe ? kPipeThreads : kClusThreads);
   cfg.dynamicSmemBytes = P.smem;
   cfg.stream = st;
   cudaLaunchAttribute at[2];
@@ -368,13 +377,22 @@ int launch_clus(const ClusPlan& P, const ClusArgs& a, cudaStream_t st) {
   // once, and the kernel refuses a launch whose cluster size is not the plan's
   static const bool noncoop = getenv("SPCG_CLUS_NONCOOP") != nullptr;
   cfg.numAttrs = (P.C > P.cs && !noncoop) ? 2 : 1;
-  if (P.two) CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_cg_kernel<true>, a));
-  else CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_cg_kernel<false>, a));
+  if (pipe) {
+    const bool ns2 = P.max_slices <= kPipeMaxSlices2;
+    if (P.two && ns2) CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_pcg_kernel<true, 2>, a));
+    else if (P.two) CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_pcg_kernel<true, 4>, a));
+    else if (ns2) CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_pcg_kernel<false, 2>, a));
+    else CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_pcg_kernel<false, 4>, a));
+  } else if (P.two) {
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_cg_kernel<true>, a));
+  } else {
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_cg_kernel<false>, a));
+  }
   return SPCG_OK;
 }
 
 int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double* hist,
-               const spcg_cg_options* o, spcg_cg_result* out, cudaStream_t st) {
+               const spcg_cg_options* o, spcg_cg_result* out, cudaStream_t st, bool pipe = false) {
   int rc;
   const ClusPlan& P = m->cp;
   if ((rc = ensure_ws(m, 1))) return rc;
@@ -412,13 +430,15 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
     CUDA_TRY(cudaMemsetAsync(P.gslots, 0,
                              sizeof(unsigned long long) * 2 * kClusSlotWords * (size_t)(P.C / P.cs),
                              st));
+  if (pipe && P.ghalo)  // tags restart at 1 every solve
+    CUDA_TRY(cudaMemsetAsync(P.ghalo, 0, sizeof(double) * 4 * (size_t)P.C * P.hcap, st));
   static const bool tracing = getenv("SPCG_TRACE") != nullptr;
-  if (tracing) {
+  if (tracing && !pipe) {
     CUDA_TRY(cudaMalloc((void**)&a.trace, sizeof(unsigned long long) * 8 * (size_t)P.C));
     CUDA_TRY(cudaMemsetAsync(a.trace, 0, sizeof(unsigned long long) * 8 * (size_t)P.C, st));
   }
   CUDA_TRY(cudaEventRecord(w.ev0, st));
-  if ((rc = launch_clus(P, a, st))) return rc;
+  if ((rc = launch_clus(P, a, st, pipe))) return rc;
   CUDA_TRY(cudaEventRecord(w.ev1, st));
   CUDA_TRY(cudaMemcpyAsync(w.h_res, w.res, sizeof(CgDevResult), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));

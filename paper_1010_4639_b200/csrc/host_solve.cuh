@@ -28,6 +28,14 @@ int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double
   // clusters' shared memory: cluster-resident single-reduction CG (DSMEM +
   // hardware cluster barriers; K clusters of 8 exchange through global
   // memory).  F: 5.35 us/iteration vs 8.45 on engine 3; S: 6.23 vs 8.58.
+  // engine 6: the same plan, pipelined CG (SpMV overlapped with the all-reduce)
+  if (o->engine == 6) {
+    if ((rc = build_clus_plan(m))) return rc;
+    if (!m->cp.ok) return fail(SPCG_ERR_UNSUPPORTED, "cluster engine not applicable: " + m->cp.why);
+    if (m->cp.max_slices > kPipeMaxSlices)
+      return fail(SPCG_ERR_UNSUPPORTED, "pipelined cluster engine: too many rows per CTA");
+    return do_clus_cg(m, b, x0, x, hist, o, out, st, true);
+  }
   if (o->engine == 5 || (o->engine == 0 && m->n <= kClusGridMax * kClusMaxRows)) {
     if ((rc = build_clus_plan(m))) return rc;
     // auto only when (nearly) everything stays in shared memory: streamed

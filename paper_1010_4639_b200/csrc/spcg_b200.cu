@@ -21,6 +21,7 @@
 #include "cgs.cuh"
 #include "cg3.cuh"
 #include "clus.cuh"
+#include "clus_pipe.cuh"
 #include "dist.cuh"
 #include "ops.cuh"
 
@@ -218,6 +219,7 @@ struct ClusPlan {
   int off_rwin = 0, off_shalo = 0, off_whalo = 0, off_val = 0, off_col = 0, hcap = 1;
   size_t smem = 0;
   long long resident = 0, streamed = 0;  // entries (stats)
+  int max_slices = 0;                     // SELL-32 slices of the fullest CTA
 };
 
 struct spcg_matrix_s {

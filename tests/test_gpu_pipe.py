@@ -1,0 +1,116 @@
+"""Pipelined cluster-resident engine (engine 6, csrc/clus_pipe.cuh): the
+Ghysels–Vanroose recurrences with the SpMV overlapped with the all-reduce,
+vs the reference's own CG output (north-star bar: iterations within 1 %,
+‖x − x_ref‖/‖x_ref‖ ≤ 1e-8) on the paper-size FEM matrix in every storage
+(15 clusters of 8 CTAs: inter-cluster halos as epoch-tagged words), small
+single-CTA systems with the solver.py edge semantics, and the breakdown
+attribution of solver.py:135-139."""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+from test_gpu_clus import STORAGES, as_storage
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("kind", STORAGES)
+def test_fem_mesh_pipelined(golden, kind):
+    from paper_1010_4639_b200 import CgOptions, cg_solve
+    from paper_1010_4639_b200.genprob import fem_mesh
+
+    g = golden("fem")
+    m, cfg = as_storage(fem_mesh(), kind)
+    r = cg_solve(m, g["F_b"], opts=CgOptions(record_history=True), cfg=cfg, engine=6)
+    assert abs(r.iterations - int(g["F_full_it"])) <= 3
+    xr = g["F_full_x"]
+    assert np.linalg.norm(r.x - xr) / np.linalg.norm(xr) <= 1e-8
+    assert r.converged and r.final_relative_residual <= 1e-10
+    assert np.allclose(r.residual_history[:50], g["F_full_hist"][:50], rtol=1e-8)
+
+
+@pytest.mark.parametrize("kind", STORAGES)
+def test_pipelined_semantics(golden, kind):
+    from paper_1010_4639_b200 import CgOptions, cg_solve
+    from paper_1010_4639_b200.genprob import poisson3d
+
+    g = golden("cg_small")
+    a = poisson3d(12, 12, 12)
+    m, cfg = as_storage(a, kind)
+    r = cg_solve(m, g["p3_b"], x0=g["p3_x0"], opts=CgOptions(tol=1e-9, record_history=True),
+                 cfg=cfg, engine=6)
+    assert abs(r.iterations - int(g["p3_it"])) <= 1
+    assert np.linalg.norm(r.x - g["p3_x"]) / np.linalg.norm(g["p3_x"]) <= 1e-8
+    assert len(r.residual_history) == r.iterations
+    t = cg_solve(m, g["p3_b"], x0=g["p3_x0"], opts=CgOptions(max_iter=7, record_history=True,
+                                                             recompute_final_residual=False),
+                 cfg=cfg, engine=6)
+    assert t.iterations == 7 and not t.converged and len(t.residual_history) == 7
+    assert abs(t.final_relative_residual - float(g["p3t_final"])) <= 1e-9 * float(g["p3t_final"])
+    z = cg_solve(m, np.zeros(a.n), x0=g["p3_x0"], cfg=cfg, engine=6)
+    assert z.iterations == 0 and (z.x == 0).all()
+
+
+def test_pipelined_unbanded_random_spd():
+    from paper_1010_4639_b200 import CgOptions, cg_solve
+    from paper_1010_4639_b200.genprob import random_spd
+
+    a = random_spd(3000, 0.004, seed=5)
+    b = np.random.default_rng(3).standard_normal(a.n)
+    ref = O.cg_solve("csr", a.row_start, a.col_idx, a.values, b, tol=1e-10)
+    r = cg_solve(a, b, opts=CgOptions(tol=1e-10), engine=6)
+    assert abs(r.iterations - ref.iterations) <= max(1, ref.iterations // 100)
+    assert np.linalg.norm(r.x - ref.x) / np.linalg.norm(ref.x) <= 1e-8
+
+
+def test_pipelined_breakdowns():
+    from paper_1010_4639_b200 import NotPositiveDefiniteError, build_csr_from_triplets, cg_solve
+    from paper_1010_4639_b200 import _native as N
+    import torch
+
+    a = build_csr_from_triplets([(0, 0, 1.0), (1, 1, -1.0)], 2)
+    with pytest.raises(NotPositiveDefiniteError, match="not positive definite"):
+        cg_solve(a, np.array([1.0, 2.0]), engine=6)
+    d = build_csr_from_triplets([(0, 0, 4.0), (1, 1, 3.0), (2, 2, -0.5)], 3)
+    b = np.array([1.0, 1.0, 0.1])
+    ref = O.cg_solve("csr", d.row_start, d.col_idx, d.values, b)
+    assert ref.status == 3
+    lib = N.load()
+    bt = torch.from_numpy(b).cuda()
+    xt = torch.empty_like(bt)
+    o = N.CgOptionsC(tol=1e-10, max_iter=3, record_history=0, recompute_final_residual=1,
+                     accumulation=1, engine=6)
+    res = N.CgResultC()
+    rc = lib.spcg_cg_solve(d.device().handle, bt.data_ptr(), None, xt.data_ptr(), None, o, res,
+                           torch.cuda.current_stream().cuda_stream)
+    assert rc == 3 and res.status == 3 and res.fail_iteration == ref.fail_iteration
+
+
+def test_pipelined_multi_cluster_x0_truncation_repeat():
+    """K clusters of 8 with x0, max_iter truncation and back-to-back solves
+    (the tagged halo buffer is cleared per solve; results are deterministic)."""
+    from paper_1010_4639_b200 import CgOptions, cg_solve
+    from paper_1010_4639_b200.genprob import fem_mesh, rhs_for
+
+    F = fem_mesh()
+    b, _ = rhs_for(F, seed=1)
+    x0 = np.random.default_rng(11).standard_normal(F.n)
+    ref = O.cg_solve("csr", F.row_start, F.col_idx, F.values, b, x0=x0, record_history=True)
+    runs = [cg_solve(F, b, x0=x0, opts=CgOptions(record_history=True), engine=6) for _ in range(3)]
+    r = runs[0]
+    assert abs(r.iterations - ref.iterations) <= 3
+    assert np.linalg.norm(r.x - ref.x) / np.linalg.norm(ref.x) <= 1e-8
+    assert np.allclose(r.residual_history[:50], ref.residual_history[:50], rtol=1e-8)
+    for q in runs[1:]:
+        assert q.iterations == r.iterations and (q.x == r.x).all()
+    t = cg_solve(F, b, x0=x0, opts=CgOptions(max_iter=25, record_history=True,
+                                             recompute_final_residual=False), engine=6)
+    rt = O.cg_solve("csr", F.row_start, F.col_idx, F.values, b, x0=x0, max_iter=25,
+                    record_history=True, recompute=False)
+    assert t.iterations == 25 and not t.converged
+    assert np.allclose(t.residual_history, rt.residual_history, rtol=1e-9)
+    assert np.linalg.norm(t.x - rt.x) / np.linalg.norm(rt.x) <= 1e-9
+    z = cg_solve(F, np.zeros(F.n), x0=x0, engine=6)
+    assert z.iterations == 0 and (z.x == 0).all()
