@@ -122,8 +122,8 @@ typedef struct {
   int32_t record_history;        /* write rel residual per iteration to hist   */
   int32_t recompute_final_residual; /* default 1 (solver.py:159-162)           */
   int32_t accumulation;          /* spcg_accumulation, SCSR only               */
-  int32_t engine;                /* 0 = auto (5 for CSR / CSC systems that
-                                    fit one thread-block cluster, else 3 when
+  int32_t engine;                /* 0 = auto (6 for systems whose rows fit
+                                    the co-resident clusters, else 3 when
                                     the system is resident on chip, else 2),
                                     1 = persistent kernel, two-reduction CG,
                                     2 = per-pass kernels (the sharded engine),
@@ -131,7 +131,10 @@ typedef struct {
                                         (Chronopoulos-Gear, resident only),
                                     4 = persistent three-pass CG,
                                     5 = cluster-resident single-reduction CG
-                                        (<= 16 CTAs, banded systems)         */
+                                        (<= 16 CTAs, banded systems),
+                                    6 = engine 5's plan with pipelined CG
+                                        (Ghysels-Vanroose: the SpMV overlaps
+                                        the all-reduce)                      */
   int32_t timing;                /* per-pass engine: CUDA-event time of every
                                     SpMV pass -> result.spmv_ms / launches   */
   int32_t row_sums;              /* 0 = auto: in the streaming CG passes, lines

@@ -41,7 +41,11 @@ int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double
     // auto only when (nearly) everything stays in shared memory: streamed
     // slices are re-read from L2 every iteration at L2 latency
     const bool resident = m->cp.streamed * 9 <= m->cp.resident;
-    if (m->cp.ok && (o->engine == 5 || resident)) return do_clus_cg(m, b, x0, x, hist, o, out, st);
+    // auto picks the pipelined form (engine 6) when its row slots hold the
+    // plan: F 4.95 vs 5.71 us/iteration, S 5.04 vs 6.18, CSC 4.90 vs 5.82
+    if (m->cp.ok && (o->engine == 5 || resident))
+      return do_clus_cg(m, b, x0, x, hist, o, out, st,
+                        o->engine == 0 && m->cp.max_slices <= kPipeMaxSlices);
     if (o->engine == 5)
       return fail(SPCG_ERR_UNSUPPORTED, "cluster engine not applicable: " + m->cp.why);
   }

@@ -125,9 +125,12 @@ def test_auto_engine_is_cluster_for_small_systems():
 
     F = fem_mesh()
     b, _ = rhs_for(F, seed=1)
-    r0 = cg_solve(F, b)            # auto
+    r0 = cg_solve(F, b)            # auto: the pipelined cluster engine
+    r6 = cg_solve(F, b, engine=6)
+    assert r0.iterations == r6.iterations and (r0.x == r6.x).all()  # deterministic
     r5 = cg_solve(F, b, engine=5)
-    assert r0.iterations == r5.iterations and (r0.x == r5.x).all()  # deterministic
+    assert r5.iterations == r6.iterations
+    assert np.linalg.norm(r6.x - r5.x) / np.linalg.norm(r5.x) <= 1e-9
     r3 = cg_solve(F, b, engine=3)  # grid-resident single reduction: same method
     assert r3.iterations == r5.iterations
     assert np.linalg.norm(r3.x - r5.x) / np.linalg.norm(r5.x) <= 1e-10
