@@ -326,8 +326,8 @@ def run_ours(args):
         kern_ms = sp_kms / sp_launch
         alg = spmv_bytes(n, nnz)
     else:  # resident systems: the whole solve is one persistent kernel
-        kern = ("clus_cg_kernel (cluster-resident CG solve, one launch) or cg1_kernel "
-                "(grid-resident, unbanded systems)")
+        kern = ("clus_pcg_kernel (pipelined cluster-resident CG solve, one launch) or "
+                "cg1_kernel (grid-resident, unbanded systems)")
         kern_ms = solve_ms
         alg = alg_solve
     achieved = alg / (kern_ms / 1e3) / 1e9
