@@ -52,6 +52,9 @@ struct PipeShared {
 };
 
 // split cluster barrier
+#ifndef SPCG_PIPE_FENCED
+#define SPCG_PIPE_FENCED 0
+#endif
 #ifndef SPCG_PIPE_ALIGNED
 #define SPCG_PIPE_ALIGNED 0
 #endif
@@ -208,7 +211,10 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   // second level (K > 1, one warp of cluster rank 0, after the slots are
   // complete): cluster sum -> own epoch-tagged global slot, poll the K slots,
   // sum in cluster order, broadcast to the cluster's tot[bank] by DSMEM
-  auto exchange = [&](int bank, uint32_t tag) {
+  // fenced: the exchange also publishes the CTAs' earlier global stores
+  // (setup / tail: scratch and x windows); inside the loop it carries only
+  // its own epoch-tagged words, so it needs no fence
+  auto exchange = [&](int bank, uint32_t tag, bool fenced) {
     double t0 = 0.0, t1 = 0.0;
     for (int c = 0; c < C; ++c) {
       t0 += cs.slot[bank][c][0];
@@ -216,7 +222,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     }
     unsigned long long* gb = A.gslots + (size_t)bank * K * kClusSlotWords;
     if (lane == 0) {
-      fence_acq_rel_gpu();
+      if (fenced) fence_acq_rel_gpu();
       volatile unsigned long long* dst = gb + kClusSlotWords * kc;
       const unsigned long long u0 = (unsigned long long)__double_as_longlong(t0);
       const unsigned long long u1 = (unsigned long long)__double_as_longlong(t1);
@@ -242,7 +248,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       c0 = __longlong_as_double((long long)((a & 0xffffffff00000000ull) | (b >> 32)));
       c1 = __longlong_as_double((long long)((c & 0xffffffff00000000ull) | (d >> 32)));
     }
-    fence_acq_rel_gpu();
+    if (fenced) fence_acq_rel_gpu();
     double s0 = 0.0, s1 = 0.0;
     for (int k = 0; k < K; ++k) {
       s0 += __shfl_sync(0xffffffffu, c0, k);
@@ -273,7 +279,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     post_partials(v0, v1, bank);
     cluster_sync_all();
     if (K > 1) {
-      if (me == 0 && wp == 0) exchange(bank, tag);
+      if (me == 0 && wp == 0) exchange(bank, tag, true);
       cluster_sync_all();
     }
     totals(bank, v0, v1);
@@ -398,7 +404,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     double ng[NS];
     spmv(ng);  // n = A w, overlapped with the all-reduce
     cluster_wait_acq();
-    if (comm && K > 1 && me == 0) exchange(bank, tag);
+    if (comm && K > 1 && me == 0) exchange(bank, tag, SPCG_PIPE_FENCED);
     send_n(ng, buf, tag);
     cluster_arrive_rel();  // B: cluster totals and intra-cluster halo n
     cluster_wait_acq();
