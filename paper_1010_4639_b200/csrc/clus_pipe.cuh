@@ -55,6 +55,12 @@ struct PipeShared {
 #ifndef SPCG_PIPE_FENCED
 #define SPCG_PIPE_FENCED 0
 #endif
+#ifndef SPCG_PIPE_DEFER
+#define SPCG_PIPE_DEFER 1
+#endif
+#ifndef SPCG_PIPE_LATE_REMOTE
+#define SPCG_PIPE_LATE_REMOTE 0
+#endif
 #ifndef SPCG_PIPE_ALIGNED
 #define SPCG_PIPE_ALIGNED 0
 #endif
@@ -294,10 +300,12 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     if (halo_local(h)) return nhalo[(size_t)buf * A.hcap + h];
     return tagged_load(gh + (((size_t)buf * G + gme) * A.hcap + h) * 2, tag);
   };
-  auto send_n = [&](const double* nv, int buf, uint32_t tag) {
+  // remote: the epoch-tagged global part (other clusters), else the DSMEM part
+  auto send_n = [&](const double* nv, int buf, uint32_t tag, bool remote) {
     for (int e = 0; e < P.nsend; ++e) {
       const ClusSend sd = e < kClusSendCache ? cs.send[e] : A.sends[P.send0 + e];
-      if (sd.dst / C != kc) {
+      if ((sd.dst / C != kc) != remote) continue;
+      if (remote) {
         volatile unsigned long long* dst = gh + ((size_t)buf * G + sd.dst) * A.hcap * 2;
 #pragma unroll
         for (int k = 0; k < NS; ++k)
@@ -389,6 +397,13 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   }
 
   double alpha = 0.0, beta = 0.0;
+  // deferred inter-cluster halo update: CSR/CSC 4.44 -> 3.95 us/iteration on
+  // F; the two-segment (SCSR) build ran 10.3 us with it (unexplained, see
+  // DESIGN), so it keeps the update in place
+  constexpr bool kDefer = SPCG_PIPE_DEFER && !TWO;
+  bool pend = false;  // inter-cluster halo rows of the last update still to do
+  int pbuf = 0;
+  uint32_t ptag = 0;
   for (long long it = 0; max_it > 0; ++it) {
     const int bank = (int)(epoch++ & 1u), buf = (int)(it & 1);
     const uint32_t tag = epoch;
@@ -401,12 +416,39 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       }
     post_partials(g, d, bank);
     cluster_arrive_rel();  // A: the slots of this iteration
+    if (kDefer && pend) {
+      // the last update's halo rows owned by other clusters: their n arrives
+      // through L2, so the load latency overlaps the partials' reduction
+      // instead of sitting before the barrier; the SpMV waits for them
+      if (!comm) {
+        const double na = -alpha;
+        for (int h = tid; h < nh; h += kPipeRowThreads)
+          if (!halo_local(h)) {
+            const double zh = mul_add_rn(halo_n(pbuf, h, ptag), beta, zhalo[h]);
+            zhalo[h] = zh;
+            const int j = halo_win(h);
+            wwin[j] = mul_add_rn(wwin[j], na, zh);
+          }
+        asm volatile("bar.sync 1, %0;" ::"r"(kPipeRowThreads) : "memory");
+      }
+      pend = false;
+    }
     double ng[NS];
     spmv(ng);  // n = A w, overlapped with the all-reduce
     cluster_wait_acq();
     if (comm && K > 1 && me == 0) exchange(bank, tag, SPCG_PIPE_FENCED);
-    send_n(ng, buf, tag);
+#if SPCG_PIPE_LATE_REMOTE
+    // (A/B only) the tagged global halo stored after arrive(B), so the
+    // release of B does not wait for it: CSR 4.31 -> 4.35, SCSR 5.06 -> 4.92
+    // us/iteration on one box (profiles/r01/s4/pipe_late.log): no clear win
+    send_n(ng, buf, tag, false);
     cluster_arrive_rel();  // B: cluster totals and intra-cluster halo n
+    send_n(ng, buf, tag, true);
+#else
+    send_n(ng, buf, tag, false);
+    send_n(ng, buf, tag, true);
+    cluster_arrive_rel();  // B: cluster totals and intra-cluster halo n
+#endif
     cluster_wait_acq();
     double g_new, d_new;
     totals(bank, g_new, d_new);
@@ -475,12 +517,16 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       for (int h = tid; h < nh; h += kPipeRowThreads) {
         // read after the own rows' update: one round trip (both tagged words
         // issued together); issuing it right after barrier B measured slower
+        if (kDefer && !halo_local(h)) continue;
         const double nv = halo_n(buf, h, tag);
         const double zh = mul_add_rn(nv, beta, zhalo[h]);
         zhalo[h] = zh;
         const int j = halo_win(h);
         wwin[j] = mul_add_rn(wwin[j], na, zh);
       }
+    pend = true;
+    pbuf = buf;
+    ptag = tag;
     __syncthreads();
   }
 

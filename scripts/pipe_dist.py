@@ -18,7 +18,8 @@ b, _ = rhs_for(F, seed=1)
 bt = torch.from_numpy(b).cuda()
 lib = N.load()
 flush = torch.empty(64 << 20, dtype=torch.float64, device="cuda")
-for kind, m, acc in (("csr", F, 1), ("sym_priv", extract_lower(F), 1), ("csc", F.to_csc(), 1)):
+for kind, m, acc in (("csr", F, 1), ("sym_priv", extract_lower(F), 1),
+                     ("sym_atomic", extract_lower(F), 0), ("csc", F.to_csc(), 1)):
     dm = m.device()
     x = torch.empty_like(bt)
     for eng in engines:
