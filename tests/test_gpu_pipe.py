@@ -114,3 +114,30 @@ def test_pipelined_multi_cluster_x0_truncation_repeat():
     assert np.linalg.norm(t.x - rt.x) / np.linalg.norm(rt.x) <= 1e-9
     z = cg_solve(F, np.zeros(F.n), x0=x0, engine=6)
     assert z.iterations == 0 and (z.x == 0).all()
+
+
+@pytest.mark.parametrize("engine", [5, 6])
+def test_multi_cluster_breakdown_attribution(engine):
+    """An indefinite FEM-shaped matrix (negative shift) on the K-cluster grid:
+    the breakdown is raised with the reference's iteration (within one: the
+    sign change of p.Ap is subject to fp64 reassociation)."""
+    from paper_1010_4639_b200 import _native as N
+    from paper_1010_4639_b200.genprob import fem_mesh, rhs_for
+    import torch
+
+    F = fem_mesh(shift=-0.5)
+    b, _ = rhs_for(fem_mesh(), seed=1)
+    ref = O.cg_solve("csr", F.row_start, F.col_idx, F.values, b)
+    lib = N.load()
+    bt = torch.from_numpy(b).cuda()
+    xt = torch.empty_like(bt)
+    o = N.CgOptionsC(tol=1e-10, max_iter=0, record_history=0, recompute_final_residual=1,
+                     accumulation=1, engine=engine)
+    res = N.CgResultC()
+    rc = lib.spcg_cg_solve(F.device().handle, bt.data_ptr(), None, xt.data_ptr(), None, o, res,
+                           torch.cuda.current_stream().cuda_stream)
+    assert rc == ref.status == res.status
+    if ref.status != 0:
+        assert abs(res.fail_iteration - ref.fail_iteration) <= 1
+    else:
+        assert abs(res.iterations - ref.iterations) <= max(1, ref.iterations // 100)
