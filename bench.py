@@ -398,8 +398,12 @@ def run_ours(args):
                           "CUDA events around the solve launch); working set %.1f MB"
                           % (solve_bytes(n, nnz, 1) / 1e6)) if small else
                          ("inputs (matrix %.1f GB) >> 126 MB L2, no flush needed" % (12 * nnz / 1e9)),
-                   "parallelism": "1 GPU; per-pass engine (tiled SpMV pass + 2 streaming passes, "
-                                  "device-resident scalars, no host round trip per iteration)"},
+                   "parallelism": ("1 GPU; per-pass engine (tiled SpMV pass + 2 streaming passes, "
+                                   "device-resident scalars, no host round trip per iteration)")
+                                  if sp_launch > 0 else
+                                  ("1 GPU; pipelined cluster-resident engine (one kernel per solve: "
+                                   "matrix in shared memory, K clusters of 8 CTAs, SpMV overlapped "
+                                   "with the all-reduce)")},
         "e2e": {"value": round(e2e_its / (e2e_ms / 1e3), 3), "unit": "iterations/s",
                 "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n + 40,
                 "path": "spcg_cg_solve_host (C-ABI, pinned host b -> x), matrix handle resident"},
