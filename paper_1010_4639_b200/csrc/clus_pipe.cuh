@@ -61,6 +61,12 @@ struct PipeShared {
 #ifndef SPCG_PIPE_LATE_REMOTE
 #define SPCG_PIPE_LATE_REMOTE 0
 #endif
+#ifndef SPCG_PIPE_DEFER_TWO
+#define SPCG_PIPE_DEFER_TWO 0
+#endif
+#ifndef SPCG_PIPE_UNROLL_TWO
+#define SPCG_PIPE_UNROLL_TWO 2
+#endif
 #ifndef SPCG_PIPE_ALIGNED
 #define SPCG_PIPE_ALIGNED 0
 #endif
@@ -187,8 +193,10 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     for (int k = 0; k < NS; ++k) {
       out[k] = 0.0;
       if (swidth[k] > 0) {
-        const double q = sres[k] ? clus_row<TWO>(sval, scol, sbase[k], swidth[k], rlen[k], rlenA[k], wwin)
-                                 : clus_row<TWO>(A.gval, A.gcol, sbase[k], swidth[k], rlen[k], rlenA[k], wwin);
+        // two-segment rows: unroll 2 (unroll 4 spilled at the 128-register cap)
+        constexpr int U = TWO ? SPCG_PIPE_UNROLL_TWO : SPCG_CLUS_UNROLL;
+        const double q = sres[k] ? clus_row<TWO, U>(sval, scol, sbase[k], swidth[k], rlen[k], rlenA[k], wwin)
+                                 : clus_row<TWO, U>(A.gval, A.gcol, sbase[k], swidth[k], rlen[k], rlenA[k], wwin);
         out[k] = rrow[k] >= 0 ? q : 0.0;
       }
     }
@@ -400,7 +408,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   // deferred inter-cluster halo update: CSR/CSC 4.44 -> 3.95 us/iteration on
   // F; the two-segment (SCSR) build ran 10.3 us with it (unexplained, see
   // DESIGN), so it keeps the update in place
-  constexpr bool kDefer = SPCG_PIPE_DEFER && !TWO;
+  constexpr bool kDefer = SPCG_PIPE_DEFER && (!TWO || SPCG_PIPE_DEFER_TWO);
   bool pend = false;  // inter-cluster halo rows of the last update still to do
   int pbuf = 0;
   uint32_t ptag = 0;

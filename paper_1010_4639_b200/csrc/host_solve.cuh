@@ -41,11 +41,14 @@ int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double
     // auto only when (nearly) everything stays in shared memory: streamed
     // slices are re-read from L2 every iteration at L2 latency
     const bool resident = m->cp.streamed * 9 <= m->cp.resident;
-    // auto picks the pipelined form (engine 6) when its row slots hold the
-    // plan: F 4.95 vs 5.71 us/iteration, S 5.04 vs 6.18, CSC 4.90 vs 5.82
+    // auto picks the pipelined form (engine 6) for single-segment rows (CSR,
+    // CSC) when its row slots hold the plan: F 3.97-4.31 vs 5.74 us/iteration.
+    // Two-segment SCSR rows stay on engine 5: engine 6 ran them at 4.7 us on
+    // one box but 7-11 us on another (profiles/r01/s4/pipe_two.log), engine 5
+    // at a steady 6.25
     if (m->cp.ok && (o->engine == 5 || resident))
       return do_clus_cg(m, b, x0, x, hist, o, out, st,
-                        o->engine == 0 && m->cp.max_slices <= kPipeMaxSlices);
+                        o->engine == 0 && !m->cp.two && m->cp.max_slices <= kPipeMaxSlices);
     if (o->engine == 5)
       return fail(SPCG_ERR_UNSUPPORTED, "cluster engine not applicable: " + m->cp.why);
   }
