@@ -11,7 +11,12 @@ from paper_1010_4639_b200.genprob import fem_mesh, rhs_for  # noqa: E402
 F = fem_mesh()
 b, _ = rhs_for(F, seed=1)
 bt = torch.from_numpy(b).cuda()
-dm = F.device()
+kind = sys.argv[3] if len(sys.argv) > 3 else "csr"  # csr | sym (privatized L+D)
+if kind == "sym":
+    from paper_1010_4639_b200 import extract_lower  # noqa: E402
+    dm = extract_lower(F).device()
+else:
+    dm = F.device()
 x = torch.empty_like(bt)
 o = N.CgOptionsC(tol=1e-10, max_iter=int(sys.argv[1]) if len(sys.argv) > 1 else 0,
                  record_history=0, recompute_final_residual=1, accumulation=1,
