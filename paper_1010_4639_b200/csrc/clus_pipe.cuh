@@ -61,6 +61,9 @@ struct PipeShared {
 #ifndef SPCG_PIPE_LATE_REMOTE
 #define SPCG_PIPE_LATE_REMOTE 0
 #endif
+#ifndef SPCG_PIPE_SPIN_NS
+#define SPCG_PIPE_SPIN_NS 0
+#endif
 #ifndef SPCG_PIPE_DEFER_TWO
 #define SPCG_PIPE_DEFER_TWO 0
 #endif
@@ -104,6 +107,9 @@ __device__ __forceinline__ double tagged_finish(const volatile unsigned long lon
                                                 uint32_t tag) {
   unsigned long long spins = 0;
   while ((uint32_t)a != tag || (uint32_t)b != tag) {
+#if SPCG_PIPE_SPIN_NS > 0
+    __nanosleep(SPCG_PIPE_SPIN_NS);  // back off: spinners slow the lines' writers
+#endif
     tagged_issue(src, a, b);
     if (++spins > kSpinLimit) asm volatile("trap;");
   }
