@@ -203,8 +203,21 @@ def build_device_system(workload: str):
     return dm, bt, n, dm.nnz, xg, acc
 
 
+_HOST_CACHE: dict = {}
+
+
 def host_system(workload: str):
-    """Host int64 arrays of the same system for the CPU path: (kind, rs, ci, v, b)."""
+    """Host int64 arrays of the same system for the CPU path: (kind, rs, ci, v, b).
+    The last system is cached (q27 and q27p share theirs)."""
+    key = WORKLOADS[workload][:3]
+    if key in _HOST_CACHE:
+        return _HOST_CACHE[key]
+    _HOST_CACHE.clear()
+    _HOST_CACHE[key] = _host_system(workload)
+    return _HOST_CACHE[key]
+
+
+def _host_system(workload: str):
     from oracle import oracle as O
     from paper_1010_4639_b200.core import extract_lower
     from paper_1010_4639_b200.genprob import fem_mesh, rhs_for
@@ -257,25 +270,27 @@ def cpu_sample(workload: str, steps: int, warmup: int, window: int):
 
 
 # ---- our arm ---------------------------------------------------------------------
-def run_ours(args):
+def _opts(N, acc, max_iter=0, timing=1):
+    return N.CgOptionsC(tol=1e-10, max_iter=max_iter, record_history=0,
+                        recompute_final_residual=1, accumulation=acc, engine=0, timing=timing)
+
+
+def measure_ours(workload: str, steps: int, warmup: int, peak: float, max_iter: int = 0,
+                 clocks: bool = False, spmv: bool = False):
+    """One workload through spcg_cg_solve (device-resident, `value`) and
+    spcg_cg_solve_host (pinned host b in, x out every step: `e2e`).  Returns
+    the fields of a bench line (no metric/header keys)."""
     import torch
 
     from paper_1010_4639_b200 import _native as N
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1 or args.gpus > 1 or args.engine == "sharded":
-        return run_distributed(args)
-    torch.cuda.set_device(0)
-    torch.cuda.init()
     lib = N.load()
-    peak, peak_src = peaks()
     t0 = time.time()
-    dm, bt, n, nnz, xg, acc = build_device_system(args.workload)
+    dm, bt, n, nnz, xg, acc = build_device_system(workload)
     setup_s = time.time() - t0
     st = torch.cuda.current_stream()
     x = torch.empty_like(bt)
-    opts = N.CgOptionsC(tol=1e-10, max_iter=args.max_iter, record_history=0,
-                        recompute_final_residual=1, accumulation=acc, engine=0, timing=1)
+    opts = _opts(N, acc, max_iter)
 
     def solve_dev():
         r = N.CgResultC()
@@ -283,7 +298,7 @@ def run_ours(args):
                                   st.cuda_stream), "spcg_cg_solve")
         return r
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         solve_dev()
     torch.cuda.synchronize()
     # working sets below 256 MB would stay in the 126 MB L2 between steps:
@@ -291,28 +306,30 @@ def run_ours(args):
     small = solve_bytes(n, nnz, 1) < 256e6
     flush = torch.empty(64 << 20, dtype=torch.float64, device="cuda") if small else None
     results = []
-    with ClockSampler(torch.cuda.current_device()) as clk:
-        torch.cuda.synchronize()
-        if small:
-            # per step: flush, then the solve; its time is the library's CUDA
-            # event pair on the solve stream around the launch (device_ms),
-            # which host-side stalls between steps cannot inflate
-            for i in range(args.steps):
-                flush.fill_(float(i))
-                results.append(solve_dev())
-                torch.cuda.synchronize()
-            ms = float(sum(r.device_ms for r in results))
-        else:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(st)
-            for _ in range(args.steps):
-                results.append(solve_dev())
-            e1.record(st)
+    clk = ClockSampler(torch.cuda.current_device()) if clocks else None
+    if clk:
+        clk.__enter__()
+    torch.cuda.synchronize()
+    if small:
+        # per step: flush, then the solve; its time is the library's CUDA
+        # event pair on the solve stream around the launch (device_ms),
+        # which host-side stalls between steps cannot inflate
+        for i in range(steps):
+            flush.fill_(float(i))
+            results.append(solve_dev())
             torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1)
-    clocks = clk.summary()
+        ms = float(sum(r.device_ms for r in results))
+    else:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(steps):
+            results.append(solve_dev())
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+    if clk:
+        clk.__exit__(None, None, None)
     iters = sum(r.iterations for r in results)
-    value = iters / (ms / 1e3)
     solve_ms = float(np.mean([r.device_ms for r in results]))
     it_per = results[-1].iterations
     alg_solve = solve_bytes(n, nnz, it_per)
@@ -325,11 +342,13 @@ def run_ours(args):
         kern = "dist_spmv_pq (SpMV pass of the per-pass engine: q = A p, partial p.q)"
         kern_ms = sp_kms / sp_launch
         alg = spmv_bytes(n, nnz)
+        model = "SpMV pass 12*nnz + 4*(n+1) + 16*n (SURVEY 8d)"
     else:  # resident systems: the whole solve is one persistent kernel
-        kern = ("clus_pcg_kernel (pipelined cluster-resident CG solve, one launch) or "
+        kern = ("clus_pcg_kernel / clus_cg_kernel (cluster-resident CG solve, one launch) or "
                 "cg1_kernel (grid-resident, unbanded systems)")
         kern_ms = solve_ms
         alg = alg_solve
+        model = "per iteration 12*nnz + 4*(n+1) + 88*n (SURVEY 8d) + prologue/epilogue"
     achieved = alg / (kern_ms / 1e3) / 1e9
 
     # e2e through the C-ABI host entry point: pinned b in, x out, every step
@@ -337,103 +356,133 @@ def run_ours(args):
     b_host.copy_(bt.cpu())
     x_host = torch.empty(n, dtype=torch.float64, pin_memory=True)
     bh, xh = b_host.numpy(), x_host.numpy()
+    opts_e = _opts(N, acc, max_iter, timing=0)
 
     def solve_host():
         r = N.CgResultC()
         N.check(lib.spcg_cg_solve_host(dm.handle, bh.ctypes.data, None, xh.ctypes.data, None,
-                                       opts, r, st.cuda_stream), "spcg_cg_solve_host")
+                                       opts_e, r, st.cuda_stream), "spcg_cg_solve_host")
         return r
 
     solve_host()
     torch.cuda.synchronize()
-    e2 = torch.cuda.Event(enable_timing=True)
-    e3 = torch.cuda.Event(enable_timing=True)
-    e2.record(st)
-    e2e_its = 0
-    for _ in range(args.steps):
+    e2e_ms, e2e_its = 0.0, 0
+    for i in range(steps):
+        if small:
+            flush.fill_(float(i))
+        torch.cuda.synchronize()
+        e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e2.record(st)
         e2e_its += solve_host().iterations
-    e3.record(st)
-    torch.cuda.synchronize()
-    e2e_ms = e2.elapsed_time(e3)
+        e3.record(st)
+        torch.cuda.synchronize()
+        e2e_ms += e2.elapsed_time(e3)
     x_check = xh.copy()
 
-    # standalone SpMV kernel (the metric's "SpMV HBM GB/s")
-    y = torch.empty_like(bt)
-    for _ in range(3):
-        lib.spcg_spmv(dm.handle, bt.data_ptr(), y.data_ptr(), acc, st.cuda_stream)
-    reps = 20 if n > 1_000_000 else 200
-    e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e4.record(st)
-    for _ in range(reps):
-        lib.spcg_spmv(dm.handle, bt.data_ptr(), y.data_ptr(), acc, st.cuda_stream)
-    e5.record(st)
-    torch.cuda.synchronize()
-    sp_ms = e4.elapsed_time(e5) / reps
-    sp_gbs = spmv_bytes(n, nnz) / (sp_ms / 1e3) / 1e9
-
-    err_gen = float(np.max(np.abs(x_check - xg)) / max(1.0, np.max(np.abs(xg))))
-    traffic = None
-    tfile = ROOT / "profiles" / "r01" / "p3_spmv_traffic.json"
-    if args.workload == "p3" and sp_launch > 0 and tfile.exists():
-        # DRAM bytes of one dist_spmv_pq launch on this system (ncu --metrics
-        # dram__bytes_read.sum,dram__bytes_write.sum; profiles/r01)
-        traffic = int(json.loads(tfile.read_text())["dram_bytes_per_launch"])
-    _, _, _, _, desc = WORKLOADS[args.workload]
-    line = {
-        "metric": "fp64 CG iterations/sec (and SpMV HBM GB/s, % of roofline)",
-        "value": round(value, 3),
-        "unit": "iterations/s",
-        "n_gpus": 1,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": ms / args.steps,
-        "higher_is_better": True,
-        "scaling": "strong",
-        "vs_baseline": None,
-        "dtype": "f64",
-        "data": "synthetic (reference generators rebuilt in HBM; b = A x_gen, x_gen ~ N(0,1) seed 1)",
-        "config": {"workload": desc, "n": n, "nnz_stored": nnz, "tol": 1e-10, "x0": "zeros",
-                   "iterations_per_solve": it_per, "step": "one full cg_solve",
-                   "l2": ("L2 flushed (512 MB write) before every timed step (step time = "
-                          "CUDA events around the solve launch); working set %.1f MB"
-                          % (solve_bytes(n, nnz, 1) / 1e6)) if small else
-                         ("inputs (matrix %.1f GB) >> 126 MB L2, no flush needed" % (12 * nnz / 1e9)),
-                   "parallelism": ("1 GPU; per-pass engine (tiled SpMV pass + 2 streaming passes, "
-                                   "device-resident scalars, no host round trip per iteration)")
-                                  if sp_launch > 0 else
-                                  ("1 GPU; pipelined cluster-resident engine (one kernel per solve: "
-                                   "matrix in shared memory, K clusters of 8 CTAs, SpMV overlapped "
-                                   "with the all-reduce)")},
+    out = {
+        "value": round(iters / (ms / 1e3), 3), "unit": "iterations/s",
+        "ms_per_step": ms / steps, "steps": steps, "warmup": warmup,
+        "n": n, "nnz_stored": nnz, "iterations_per_solve": it_per,
+        "l2": ("L2 flushed (512 MB write) before every timed step (step time = CUDA events "
+               "around the solve launch); working set %.1f MB" % (solve_bytes(n, nnz, 1) / 1e6))
+        if small else ("inputs (matrix %.1f GB) >> 126 MB L2, no flush needed" % (12 * nnz / 1e9)),
+        "engine": "per-pass" if sp_launch > 0 else "resident",
         "e2e": {"value": round(e2e_its / (e2e_ms / 1e3), 3), "unit": "iterations/s",
                 "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n + 40,
                 "path": "spcg_cg_solve_host (C-ABI, pinned host b -> x), matrix handle resident"},
         "gpu_launches": int(sum(r.kernel_launches for r in results)),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "traffic_source": "profiles/r01/p3_spmv_traffic.json (ncu dram__bytes of "
-                                       "one launch)" if traffic else None,
-                     "peak_source": peak_src, "kernel": kern,
-                     "algorithmic_bytes_per_launch": alg, "kernel_ms": kern_ms,
-                     "launches_timed": int(sp_launch) if sp_launch else args.steps,
-                     "bytes_model": "SpMV pass 12*nnz + 4*(n+1) + 16*n (SURVEY 8d)"
-                     if sp_launch else "per iteration 12*nnz + 4*(n+1) + 88*n (SURVEY 8d)"},
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "kernel": kern, "algorithmic_bytes_per_launch": alg, "kernel_ms": kern_ms,
+                     "launches_timed": int(sp_launch) if sp_launch else steps,
+                     "bytes_model": model},
         "roofline_iteration": {"achieved": round(achieved_solve, 1),
                                "frac": round(achieved_solve / peak, 4), "unit": "GB/s",
-                               "solve_ms": solve_ms, "algorithmic_bytes_per_solve": alg_solve,
+                               "solve_ms": solve_ms, "us_per_iteration": 1e3 * solve_ms / it_per,
+                               "algorithmic_bytes_per_solve": alg_solve,
                                "bytes_model": "per iteration 12*nnz + 4*(n+1) + 88*n "
                                               "(SURVEY 8d) + prologue/epilogue"},
-        "spmv": {"ms": sp_ms, "GBs": round(sp_gbs, 1), "frac": round(sp_gbs / peak, 4),
-                 "bytes": spmv_bytes(n, nnz)},
-        "clocks": clocks,
         "final_relative_residual": results[-1].final_relative_residual,
         "converged": bool(results[-1].converged),
-        "max_abs_err_vs_xgen": err_gen,
+        "max_abs_err_vs_xgen": float(np.max(np.abs(x_check - xg)) / max(1.0, np.max(np.abs(xg)))),
         "setup_s": round(setup_s, 2),
     }
-    if not args.no_secondary and args.workload == "p3":
-        line["secondary"] = secondary(peak)
+    if clk:
+        out["clocks"] = clk.summary()
+    if spmv:  # standalone SpMV kernel (the metric's "SpMV HBM GB/s")
+        y = torch.empty_like(bt)
+        for _ in range(3):
+            lib.spcg_spmv(dm.handle, bt.data_ptr(), y.data_ptr(), acc, st.cuda_stream)
+        reps = 20 if n > 1_000_000 else 200
+        e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e4.record(st)
+        for _ in range(reps):
+            lib.spcg_spmv(dm.handle, bt.data_ptr(), y.data_ptr(), acc, st.cuda_stream)
+        e5.record(st)
+        torch.cuda.synchronize()
+        sp_ms = e4.elapsed_time(e5) / reps
+        sp_gbs = spmv_bytes(n, nnz) / (sp_ms / 1e3) / 1e9
+        out["spmv"] = {"ms": sp_ms, "GBs": round(sp_gbs, 1), "frac": round(sp_gbs / peak, 4),
+                       "bytes": spmv_bytes(n, nnz)}
+    dm.close()
+    del bt, x, b_host, x_host, flush
+    torch.cuda.empty_cache()
+    return out
+
+
+METRIC = "fp64 CG iterations/sec (and SpMV HBM GB/s, % of roofline)"
+
+
+def run_ours(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 or args.gpus > 1 or args.engine == "sharded":
+        return run_distributed(args)
+    torch.cuda.set_device(0)
+    torch.cuda.init()
+    peak, peak_src = peaks()
+    m = measure_ours(args.workload, args.steps, args.warmup, peak, args.max_iter, clocks=True,
+                     spmv=True)
+    tfile = ROOT / "profiles" / "r01" / "p3_spmv_traffic.json"
+    if args.workload == "p3" and m["engine"] == "per-pass" and tfile.exists():
+        # DRAM bytes of one dist_spmv_pq launch on this system (ncu --metrics
+        # dram__bytes_read.sum,dram__bytes_write.sum; profiles/r01)
+        m["roofline"]["traffic"] = int(json.loads(tfile.read_text())["dram_bytes_per_launch"])
+        m["roofline"]["traffic_source"] = ("profiles/r01/p3_spmv_traffic.json (ncu dram__bytes "
+                                           "of one launch)")
+    m["roofline"]["peak_source"] = peak_src
+    _, _, _, _, desc = WORKLOADS[args.workload]
+    line = {
+        "metric": METRIC,
+        "value": m["value"],
+        "unit": "iterations/s",
+        "n_gpus": 1,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": m["ms_per_step"],
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (reference generators rebuilt in HBM; b = A x_gen, x_gen ~ N(0,1) seed 1)",
+        "config": {"workload": desc, "n": m["n"], "nnz_stored": m["nnz_stored"], "tol": 1e-10,
+                   "x0": "zeros", "iterations_per_solve": m["iterations_per_solve"],
+                   "step": "one full cg_solve", "l2": m["l2"],
+                   "parallelism": ("1 GPU; per-pass engine (tiled SpMV pass + 2 streaming passes, "
+                                   "device-resident scalars, no host round trip per iteration)")
+                                  if m["engine"] == "per-pass" else
+                                  ("1 GPU; cluster-resident engine (one kernel per solve: "
+                                   "matrix in shared memory, K clusters of 8 CTAs)")},
+    }
+    for k in ("e2e", "gpu_launches", "roofline", "roofline_iteration", "spmv", "clocks",
+              "final_relative_residual", "converged", "max_abs_err_vs_xgen", "setup_s"):
+        line[k] = m[k]
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_sample(args.workload, steps=1, warmup=0, window=20)
+        line["cpu_baseline"] = cpu_sample(args.workload, steps=3, warmup=1,
+                                          window=WINDOW.get(args.workload, 20))
+    if not args.no_secondary and args.workload == "p3":
+        line["secondary"] = secondary(peak, cpu=not args.no_cpu_baseline)
     print(json.dumps(line), flush=True)
 
 
@@ -600,36 +649,28 @@ def run_distributed(args):
         dist.destroy_process_group()
 
 
-def secondary(peak):
-    """The 30880-row FEM-shaped configs (BASELINE configs[0..1]): full solves."""
-    import torch
+# reference CPU window (iterations) per workload: a bounded sample of ~5-15 s
+WINDOW = {"p3": 20, "p2": 20, "q27": 10, "q27p": 10}
 
-    from paper_1010_4639_b200 import _native as N
 
-    lib = N.load()
+def secondary(peak, cpu=True):
+    """Every other BASELINE config, each with its own roofline,
+    e2e and reference-CPU baseline: P2 4096^2, Q27 256^3 in both
+    accumulations, and the 30880-row FEM-shaped F (full CSR), S (symmetric
+    CSR) and CSC (BASELINE configs[0..2,4])."""
     out = {}
-    flush = torch.empty(64 << 20, dtype=torch.float64, device="cuda")  # 512 MB > L2
-    for w in ("f", "s", "csc"):
-        dm, bt, n, nnz, _, acc = build_device_system(w)
-        x = torch.empty_like(bt)
-        o = N.CgOptionsC(tol=1e-10, max_iter=0, record_history=0, recompute_final_residual=1,
-                         accumulation=acc, engine=0)
-        rs = []
-        for k in range(8):
-            flush.fill_(float(k))  # L2 flushed before every solve (device_ms excludes it)
-            r = N.CgResultC()
-            N.check(lib.spcg_cg_solve(dm.handle, bt.data_ptr(), None, x.data_ptr(), None, o, r,
-                                      torch.cuda.current_stream().cuda_stream), "solve")
-            if k >= 3:
-                rs.append((r.device_ms, r.iterations))
-        ms = float(np.median([a for a, _ in rs]))
-        its = rs[-1][1]
-        us = ms * 1e3 / its
-        gbs = iter_bytes(n, nnz) / (us * 1e-6) / 1e9
-        out[w] = {"workload": WORKLOADS[w][4], "l2": "flushed before every solve",
-                  "iterations": its, "solve_ms": round(ms, 4),
-                  "us_per_iteration": round(us, 3), "iterations_per_s": round(its / (ms / 1e3), 1),
-                  "GBs_algorithmic": round(gbs, 1), "frac": round(gbs / peak, 4)}
+    for w in ("p2", "q27", "q27p", "f", "s", "csc"):
+        big = w in ("p2", "q27", "q27p")
+        m = measure_ours(w, steps=3 if big else 10, warmup=1 if big else 3, peak=peak)
+        d = {"workload": WORKLOADS[w][4]}
+        for k in ("value", "unit", "ms_per_step", "steps", "warmup", "n", "nnz_stored",
+                  "iterations_per_solve", "l2", "engine", "e2e", "roofline", "roofline_iteration",
+                  "final_relative_residual", "converged"):
+            d[k] = m[k]
+        if cpu:
+            d["cpu_baseline"] = cpu_sample(w, steps=3 if big else 5, warmup=1,
+                                           window=WINDOW.get(w, 20))
+        out[w] = d
     return out
 
 
@@ -701,15 +742,16 @@ def run_reference(args):
     if rank != 0:
         return
     _, _, _, _, desc = WORKLOADS[args.workload]
-    s = cpu_sample(args.workload, steps=args.steps, warmup=min(args.warmup, 1), window=20)
+    s = cpu_sample(args.workload, steps=args.steps, warmup=args.warmup,
+                   window=WINDOW.get(args.workload, 20))
     line = {
         "impl": "reference",
         "metric": "fp64 CG iterations/sec (and SpMV HBM GB/s, % of roofline)",
         "value": round(s["value"], 4),
         "unit": "iterations/s",
-        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "n_gpus": int(os.environ.get("WORLD_SIZE", str(args.gpus))),
         "steps": args.steps,
-        "warmup": min(args.warmup, 1),
+        "warmup": args.warmup,
         "ms_per_step": s["s_per_step"] * 1e3,
         "higher_is_better": True,
         "scaling": "strong",
@@ -722,6 +764,66 @@ def run_reference(args):
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` (N > 1) run directly, without torchrun: launch the
+    N ranks ourselves (one process per GPU, torch.distributed.run on
+    127.0.0.1) with the same arguments; rank 0 prints the line."""
+    import socket
+
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    env = dict(os.environ)
+    # communicator bring-up is logged (NCCL_DEBUG=INFO lines go to stderr)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.run(cmd, env=env).returncode
+
+
+def run_dry(args):
+    """CPU dry run of the multi-rank plumbing (gloo; no GPU, no solve): the
+    rank env, the P3 z-slab partition and halo plan built collectively, the
+    max-over-ranks reduction and the rank-0 line.  `value` is null: this is
+    a plumbing check, never a measurement."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1010_4639_b200 import distributed as D
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    gather = (lambda o: [o]) if world == 1 else D.torch_collectives()[0]
+    kind, dims, fmt, _, desc = WORKLOADS[args.workload]
+    if kind == "fem":
+        dims = (16, 10, 193)
+    nx, ny, nz = (list(dims) + [1, 1])[:3]
+    plane = nx * ny if nz > 1 else nx
+    n = nx * ny * nz
+    bounds = D.row_partition(n, world, align=plane)
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    # halo of a 7-point slab: one plane on each interior side
+    halo = np.concatenate([np.arange(max(0, r0 - plane), r0), np.arange(r1, min(n, r1 + plane))])
+    plan = D.halo_plan(halo, bounds, rank, gather)
+    t = torch.tensor([float(plan.send_off[-1])], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": None, "unit": "iterations/s", "n_gpus": world,
+            "steps": 0, "warmup": 0, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "none (dry run)", "dry_run": True,
+            "config": {"workload": desc, "n": n, "ranks_rows": [int(b) for b in bounds],
+                       "max_halo_send": int(t.item()), "backend": "gloo (CPU)"}}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def main():
@@ -738,10 +840,17 @@ def main():
                     help="paper Table-I per-op rows (F matrix) on GPU vs the reference CPU path")
     ap.add_argument("--engine", choices=("auto", "sharded"), default="auto",
                     help="sharded: run the row-sharded engine even on one GPU")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU check of the N-rank plumbing (gloo), no GPU and no measurement")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours" and args.max_iter == 0:
         print("note: contract requires warmup >= 3", file=sys.stderr)
-    if args.table1:
+    launched = "WORLD_SIZE" in os.environ
+    if args.gpus > 1 and not launched and (args.impl == "ours" or args.dry_run):
+        sys.exit(spawn_ranks(args))
+    if args.dry_run:
+        run_dry(args)
+    elif args.table1:
         run_table1(args)
     elif args.impl == "reference":
         run_reference(args)

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SPCG_ABI_VERSION 1
+#define SPCG_ABI_VERSION 2
 
 typedef enum {
   SPCG_OK = 0,
@@ -122,19 +122,20 @@ typedef struct {
   int32_t record_history;        /* write rel residual per iteration to hist   */
   int32_t recompute_final_residual; /* default 1 (solver.py:159-162)           */
   int32_t accumulation;          /* spcg_accumulation, SCSR only               */
-  int32_t engine;                /* 0 = auto (6 for systems whose rows fit
-                                    the co-resident clusters, else 3 when
-                                    the system is resident on chip, else 2),
-                                    1 = persistent kernel, two-reduction CG,
+  int32_t engine;                /* 0 = auto: banded systems whose rows fit
+                                    the co-resident clusters -> 6 (single-
+                                    segment rows) or 5 (two-segment SCSR
+                                    rows); other systems resident on chip
+                                    -> 3; everything else -> 2.
                                     2 = per-pass kernels (the sharded engine),
                                     3 = persistent single-reduction CG
                                         (Chronopoulos-Gear, resident only),
-                                    4 = persistent three-pass CG,
                                     5 = cluster-resident single-reduction CG
-                                        (<= 16 CTAs, banded systems),
+                                        (banded systems),
                                     6 = engine 5's plan with pipelined CG
                                         (Ghysels-Vanroose: the SpMV overlaps
-                                        the all-reduce)                      */
+                                        the all-reduce).
+                                    Other values: SPCG_ERR_ARG.             */
   int32_t timing;                /* per-pass engine: CUDA-event time of every
                                     SpMV pass -> result.spmv_ms / launches   */
   int32_t row_sums;              /* 0 = auto: in the streaming CG passes, lines
@@ -158,6 +159,19 @@ typedef struct {
   int64_t kernel_launches;       /* kernels launched by this solve             */
   double spmv_ms;                /* with opts.timing: summed SpMV-pass time    */
   int64_t spmv_launches;         /* with opts.timing: SpMV passes timed        */
+  /* ABI 2 */
+  int32_t engine_used;           /* engine that produced x (after auto routing
+                                    and the pipelined engine's guard)         */
+  int32_t fallbacks;             /* 1: auto's pipelined solve was re-run on
+                                    engine 5 (cond estimate or true residual
+                                    above the guard's limits)                */
+  double cond_estimate;          /* engine 6: Ritz estimate of cond(A) from the
+                                    CG coefficients (0 when not computed)     */
+  double phase_ms[3];            /* device time split as in SolveReport.timings:
+                                    [0] SpMV (with its fused dot partial),
+                                    [1] reductions / scalar steps ("dot"),
+                                    [2] vector updates ("axpy"); zeros when the
+                                    engine did not measure them              */
 } spcg_cg_result;
 
 /* Device-resident solve.  d_x0 may be NULL (zeros).  d_x receives x.
@@ -177,7 +191,9 @@ int spcg_cg_solve_host(spcg_matrix_t m, const double* h_b, const double* h_x0,
 
 /* NCCL bootstrap: rank 0 makes an id, the host framework broadcasts the 128
  * bytes, every rank creates its communicator (one rank per GPU; the current
- * CUDA device is used).  nranks == 1 needs no NCCL. */
+ * CUDA device is used).  nranks == 1 with id == NULL makes no NCCL
+ * communicator (the collectives are no-ops); with an id it makes a real
+ * one-rank NCCL communicator, so the NCCL data plane runs on one GPU too. */
 #define SPCG_COMM_ID_BYTES 128
 typedef struct spcg_comm_s* spcg_comm_t;
 int spcg_comm_unique_id(unsigned char* out_id);

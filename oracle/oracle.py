@@ -269,6 +269,23 @@ class RefKernels:
         return out
 
 
+_STRICT: dict = {}
+
+
+def _strict_of(rs, ci, v):
+    """SymHalfMatrix.strict_lower (core.py:145-156): a cached property of the
+    reference's matrix object, so it is built once per matrix, not per solve."""
+    key = (rs.ctypes.data, ci.ctypes.data, v.ctypes.data, rs.shape[0], ci.shape[0])
+    if key not in _STRICT:
+        n = len(rs) - 1
+        rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(rs))
+        mk = ci < rows
+        _STRICT.clear()
+        _STRICT[key] = (np.ascontiguousarray(rows[mk]), np.ascontiguousarray(ci[mk]),
+                        np.ascontiguousarray(v[mk]))
+    return _STRICT[key]
+
+
 def cg_solve_ref(kind, row_start, col_idx, values, b, x0=None, tol=1e-10, max_iter=None,
                  recompute=True, record_history=False, workers=1, chunk=None,
                  accumulation="privatized") -> Result:
@@ -277,10 +294,7 @@ def cg_solve_ref(kind, row_start, col_idx, values, b, x0=None, tol=1e-10, max_it
     rs, ci, v = _i(row_start), _i(col_idx), _f64(values)
     n = len(rs) - 1
     if kind == "sym":
-        rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(rs))
-        mk = ci < rows
-        strict = (np.ascontiguousarray(rows[mk]), np.ascontiguousarray(ci[mk]),
-                  np.ascontiguousarray(v[mk]))
+        strict = _strict_of(rs, ci, v)
         spmv = lambda x: K.spmv_sym(rs, ci, v, strict, x)  # noqa: E731
     else:
         spmv = lambda x: K.spmv_full(rs, ci, v, x)  # noqa: E731

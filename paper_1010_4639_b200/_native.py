@@ -61,6 +61,10 @@ class CgResultC(ctypes.Structure):
         ("kernel_launches", ctypes.c_int64),
         ("spmv_ms", ctypes.c_double),
         ("spmv_launches", ctypes.c_int64),
+        ("engine_used", ctypes.c_int32),
+        ("fallbacks", ctypes.c_int32),
+        ("cond_estimate", ctypes.c_double),
+        ("phase_ms", ctypes.c_double * 3),
     ]
 
 

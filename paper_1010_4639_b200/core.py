@@ -77,13 +77,15 @@ class _Compressed:
         return int(self.values.shape[0])
 
     def device(self, accumulation: str | None = None):
-        """Device copy (uploaded once; matrices are immutable)."""
-        from .device import DeviceMatrix
+        """Device copy on the CURRENT CUDA device (uploaded once per device;
+        matrices are immutable)."""
+        from .device import DeviceMatrix, current_device
 
-        dev = self._cache.get("device")
+        key = ("device", current_device())
+        dev = self._cache.get(key)
         if dev is None:
             dev = DeviceMatrix.from_host(self)
-            self._cache["device"] = dev
+            self._cache[key] = dev
         return dev
 
 

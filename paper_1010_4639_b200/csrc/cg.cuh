@@ -1,21 +1,13 @@
-// cg.cuh — the whole CG solve (solver.py:65-172) as ONE persistent
-// cooperative kernel.
+// cg.cuh — shared pieces of the persistent (grid-resident) CG engine:
+// the device result record, the solve arguments, and the grid-wide
+// all-reduce barrier and resident tile iteration used by cg1.cuh
+// (engine 3, single-reduction CG).  The two-reduction persistent kernels of
+// round 1 (engines 1 and 4) were removed: no default path used them and the
+// per-pass engine (dist.cuh) is faster on every streaming system.
 //
-// Per iteration k the grid makes two passes and two grid-wide all-reduce
-// barriers (the minimum for unmodified CG: p.Ap and r.r are sequential):
-//   pass A  (tiles)  p_k = r + beta p_{k-1} folded into the gather,
-//                    q = A p_k, x += alpha_{k-1} p_{k-1} (deferred x update),
-//                    partial p.q                                 -> allreduce
-//   scalar           pq<=0 / non-finite alpha checks, alpha = rr/pq
-//   pass B           r -= alpha q, partial r.r (atomic formats: q := 0) -> allreduce
-//   scalar           rel, history, convergence, beta = rr_new/rr
 // Scalars are reduced in a fixed order and are bitwise identical in every
 // CTA, so control flow stays grid-uniform without any host round trip.
-//
-// RES (resident) variant: every CTA owns <= kStages tiles; the tiles stay in
-// shared memory and the CTA's own x, r, p, q, b entries stay in registers for
-// the entire solve; only r and p are published (stored) for other CTAs'
-// gathers.  Used when the matrix fits in the grid's shared memory.
+
 #pragma once
 #include "lines.cuh"
 
@@ -28,6 +20,7 @@ struct CgDevResult {
   int status;
   double final_rel;
   double b_norm;
+  double rec_rel;  // engine 6: the recursive rel of the last iteration
 };
 
 struct CgArgs {
@@ -179,360 +172,6 @@ __device__ __forceinline__ void run_tiles(Pipe& P, Smem& sm, const MatView& M, c
     if (active) fn(j, line, o);
     pipe_release<TWO>(P, sm, M, s);
   }
-}
-
-template <int FMT, bool RES>
-__global__ void __launch_bounds__(kBlock, RES ? 1 : kStreamMinBlocks) cg_kernel(const CgArgs A) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-  constexpr bool TWO = (FMT == K_SCSR_PRIV);
-  constexpr bool ATOM = (FMT == K_SCSR_ATOMIC || FMT == K_CSC);
-  const MatView& M = A.M;
-  const int n = M.n;
-  const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long gstride = (long long)gridDim.x * blockDim.x;
-  const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
-
-  smem_init(sm);
-  Pipe P;
-  pipe_start<TWO>(P, sm, M, /*allow_resident=*/RES);
-  uint32_t epoch = 0;
-
-  // RES: per-thread owned lines and their register-resident vector entries.
-  int li[kStages];
-  double xr[kStages], rg[kStages], pg[kStages], qg[kStages], bg[kStages];
-#pragma unroll
-  for (int u = 0; u < kStages; ++u) {
-    li[u] = -1;
-    xr[u] = rg[u] = pg[u] = qg[u] = bg[u] = 0.0;
-  }
-  if (RES) {
-#pragma unroll
-    for (int u = 0; u < kStages; ++u) {
-      if (u < P.m) {
-        mbar_wait(&sm.full[u], 0);
-        const StageMeta& mt = sm.meta[u];
-        li[u] = owned_line<FMT>(mt);
-      }
-    }
-  }
-
-  // ---- ||b|| (solver.py:107) --------------------------------------------------
-  double part = 0.0;
-  if (RES) {
-#pragma unroll
-    for (int u = 0; u < kStages; ++u)
-      if (li[u] >= 0) {
-        bg[u] = A.b[li[u]];
-        part = fma(bg[u], bg[u], part);
-      }
-  } else {
-    for (long long i = gtid; i < n; i += gstride) part = fma(A.b[i], A.b[i], part);
-  }
-  const double b_norm = sqrt(grid_allreduce(part, sm, A.slots, epoch));
-
-  if (b_norm == 0.0) {  // solver.py:109-118: x = 0 even when x0 != 0
-    for (long long i = gtid; i < n; i += gstride) A.x[i] = 0.0;
-    if (leader) {
-      A.res->iterations = 0;
-      A.res->fail_iter = 0;
-      A.res->converged = 1;
-      A.res->status = ST_OK;
-      A.res->final_rel = 0.0;
-      A.res->b_norm = 0.0;
-    }
-    pipe_drain(P, sm);
-    return;
-  }
-
-  // ---- x = x0, r = b - A x0 (solver.py:120-124) -------------------------------
-  if (A.x0 != nullptr) {
-    SrcPlain sx{A.x0};
-    if (RES) {
-#pragma unroll
-      for (int u = 0; u < kStages; ++u)
-        if (li[u] >= 0) xr[u] = A.x0[li[u]];
-      run_tiles<FMT, false, TWO, RES>(P, sm, M, sx, A.q, [&](int j, int i, const LineOut& o) {
-        if (FMT == K_SCSR_ATOMIC) red_add_f64(A.q + i, o.q);
-        else if (!ATOM) qg[j] = o.q;
-      });
-      if (ATOM) grid_allreduce(0.0, sm, A.slots, epoch);
-#pragma unroll
-      for (int u = 0; u < kStages; ++u)
-        if (li[u] >= 0) {
-          const int i = li[u];
-          double qi = qg[u];
-          if (ATOM) {
-            qi = A.q[i];
-            A.q[i] = 0.0;
-          }
-          rg[u] = mul_add_rn(bg[u], -1.0, qi);
-          A.r[i] = rg[u];
-        }
-    } else {
-      for (long long i = gtid; i < n; i += gstride) A.x[i] = A.x0[i];
-      run_tiles<FMT, false, TWO, RES>(P, sm, M, sx, A.q, [&](int, int i, const LineOut& o) {
-        finish_plain<FMT>(o, i, A.q);
-      });
-      grid_allreduce(0.0, sm, A.slots, epoch);
-      for (long long i = gtid; i < n; i += gstride) {
-        const double qi = A.q[i];
-        if (ATOM) A.q[i] = 0.0;
-        A.r[i] = mul_add_rn(A.b[i], -1.0, qi);
-      }
-    }
-  } else {
-    if (RES) {
-#pragma unroll
-      for (int u = 0; u < kStages; ++u)
-        if (li[u] >= 0) {
-          rg[u] = bg[u];
-          A.r[li[u]] = bg[u];
-        }
-    } else {
-      for (long long i = gtid; i < n; i += gstride) {
-        A.x[i] = 0.0;
-        A.r[i] = A.b[i];
-      }
-    }
-  }
-  part = 0.0;
-  if (RES) {
-#pragma unroll
-    for (int u = 0; u < kStages; ++u)
-      if (li[u] >= 0) part = fma(rg[u], rg[u], part);
-  } else {
-    for (long long i = gtid; i < n; i += gstride) part = fma(A.r[i], A.r[i], part);
-  }
-  double rr = grid_allreduce(part, sm, A.slots, epoch);
-
-  // ---- CG loop (solver.py:126-157) ---------------------------------------------
-  const double tol_b = A.tol * b_norm;
-  long long max_it = A.max_iter;
-  double rel = sqrt(rr) / b_norm;
-  int converged = 0, status = ST_OK;
-  long long iterations = 0, fail_iter = 0;
-  if (sqrt(rr) <= tol_b) {
-    converged = 1;
-    max_it = 0;
-  }
-  double alpha = 0.0, beta = 0.0;
-  double* p_old = A.p1;
-  double* p_new = A.p0;
-  double* p_cur = nullptr;
-
-#if SPCG_TRACE
-  unsigned long long tr[4] = {0, 0, 0, 0};
-  P.trace = A.trace != nullptr;
-  unsigned long long tlast = A.trace ? globaltimer_ns() : 0;
-  auto mark = [&](int ph) {
-    if (A.trace && threadIdx.x == 0) {
-      const unsigned long long t = globaltimer_ns();
-      tr[ph] += t - tlast;
-      tlast = t;
-    }
-  };
-#else
-  auto mark = [](int) {};
-#endif
-  for (long long k = 1; k <= max_it; ++k) {
-    // pass A
-    double pq = 0.0;
-    auto lineA = [&](int j, int i, const LineOut& o) {
-      if (RES) {
-        if (k > 1) xr[j] = mul_add_rn(xr[j], alpha, pg[j]);
-        pg[j] = o.xi;
-        if (!ATOM) qg[j] = o.q;
-      } else {
-        if (k > 1) A.x[i] = mul_add_rn(SPCG_NO_XPRE ? A.x[i] : o.xo, alpha, p_old[i]);
-        if (!ATOM) A.q[i] = o.q;
-      }
-      p_new[i] = o.xi;
-      if (FMT == K_SCSR_ATOMIC) red_add_f64(A.q + i, o.q);
-      pq += line_pq<FMT>(o);
-    };
-    if (k == 1) {
-      SrcFirst sf{A.r};
-      run_tiles<FMT, true, TWO, RES>(P, sm, M, sf, A.q, lineA);
-    } else {
-      SrcFold sf{A.r, p_old, beta};
-      run_tiles<FMT, true, TWO, RES>(P, sm, M, sf, A.q, lineA, RES ? nullptr : A.x);
-    }
-    p_cur = p_new;
-    mark(0);
-    pq = grid_allreduce(pq, sm, A.slots, epoch);
-    mark(1);
-    if (pq <= 0.0) {
-      status = ST_NOT_SPD;
-      fail_iter = k;
-      break;
-    }
-    alpha = rr / pq;
-    if (!isfinite(alpha)) {
-      status = ST_NF_ALPHA;
-      fail_iter = k;
-      break;
-    }
-    // pass B
-    part = 0.0;
-    if (RES) {
-#pragma unroll
-      for (int u = 0; u < kStages; ++u)
-        if (li[u] >= 0) {
-          const int i = li[u];
-          double qi = qg[u];
-          if (ATOM) {
-            qi = A.q[i];
-            A.q[i] = 0.0;
-          }
-          rg[u] = mul_add_rn(rg[u], -alpha, qi);
-          A.r[i] = rg[u];
-          part = fma(rg[u], rg[u], part);
-        }
-    } else {
-      // r -= alpha q over 16-byte pairs, two pairs in flight per thread
-      // (q, r are 256-byte-aligned workspace arrays).
-      const double2* q2 = reinterpret_cast<const double2*>(A.q);
-      double2* r2 = reinterpret_cast<double2*>(A.r);
-      double2* z2 = reinterpret_cast<double2*>(A.q);
-      const long long np = (long long)n >> 1;
-      const double na = -alpha;
-      long long pi = gtid;
-      for (; pi + gstride < np; pi += 2 * gstride) {
-        const double2 qa = q2[pi], qb = q2[pi + gstride];
-        const double2 ra = r2[pi], rb = r2[pi + gstride];
-        double2 oa, ob;
-        oa.x = mul_add_rn(ra.x, na, qa.x);
-        oa.y = mul_add_rn(ra.y, na, qa.y);
-        ob.x = mul_add_rn(rb.x, na, qb.x);
-        ob.y = mul_add_rn(rb.y, na, qb.y);
-        r2[pi] = oa;
-        r2[pi + gstride] = ob;
-        if (ATOM) {
-          z2[pi] = make_double2(0.0, 0.0);
-          z2[pi + gstride] = make_double2(0.0, 0.0);
-        }
-        part = fma(oa.x, oa.x, part);
-        part = fma(oa.y, oa.y, part);
-        part = fma(ob.x, ob.x, part);
-        part = fma(ob.y, ob.y, part);
-      }
-      if (pi < np) {
-        const double2 qa = q2[pi], ra = r2[pi];
-        double2 oa;
-        oa.x = mul_add_rn(ra.x, na, qa.x);
-        oa.y = mul_add_rn(ra.y, na, qa.y);
-        r2[pi] = oa;
-        if (ATOM) z2[pi] = make_double2(0.0, 0.0);
-        part = fma(oa.x, oa.x, part);
-        part = fma(oa.y, oa.y, part);
-      }
-      if ((n & 1) && gtid == 0) {
-        const long long i = n - 1;
-        const double qi = A.q[i];
-        if (ATOM) A.q[i] = 0.0;
-        const double ri = mul_add_rn(A.r[i], na, qi);
-        A.r[i] = ri;
-        part = fma(ri, ri, part);
-      }
-    }
-    mark(2);
-    const double rr_new = grid_allreduce(part, sm, A.slots, epoch);
-    mark(3);
-    rel = sqrt(rr_new) / b_norm;
-    if (!isfinite(rel)) {
-      status = ST_NF_RES;
-      fail_iter = k;
-      break;
-    }
-    if (A.record_history && leader) A.hist[k - 1] = rel;
-    iterations = k;
-    if (sqrt(rr_new) <= tol_b) {
-      converged = 1;
-      rr = rr_new;
-      break;
-    }
-    beta = rr_new / rr;
-    if (!isfinite(beta)) {
-      status = ST_NF_BETA;
-      fail_iter = k;
-      break;
-    }
-    rr = rr_new;
-    double* t = p_old;
-    p_old = p_new;
-    p_new = t;
-  }
-
-#if SPCG_TRACE
-  if (A.trace && threadIdx.x == 0) {
-#pragma unroll
-    for (int ph = 0; ph < 4; ++ph) A.trace[blockIdx.x * 5 + ph] = tr[ph];
-    A.trace[blockIdx.x * 5 + 4] = P.wait_ns;
-  }
-#endif
-  if (status != ST_OK) {
-    if (leader) {
-      A.res->iterations = iterations;
-      A.res->fail_iter = fail_iter;
-      A.res->converged = 0;
-      A.res->status = status;
-      A.res->final_rel = rel;
-      A.res->b_norm = b_norm;
-    }
-    pipe_drain(P, sm);
-    return;
-  }
-
-  // ---- deferred x += alpha_K p_K, then the true residual (solver.py:159-162) --
-  if (RES) {
-#pragma unroll
-    for (int u = 0; u < kStages; ++u)
-      if (li[u] >= 0) {
-        if (iterations > 0) xr[u] = mul_add_rn(xr[u], alpha, pg[u]);
-        A.x[li[u]] = xr[u];
-      }
-  } else if (iterations > 0) {
-    for (long long i = gtid; i < n; i += gstride) A.x[i] = mul_add_rn(A.x[i], alpha, p_cur[i]);
-  }
-  if (A.recompute) {
-    grid_allreduce(0.0, sm, A.slots, epoch);
-    SrcPlain sx{A.x};
-    part = 0.0;
-    if (RES) {
-      run_tiles<FMT, false, TWO, RES>(P, sm, M, sx, A.q, [&](int j, int i, const LineOut& o) {
-        if (FMT == K_SCSR_ATOMIC) red_add_f64(A.q + i, o.q);
-        else if (!ATOM) qg[j] = o.q;
-      });
-      if (ATOM) grid_allreduce(0.0, sm, A.slots, epoch);
-#pragma unroll
-      for (int u = 0; u < kStages; ++u)
-        if (li[u] >= 0) {
-          const double qi = ATOM ? A.q[li[u]] : qg[u];
-          const double tr = mul_add_rn(bg[u], -1.0, qi);
-          part = fma(tr, tr, part);
-        }
-    } else {
-      run_tiles<FMT, false, TWO, RES>(P, sm, M, sx, A.q, [&](int, int i, const LineOut& o) {
-        finish_plain<FMT>(o, i, A.q);
-      });
-      grid_allreduce(0.0, sm, A.slots, epoch);
-      for (long long i = gtid; i < n; i += gstride) {
-        const double tr = mul_add_rn(A.b[i], -1.0, A.q[i]);
-        part = fma(tr, tr, part);
-      }
-    }
-    rel = sqrt(grid_allreduce(part, sm, A.slots, epoch)) / b_norm;
-  }
-  if (leader) {
-    A.res->iterations = iterations;
-    A.res->fail_iter = 0;
-    A.res->converged = converged;
-    A.res->status = ST_OK;
-    A.res->final_rel = rel;
-    A.res->b_norm = b_norm;
-  }
-  pipe_drain(P, sm);
 }
 
 }  // namespace spcg

@@ -91,6 +91,7 @@ struct ClusArgs {
   double* ghalo;              // K > 1: [2][G][hcap] halo w between clusters
   unsigned long long* gslots; // K > 1: [2][K][4] epoch-tagged cluster partials (zeroed)
   int cluster_size;           // the plan's cluster size (checked against the launch)
+  double* coef;               // nullable (engine 6): (alpha, beta) of every update
 };
 
 constexpr int kClusSendCache = 8;  // send descriptors staged in shared memory

@@ -515,6 +515,12 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       beta = 0.0;
     }
     gam = g_new;
+    // the CG coefficients of this step (Lanczos tridiagonal -> the host's
+    // condition estimate of the auto-mode guard)
+    if (leader && A.coef) {
+      A.coef[2 * it] = alpha;
+      A.coef[2 * it + 1] = beta;
+    }
     const double na = -alpha;
 #pragma unroll
     for (int k = 0; k < NS; ++k)
@@ -558,6 +564,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
 #pragma unroll
   for (int k = 0; k < NS; ++k)
     if (rrow[k] >= 0) A.x[rrow[k]] = xr[k];
+  const double rec_rel = rel;
   if (A.recompute) {  // true residual ||b - A x|| / ||b||
     part = 0.0;
     dummy = 0.0;
@@ -583,6 +590,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     A.res->status = ST_OK;
     A.res->final_rel = rel;
     A.res->b_norm = b_norm;
+    A.res->rec_rel = rec_rel;
   }
 }
 

@@ -391,8 +391,63 @@ int launch_clus(const ClusPlan& P, const ClusArgs& a, cudaStream_t st, bool pipe
   return SPCG_OK;
 }
 
+// Extreme eigenvalues of CG's Lanczos tridiagonal T_k from the step
+// coefficients (alpha_j, beta_j), beta_0 = 0:
+//   T_jj = 1/alpha_j + beta_j/alpha_{j-1},  T_{j-1,j} = sqrt(beta_j)/alpha_{j-1}
+// by Sturm-sequence bisection; returns theta_max / theta_min (the Ritz
+// estimate of cond(A): the extreme Ritz values converge first) or 0.
+double lanczos_cond(const std::vector<double>& ab, long long k) {
+  if (k < 2) return 0.0;
+  std::vector<double> d((size_t)k), e2((size_t)k, 0.0);
+  double lo = 1e300, hi = -1e300;
+  for (long long j = 0; j < k; ++j) {
+    const double a = ab[2 * j], bb = j ? ab[2 * j + 1] : 0.0, ap = j ? ab[2 * (j - 1)] : 1.0;
+    if (!(a > 0.0) || !(bb >= 0.0)) return 0.0;
+    d[j] = 1.0 / a + (j ? bb / ap : 0.0);
+    e2[j] = j ? bb / (ap * ap) : 0.0;
+  }
+  for (long long j = 0; j < k; ++j) {  // Gershgorin interval of T
+    const double r = (j ? std::sqrt(e2[j]) : 0.0) + (j + 1 < k ? std::sqrt(e2[j + 1]) : 0.0);
+    lo = std::min(lo, d[j] - r);
+    hi = std::max(hi, d[j] + r);
+  }
+  auto below = [&](double x) {  // eigenvalues of T smaller than x
+    int c = 0;
+    double q = 1.0;
+    for (long long j = 0; j < k; ++j) {
+      q = d[j] - x - (j ? e2[j] / q : 0.0);
+      if (q == 0.0) q = -1e-300;
+      if (q < 0.0) ++c;
+    }
+    return c;
+  };
+  auto kth = [&](int idx) {  // idx-th smallest eigenvalue (0-based)
+    double a = lo, z = hi;
+    for (int it = 0; it < 200 && z - a > 1e-15 * std::max(std::fabs(a), std::fabs(z)); ++it) {
+      const double mid = 0.5 * (a + z);
+      if (below(mid) > idx) z = mid;
+      else a = mid;
+    }
+    return 0.5 * (a + z);
+  };
+  const double tmin = kth(0), tmax = kth((int)k - 1);
+  return tmin > 0.0 ? tmax / tmin : 0.0;
+}
+
+// Auto-mode guard of the pipelined engine: Ghysels-Vanroose CG follows the
+// reference's iterates to fp64 reassociation only while the system is
+// reasonably conditioned; measured on the F-mesh family and 2-D Poisson
+// (tests/test_gpu_conditioning.py, profiles/r02/cond_sweep.jsonl):
+// ||x6 - x_ref|| / ||x_ref|| <= 3e-9 up to cond ~ 8e4, 6.5e-8 at 1.9e5,
+// 1e-6 at 1.9e6; and at tol 1e-12 the true residual ends 16x above tol.
+// Above either limit the auto mode re-solves on engine 5 (standard-order
+// single-reduction CG, within 1e-9 of the reference in the same sweep).
+constexpr double kPipeCondMax = 1.0e5;
+constexpr double kPipeTrueResMax = 2.0;  // true rel residual / tol
+
 int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double* hist,
-               const spcg_cg_options* o, spcg_cg_result* out, cudaStream_t st, bool pipe = false) {
+               const spcg_cg_options* o, spcg_cg_result* out, cudaStream_t st, bool pipe = false,
+               bool guard = false) {
   int rc;
   const ClusPlan& P = m->cp;
   if ((rc = ensure_ws(m, 1))) return rc;
@@ -400,6 +455,13 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
   const long long max_iter = o->max_iter > 0 ? o->max_iter : std::max(1, m->n);
   if (o->record_history && hist == nullptr)
     return fail(SPCG_ERR_ARG, "record_history needs a history buffer");
+  guard = guard && pipe;
+  if (guard && w.coef_cap < max_iter) {
+    if (w.coef) cudaFree(w.coef);
+    w.coef = nullptr;
+    if ((rc = dmalloc((void**)&w.coef, sizeof(double) * 2 * (size_t)max_iter, nullptr))) return rc;
+    w.coef_cap = max_iter;
+  }
   ClusArgs a{};
   a.ctas = P.ctas;
   a.slices = P.slices;
@@ -416,7 +478,9 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
   a.tol = o->tol;
   a.max_iter = max_iter;
   a.record_history = o->record_history;
-  a.recompute = o->recompute_final_residual;
+  // the guard judges the TRUE residual, computed even when not requested
+  a.recompute = o->recompute_final_residual || guard;
+  a.coef = guard ? w.coef : nullptr;
   a.off_rwin = P.off_rwin;
   a.off_shalo = P.off_shalo;
   a.off_whalo = P.off_whalo;
@@ -482,16 +546,36 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
       fprintf(stderr, "\n");
     }
   }
+  double cond = 0.0;
+  if (guard && r.status == SPCG_OK && r.iterations >= 2) {
+    std::vector<double> ab(2 * (size_t)r.iterations);
+    CUDA_TRY(cudaMemcpy(ab.data(), w.coef, sizeof(double) * ab.size(), cudaMemcpyDeviceToHost));
+    cond = lanczos_cond(ab, r.iterations);
+    if (cond > kPipeCondMax || r.final_rel > kPipeTrueResMax * o->tol) {
+      // re-solve on engine 5; the reported time covers both solves
+      rc = do_clus_cg(m, b, x0, x, hist, o, out, st, false, false);
+      out->device_ms += ms;
+      out->kernel_launches += 1;
+      out->fallbacks = 1;
+      out->cond_estimate = cond;
+      return rc;
+    }
+  }
   out->iterations = r.iterations;
   out->converged = r.converged;
   out->status = r.status;
   out->fail_iteration = r.fail_iter;
-  out->final_relative_residual = r.final_rel;
+  out->final_relative_residual =
+      (pipe && !o->recompute_final_residual && r.status == SPCG_OK) ? r.rec_rel : r.final_rel;
   out->b_norm = r.b_norm;
   out->device_ms = ms;
   out->kernel_launches = 1;
   out->spmv_ms = 0.0;
   out->spmv_launches = 0;
+  out->engine_used = pipe ? 6 : 5;
+  out->fallbacks = 0;
+  out->cond_estimate = cond;
+  out->phase_ms[0] = out->phase_ms[1] = out->phase_ms[2] = 0.0;
   if (r.status != SPCG_OK) {
     const char* what = r.status == SPCG_ERR_NOT_SPD ? "matrix not positive definite"
                        : r.status == SPCG_ERR_NONFINITE_ALPHA ? "non-finite alpha"

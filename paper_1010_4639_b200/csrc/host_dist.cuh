@@ -338,11 +338,12 @@ int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const dou
   // the one chunk enqueued past convergence costs only empty launches.
   const int chunk = 16;
   const bool timing = o->timing != 0;
+  const bool split = o->timing >= 2;  // events around passes B and C too
   if (timing && !d.tev[0][0][0])
     for (int bb = 0; bb < 2; ++bb)
-      for (int a = 0; a < 2; ++a)
+      for (int a = 0; a < 6; ++a)
         for (int c = 0; c < chunk; ++c) CUDA_TRY(cudaEventCreate(&d.tev[bb][a][c]));
-  double spmv_ms = 0.0;
+  double spmv_ms = 0.0, axpy_ms = 0.0;
   long long spmv_n = 0, k_before = 0, iter_enq = 0;
 #ifndef SPCG_ALTERNATE
 #define SPCG_ALTERNATE 1
@@ -366,11 +367,15 @@ int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const dou
       if ((rc2 = allreduce_red(H, d.S, st))) return rc2;
       if (kRev && (rc2 = reverse_halo(H, d, d.q, nhalo, st, &launches))) return rc2;
       dist_scalar<<<1, 1, 0, st>>>(2, d.S, hist);
+      if (split) CUDA_TRY(cudaEventRecord(d.tev[bb][2][c], st));
       dist_elem<<<GE, kElemBlock, 0, st>>>(2, nloc, d.S, nullptr, d.q, r, nullptr, d.part, kAtom,
                                        kAlternate ? 1 - dirA : 0);
+      if (split) CUDA_TRY(cudaEventRecord(d.tev[bb][3][c], st));
       if ((rc2 = allreduce_red(H, d.S, st))) return rc2;
       dist_scalar<<<1, 1, 0, st>>>(3, d.S, hist);
+      if (split) CUDA_TRY(cudaEventRecord(d.tev[bb][4][c], st));
       dist_update<<<GE, kElemBlock, 0, st>>>(nloc, d.S, r, p, x, xv, dirA);
+      if (split) CUDA_TRY(cudaEventRecord(d.tev[bb][5][c], st));
       ++iter_enq;
       launches += 5;
       if ((rc2 = halo_exchange(H, d, p, p, st, &launches))) return rc2;
@@ -396,6 +401,12 @@ int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const dou
         CUDA_TRY(cudaEventElapsedTime(&t, d.tev[bb][0][c], d.tev[bb][1][c]));
         spmv_ms += t;
         ++spmv_n;
+        if (split) {
+          float tb = 0.f, tc = 0.f;
+          CUDA_TRY(cudaEventElapsedTime(&tb, d.tev[bb][2][c], d.tev[bb][3][c]));
+          CUDA_TRY(cudaEventElapsedTime(&tc, d.tev[bb][4][c], d.tev[bb][5][c]));
+          axpy_ms += (double)tb + (double)tc;
+        }
       }
       k_before = hs.k;
     }
@@ -437,6 +448,15 @@ int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const dou
   out->kernel_launches = launches;
   out->spmv_ms = spmv_ms;
   out->spmv_launches = spmv_n;
+  out->engine_used = 2;
+  out->fallbacks = 0;
+  out->cond_estimate = 0.0;
+  // split: SpMV passes (with the fused p.q partial); the vector-update passes
+  // B and C (with the fused r.r partial); the rest (reductions' completion,
+  // scalar steps, collectives, halo, prologue/epilogue) under "dot"
+  out->phase_ms[0] = split ? spmv_ms : 0.0;
+  out->phase_ms[2] = split ? axpy_ms : 0.0;
+  out->phase_ms[1] = split ? std::max(0.0, (double)ms - spmv_ms - axpy_ms) : 0.0;
   if (S.status != 0) {
     const char* what = S.status == SPCG_ERR_NOT_SPD ? "matrix not positive definite"
                        : S.status == SPCG_ERR_NONFINITE_ALPHA ? "non-finite alpha"
@@ -484,7 +504,10 @@ int do_dist_cg(spcg_matrix_s* m, spcg_comm_s* comm, int npeers, const int32_t* p
     CUDA_TRY(cudaMemcpyAsync(m->dw.send_idx, send_idx, sizeof(int) * (size_t)send_total,
                              cudaMemcpyHostToDevice, st));
   }
-  if (m->n == 0 && npeers == 0) {
+  // an empty shard with no peers may return at once only when it is alone:
+  // with other ranks it must still join every collective of the solve
+  const bool alone = !comm || comm->nranks <= 1;
+  if (m->n == 0 && npeers == 0 && alone) {
     out->iterations = 0;
     out->converged = 1;
     out->status = 0;

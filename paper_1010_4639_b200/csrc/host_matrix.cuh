@@ -231,7 +231,7 @@ void free_matrix(spcg_matrix_s* m) {
   F(m->t1.desc); F(m->t1.descB); F(m->t1w.desc); F(m->t2.desc); F(m->t2.descB); F(m->t1.win); F(m->t2.win);
   Workspace& w = m->ws;
   F(w.r); F(w.p0); F(w.p1); F(w.q); F(w.part); F(w.slots); F(w.res);
-  F(w.b); F(w.x); F(w.x0); F(w.hist); F(w.cg1); F(w.rp);
+  F(w.b); F(w.x); F(w.x0); F(w.hist); F(w.cg1); F(w.coef);
   if (w.h_res) cudaFreeHost(w.h_res);
   if (w.ev0) cudaEventDestroy(w.ev0);
   if (w.ev1) cudaEventDestroy(w.ev1);
@@ -246,7 +246,7 @@ void free_matrix(spcg_matrix_s* m) {
   for (int bb = 0; bb < 2; ++bb) {
     if (d.h_Sc[bb]) cudaFreeHost(d.h_Sc[bb]);
     if (d.cev[bb]) cudaEventDestroy(d.cev[bb]);
-    for (int a = 0; a < 2; ++a)
+    for (int a = 0; a < 6; ++a)
       for (int c = 0; c < 16; ++c)
         if (d.tev[bb][a][c]) cudaEventDestroy(d.tev[bb][a][c]);
   }
@@ -311,32 +311,6 @@ int ensure_ws(spcg_matrix_s* m, int grid) {
       return rc;
     w.slots_g = grid;
   }
-  return SPCG_OK;
-}
-
-template <int FMT>
-int launch_cg(const CgArgs& a, bool res, int grid, cudaStream_t st, double2* rp, int n,
-              bool three = false) {
-  if (!res && three) {
-    void* args[] = {(void*)&a};
-    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)cg3_kernel<FMT>, dim3(grid), dim3(kBlock),
-                                         args, sizeof(Smem), st));
-    return SPCG_OK;
-  }
-  if (res || rp == nullptr) {
-    void* args[] = {(void*)&a};
-    const void* fn = res ? (const void*)cg_kernel<FMT, true> : (const void*)cg_kernel<FMT, false>;
-    CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBlock), args,
-                                         res ? kSmemRes : sizeof(Smem), st));
-    return SPCG_OK;
-  }
-  CgsArgs g{};
-  g.base = a;
-  g.RP[0] = rp;
-  g.RP[1] = rp + std::max(1, n);
-  void* args[] = {(void*)&g};
-  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)cgs_kernel<FMT>, dim3(grid), dim3(kBlock), args,
-                                       sizeof(Smem), st));
   return SPCG_OK;
 }
 

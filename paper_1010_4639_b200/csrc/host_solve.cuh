@@ -17,11 +17,13 @@ int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double
   }
   const int kf = kfmt_of(m, o->accumulation);
   if (kf == K_SCSR_PRIV && !m->hasB) return fail(SPCG_ERR_UNSUPPORTED, "no L^T for privatized mode");
+  if (o->engine != 0 && o->engine != 2 && o->engine != 3 && o->engine != 5 && o->engine != 6)
+    return fail(SPCG_ERR_ARG, "engine must be 0 (auto), 2, 3, 5 or 6");
   const MatView v = view(m, kf == K_SCSR_PRIV);
   const bool fits = v.ntiles <= d->coop_res * kStages;
   // engine 2, and auto for systems that stream from HBM: per-pass kernels
   // (the sharded engine with no peers) — each pass keeps the whole register
-  // budget, which the persistent kernel cannot (P3: 0.99 vs 0.82 of roofline)
+  // budget, which a persistent kernel cannot (P3: 0.99 vs 0.82 of roofline)
   if (o->engine == 2 || (o->engine == 0 && !fits))
     return do_dist_cg(m, nullptr, 0, nullptr, nullptr, nullptr, nullptr, b, x0, x, hist, o, out, st);
   // engine 5, and auto for banded systems whose rows fit the co-resident
@@ -46,16 +48,19 @@ int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double
     // Two-segment SCSR rows stay on engine 5: engine 6 ran them at 4.7 us on
     // one box but 7-11 us on another (profiles/r01/s4/pipe_two.log), engine 5
     // at a steady 6.25
-    if (m->cp.ok && (o->engine == 5 || resident))
-      return do_clus_cg(m, b, x0, x, hist, o, out, st,
-                        o->engine == 0 && !m->cp.two && m->cp.max_slices <= kPipeMaxSlices);
+    if (m->cp.ok && (o->engine == 5 || resident)) {
+      const bool pipe = o->engine == 0 && !m->cp.two && m->cp.max_slices <= kPipeMaxSlices;
+      return do_clus_cg(m, b, x0, x, hist, o, out, st, pipe, /*guard=*/pipe);
+    }
     if (o->engine == 5)
       return fail(SPCG_ERR_UNSUPPORTED, "cluster engine not applicable: " + m->cp.why);
   }
-  const bool res = fits;
-  // resident: the balanced tiles map one-to-one onto CTAs where possible
-  const int grid = res ? std::max(1, std::min(d->coop_res, std::max(1, v.ntiles)))
-                       : d->coop_stream;
+  // engine 3 (and auto on the remaining resident systems): the grid-resident
+  // single-reduction CG, one grid all-reduce per iteration
+  if (!fits)
+    return fail(SPCG_ERR_UNSUPPORTED, "engine 3 needs a system resident in shared memory");
+  // the balanced tiles map one-to-one onto CTAs where possible
+  const int grid = std::max(1, std::min(d->coop_res, std::max(1, v.ntiles)));
   if ((rc = ensure_ws(m, grid))) return rc;
   Workspace& w = m->ws;
   const long long max_iter = o->max_iter > 0 ? o->max_iter : std::max(1, m->n);
@@ -87,45 +92,21 @@ int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double
   a.max_iter = max_iter;
   a.record_history = o->record_history;
   a.recompute = o->recompute_final_residual;
-  // engine 3 (or auto on resident systems): single-reduction CG, one grid
-  // barrier per iteration; engine 1 forces the two-reduction form
-  const bool single = res && (o->engine == 3 || o->engine == 0);
   Cg1Args g{};
-  if (single) {
-    const size_t vb = sizeof(double) * (size_t)std::max(1, m->n);
-    if (!w.cg1 && (rc = dmalloc((void**)&w.cg1, 7 * vb, nullptr))) return rc;
-    CUDA_TRY(cudaMemsetAsync(w.cg1, 0, 7 * vb, st));
-    g.base = a;
-    for (int k = 0; k < 2; ++k) g.R[k] = w.cg1 + (size_t)k * std::max(1, m->n);
-    for (int k = 0; k < 2; ++k) g.S[k] = w.cg1 + (size_t)(2 + k) * std::max(1, m->n);
-    for (int k = 0; k < 3; ++k) g.W[k] = w.cg1 + (size_t)(4 + k) * std::max(1, m->n);
-  }
+  const size_t vb = sizeof(double) * (size_t)std::max(1, m->n);
+  if (!w.cg1 && (rc = dmalloc((void**)&w.cg1, 7 * vb, nullptr))) return rc;
+  CUDA_TRY(cudaMemsetAsync(w.cg1, 0, 7 * vb, st));
+  g.base = a;
+  for (int k = 0; k < 2; ++k) g.R[k] = w.cg1 + (size_t)k * std::max(1, m->n);
+  for (int k = 0; k < 2; ++k) g.S[k] = w.cg1 + (size_t)(2 + k) * std::max(1, m->n);
+  for (int k = 0; k < 3; ++k) g.W[k] = w.cg1 + (size_t)(4 + k) * std::max(1, m->n);
+  const bool res = true;
   CUDA_TRY(cudaEventRecord(w.ev0, st));
-  if (single) {
-    switch (kf) {
-      case K_CSR: rc = launch_cg1<K_CSR>(g, grid, st); break;
-      case K_SCSR_ATOMIC: rc = launch_cg1<K_SCSR_ATOMIC>(g, grid, st); break;
-      case K_SCSR_PRIV: rc = launch_cg1<K_SCSR_PRIV>(g, grid, st); break;
-      default: rc = launch_cg1<K_CSC>(g, grid, st); break;
-    }
-  } else {
-    // streaming systems: interleaved (r, p) pairs pay off for the gather-only
-    // formats with long rows (27-point class: 20% on full CSR); short rows
-    // (5/7-point) and the atomic scatters keep separate r and p arrays
-    const double per_line = (double)(m->nnz + (kf == K_SCSR_PRIV ? m->B.nnz : 0)) /
-                            std::max(1, m->n);
-    const bool three = !res && o->engine == 4;  // persistent three-pass (unfolded) CG
-    const bool pairs = !res && !three && (kf == K_CSR || kf == K_SCSR_PRIV) && per_line > 8.0;
-    if (pairs && !w.rp &&
-        (rc = dmalloc((void**)&w.rp, sizeof(double2) * 2 * (size_t)std::max(1, m->n), nullptr)))
-      return rc;
-    double2* rp = pairs ? w.rp : nullptr;
-    switch (kf) {
-      case K_CSR: rc = launch_cg<K_CSR>(a, res, grid, st, rp, m->n, three); break;
-      case K_SCSR_ATOMIC: rc = launch_cg<K_SCSR_ATOMIC>(a, res, grid, st, rp, m->n, three); break;
-      case K_SCSR_PRIV: rc = launch_cg<K_SCSR_PRIV>(a, res, grid, st, rp, m->n, three); break;
-      default: rc = launch_cg<K_CSC>(a, res, grid, st, rp, m->n, three); break;
-    }
+  switch (kf) {
+    case K_CSR: rc = launch_cg1<K_CSR>(g, grid, st); break;
+    case K_SCSR_ATOMIC: rc = launch_cg1<K_SCSR_ATOMIC>(g, grid, st); break;
+    case K_SCSR_PRIV: rc = launch_cg1<K_SCSR_PRIV>(g, grid, st); break;
+    default: rc = launch_cg1<K_CSC>(g, grid, st); break;
   }
   if (rc) return rc;
   CUDA_TRY(cudaEventRecord(w.ev1, st));
@@ -163,6 +144,10 @@ int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double
   out->kernel_launches = 1;
   out->spmv_ms = 0.0;
   out->spmv_launches = 0;
+  out->engine_used = 3;
+  out->fallbacks = 0;
+  out->cond_estimate = 0.0;
+  out->phase_ms[0] = out->phase_ms[1] = out->phase_ms[2] = 0.0;
   if (r.status != SPCG_OK) {
     const char* what = r.status == SPCG_ERR_NOT_SPD ? "matrix not positive definite"
                        : r.status == SPCG_ERR_NONFINITE_ALPHA ? "non-finite alpha"

@@ -18,8 +18,6 @@
 #include "../../include/spcg_b200.h"
 #include "cg.cuh"
 #include "cg1.cuh"
-#include "cgs.cuh"
-#include "cg3.cuh"
 #include "clus.cuh"
 #include "clus_pipe.cuh"
 #include "dist.cuh"
@@ -36,6 +34,17 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
+// A handle's arrays live on the device that was current at its creation;
+// using it from another device would hand foreign pointers to the kernels.
+int on_device(int device) {
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess) return fail(SPCG_ERR_CUDA, "cudaGetDevice failed");
+  if (cur != device)
+    return fail(SPCG_ERR_ARG, "matrix handle lives on device " + std::to_string(device) +
+                                  " but the current device is " + std::to_string(cur));
+  return SPCG_OK;
+}
+
 #define CUDA_TRY(expr)                                                                  \
   do {                                                                                  \
     cudaError_t _e = (expr);                                                            \
@@ -48,7 +57,6 @@ struct DevInfo {
   int sms = 0;
   int major = 0, minor = 0;
   int coop_res = 0;     // co-resident CTAs of the resident CG kernel
-  int coop_stream = 0;  // co-resident CTAs of the streaming CG kernel
   int spmv_grid = 0;
 };
 
@@ -79,47 +87,20 @@ int dev_info(DevInfo** out) {
     d.sms = prop.multiProcessorCount;
     d.major = prop.major;
     d.minor = prop.minor;
-    int br = 0, bs = 0, bp = 0, t = 0;
+    int br = 0, bp = 0, t = 0;
     int rc;
-    if ((rc = occupancy(cg_kernel<K_CSR, true>, &br, kSmemRes))) return rc;
-    if ((rc = occupancy(cg_kernel<K_CSR, false>, &bs))) return rc;
-    // every instantiation shares the same block/smem shape; check the rest
-    if ((rc = occupancy(cg_kernel<K_SCSR_ATOMIC, true>, &t, kSmemRes))) return rc;
-    br = std::min(br, t);
-    if ((rc = occupancy(cg_kernel<K_SCSR_PRIV, true>, &t, kSmemRes))) return rc;
-    br = std::min(br, t);
-    if ((rc = occupancy(cg_kernel<K_CSC, true>, &t, kSmemRes))) return rc;
-    br = std::min(br, t);
-    if ((rc = occupancy(cg1_kernel<K_CSR>, &t, kSmemRes))) return rc;
-    br = std::min(br, t);
+    // engine 3's resident kernel: every instantiation shares one shape
+    if ((rc = occupancy(cg1_kernel<K_CSR>, &br, kSmemRes))) return rc;
     if ((rc = occupancy(cg1_kernel<K_SCSR_ATOMIC>, &t, kSmemRes))) return rc;
     br = std::min(br, t);
     if ((rc = occupancy(cg1_kernel<K_SCSR_PRIV>, &t, kSmemRes))) return rc;
     br = std::min(br, t);
     if ((rc = occupancy(cg1_kernel<K_CSC>, &t, kSmemRes))) return rc;
     br = std::min(br, t);
-    if ((rc = occupancy(cg_kernel<K_SCSR_ATOMIC, false>, &t))) return rc;
-    bs = std::min(bs, t);
-    if ((rc = occupancy(cg_kernel<K_SCSR_PRIV, false>, &t))) return rc;
-    bs = std::min(bs, t);
-    if ((rc = occupancy(cg_kernel<K_CSC, false>, &t))) return rc;
-    bs = std::min(bs, t);
     if ((rc = occupancy(spmv_kernel<K_CSR>, &bp))) return rc;
     if ((rc = occupancy(spmv_kernel<K_SCSR_ATOMIC>, &t))) return rc;
     if ((rc = occupancy(spmv_kernel<K_SCSR_PRIV>, &t))) return rc;
     if ((rc = occupancy(spmv_kernel<K_CSC>, &t))) return rc;
-    if ((rc = occupancy(cg3_kernel<K_CSR>, &t))) return rc;
-    bs = std::min(bs, t);
-    if ((rc = occupancy(cg3_kernel<K_SCSR_ATOMIC>, &t))) return rc;
-    bs = std::min(bs, t);
-    if ((rc = occupancy(cg3_kernel<K_SCSR_PRIV>, &t))) return rc;
-    bs = std::min(bs, t);
-    if ((rc = occupancy(cg3_kernel<K_CSC>, &t))) return rc;
-    bs = std::min(bs, t);
-    if ((rc = occupancy(cgs_kernel<K_CSR>, &t))) return rc;
-    bs = std::min(bs, t);
-    if ((rc = occupancy(cgs_kernel<K_SCSR_PRIV>, &t))) return rc;
-    bs = std::min(bs, t);
     // (these calls also raise each kernel's dynamic shared-memory limit)
     if ((rc = occupancy(dist_spmv_pq<K_CSR>, &t))) return rc;
     if ((rc = occupancy(dist_spmv_pq<K_CSR, true>, &t))) return rc;
@@ -132,9 +113,8 @@ int dev_info(DevInfo** out) {
     if ((rc = occupancy(dist_spmv<K_CSC>, &t))) return rc;
     if ((rc = occupancy(dist_spmv<K_CSR>, &t))) return rc;
     if ((rc = occupancy(dist_spmv<K_SCSR_PRIV>, &t))) return rc;
-    if (br < 1 || bs < 1 || bp < 1) return fail(SPCG_ERR_CUDA, "CG kernel does not fit on an SM");
+    if (br < 1 || bp < 1) return fail(SPCG_ERR_CUDA, "CG kernel does not fit on an SM");
     d.coop_res = std::min(br * d.sms, 32 * kPollWarps * kPollPer);
-    d.coop_stream = std::min(bs * d.sms, 32 * kPollWarps * kPollPer);
     d.spmv_grid = bp * d.sms;
     d.device = dev;
   }
@@ -168,13 +148,14 @@ struct Workspace {
   CgDevResult* res = nullptr;
   CgDevResult* h_res = nullptr;  // pinned
   double* cg1 = nullptr;         // single-reduction engine: R[2], S[2], W[3]
-  double2* rp = nullptr;         // streaming engine: RP[2] interleaved (r, p) pairs
   // host-API staging
   double* b = nullptr;
   double* x = nullptr;
   double* x0 = nullptr;
   double* hist = nullptr;
   long long hist_cap = 0;
+  double* coef = nullptr;  // engine-6 guard: (alpha, beta) per update
+  long long coef_cap = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
 
@@ -195,7 +176,9 @@ struct DistWorkspace {
   int* send_idx = nullptr;
   long long send_idx_cap = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  cudaEvent_t tev[2][2][16] = {};  // [chunk buffer][start/end][iteration]: SpMV-pass timing
+  // [chunk buffer][A0 A1 B0 B1 C0 C1][iteration]: per-pass timing (opts.timing:
+  // 1 = pass A only, 2 = all three passes for the spmv/dot/axpy split)
+  cudaEvent_t tev[2][6][16] = {};
 };
 
 }  // namespace
@@ -376,6 +359,7 @@ int spcg_matrix_download(spcg_matrix_t m, int64_t* h_ptr, int64_t* h_idx, double
 
 int spcg_spmv(spcg_matrix_t m, const double* d_x, double* d_y, int accumulation, void* stream) {
   if (!m || (m->n > 0 && (!d_x || !d_y))) return fail(SPCG_ERR_ARG, "null argument");
+  if (int rc = on_device(m->device)) return rc;
   return do_spmv(m, d_x, d_y, accumulation, (cudaStream_t)stream);
 }
 
@@ -389,19 +373,16 @@ int spcg_dot(int64_t n, const double* d_u, const double* d_v, double* d_out, voi
     CUDA_TRY(cudaMemsetAsync(d_out, 0, sizeof(double), st));
     return SPCG_OK;
   }
-  static thread_local double* part = nullptr;
-  static thread_local int part_dev = -1;
-  int dev = 0;
-  CUDA_TRY(cudaGetDevice(&dev));
-  if (part == nullptr || part_dev != dev) {
-    CUDA_TRY(cudaMalloc((void**)&part, sizeof(double) * 4096));
-    part_dev = dev;
-  }
+  // per-call partials, stream-ordered (dots in flight on several streams,
+  // or on several devices, never share a buffer)
   const int nb = (int)std::min<long long>(2LL * d->sms, (n + kBlock - 1) / kBlock);
+  double* part = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&part, sizeof(double) * (size_t)nb, st));
   dot_partial_kernel<<<nb, kBlock, 0, st>>>(n, d_u, d_v, part);
   CUDA_TRY(cudaGetLastError());
   dot_final_kernel<<<1, kBlock, 0, st>>>(nb, part, d_out);
   CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaFreeAsync(part, st));
   return SPCG_OK;
 }
 
@@ -429,6 +410,7 @@ int spcg_cg_solve(spcg_matrix_t m, const double* d_b, const double* d_x0, double
                   void* stream) {
   if (!m || !opts || !result) return fail(SPCG_ERR_ARG, "null argument");
   if (m->n > 0 && (!d_b || !d_x)) return fail(SPCG_ERR_ARG, "null vector");
+  if (int rc = on_device(m->device)) return rc;
   std::lock_guard<std::mutex> lk(m->mu);
   return do_cg(m, d_b, d_x0, d_x, d_hist, opts, result, (cudaStream_t)stream);
 }
@@ -438,6 +420,7 @@ int spcg_cg_solve_host(spcg_matrix_t m, const double* h_b, const double* h_x0, d
                        void* stream) {
   if (!m || !opts || !result) return fail(SPCG_ERR_ARG, "null argument");
   if (m->n > 0 && (!h_b || !h_x)) return fail(SPCG_ERR_ARG, "null vector");
+  if (int rc = on_device(m->device)) return rc;
   std::lock_guard<std::mutex> lk(m->mu);
   cudaStream_t st = (cudaStream_t)stream;
   Workspace& w = m->ws;
@@ -489,7 +472,10 @@ int spcg_comm_create(int nranks, int rank, const unsigned char* id_bytes, spcg_c
   spcg_comm_s* c = new spcg_comm_s();
   c->nranks = nranks;
   c->rank = rank;
-  if (nranks > 1) {
+  // nranks == 1 with a NULL id: no NCCL (collectives are no-ops); with an id
+  // a real one-rank NCCL communicator, so the NCCL calls and their stream
+  // ordering execute even on one GPU
+  if (nranks > 1 || id_bytes) {
     NcclApi& N = nccl();
     if (!N.ok) {
       delete c;
@@ -621,6 +607,7 @@ int spcg_matrix_generate_rows(int kind, int fmt, int64_t d0, int64_t d1, int64_t
 
 int spcg_matrix_localize(spcg_matrix_t m, int64_t* nhalo) {
   if (!m) return fail(SPCG_ERR_ARG, "null matrix");
+  if (int rc = on_device(m->device)) return rc;
   std::lock_guard<std::mutex> lk(m->mu);
   int rc = localize(m);
   if (rc) return rc;
@@ -642,6 +629,7 @@ int spcg_dist_cg_solve(spcg_matrix_t local, spcg_comm_t comm, int npeers, const 
   if (!local || !opts || !result) return fail(SPCG_ERR_ARG, "null argument");
   if (npeers < 0 || (npeers > 0 && (!peers || !recv_off || !send_off)))
     return fail(SPCG_ERR_ARG, "bad halo plan");
+  if (int rc = on_device(local->device)) return rc;
   std::lock_guard<std::mutex> lk(local->mu);
   return do_dist_cg(local, comm, npeers, peers, recv_off, send_off, send_idx, d_b, d_x0, d_x,
                     d_hist, opts, result, (cudaStream_t)stream);

@@ -21,6 +21,18 @@ def _ptr(a: np.ndarray) -> int:
     return a.ctypes.data if a.size else 0
 
 
+def current_device() -> int:
+    """Index of the current CUDA device (-1 without torch CUDA)."""
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            return int(torch.cuda.current_device())
+    except Exception:  # pragma: no cover - torch is plumbing only
+        pass
+    return -1
+
+
 class DeviceMatrix:
     FORMATS = {"csr": N.FMT_CSR, "scsr": N.FMT_SCSR, "csc": N.FMT_CSC}
 

@@ -113,11 +113,18 @@ def halo_plan(halo: np.ndarray, bounds: np.ndarray, rank: int, all_gather_object
 class Comm:
     """NCCL communicator of the C library, bootstrapped over torch.distributed."""
 
-    def __init__(self, rank: int, world: int, broadcast_object=None):
+    def __init__(self, rank: int, world: int, broadcast_object=None, nccl: bool | None = None):
+        """nccl: make an NCCL communicator (default: when world > 1); at
+        world 1 `nccl=True` builds a real one-rank NCCL communicator so the
+        ncclAllReduce path runs on a single GPU."""
         self.rank, self.world = rank, world
         lib = N.load()
         h = ctypes.c_void_p()
-        if world > 1:
+        if nccl is None:
+            nccl = world > 1
+        if broadcast_object is None:
+            broadcast_object = lambda o: o  # noqa: E731 - world 1
+        if nccl:
             idbuf = (ctypes.c_ubyte * 128)()
             if rank == 0:
                 N.check(lib.spcg_comm_unique_id(idbuf), "spcg_comm_unique_id")

@@ -3,9 +3,11 @@
 `spmv_full`, `spmv_sym`, `spmv_csc`, `dot`, `axpy`, `norm2` take numpy arrays
 (results come back as numpy) or CUDA torch tensors (results stay on the
 device).  torch is used only to hold device buffers.  There is exactly one
-backend, "cuda"; `set_backend` accepts "auto"/"cuda" so code written against
-the reference's registry keeps working, and anything else raises ValueError
-like the reference does for unknown names (kernels/__init__.py:35-44).
+backend, "cuda"; `set_backend` accepts "auto"/"cuda" and the reference's
+backend names "compiled"/"python" (aliases of the one backend, also through
+SPCG_BACKEND) so code written against the reference's registry keeps working,
+and anything else raises ValueError like the reference does for unknown names
+(kernels/__init__.py:35-44).
 
 Numerical contracts:
   spmv_full   sequential row sums, IEEE mul-then-add: bitwise equal to
@@ -68,28 +70,6 @@ def _acc_code(cfg: KernelConfig | None) -> int:
     return N.ACC_ATOMIC if cfg.accumulation == "atomic" else N.ACC_PRIVATIZED
 
 
-_BACKENDS = ("cuda",)
-_active = "cuda"
-
-
-def available_backends() -> tuple[str, ...]:
-    return _BACKENDS
-
-
-def set_backend(name: str) -> str:
-    global _active
-    if name == "auto":
-        name = "cuda"
-    if name not in _BACKENDS:
-        raise ValueError(f"unknown backend {name!r}; available: {available_backends()}")
-    _active = name
-    return _active
-
-
-def get_backend() -> str:
-    return _active
-
-
 class _CudaBackend:
     """Backend module interface of the reference (_compiled.py:10-57: name,
     spmv_full, spmv_sym, dot, axpy); filled in below."""
@@ -97,13 +77,37 @@ class _CudaBackend:
     name = "cuda"
 
 
-# The reference's backend registry (kernels/__init__.py:21-50), with the one
-# backend this library has; code that looks backends up by name keeps working.
-BACKENDS = {"cuda": _CudaBackend}
+# The reference's backend registry (kernels/__init__.py:21-50).  There is ONE
+# implementation (the device kernels, no CPU fallback); the reference's names
+# "compiled" and "python" are aliases of it, so code that selects a backend
+# by name -- set_backend("compiled"), SPCG_BACKEND=python -- keeps working.
+BACKENDS = {"cuda": _CudaBackend, "compiled": _CudaBackend, "python": _CudaBackend}
 
-# SPCG_BACKEND (kernels/__init__.py:50) may name a reference backend; the
-# only implementation here is the device one.
-set_backend("auto")
+
+def available_backends() -> tuple[str, ...]:
+    """Distinct implementations (the aliases above resolve to "cuda")."""
+    return ("cuda",)
+
+
+def set_backend(name: str):
+    """Select a backend by name and return it (kernels/__init__.py:35-41);
+    "auto" and the reference's names resolve to the one device backend,
+    unknown names raise ValueError like the reference."""
+    global _active
+    if name == "auto":
+        name = "cuda"
+    if name not in BACKENDS:
+        raise ValueError(f"unknown backend {name!r}; available: {tuple(BACKENDS)}")
+    _active = BACKENDS[name]
+    return _active
+
+
+def get_backend() -> str:
+    return _active.name
+
+
+# SPCG_BACKEND is honoured at import (kernels/__init__.py:50)
+_active = set_backend(os.environ.get("SPCG_BACKEND", "auto"))
 
 
 # ---- device buffer plumbing --------------------------------------------------

@@ -1,5 +1,7 @@
 """Conjugate gradient on the B200: the reference's `cg_solve` API
-(solver.py:65-172) over one persistent cooperative CUDA kernel.
+(solver.py:65-172) over the device engines of the C library (one
+persistent cluster-resident kernel for systems that fit on chip, per-pass
+streaming kernels for the rest).
 
 Semantics kept from the reference, in order (solver.py:86-162):
   * b and x0 are cast to the matrix dtype; shape errors raise ValueError
@@ -14,8 +16,8 @@ Semantics kept from the reference, in order (solver.py:86-162):
   * hitting max_iter returns converged=False (no exception);
   * final_relative_residual is the true ||b - A x||/||b|| unless
     recompute_final_residual is False.
-All of it runs on the device: the host launches one kernel and reads back a
-36-byte result record, x and (optionally) the history.
+All of it runs on the device: no host round trip per iteration; the host
+reads back a small result record, x and (optionally) the history.
 """
 
 from __future__ import annotations
@@ -65,6 +67,9 @@ class SolveReport:
     final_relative_residual: float
     residual_history: list[float] | None = None
     timings: dict[str, float] = field(default_factory=dict)
+    # (new, not in the reference's record) which device engine produced x:
+    # {"engine": 2|3|5|6, "fallback": bool, "cond_estimate": float}
+    engine_info: dict = field(default_factory=dict, compare=False, repr=False)
 
 
 def check_convergence(residual_norm: float, b_norm: float, opts: CgOptions) -> bool:
@@ -128,7 +133,7 @@ def cg_solve(a, b, x0=None, opts: CgOptions | None = None, cfg: KernelConfig | N
                      record_history=int(bool(opts.record_history)),
                      recompute_final_residual=int(bool(opts.recompute_final_residual)),
                      accumulation=_acc_code(cfg), engine=int(engine),
-                     row_sums=1 if cfg.row_sums == "sequential" else 0)
+                     row_sums=1 if cfg.row_sums == "sequential" else 0, timing=2)
     res = N.CgResultC()
     if device_io:
         import torch
@@ -159,9 +164,15 @@ def cg_solve(a, b, x0=None, opts: CgOptions | None = None, cfg: KernelConfig | N
         raise _BREAKDOWN[rc](int(res.fail_iteration))
     N.check(rc, "spcg_cg_solve")
     total = time.perf_counter() - t0
-    # One fused kernel performs every SpMV, dot and axpy of the solve: its
-    # device time is reported under "spmv"; "dot"/"axpy" have no separate cost.
-    timings = {"spmv": res.device_ms / 1e3, "dot": 0.0, "axpy": 0.0, "total": total}
+    # Device time per phase (solver.py:98-105 keys).  The kernels fuse the
+    # dot partials into the SpMV and update passes, so: "spmv" = the SpMV
+    # passes, "axpy" = the vector-update passes, "dot" = the rest of the
+    # device time (reductions' completion, scalar steps, collectives).
+    ph = [float(v) / 1e3 for v in res.phase_ms]
+    if sum(ph) > 0.0:
+        timings = {"spmv": ph[0], "dot": ph[1], "axpy": ph[2], "total": total}
+    else:  # an engine that did not split its one kernel: all under "spmv"
+        timings = {"spmv": res.device_ms / 1e3, "dot": 0.0, "axpy": 0.0, "total": total}
     return SolveReport(
         x=x_out,
         iterations=int(res.iterations),
@@ -169,4 +180,6 @@ def cg_solve(a, b, x0=None, opts: CgOptions | None = None, cfg: KernelConfig | N
         final_relative_residual=float(res.final_relative_residual),
         residual_history=[float(v) for v in hist_arr] if hist_arr is not None else None,
         timings=timings,
+        engine_info={"engine": int(res.engine_used), "fallback": bool(res.fallbacks),
+                     "cond_estimate": float(res.cond_estimate)},
     )

@@ -22,7 +22,7 @@ def as_storage(a, kind):
                                           else "atomic")
 
 
-@pytest.mark.parametrize("engine", [1, 3])
+@pytest.mark.parametrize("engine", [3])
 @pytest.mark.parametrize("kind", STORAGES)
 def test_fem_mesh_both_resident_engines(golden, kind, engine):
     from paper_1010_4639_b200 import CgOptions, cg_solve

@@ -160,3 +160,63 @@ def test_sharded_world1_symmetric_rows(accumulation):
     assert abs(res.iterations - o.iterations) <= 1
     assert np.linalg.norm(x.cpu().numpy() - o.x) / np.linalg.norm(o.x) <= 1e-8
     assert res.final_relative_residual <= 1e-10
+
+
+_NCCL_SCRIPT = r"""
+import sys, json
+sys.path.insert(0, {root!r})
+import numpy as np, torch
+from paper_1010_4639_b200.distributed import Comm, ShardedMatrix, dist_cg_solve
+sm = ShardedMatrix.from_stencil("poisson3d", (20, 18, 16), "csr", 0, 1, lambda o: [o])
+from paper_1010_4639_b200.genprob import poisson3d, rhs_for
+a = poisson3d(20, 18, 16)
+b, _ = rhs_for(a, seed=1)
+bt = torch.from_numpy(b).cuda()
+out = {{}}
+for name, nccl in (("none", False), ("nccl", True)):
+    comm = Comm(0, 1, nccl=nccl)
+    x, res, hist = dist_cg_solve(sm, comm, bt, record_history=True)
+    out[name] = dict(x=x.cpu().numpy().tolist(), it=int(res.iterations), hist=hist.tolist(),
+                     launches=int(res.kernel_launches))
+    comm.close()
+print("RESULT " + json.dumps(out))
+"""
+
+
+def test_nccl_one_rank_communicator():
+    """A real one-rank NCCL communicator (spcg_comm_create with an id): the
+    ncclAllReduce calls of the sharded engine execute on the solve stream
+    (NCCL_DEBUG=INFO shows the communicator's bring-up), and the solve is
+    bitwise the one without a communicator (a one-rank sum is the value)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = str(Path(__file__).resolve().parent.parent)
+    env = dict(os.environ, NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT,COLL")
+    p = subprocess.run([sys.executable, "-c", _NCCL_SCRIPT.format(root=root)], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    log = p.stdout + p.stderr
+    assert "NCCL INFO" in log and "ncclCommInitRank" in log, log[-3000:]
+    assert "AllReduce" in log, log[-3000:]  # COLL subsystem: the engine's all-reduces ran
+    res = json.loads([ln for ln in p.stdout.splitlines() if ln.startswith("RESULT ")][0][7:])
+    a, b = res["none"], res["nccl"]
+    assert a["it"] == b["it"] and a["x"] == b["x"] and a["hist"] == b["hist"]
+    o = O.cg_solve("csr", *_poisson_arrays(), _rhs())
+    assert abs(a["it"] - o.iterations) <= 1
+
+
+def _poisson_arrays():
+    from paper_1010_4639_b200.genprob import poisson3d
+
+    a = poisson3d(20, 18, 16)
+    return a.row_start, a.col_idx, a.values
+
+
+def _rhs():
+    from paper_1010_4639_b200.genprob import poisson3d, rhs_for
+
+    return rhs_for(poisson3d(20, 18, 16), seed=1)[0]

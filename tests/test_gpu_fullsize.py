@@ -1,16 +1,40 @@
-"""BASELINE.json's full-size configurations on the B200, checked against the
-reference's own golden runs (compiled reference backend,
-tol 1e-10, x0 = 0, b = A x_gen with x_gen = default_rng(1).standard_normal(n)):
-P2 4096^2 -> 7,387 iterations, P3 400^3 -> 944, Q27 256^3 (symmetric half) ->
-457.  The reference's x is not stored at these sizes, so the size-independent
-properties are checked instead: the iteration count (+-1 %), the true relative
-residual, the error against x_gen (the survey's 3.1e-6 / 1.4e-7 level), and
-that every storage of the same operator gives the same SpMV to 1e-12."""
+"""BASELINE.json's full-size configurations on the B200, against the
+REFERENCE's own CG output on the same inputs (tests/golden/fullsize_*.npz,
+made by scripts/make_golden_fullsize.py: /root/reference's spcg.cg_solve,
+solver.py:65-172, over its compiled _ckernels, workers = 8, privatized;
+tol 1e-10, x0 = 0, b = spmv_full(A, x_gen), x_gen = default_rng(1)
+.standard_normal(n), the cmd_gen recipe of cli.py:91-93):
+
+  P2 4096^2 -> 7,387 iterations, P3 400^3 -> 944, Q27 256^3 (symmetric
+  half, both accumulations) -> 457.
+
+Checked (north-star bar): iterations within +-1 %; ||x - x_ref|| /
+||x_ref|| <= 1e-8 on the committed strided subsample x_ref[::977] (64 K / 17 K
+entries) and through the full vector's norm; the recorded recursive residual
+history within 1e-8 (relative) of the reference's over the first 50
+iterations and within 1e-6 over all of them; the true final residual.  The
+one whole-vector comparison (every entry) is scripts/fullsize_parity.py,
+run once on a GPU box (profiles/r02/fullsize_parity.json)."""
 
 import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
+
+CONFIGS = {
+    "p2": ("poisson2d", (4096, 4096), "csr"),
+    "p3": ("poisson3d", (400, 400, 400), "csr"),
+    "q27": ("stencil27", (256, 256, 256), "scsr"),
+}
+
+
+def _golden(name):
+    from conftest import GOLDEN
+
+    p = GOLDEN / f"fullsize_{name}.npz"
+    if not p.exists():
+        pytest.skip(f"{p.name} not generated (scripts/make_golden_fullsize.py)")
+    return np.load(p)
 
 
 def _system(kind, dims, fmt):
@@ -24,60 +48,79 @@ def _system(kind, dims, fmt):
     xg = torch.from_numpy(np.random.default_rng(1).standard_normal(dm.n)).cuda()
     b = torch.empty_like(xg)
     N.check(N.load().spcg_spmv(full.handle, xg.data_ptr(), b.data_ptr(), N.ACC_PRIVATIZED, 0), "b")
+    torch.cuda.synchronize()
     return dm, full, xg, b
 
 
-def _solve(dm, b, acc):
+def _solve(dm, b, acc, max_iter):
     import torch
 
     from paper_1010_4639_b200 import _native as N
 
     x = torch.empty_like(b)
-    o = N.CgOptionsC(tol=1e-10, max_iter=0, record_history=0, recompute_final_residual=1,
+    hist = torch.empty(max_iter, dtype=torch.float64, device=b.device)
+    o = N.CgOptionsC(tol=1e-10, max_iter=max_iter, record_history=1, recompute_final_residual=1,
                      accumulation=acc, engine=0)
     r = N.CgResultC()
-    N.check(N.load().spcg_cg_solve(dm.handle, b.data_ptr(), None, x.data_ptr(), None, o, r, 0),
-            "solve")
-    return x, r
+    N.check(N.load().spcg_cg_solve(dm.handle, b.data_ptr(), None, x.data_ptr(), hist.data_ptr(),
+                                   o, r, 0), "solve")
+    return x, r, hist[: r.iterations].cpu().numpy()
 
 
-@pytest.mark.parametrize("kind,dims,ref_its,err_bound", [
-    ("poisson2d", (4096, 4096), 7387, 1e-5),
-    ("poisson3d", (400, 400, 400), 944, 1e-6),
-])
-def test_poisson_full_size(kind, dims, ref_its, err_bound):
+def _check(g, x, r, hist):
     import torch
 
-    dm, _, xg, b = _system(kind, dims, "csr")
-    x, r = _solve(dm, b, 1)
-    assert abs(r.iterations - ref_its) <= max(1, ref_its // 100)
-    assert r.converged and r.final_relative_residual <= 1e-10
-    err = float(torch.linalg.norm(x - xg) / torch.linalg.norm(xg))
-    assert err <= err_bound, err
+    its = int(g["iterations"])
+    assert r.converged
+    assert abs(r.iterations - its) <= max(1, its // 100), (r.iterations, its)
+    stride = int(g["stride"])
+    xs = x[::stride].cpu().numpy()
+    xr = g["x_sub"]
+    assert xs.shape == xr.shape
+    err_sub = np.linalg.norm(xs - xr) / np.linalg.norm(xr)
+    assert err_sub <= 1e-8, err_sub
+    xn = float(torch.linalg.norm(x))
+    assert abs(xn - float(g["x_norm"])) <= 1e-8 * float(g["x_norm"])
+    assert r.final_relative_residual <= max(1e-10, 2 * float(g["final_rel"]))
+    h = g["residual_history"]
+    k = min(len(hist), len(h))
+    assert np.allclose(hist[:50], h[:50], rtol=1e-8, atol=0)
+    assert np.max(np.abs(hist[:k] - h[:k]) / h[:k]) <= 1e-6
+    return err_sub
 
 
-def test_q27_full_size_both_accumulations():
+@pytest.mark.parametrize("name", ["p2", "p3"])
+def test_poisson_full_size_vs_reference(name):
+    g = _golden(name)
+    kind, dims, fmt = CONFIGS[name]
+    dm, _, _, b = _system(kind, dims, fmt)
+    assert dm.n == int(g["n"]) and dm.nnz == int(g["stored_nnz"])
+    x, r, hist = _solve(dm, b, 1, int(g["n"]))
+    _check(g, x, r, hist)
+
+
+def test_q27_full_size_both_accumulations_vs_reference():
     import torch
 
     from paper_1010_4639_b200 import _native as N
 
-    dm, full, xg, b = _system("stencil27", (256, 256, 256), "scsr")
+    g = _golden("q27")
+    kind, dims, fmt = CONFIGS["q27"]
+    dm, full, xg, b = _system(kind, dims, fmt)
+    assert dm.n == int(g["n"]) and dm.nnz == int(g["stored_nnz"])
     lib = N.load()
     # SpMV: privatized SCSR and atomic SCSR against the full CSR of the same operator
-    y_full = torch.empty_like(xg)
-    y_priv = torch.empty_like(xg)
-    y_atom = torch.empty_like(xg)
+    y_full, y_priv, y_atom = (torch.empty_like(xg) for _ in range(3))
     N.check(lib.spcg_spmv(full.handle, xg.data_ptr(), y_full.data_ptr(), 1, 0), "full")
     N.check(lib.spcg_spmv(dm.handle, xg.data_ptr(), y_priv.data_ptr(), 1, 0), "priv")
     N.check(lib.spcg_spmv(dm.handle, xg.data_ptr(), y_atom.data_ptr(), 0, 0), "atom")
     scale = float(torch.linalg.norm(y_full, ord=float("inf")))
     assert float((y_priv - y_full).abs().max()) <= 1e-12 * scale
     assert float((y_atom - y_full).abs().max()) <= 1e-12 * scale
+    full.close()
     xs = []
     for acc in (1, 0):
-        x, r = _solve(dm, b, acc)
-        assert abs(r.iterations - 457) <= 4
-        assert r.converged and r.final_relative_residual <= 1e-10
-        assert float(torch.linalg.norm(x - xg) / torch.linalg.norm(xg)) <= 1e-6
+        x, r, hist = _solve(dm, b, acc, int(g["n"]))
+        _check(g, x, r, hist)
         xs.append(x)
     assert float(torch.linalg.norm(xs[0] - xs[1]) / torch.linalg.norm(xs[0])) <= 1e-8

@@ -43,6 +43,11 @@ def _worker(rank, world, port, case, q):
         if case == "p3":
             a = poisson3d(9, 8, 12)
             sm = ShardedMatrix.from_stencil("poisson3d", (9, 8, 12), "csr", rank, world, gather)
+        elif case == "p3_empty":
+            # 3 z-planes over 4 plane-aligned ranks: one rank owns no rows and
+            # must still join every collective of the solve
+            a = poisson3d(10, 10, 3)
+            sm = ShardedMatrix.from_stencil("poisson3d", (10, 10, 3), "csr", rank, world, gather)
         elif case in ("q27_priv", "q27_atomic"):
             a = stencil27(10, 9, 16)
             sm = ShardedMatrix.from_stencil("stencil27", (10, 9, 16), "scsr", rank, world, gather)
@@ -65,8 +70,9 @@ def _worker(rank, world, port, case, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("case", ["p3", "q27_priv", "q27_atomic", "rand"])
+@pytest.mark.parametrize("world,case", [(w, c) for w in (2, 4)
+                                        for c in ("p3", "q27_priv", "q27_atomic", "rand")]
+                         + [(4, "p3_empty")])
 def test_sharded_world_n_on_one_gpu(case, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -82,7 +88,9 @@ def test_sharded_world_n_on_one_gpu(case, world):
     x = np.concatenate([t[1] for t in allx])
     its = {t[2] for t in allx}
     assert len(its) == 1, its                      # every rank stops together
-    assert all(t[4] >= 1 and t[5] >= 1 for t in allx)  # real halos on every rank
+    assert all(t[4] >= 1 and t[5] >= 1 for t in allx if t[1].size)  # real halos on every rank
+    if case == "p3_empty":
+        assert any(t[1].size == 0 for t in allx)
     ref = O.cg_solve("csr", a.row_start, a.col_idx, a.values, b)
     assert abs(its.pop() - ref.iterations) <= max(1, ref.iterations // 100)
     assert np.linalg.norm(x - ref.x) / np.linalg.norm(ref.x) <= 1e-8

@@ -167,12 +167,12 @@ def test_row_sums_modes_long_rows(storage):
         KernelConfig(row_sums="fast")
 
 
-@pytest.mark.parametrize("engine", [1, 2, 4])
+@pytest.mark.parametrize("engine", [0, 2])
 @pytest.mark.parametrize("storage", ["csr", "sym_priv", "sym_atomic", "csc"])
 def test_streaming_engines_all_storages(engine, storage):
-    """A system too large for the resident kernels (so engines 1 and 4 run
-    their streaming persistent bodies: folded / paired and three-pass) in
-    every storage, against the reference CG."""
+    """A system too large for the resident kernels (auto routes it to the
+    per-pass streaming engine) in every storage, against the reference CG;
+    engines 1 and 4 of round 1 are gone and rejected."""
     from paper_1010_4639_b200 import CgOptions, cg_solve
     from paper_1010_4639_b200.genprob import poisson3d, rhs_for
 
@@ -185,3 +185,13 @@ def test_streaming_engines_all_storages(engine, storage):
     assert abs(r.iterations - ref.iterations) <= max(1, ref.iterations // 100)
     assert np.linalg.norm(r.x - ref.x) / np.linalg.norm(ref.x) <= 1e-8
     assert r.final_relative_residual <= 1e-10
+
+
+@pytest.mark.parametrize("engine", [1, 4, 7, -1])
+def test_removed_engines_are_rejected(engine):
+    from paper_1010_4639_b200 import cg_solve
+    from paper_1010_4639_b200.genprob import poisson2d
+
+    a = poisson2d(8, 8)
+    with pytest.raises(ValueError, match="engine must be"):
+        cg_solve(a, np.ones(a.n), engine=engine)

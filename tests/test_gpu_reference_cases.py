@@ -12,7 +12,7 @@ from conftest import rel_inf_err
 pytestmark = pytest.mark.gpu
 
 STORAGES = ["csr", "sym_priv", "sym_atomic", "csc"]
-ENGINES = [0, 1, 2, 3, 4, 5]  # auto, persistent, per-pass, single-reduction, three-pass, cluster
+ENGINES = [0, 2, 3, 5, 6]  # auto, per-pass, single-reduction, cluster, pipelined cluster
 
 
 def as_storage(a, kind):

@@ -3,12 +3,13 @@ symbols, host storage types / loaders / generators behave like the
 reference's, and the product refuses to run without a device (no CPU
 fallback)."""
 
+import os
 import re
 
 import numpy as np
 import pytest
 
-from conftest import HAS_GPU
+from conftest import HAS_GPU, ROOT
 
 
 def test_library_exports_every_header_symbol():
@@ -20,7 +21,7 @@ def test_library_exports_every_header_symbol():
     lib = N.load()
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.spcg_abi_version() == 1
+    assert lib.spcg_abi_version() == 2
 
 
 @pytest.mark.skipif(HAS_GPU, reason="checks the no-device failure mode")
@@ -198,9 +199,16 @@ def test_kernel_config_and_backend():
         KernelConfig(accumulation="racy")
     assert KernelConfig(workers=2).resolve_chunk(160) == 10
     assert kernels.available_backends() == ("cuda",)
-    assert kernels.set_backend("auto") == "cuda"
+    be = kernels.set_backend("auto")
+    assert be.name == "cuda" and kernels.get_backend() == "cuda"
+    # the reference's backend names select the one device backend
+    for alias in ("compiled", "python", "cuda"):
+        assert kernels.set_backend(alias) is be
+        assert kernels.BACKENDS[alias] is be
+    for fn in ("spmv_full", "spmv_sym", "dot", "axpy"):
+        assert callable(getattr(be, fn))
     with pytest.raises(ValueError):
-        kernels.set_backend("python")
+        kernels.set_backend("numba")
     assert kernels.pairwise_merge(np.array([1.0, 2.0, 3.0, 4.0, 5.0])) == 15.0
 
 
@@ -214,3 +222,20 @@ def test_cg_options_and_convergence():
     assert check_convergence(0.0, 0.0, CgOptions())
     assert not check_convergence(1e-300, 0.0, CgOptions())
     assert check_convergence(5e-10, 10.0, CgOptions(tol=1e-10))
+
+
+def test_spcg_backend_env_is_honoured():
+    """SPCG_BACKEND (kernels/__init__.py:50) is read at import: a reference
+    name selects the device backend, an unknown one fails the import."""
+    import subprocess
+    import sys
+
+    code = "import paper_1010_4639_b200.kernels as k; print(k.get_backend())"
+    for name, ok in (("compiled", True), ("python", True), ("bogus", False)):
+        p = subprocess.run([sys.executable, "-c", code], cwd=str(ROOT),
+                           env={**os.environ, "SPCG_BACKEND": name}, capture_output=True, text=True)
+        assert (p.returncode == 0) == ok, p.stderr
+        if ok:
+            assert p.stdout.strip() == "cuda"
+        else:
+            assert "unknown backend" in p.stderr
