@@ -243,6 +243,40 @@ int spcg_dist_cg_solve(spcg_matrix_t local, spcg_comm_t comm, int npeers,
                        const double* d_b, const double* d_x0, double* d_x, double* d_hist,
                        const spcg_cg_options* opts, spcg_cg_result* result, void* stream);
 
+/* ---- device-initiated transport (no host collective per iteration) -------
+ * A per-rank plan of the same halo layout as spcg_dist_cg_solve.  Peers write
+ * straight into this rank's memory: the two scalar all-reduces of every
+ * iteration go through epoch-tagged mailboxes (each rank's last CTA of a
+ * reducing pass posts its partial to every rank, polls its own mailbox and
+ * sums the partials in rank order), the halo of p is stored by the pass that
+ * computes it into the neighbours' p_ext (remote stores over NVLink), and the
+ * single-pass SCSR scatter sends its transposed contributions to their
+ * owners as remote fp64 reds.  Bootstrap: every rank exports a blob (CUDA IPC
+ * handles of the buffers peers write, its row layout), the host framework
+ * all-gathers the nranks blobs in rank order, every rank connects.  Ranks of
+ * ONE process on ONE device are connected by plain pointers and can be
+ * solved together in one launch per pass (spcg_dist_group_solve: "virtual
+ * ranks", how the protocol is tested on a single GPU). */
+#define SPCG_P2P_BLOB_BYTES 1024
+typedef struct spcg_dist_plan_s* spcg_dist_plan_t;
+int spcg_dist_plan_create(spcg_matrix_t local, int rank, int nranks, int npeers,
+                          const int32_t* peers, const int64_t* recv_off, const int64_t* send_off,
+                          const int32_t* send_idx, spcg_dist_plan_t* out);
+int spcg_dist_plan_destroy(spcg_dist_plan_t plan);
+int spcg_dist_plan_export(spcg_dist_plan_t plan, unsigned char* blob /* SPCG_P2P_BLOB_BYTES */);
+int spcg_dist_plan_connect(spcg_dist_plan_t plan,
+                           const unsigned char* blobs /* nranks x SPCG_P2P_BLOB_BYTES */);
+/* One rank's share (one process per GPU), same semantics as spcg_dist_cg_solve. */
+int spcg_dist_plan_solve(spcg_dist_plan_t plan, const double* d_b, const double* d_x0, double* d_x,
+                         double* d_hist, const spcg_cg_options* opts, spcg_cg_result* result,
+                         void* stream);
+/* All nranks plans of this process (same device): every pass is ONE launch
+ * over all ranks' data.  d_b / d_x0 (NULL or per rank) / d_x: per-rank
+ * device vectors; d_hist: rank 0's history; results[nranks]. */
+int spcg_dist_group_solve(int nranks, spcg_dist_plan_t* plans, const double* const* d_b,
+                          const double* const* d_x0, double* const* d_x, double* d_hist,
+                          const spcg_cg_options* opts, spcg_cg_result* results, void* stream);
+
 /* ---- library ------------------------------------------------------------ */
 
 const char* spcg_last_error(void);

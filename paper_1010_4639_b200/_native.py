@@ -113,6 +113,14 @@ SIGNATURES = {
         [_vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.POINTER(CgOptionsC),
          ctypes.POINTER(CgResultC), _vp],
     ),
+    "spcg_dist_plan_create": (_i32, [_vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, ctypes.POINTER(_vp)]),
+    "spcg_dist_plan_destroy": (_i32, [_vp]),
+    "spcg_dist_plan_export": (_i32, [_vp, _vp]),
+    "spcg_dist_plan_connect": (_i32, [_vp, _vp]),
+    "spcg_dist_plan_solve": (
+        _i32, [_vp, _vp, _vp, _vp, _vp, ctypes.POINTER(CgOptionsC), ctypes.POINTER(CgResultC), _vp]),
+    "spcg_dist_group_solve": (
+        _i32, [_i32, _vp, _vp, _vp, _vp, _vp, ctypes.POINTER(CgOptionsC), _vp, _vp]),
     "spcg_last_error": (ctypes.c_char_p, []),
     "spcg_abi_version": (_i32, []),
     "spcg_device_info": (

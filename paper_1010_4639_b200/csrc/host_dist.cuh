@@ -157,6 +157,8 @@ int ensure_dist_ws(spcg_matrix_s* m, long long send_total) {
     if ((rc = dmalloc((void**)&d.q, eb, nullptr))) return rc;
     if ((rc = dmalloc((void**)&d.part, sizeof(double) * 4096, nullptr))) return rc;
     if ((rc = dmalloc((void**)&d.S, sizeof(StepState), nullptr))) return rc;
+    CUDA_TRY(cudaMemset(d.S, 0, sizeof(StepState)));
+    if (!d.args && (rc = dmalloc((void**)&d.args, sizeof(DistArgs), nullptr))) return rc;
     CUDA_TRY(cudaMallocHost((void**)&d.h_S, sizeof(StepState)));
     for (int c = 0; c < 2; ++c) {
       CUDA_TRY(cudaMallocHost((void**)&d.h_Sc[c], sizeof(StepState)));
@@ -277,186 +279,327 @@ int allreduce_red(const HaloPlan& H, StepState* S, cudaStream_t st) {
   return SPCG_OK;
 }
 
+// ---- device-initiated transport: per-rank plan (spcg_dist_plan_t) ----------
+// What peers write into lives in plain cudaMalloc allocations of this rank,
+// exported by CUDA IPC (one process per GPU) or shared as raw pointers (ranks
+// of one process on one GPU: the virtual-rank group launch).
+struct P2PBlob {
+  uint32_t magic, version;
+  int32_t rank, nranks, device, pid;
+  int64_t nloc, row0;
+  int64_t recv_off_by_src[kMaxRanks];  // offset of src's values in my halo (-1: none)
+  cudaIpcMemHandle_t h_mbox, h_hflag, h_p, h_tmp, h_q;
+  uint64_t mbox, hflag, p, tmp, q;     // raw pointers (same-process connect)
+};
+static_assert(sizeof(P2PBlob) <= SPCG_P2P_BLOB_BYTES, "blob too large");
+constexpr uint32_t kBlobMagic = 0x50324350u;  // "PC2P"
+
+}  // namespace
+
+struct spcg_dist_plan_s {
+  spcg_matrix_s* m = nullptr;
+  int rank = 0, nranks = 1;
+  std::vector<int32_t> peers;
+  std::vector<int64_t> recv_off, send_off;
+  std::vector<int32_t> send_idx;
+  unsigned long long* mbox = nullptr;   // [2][R][2]
+  unsigned long long* hflag = nullptr;  // [R][2]
+  unsigned char* thalo = nullptr;
+  SendRun* runs = nullptr;
+  int nruns = 0;
+  int* send_peer = nullptr;
+  long long* send_dst = nullptr;
+  int* ghost_peer = nullptr;
+  int* ghost_dst = nullptr;
+  long long nghost = 0;
+  bool connected = false;
+  DistArgs peer{};                   // peer pointer tables (filled by connect)
+  std::vector<void*> opened;         // IPC mappings to close
+  DistArgs* d_args = nullptr;        // device copy for solo solves
+};
+
+namespace {
+
+void free_plan(spcg_dist_plan_s* P) {
+  for (void* q : P->opened) cudaIpcCloseMemHandle(q);
+  P->opened.clear();
+  for (void* q : {(void*)P->mbox, (void*)P->hflag, (void*)P->thalo, (void*)P->runs,
+                  (void*)P->send_peer, (void*)P->send_dst, (void*)P->ghost_peer,
+                  (void*)P->ghost_dst, (void*)P->d_args})
+    if (q) cudaFree(q);
+}
+
+// The streaming tile view of a (localized) handle and its per-tile halo flags.
+MatView dist_view(const spcg_matrix_s* m, int kf) { return view_stream(m, kf == K_SCSR_PRIV); }
+
+int build_thalo(spcg_matrix_s* m, int kf, unsigned char** out) {
+  const MatView v = dist_view(m, kf);
+  int rc;
+  if ((rc = dmalloc((void**)out, std::max<size_t>(1, (size_t)v.ntiles), nullptr))) return rc;
+  if (v.ntiles > 0) {
+    tile_halo_kernel<<<std::min(v.ntiles, 148 * 8), 256>>>(
+        v.tdesc, kf == K_SCSR_PRIV ? v.tdescB : nullptr, v.ntiles, v.idxA,
+        kf == K_SCSR_PRIV ? v.idxB : nullptr, (long long)m->n, *out);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaDeviceSynchronize());
+  }
+  return SPCG_OK;
+}
+
+// ---- the per-pass loop, shared by every transport ----------------------------
+// nv DistArgs (device array dA, host copies hA): nv = 1 for one rank per
+// process (host transports, or the device transport across GPUs), nv = R for
+// the virtual-rank group on one GPU.  H: the host transport (fused == 0 only).
 template <int FMT>
-int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const double* x0, double* x,
-                 double* hist, const spcg_cg_options* o, spcg_cg_result* out, cudaStream_t st) {
+int run_dist(const std::vector<DistArgs>& hA, DistArgs* dA, const HaloPlan* H, const MatView& v,
+             const spcg_cg_options* o, std::vector<StepState*> h_state,
+             const std::vector<spcg_matrix_s*>& mats, spcg_cg_result* out, cudaStream_t st) {
   DevInfo* di;
   int rc;
   if ((rc = dev_info(&di))) return rc;
-  DistWorkspace& d = m->dw;
-  const MatView v = view_stream(m, FMT == K_SCSR_PRIV);
-  const long long nloc = m->n, next = d.next;
-  const int G = std::max(1, std::min(std::max(1, v.ntiles), di->spmv_grid));
+  const int nv = (int)hA.size();
+  const bool fused = hA[0].fused != 0;
+  const bool wide = FMT == K_CSR && v.wide;
+  int G = 1;
+  for (const DistArgs& a : hA)
+    G = std::max(G, std::min(std::max(1, a.M.ntiles), di->spmv_grid));
   const int GE = 2 * di->sms;
   const size_t sm = sizeof(Smem);
-  const int xv = (((uintptr_t)x) & 15) == 0;
   constexpr int kAtom = (FMT == K_SCSR_ATOMIC || FMT == K_CSC) ? 1 : 0;
-  double* p = d.p_ext[0];  // p_ext = [own p | halo]
-  double* r = d.r_ext;
-  long long launches = 0;
-  StepState init{};
-  init.tol = o->tol;
-  init.max_it = o->max_iter > 0 ? o->max_iter
-                                : std::max<long long>(1, std::max<long long>(m->n_global, m->n));
-  init.record = o->record_history && hist;
-  init.x0_given = x0 != nullptr;
-  CUDA_TRY(cudaMemcpyAsync(d.S, &init, sizeof(StepState), cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaMemsetAsync(p, 0, sizeof(double) * (size_t)next, st));
-  if (kAtom) CUDA_TRY(cudaMemsetAsync(d.q, 0, sizeof(double) * (size_t)std::max(1LL, next), st));
-  const long long nhalo = next - nloc;
   constexpr bool kRev = (FMT == K_SCSR_ATOMIC);  // transposed scatters reach halo rows
-  CUDA_TRY(cudaEventRecord(d.ev0, st));
-  // ||b|| (solver.py:107)
-  dist_elem<<<GE, kElemBlock, 0, st>>>(0, nloc, d.S, b, nullptr, nullptr, nullptr, d.part, 0);
-  if ((rc = allreduce_red(H, d.S, st))) return rc;
-  dist_scalar<<<1, 1, 0, st>>>(0, d.S, hist);
-  // x = x0, r = b - A x0, p = r (solver.py:120-124)
-  dist_x<<<GE, kElemBlock, 0, st>>>(0, nloc, d.S, x0, x);
-  launches += 3;
-  if (x0) {
-    CUDA_TRY(cudaMemcpyAsync(d.tmp_ext, x0, sizeof(double) * (size_t)nloc,
-                             cudaMemcpyDeviceToDevice, st));
-    if ((rc = halo_exchange(H, d, x0, d.tmp_ext, st, &launches))) return rc;
-    if (FMT == K_CSR && v.wide) dist_spmv<K_CSR, true><<<G, kBlock, sm, st>>>(v, d.tmp_ext, d.q);
-    else dist_spmv<FMT><<<G, kBlock, sm, st>>>(v, d.tmp_ext, d.q);
-    if (kRev && (rc = reverse_halo(H, d, d.q, nhalo, st, &launches))) return rc;
-    dist_elem<<<GE, kElemBlock, 0, st>>>(1, nloc, d.S, b, d.q, r, p, d.part, kAtom);
-    launches += 2;
-  } else {
-    dist_elem<<<GE, kElemBlock, 0, st>>>(1, nloc, d.S, b, nullptr, r, p, d.part, 0);
-    ++launches;
+  const bool ghosts = fused && kRev && hA[0].nranks > 1;
+  bool any_push = false;  // some rank's send runs do not fit pass C
+  for (const DistArgs& a : hA) any_push |= fused && a.nruns > kRunCache;
+  DistWorkspace& d0 = mats[0]->dw;
+  long long launches = 0;
+  // solve state (the device transport's sequence counters rseq / hseq at the
+  // end of StepState persist across solves: every rank keeps them in step)
+  for (int r = 0; r < nv; ++r) {
+    StepState init{};
+    init.tol = o->tol;
+    init.max_it = o->max_iter > 0
+                      ? o->max_iter
+                      : std::max<long long>(1, std::max<long long>(mats[r]->n_global, mats[r]->n));
+    init.record = o->record_history && hA[r].hist;
+    init.x0_given = hA[r].x0 != nullptr;
+    CUDA_TRY(cudaMemcpyAsync(hA[r].S, &init, offsetof(StepState, rseq), cudaMemcpyHostToDevice, st));
+    const long long next = mats[r]->dw.next;
+    CUDA_TRY(cudaMemsetAsync(hA[r].p, 0, sizeof(double) * (size_t)next, st));
+    if (kAtom) CUDA_TRY(cudaMemsetAsync(hA[r].q, 0, sizeof(double) * (size_t)std::max(1LL, next), st));
   }
-  if ((rc = allreduce_red(H, d.S, st))) return rc;
-  dist_scalar<<<1, 1, 0, st>>>(1, d.S, hist);
+  const int GG = nv * G, GGE = nv * GE;
+  StepState* S0 = hA[0].S;
+  double* hist0 = hA[0].hist;
+  auto host_reduce = [&](int op) -> int {  // host transports: all-reduce + scalar kernel
+    if (fused) return SPCG_OK;
+    int rc2;
+    if ((rc2 = allreduce_red(*H, S0, st))) return rc2;
+    dist_scalar<<<1, 1, 0, st>>>(op, S0, hist0);
+    ++launches;
+    return SPCG_OK;
+  };
+  // halo of an own vector into the neighbours' extended `dst`
+  auto halo = [&](int srcsel, int dstsel, const double* hsrc, double* hdst) -> int {
+    if (fused) {
+      if (hA[0].nranks > 1) {
+        dist_push<<<GGE, kElemBlock, 0, st>>>(dA, GE, srcsel, dstsel, 0);
+        ++launches;
+      }
+      return SPCG_OK;
+    }
+    return halo_exchange(*H, d0, hsrc, hdst, st, &launches);
+  };
+  // tile kernels: one rank -> its DistArgs by value (view in the parameter
+  // bank, rev / tree set per launch); several -> the device array
+  DistArgs a1 = hA[0];
+  a1.M.cta0 = 0;
+  a1.M.ncta = 0;
+  const bool grp = nv > 1;
+  auto spmv_once = [&]() -> int {  // q = A tmp (x0 / true residual)
+    // device transport: the kernel waits for the halo of the push just done
+    a1.M.rev = 0;
+    a1.M.tree = 0;
+    if (wide) {
+      if (grp) dist_spmv<K_CSR, true, true><<<GG, kBlock, sm, st>>>(a1, dA, G);
+      else dist_spmv<K_CSR, true, false><<<G, kBlock, sm, st>>>(a1, dA, G);
+    } else {
+      if (grp) dist_spmv<FMT, false, true><<<GG, kBlock, sm, st>>>(a1, dA, G);
+      else dist_spmv<FMT, false, false><<<G, kBlock, sm, st>>>(a1, dA, G);
+    }
+    ++launches;
+    if (kRev) {
+      if (ghosts) {
+        dist_ghost_push<<<GGE, kElemBlock, 0, st>>>(dA, GE, -1);
+        ++launches;
+      } else if (!fused) {
+        int rc2;
+        if ((rc2 = reverse_halo(*H, d0, hA[0].q, d0.next - hA[0].nloc, st, &launches))) return rc2;
+      }
+    }
+    return SPCG_OK;
+  };
+  CUDA_TRY(cudaEventRecord(d0.ev0, st));
+  // ||b|| (solver.py:107)
+  dist_elem<<<GGE, kElemBlock, 0, st>>>(dA, GE, 0, 0, 0);
   ++launches;
-  if ((rc = halo_exchange(H, d, p, p, st, &launches))) return rc;
+  if ((rc = host_reduce(0))) return rc;
+  // x = x0, r = b - A x0, p = r (solver.py:120-124)
+  dist_x<<<GGE, kElemBlock, 0, st>>>(dA, GE, 0);
+  ++launches;
+  const bool have_x0 = hA[0].x0 != nullptr;
+  if (have_x0) {
+    if ((rc = halo(1, 1, hA[0].x0, hA[0].tmp))) return rc;
+    if ((rc = spmv_once())) return rc;
+  }
+  dist_elem<<<GGE, kElemBlock, 0, st>>>(dA, GE, 1, have_x0 ? 1 : 0, 0);
+  ++launches;
+  if ((rc = host_reduce(1))) return rc;
+  if ((rc = halo(0, 0, hA[0].p, hA[0].p))) return rc;
   CUDA_TRY(cudaGetLastError());
   // CG loop; the host enqueues chunks of iterations and polls the device-side
   // done flag of chunk c while chunk c + 1 is already queued (double
   // buffered), so the GPU never idles while the host enqueues.  Iterations
-  // after `done` are no-ops on every rank, so the NCCL calls stay matched;
+  // after `done` are no-ops on every rank, so the collectives stay matched;
   // the one chunk enqueued past convergence costs only empty launches.
   const int chunk = 16;
   const bool timing = o->timing != 0;
   const bool split = o->timing >= 2;  // events around passes B and C too
-  if (timing && !d.tev[0][0][0])
+  if (timing && !d0.tev[0][0][0])
     for (int bb = 0; bb < 2; ++bb)
       for (int a = 0; a < 6; ++a)
-        for (int c = 0; c < chunk; ++c) CUDA_TRY(cudaEventCreate(&d.tev[bb][a][c]));
+        for (int c = 0; c < chunk; ++c) CUDA_TRY(cudaEventCreate(&d0.tev[bb][a][c]));
   double spmv_ms = 0.0, axpy_ms = 0.0;
   long long spmv_n = 0, k_before = 0, iter_enq = 0;
 #ifndef SPCG_ALTERNATE
 #define SPCG_ALTERNATE 1
 #endif
   constexpr bool kAlternate = SPCG_ALTERNATE != 0;
+  const int tree = o->row_sums == 0;  // auto: reassociated long-row sums in pass A
+  const int post = ghosts ? 0 : 1;
   auto enqueue_chunk = [&](int bb) -> int {
     for (int c = 0; c < chunk; ++c) {
-      if (timing) CUDA_TRY(cudaEventRecord(d.tev[bb][0][c], st));
+      if (timing) CUDA_TRY(cudaEventRecord(d0.tev[bb][0][c], st));
       // alternate traversal directions pass to pass (A, B, C, A, ...): each
       // pass starts on the lines the previous one wrote last (still in L2)
       const int dirA = kAlternate ? (int)((iter_enq & 1) == 0) : 0;
-      MatView va = v;
-      va.rev = dirA;
-      va.tree = o->row_sums == 0;  // auto: reassociated long-row sums in pass A
-      if (FMT == K_CSR && v.wide)
-        dist_spmv_pq<K_CSR, true><<<G, kBlock, sm, st>>>(va, d.S, p, d.q, d.part);
-      else
-        dist_spmv_pq<FMT><<<G, kBlock, sm, st>>>(va, d.S, p, d.q, d.part);
-      if (timing) CUDA_TRY(cudaEventRecord(d.tev[bb][1][c], st));
+      a1.M.rev = dirA;
+      a1.M.tree = tree;
+      if (wide) {
+        if (grp) dist_spmv_pq<K_CSR, true, true><<<GG, kBlock, sm, st>>>(a1, dA, G, dirA, tree, post);
+        else dist_spmv_pq<K_CSR, true, false><<<G, kBlock, sm, st>>>(a1, dA, G, dirA, tree, post);
+      } else {
+        if (grp) dist_spmv_pq<FMT, false, true><<<GG, kBlock, sm, st>>>(a1, dA, G, dirA, tree, post);
+        else dist_spmv_pq<FMT, false, false><<<G, kBlock, sm, st>>>(a1, dA, G, dirA, tree, post);
+      }
+      if (timing) CUDA_TRY(cudaEventRecord(d0.tev[bb][1][c], st));
       int rc2;
-      if ((rc2 = allreduce_red(H, d.S, st))) return rc2;
-      if (kRev && (rc2 = reverse_halo(H, d, d.q, nhalo, st, &launches))) return rc2;
-      dist_scalar<<<1, 1, 0, st>>>(2, d.S, hist);
-      if (split) CUDA_TRY(cudaEventRecord(d.tev[bb][2][c], st));
-      dist_elem<<<GE, kElemBlock, 0, st>>>(2, nloc, d.S, nullptr, d.q, r, nullptr, d.part, kAtom,
-                                       kAlternate ? 1 - dirA : 0);
-      if (split) CUDA_TRY(cudaEventRecord(d.tev[bb][3][c], st));
-      if ((rc2 = allreduce_red(H, d.S, st))) return rc2;
-      dist_scalar<<<1, 1, 0, st>>>(3, d.S, hist);
-      if (split) CUDA_TRY(cudaEventRecord(d.tev[bb][4][c], st));
-      dist_update<<<GE, kElemBlock, 0, st>>>(nloc, d.S, r, p, x, xv, dirA);
-      if (split) CUDA_TRY(cudaEventRecord(d.tev[bb][5][c], st));
+      if (!fused) {
+        if ((rc2 = allreduce_red(*H, S0, st))) return rc2;
+        if (kRev && (rc2 = reverse_halo(*H, d0, hA[0].q, d0.next - hA[0].nloc, st, &launches)))
+          return rc2;
+        dist_scalar<<<1, 1, 0, st>>>(2, S0, hist0);
+        ++launches;
+      } else if (ghosts) {
+        dist_ghost_push<<<GGE, kElemBlock, 0, st>>>(dA, GE, 2);
+        ++launches;
+      }
+      if (split) CUDA_TRY(cudaEventRecord(d0.tev[bb][2][c], st));
+      dist_elem<<<GGE, kElemBlock, 0, st>>>(dA, GE, 2, 0, kAlternate ? 1 - dirA : 0);
+      if (split) CUDA_TRY(cudaEventRecord(d0.tev[bb][3][c], st));
+      if ((rc2 = host_reduce(3))) return rc2;
+      if (split) CUDA_TRY(cudaEventRecord(d0.tev[bb][4][c], st));
+      dist_update<<<GGE, kElemBlock, 0, st>>>(dA, GE, dirA);
+      if (split) CUDA_TRY(cudaEventRecord(d0.tev[bb][5][c], st));
       ++iter_enq;
-      launches += 5;
-      if ((rc2 = halo_exchange(H, d, p, p, st, &launches))) return rc2;
+      launches += 3;
+      if (fused) {
+        if (any_push) {
+          dist_push<<<GGE, kElemBlock, 0, st>>>(dA, GE, 0, 0, 1);
+          ++launches;
+        }
+      } else if ((rc2 = halo_exchange(*H, d0, hA[0].p, hA[0].p, st, &launches))) {
+        return rc2;
+      }
     }
     CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaMemcpyAsync(d.h_Sc[bb], d.S, sizeof(StepState), cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaEventRecord(d.cev[bb], st));
+    CUDA_TRY(cudaMemcpyAsync(d0.h_Sc[bb], S0, sizeof(StepState), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaEventRecord(d0.cev[bb], st));
     return SPCG_OK;
   };
   // the host-callback transport synchronises inside every exchange: no
   // point (and no room) for a second chunk in flight
-  const bool two = H.hc == nullptr;
+  const bool two = fused || H->hc == nullptr;
   if ((rc = enqueue_chunk(0))) return rc;
+  StepState fin{};
   for (long long ci = 0;; ++ci) {
     const int bb = (int)(ci & 1);
     if (two && (rc = enqueue_chunk(bb ^ 1))) return rc;
-    CUDA_TRY(cudaEventSynchronize(d.cev[bb]));
-    const StepState& hs = *d.h_Sc[bb];
+    CUDA_TRY(cudaEventSynchronize(d0.cev[bb]));
+    const StepState& hs = *d0.h_Sc[bb];
     if (timing) {  // only the passes that did work (later ones returned at once)
       const long long ran = std::min<long long>(chunk, hs.k - k_before + (hs.status != 0 ? 1 : 0));
       for (long long c = 0; c < ran; ++c) {
         float t = 0.f;
-        CUDA_TRY(cudaEventElapsedTime(&t, d.tev[bb][0][c], d.tev[bb][1][c]));
+        CUDA_TRY(cudaEventElapsedTime(&t, d0.tev[bb][0][c], d0.tev[bb][1][c]));
         spmv_ms += t;
         ++spmv_n;
         if (split) {
           float tb = 0.f, tc = 0.f;
-          CUDA_TRY(cudaEventElapsedTime(&tb, d.tev[bb][2][c], d.tev[bb][3][c]));
-          CUDA_TRY(cudaEventElapsedTime(&tc, d.tev[bb][4][c], d.tev[bb][5][c]));
+          CUDA_TRY(cudaEventElapsedTime(&tb, d0.tev[bb][2][c], d0.tev[bb][3][c]));
+          CUDA_TRY(cudaEventElapsedTime(&tc, d0.tev[bb][4][c], d0.tev[bb][5][c]));
           axpy_ms += (double)tb + (double)tc;
         }
       }
       k_before = hs.k;
     }
     if (hs.done) {
-      *d.h_S = hs;
+      fin = hs;
       break;
     }
     if (!two && (rc = enqueue_chunk(bb ^ 1))) return rc;
   }
   // a converged solve skipped its pass C: x += alpha_K p_K; then the true residual
-  dist_x<<<GE, kElemBlock, 0, st>>>(1, nloc, d.S, p, x);
+  dist_x<<<GGE, kElemBlock, 0, st>>>(dA, GE, 1);
   ++launches;
-  if (o->recompute_final_residual && d.h_S->status == 0 && d.h_S->b_norm != 0.0) {
-    CUDA_TRY(cudaMemcpyAsync(d.tmp_ext, x, sizeof(double) * (size_t)nloc,
-                             cudaMemcpyDeviceToDevice, st));
-    if ((rc = halo_exchange(H, d, x, d.tmp_ext, st, &launches))) return rc;
-    if (FMT == K_CSR && v.wide) dist_spmv<K_CSR, true><<<G, kBlock, sm, st>>>(v, d.tmp_ext, d.q);
-    else dist_spmv<FMT><<<G, kBlock, sm, st>>>(v, d.tmp_ext, d.q);
-    if (kRev && (rc = reverse_halo(H, d, d.q, nhalo, st, &launches))) return rc;
-    dist_elem<<<GE, kElemBlock, 0, st>>>(3, nloc, d.S, b, d.q, nullptr, nullptr, d.part, 0);
-    if ((rc = allreduce_red(H, d.S, st))) return rc;
-    dist_true_rel<<<1, 1, 0, st>>>(d.S);
-    launches += 3;
+  if (o->recompute_final_residual && fin.status == 0 && fin.b_norm != 0.0) {
+    dist_x<<<GGE, kElemBlock, 0, st>>>(dA, GE, 2);
+    ++launches;
+    if ((rc = halo(2, 1, hA[0].x, hA[0].tmp))) return rc;
+    if ((rc = spmv_once())) return rc;
+    dist_elem<<<GGE, kElemBlock, 0, st>>>(dA, GE, 3, 0, 0);
+    ++launches;
+    if ((rc = host_reduce(4))) return rc;
   }
-  CUDA_TRY(cudaEventRecord(d.ev1, st));
-  CUDA_TRY(cudaMemcpyAsync(d.h_S, d.S, sizeof(StepState), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaEventRecord(d0.ev1, st));
+  for (int r = 0; r < nv; ++r)
+    CUDA_TRY(cudaMemcpyAsync(h_state[r], hA[r].S, sizeof(StepState), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   CUDA_TRY(cudaGetLastError());
   float ms = 0.f;
-  CUDA_TRY(cudaEventElapsedTime(&ms, d.ev0, d.ev1));
-  const StepState& S = *d.h_S;
-  out->iterations = S.k;
-  out->converged = S.converged;
-  out->status = S.status;
-  out->fail_iteration = S.fail_iter;
-  out->final_relative_residual = S.rel;
-  out->b_norm = S.b_norm;
-  out->device_ms = ms;
-  out->kernel_launches = launches;
-  out->spmv_ms = spmv_ms;
-  out->spmv_launches = spmv_n;
-  out->engine_used = 2;
-  out->fallbacks = 0;
-  out->cond_estimate = 0.0;
-  // split: SpMV passes (with the fused p.q partial); the vector-update passes
-  // B and C (with the fused r.r partial); the rest (reductions' completion,
-  // scalar steps, collectives, halo, prologue/epilogue) under "dot"
-  out->phase_ms[0] = split ? spmv_ms : 0.0;
-  out->phase_ms[2] = split ? axpy_ms : 0.0;
-  out->phase_ms[1] = split ? std::max(0.0, (double)ms - spmv_ms - axpy_ms) : 0.0;
+  CUDA_TRY(cudaEventElapsedTime(&ms, d0.ev0, d0.ev1));
+  for (int r = 0; r < nv; ++r) {
+    const StepState& S = *h_state[r];
+    spcg_cg_result& R = out[r];
+    R = spcg_cg_result{};
+    R.iterations = S.k;
+    R.converged = S.converged;
+    R.status = S.status;
+    R.fail_iteration = S.fail_iter;
+    R.final_relative_residual = S.rel;
+    R.b_norm = S.b_norm;
+    R.device_ms = ms;
+    R.kernel_launches = launches;
+    R.spmv_ms = spmv_ms;
+    R.spmv_launches = spmv_n;
+    R.engine_used = 2;
+    // split: SpMV passes (with the fused p.q partial); the vector-update
+    // passes B and C (with the fused r.r partial); the rest (reductions'
+    // completion, scalar steps, collectives, halo, prologue) under "dot"
+    R.phase_ms[0] = split ? spmv_ms : 0.0;
+    R.phase_ms[2] = split ? axpy_ms : 0.0;
+    R.phase_ms[1] = split ? std::max(0.0, (double)ms - spmv_ms - axpy_ms) : 0.0;
+  }
+  const StepState& S = *h_state[0];
   if (S.status != 0) {
     const char* what = S.status == SPCG_ERR_NOT_SPD ? "matrix not positive definite"
                        : S.status == SPCG_ERR_NONFINITE_ALPHA ? "non-finite alpha"
@@ -465,6 +608,40 @@ int dist_solve_t(spcg_matrix_s* m, const HaloPlan& H, const double* b, const dou
     return fail(S.status, std::string(what) + " at iteration " + std::to_string(S.fail_iter));
   }
   return SPCG_OK;
+}
+
+// Host-side DistArgs of one rank (no device-transport fields).
+DistArgs base_args(spcg_matrix_s* m, int kf, const double* b, const double* x0, double* x,
+                   double* hist, const spcg_cg_options* o) {
+  DistWorkspace& d = m->dw;
+  DistArgs A{};
+  A.M = dist_view(m, kf);
+  A.S = d.S;
+  A.p = d.p_ext[0];
+  A.r = d.r_ext;
+  A.q = d.q;
+  A.x = x;
+  A.b = b;
+  A.x0 = x0;
+  A.tmp = d.tmp_ext;
+  A.hist = o->record_history ? hist : nullptr;
+  A.part = d.part;
+  A.nloc = m->n;
+  A.rank = 0;
+  A.nranks = 1;
+  A.zq = (kf == K_SCSR_ATOMIC || kf == K_CSC) ? 1 : 0;
+  A.xv = (((uintptr_t)x) & 15) == 0;
+  return A;
+}
+
+template <int FMT>
+int dispatch_fmt_host(spcg_matrix_s* m, const HaloPlan& H, const double* b, const double* x0,
+                      double* x, double* hist, const spcg_cg_options* o, spcg_cg_result* out,
+                      cudaStream_t st) {
+  DistWorkspace& d = m->dw;
+  std::vector<DistArgs> hA{base_args(m, FMT, b, x0, x, hist, o)};
+  CUDA_TRY(cudaMemcpyAsync(d.args, hA.data(), sizeof(DistArgs), cudaMemcpyHostToDevice, st));
+  return run_dist<FMT>(hA, d.args, &H, hA[0].M, o, {d.h_S}, {m}, out, st);
 }
 
 int do_dist_cg(spcg_matrix_s* m, spcg_comm_s* comm, int npeers, const int32_t* peers,
@@ -508,16 +685,297 @@ int do_dist_cg(spcg_matrix_s* m, spcg_comm_s* comm, int npeers, const int32_t* p
   // with other ranks it must still join every collective of the solve
   const bool alone = !comm || comm->nranks <= 1;
   if (m->n == 0 && npeers == 0 && alone) {
-    out->iterations = 0;
+    *out = spcg_cg_result{};
     out->converged = 1;
-    out->status = 0;
-    out->final_relative_residual = 0.0;
+    out->engine_used = 2;
     return SPCG_OK;
   }
   switch (kf) {
-    case K_CSR: return dist_solve_t<K_CSR>(m, H, b, x0, x, hist, o, out, st);
-    case K_SCSR_PRIV: return dist_solve_t<K_SCSR_PRIV>(m, H, b, x0, x, hist, o, out, st);
-    case K_SCSR_ATOMIC: return dist_solve_t<K_SCSR_ATOMIC>(m, H, b, x0, x, hist, o, out, st);
-    default: return dist_solve_t<K_CSC>(m, H, b, x0, x, hist, o, out, st);
+    case K_CSR: return dispatch_fmt_host<K_CSR>(m, H, b, x0, x, hist, o, out, st);
+    case K_SCSR_PRIV: return dispatch_fmt_host<K_SCSR_PRIV>(m, H, b, x0, x, hist, o, out, st);
+    case K_SCSR_ATOMIC: return dispatch_fmt_host<K_SCSR_ATOMIC>(m, H, b, x0, x, hist, o, out, st);
+    default: return dispatch_fmt_host<K_CSC>(m, H, b, x0, x, hist, o, out, st);
   }
+}
+
+// ---- device transport: plan creation, export / connect, solves --------------
+int plan_create(spcg_matrix_s* m, int rank, int nranks, int npeers, const int32_t* peers,
+                const int64_t* recv_off, const int64_t* send_off, const int32_t* send_idx,
+                spcg_dist_plan_s** out) {
+  if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks)
+    return fail(SPCG_ERR_ARG, "device transport: 1 <= nranks <= " + std::to_string(kMaxRanks));
+  if (m->is_rows && !m->localized) return fail(SPCG_ERR_ARG, "call spcg_matrix_localize first");
+  if (npeers < 0 || (npeers > 0 && (!peers || !recv_off || !send_off)))
+    return fail(SPCG_ERR_ARG, "bad halo plan");
+  const long long nhalo = (long long)m->halo.size();
+  if ((npeers > 0 ? recv_off[npeers] : 0) != nhalo)
+    return fail(SPCG_ERR_ARG, "receive plan does not cover the halo");
+  const long long send_total = npeers > 0 ? send_off[npeers] : 0;
+  for (int k = 0; k < npeers; ++k)
+    if (peers[k] < 0 || peers[k] >= nranks || peers[k] == rank || (k && peers[k] <= peers[k - 1]))
+      return fail(SPCG_ERR_ARG, "peers must be ascending ranks other than this one");
+  for (long long s = 0; s < send_total; ++s)
+    if (!send_idx || send_idx[s] < 0 || send_idx[s] >= m->n)
+      return fail(SPCG_ERR_ARG, "send index out of range");
+  int rc;
+  if ((rc = ensure_dist_ws(m, send_total))) return rc;
+  auto* P = new spcg_dist_plan_s();
+  P->m = m;
+  P->rank = rank;
+  P->nranks = nranks;
+  P->peers.assign(peers, peers + npeers);
+  P->recv_off.assign(recv_off ? recv_off : nullptr, recv_off ? recv_off + npeers + 1 : nullptr);
+  P->send_off.assign(send_off ? send_off : nullptr, send_off ? send_off + npeers + 1 : nullptr);
+  if (npeers == 0) {
+    P->recv_off.assign(1, 0);
+    P->send_off.assign(1, 0);
+  }
+  P->send_idx.assign(send_idx ? send_idx : nullptr, send_idx ? send_idx + send_total : nullptr);
+  const size_t mb = sizeof(unsigned long long) * 2 * 2 * (size_t)nranks;
+  const size_t hb = sizeof(unsigned long long) * 2 * (size_t)nranks;
+  if ((rc = dmalloc((void**)&P->mbox, mb, nullptr)) || (rc = dmalloc((void**)&P->hflag, hb, nullptr)) ||
+      (rc = dmalloc((void**)&P->d_args, sizeof(DistArgs), nullptr))) {
+    free_plan(P);
+    delete P;
+    return rc;
+  }
+  CUDA_TRY(cudaMemset(P->mbox, 0, mb));
+  CUDA_TRY(cudaMemset(P->hflag, 0, hb));
+  // the sequence counters start at 0 on every rank
+  CUDA_TRY(cudaMemset(m->dw.S, 0, sizeof(StepState)));
+  *out = P;
+  return SPCG_OK;
+}
+
+int plan_export(spcg_dist_plan_s* P, unsigned char* blob_out) {
+  spcg_matrix_s* m = P->m;
+  P2PBlob B;
+  memset(&B, 0, sizeof(B));
+  B.magic = kBlobMagic;
+  B.version = SPCG_ABI_VERSION;
+  B.rank = P->rank;
+  B.nranks = P->nranks;
+  B.device = m->device;
+  B.pid = (int32_t)getpid();
+  B.nloc = m->n;
+  B.row0 = m->is_rows ? m->row0 : 0;
+  for (int s = 0; s < kMaxRanks; ++s) B.recv_off_by_src[s] = -1;
+  for (size_t k = 0; k < P->peers.size(); ++k) B.recv_off_by_src[P->peers[k]] = P->recv_off[k];
+  DistWorkspace& d = m->dw;
+  CUDA_TRY(cudaIpcGetMemHandle(&B.h_mbox, P->mbox));
+  CUDA_TRY(cudaIpcGetMemHandle(&B.h_hflag, P->hflag));
+  CUDA_TRY(cudaIpcGetMemHandle(&B.h_p, d.p_ext[0]));
+  CUDA_TRY(cudaIpcGetMemHandle(&B.h_tmp, d.tmp_ext));
+  CUDA_TRY(cudaIpcGetMemHandle(&B.h_q, d.q));
+  B.mbox = (uint64_t)(uintptr_t)P->mbox;
+  B.hflag = (uint64_t)(uintptr_t)P->hflag;
+  B.p = (uint64_t)(uintptr_t)d.p_ext[0];
+  B.tmp = (uint64_t)(uintptr_t)d.tmp_ext;
+  B.q = (uint64_t)(uintptr_t)d.q;
+  memset(blob_out, 0, SPCG_P2P_BLOB_BYTES);
+  memcpy(blob_out, &B, sizeof(B));
+  return SPCG_OK;
+}
+
+// Map every peer's buffers (IPC, or raw pointers within this process) and
+// build this rank's sender tables: send runs / entries with destinations in
+// the receivers' extended vectors, and the reverse-halo ghost destinations.
+int plan_connect(spcg_dist_plan_s* P, const unsigned char* blobs) {
+  if (P->connected) return SPCG_OK;
+  const int R = P->nranks, me = P->rank;
+  std::vector<P2PBlob> B((size_t)R);
+  for (int k = 0; k < R; ++k) {
+    memcpy(&B[(size_t)k], blobs + (size_t)k * SPCG_P2P_BLOB_BYTES, sizeof(P2PBlob));
+    if (B[k].magic != kBlobMagic || B[k].rank != k || B[k].nranks != R)
+      return fail(SPCG_ERR_ARG, "peer blob " + std::to_string(k) + " is not a plan export of rank " +
+                                    std::to_string(k) + " of " + std::to_string(R));
+  }
+  const int mypid = (int)getpid();
+  DistArgs& T = P->peer;
+  auto open = [&](int k, const cudaIpcMemHandle_t& h, uint64_t raw, void** dst) -> int {
+    if (k == me || B[k].pid == mypid) {
+      if (B[k].device != P->m->device)
+        return fail(SPCG_ERR_UNSUPPORTED, "ranks of one process must share the device");
+      *dst = (void*)(uintptr_t)raw;
+      return SPCG_OK;
+    }
+    CUDA_TRY(cudaIpcOpenMemHandle(dst, h, cudaIpcMemLazyEnablePeerAccess));
+    P->opened.push_back(*dst);
+    return SPCG_OK;
+  };
+  int rc;
+  std::vector<bool> sendto((size_t)R, false), recvfrom((size_t)R, false);
+  for (size_t k = 0; k < P->peers.size(); ++k) {
+    const int pk = P->peers[k];
+    if (P->send_off[k + 1] > P->send_off[k]) sendto[(size_t)pk] = true;
+    if (P->recv_off[k + 1] > P->recv_off[k]) recvfrom[(size_t)pk] = true;
+  }
+  for (int k = 0; k < R; ++k) {
+    if ((rc = open(k, B[k].h_mbox, B[k].mbox, (void**)&T.peer_mbox[k]))) return rc;
+    if (k == me) continue;
+    if (sendto[k]) {
+      if ((rc = open(k, B[k].h_hflag, B[k].hflag, (void**)&T.peer_hflag[k]))) return rc;
+      if ((rc = open(k, B[k].h_p, B[k].p, (void**)&T.peer_p[k]))) return rc;
+      if ((rc = open(k, B[k].h_tmp, B[k].tmp, (void**)&T.peer_tmp[k]))) return rc;
+    }
+    if (recvfrom[k] && (rc = open(k, B[k].h_q, B[k].q, (void**)&T.peer_q[k]))) return rc;
+  }
+  T.nrecv = 0;
+  T.nsendpeers = 0;
+  for (int k = 0; k < R; ++k) {
+    if (recvfrom[k]) T.recv_from[T.nrecv++] = k;
+    if (sendto[k]) T.send_to[T.nsendpeers++] = k;
+  }
+  // sender tables
+  const long long total = P->send_off.back();
+  std::vector<int> speer((size_t)std::max(1LL, total));
+  std::vector<long long> sdst((size_t)std::max(1LL, total));
+  std::vector<SendRun> runs;
+  for (size_t k = 0; k < P->peers.size(); ++k) {
+    const int pk = P->peers[k];
+    const long long roff = B[pk].recv_off_by_src[me];
+    if (P->send_off[k + 1] > P->send_off[k] && roff < 0)
+      return fail(SPCG_ERR_ARG, "rank " + std::to_string(pk) + " expects no values from rank " +
+                                    std::to_string(me));
+    for (long long s = P->send_off[k]; s < P->send_off[k + 1]; ++s) {
+      speer[(size_t)s] = pk;
+      sdst[(size_t)s] = B[pk].nloc + roff + (s - P->send_off[k]);
+      const int row = P->send_idx[(size_t)s];
+      if (!runs.empty() && runs.back().peer == pk && runs.back().hi == row &&
+          runs.back().dst + (runs.back().hi - runs.back().lo) == sdst[(size_t)s]) {
+        runs.back().hi++;
+      } else {
+        runs.push_back(SendRun{row, row + 1, pk, 0, sdst[(size_t)s]});
+      }
+    }
+  }
+  P->nruns = (int)runs.size();
+  if ((rc = dmalloc((void**)&P->runs, sizeof(SendRun) * std::max<size_t>(1, runs.size()), nullptr)) ||
+      (rc = dmalloc((void**)&P->send_peer, sizeof(int) * speer.size(), nullptr)) ||
+      (rc = dmalloc((void**)&P->send_dst, sizeof(long long) * sdst.size(), nullptr)))
+    return rc;
+  if (!runs.empty())
+    CUDA_TRY(cudaMemcpy(P->runs, runs.data(), sizeof(SendRun) * runs.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(P->send_peer, speer.data(), sizeof(int) * speer.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(P->send_dst, sdst.data(), sizeof(long long) * sdst.size(), cudaMemcpyHostToDevice));
+  if (total > 0)
+    CUDA_TRY(cudaMemcpy(P->m->dw.send_idx, P->send_idx.data(), sizeof(int) * (size_t)total,
+                        cudaMemcpyHostToDevice));
+  // reverse halo: ghost h (a halo column owned by peer k) -> k's local row
+  const std::vector<long long>& halo = P->m->halo;
+  P->nghost = (long long)halo.size();
+  std::vector<int> gpeer((size_t)std::max(1LL, P->nghost)), gdst((size_t)std::max(1LL, P->nghost));
+  for (size_t k = 0; k < P->peers.size(); ++k)
+    for (long long h = P->recv_off[k]; h < P->recv_off[k + 1]; ++h) {
+      gpeer[(size_t)h] = P->peers[k];
+      gdst[(size_t)h] = (int)(halo[(size_t)h] - B[P->peers[k]].row0);
+    }
+  if ((rc = dmalloc((void**)&P->ghost_peer, sizeof(int) * gpeer.size(), nullptr)) ||
+      (rc = dmalloc((void**)&P->ghost_dst, sizeof(int) * gdst.size(), nullptr)))
+    return rc;
+  CUDA_TRY(cudaMemcpy(P->ghost_peer, gpeer.data(), sizeof(int) * gpeer.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(P->ghost_dst, gdst.data(), sizeof(int) * gdst.size(), cudaMemcpyHostToDevice));
+  P->connected = true;
+  return SPCG_OK;
+}
+
+// DistArgs of a connected plan for one solve.
+int plan_args(spcg_dist_plan_s* P, int kf, const double* b, const double* x0, double* x,
+              double* hist, const spcg_cg_options* o, DistArgs& A) {
+  spcg_matrix_s* m = P->m;
+  A = base_args(m, kf, b, x0, x, hist, o);
+  if (!P->thalo) {
+    int rc;
+    if ((rc = build_thalo(m, kf, &P->thalo))) return rc;
+  }
+  const DistArgs& T = P->peer;
+  A.thalo = P->thalo;
+  A.rank = P->rank;
+  A.nranks = P->nranks;
+  A.fused = 1;
+  A.nrecv = T.nrecv;
+  memcpy(A.recv_from, T.recv_from, sizeof(A.recv_from));
+  A.mbox = P->mbox;
+  A.hflag = P->hflag;
+  memcpy(A.peer_mbox, T.peer_mbox, sizeof(A.peer_mbox));
+  memcpy(A.peer_hflag, T.peer_hflag, sizeof(A.peer_hflag));
+  memcpy(A.peer_p, T.peer_p, sizeof(A.peer_p));
+  memcpy(A.peer_tmp, T.peer_tmp, sizeof(A.peer_tmp));
+  memcpy(A.peer_q, T.peer_q, sizeof(A.peer_q));
+  A.nsendpeers = T.nsendpeers;
+  memcpy(A.send_to, T.send_to, sizeof(A.send_to));
+  A.nruns = P->nruns;
+  A.runs = P->runs;
+  A.send_total = P->send_off.back();
+  A.send_idx = m->dw.send_idx;
+  A.send_peer = P->send_peer;
+  A.send_dst = P->send_dst;
+  A.nghost = P->nghost;
+  A.ghost_peer = P->ghost_peer;
+  A.ghost_dst = P->ghost_dst;
+  return SPCG_OK;
+}
+
+template <int FMT>
+int group_solve_t(int nranks, spcg_dist_plan_s* const* plans, const double* const* b,
+                  const double* const* x0, double* const* x, double* hist,
+                  const spcg_cg_options* o, spcg_cg_result* out, cudaStream_t st,
+                  DistArgs* d_args) {
+  std::vector<DistArgs> hA((size_t)nranks);
+  std::vector<StepState*> hs((size_t)nranks);
+  std::vector<spcg_matrix_s*> ms((size_t)nranks);
+  int rc;
+  for (int r = 0; r < nranks; ++r) {
+    spcg_dist_plan_s* P = plans[r];
+    if ((rc = plan_args(P, FMT, b[r], x0 ? x0[r] : nullptr, x[r], r == 0 ? hist : nullptr, o,
+                        hA[(size_t)r])))
+      return rc;
+    hs[(size_t)r] = P->m->dw.h_S;
+    ms[(size_t)r] = P->m;
+  }
+  for (int r = 1; r < nranks; ++r)
+    if (hA[(size_t)r].M.wide != hA[0].M.wide)
+      return fail(SPCG_ERR_UNSUPPORTED, "ranks of one launch need the same tile layout");
+  CUDA_TRY(cudaMemcpyAsync(d_args, hA.data(), sizeof(DistArgs) * (size_t)nranks,
+                           cudaMemcpyHostToDevice, st));
+  return run_dist<FMT>(hA, d_args, nullptr, hA[0].M, o, hs, ms, out, st);
+}
+
+int plan_solve_checked(int nranks, spcg_dist_plan_s* const* plans, const double* const* b,
+                       const double* const* x0, double* const* x, double* hist,
+                       const spcg_cg_options* o, spcg_cg_result* out, cudaStream_t st) {
+  if (!(o->tol > 0.0)) return fail(SPCG_ERR_ARG, "tol must be > 0");
+  if (o->record_history && !hist) return fail(SPCG_ERR_ARG, "record_history needs a history buffer");
+  const int kf = kfmt_of(plans[0]->m, o->accumulation);
+  for (int r = 0; r < nranks; ++r) {
+    spcg_dist_plan_s* P = plans[r];
+    if (!P->connected) return fail(SPCG_ERR_ARG, "plan not connected (spcg_dist_plan_connect)");
+    if (kfmt_of(P->m, o->accumulation) != kf) return fail(SPCG_ERR_ARG, "ranks differ in format");
+    if (int rc = on_device(P->m->device)) return rc;
+  }
+  if (kf == K_CSC && plans[0]->nranks > 1) return fail(SPCG_ERR_UNSUPPORTED, "sharded CSC is not supported");
+  if (kf == K_SCSR_PRIV && !plans[0]->m->hasB) return fail(SPCG_ERR_UNSUPPORTED, "SCSR needs its L^T rows");
+  // the launch's DistArgs array: the plan's own slot for one rank, a
+  // temporary one for a group
+  DistArgs* d_args = plans[0]->d_args;
+  if (nranks > 1) {
+    int rc;
+    if ((rc = dmalloc((void**)&d_args, sizeof(DistArgs) * (size_t)nranks, nullptr))) return rc;
+  }
+  int rc;
+  switch (kf) {
+    case K_CSR: rc = group_solve_t<K_CSR>(nranks, plans, b, x0, x, hist, o, out, st, d_args); break;
+    case K_SCSR_PRIV:
+      rc = group_solve_t<K_SCSR_PRIV>(nranks, plans, b, x0, x, hist, o, out, st, d_args);
+      break;
+    case K_SCSR_ATOMIC:
+      rc = group_solve_t<K_SCSR_ATOMIC>(nranks, plans, b, x0, x, hist, o, out, st, d_args);
+      break;
+    default: rc = group_solve_t<K_CSC>(nranks, plans, b, x0, x, hist, o, out, st, d_args); break;
+  }
+  if (nranks > 1) {
+    cudaStreamSynchronize(st);
+    cudaFree(d_args);
+  }
+  return rc;
 }

@@ -13,6 +13,8 @@
 #include <vector>
 
 #include <dlfcn.h>
+#include <unistd.h>
+#include <cstddef>
 #include <nccl.h>
 
 #include "../../include/spcg_b200.h"
@@ -102,17 +104,18 @@ int dev_info(DevInfo** out) {
     if ((rc = occupancy(spmv_kernel<K_SCSR_PRIV>, &t))) return rc;
     if ((rc = occupancy(spmv_kernel<K_CSC>, &t))) return rc;
     // (these calls also raise each kernel's dynamic shared-memory limit)
-    if ((rc = occupancy(dist_spmv_pq<K_CSR>, &t))) return rc;
-    if ((rc = occupancy(dist_spmv_pq<K_CSR, true>, &t))) return rc;
-    if ((rc = occupancy(dist_spmv<K_CSR, true>, &t))) return rc;
     if ((rc = occupancy(spmv_kernel<K_CSR, true>, &t))) return rc;
-    if ((rc = occupancy(dist_spmv_pq<K_SCSR_PRIV>, &t))) return rc;
-    if ((rc = occupancy(dist_spmv_pq<K_SCSR_ATOMIC>, &t))) return rc;
-    if ((rc = occupancy(dist_spmv_pq<K_CSC>, &t))) return rc;
-    if ((rc = occupancy(dist_spmv<K_SCSR_ATOMIC>, &t))) return rc;
-    if ((rc = occupancy(dist_spmv<K_CSC>, &t))) return rc;
-    if ((rc = occupancy(dist_spmv<K_CSR>, &t))) return rc;
-    if ((rc = occupancy(dist_spmv<K_SCSR_PRIV>, &t))) return rc;
+#define SPCG_OCC_DIST(F, W)                                                    \
+  if ((rc = occupancy(dist_spmv_pq<F, W, false>, &t))) return rc;              \
+  if ((rc = occupancy(dist_spmv_pq<F, W, true>, &t))) return rc;               \
+  if ((rc = occupancy(dist_spmv<F, W, false>, &t))) return rc;                 \
+  if ((rc = occupancy(dist_spmv<F, W, true>, &t))) return rc;
+    SPCG_OCC_DIST(K_CSR, false)
+    SPCG_OCC_DIST(K_CSR, true)
+    SPCG_OCC_DIST(K_SCSR_PRIV, false)
+    SPCG_OCC_DIST(K_SCSR_ATOMIC, false)
+    SPCG_OCC_DIST(K_CSC, false)
+#undef SPCG_OCC_DIST
     if (br < 1 || bp < 1) return fail(SPCG_ERR_CUDA, "CG kernel does not fit on an SM");
     d.coop_res = std::min(br * d.sms, 32 * kPollWarps * kPollPer);
     d.spmv_grid = bp * d.sms;
@@ -179,6 +182,7 @@ struct DistWorkspace {
   // [chunk buffer][A0 A1 B0 B1 C0 C1][iteration]: per-pass timing (opts.timing:
   // 1 = pass A only, 2 = all three passes for the spmv/dot/axpy split)
   cudaEvent_t tev[2][6][16] = {};
+  DistArgs* args = nullptr;  // device copy of the rank's DistArgs (host transports)
 };
 
 }  // namespace
@@ -633,6 +637,69 @@ int spcg_dist_cg_solve(spcg_matrix_t local, spcg_comm_t comm, int npeers, const 
   std::lock_guard<std::mutex> lk(local->mu);
   return do_dist_cg(local, comm, npeers, peers, recv_off, send_off, send_idx, d_b, d_x0, d_x,
                     d_hist, opts, result, (cudaStream_t)stream);
+}
+
+int spcg_dist_plan_create(spcg_matrix_t local, int rank, int nranks, int npeers,
+                          const int32_t* peers, const int64_t* recv_off, const int64_t* send_off,
+                          const int32_t* send_idx, spcg_dist_plan_t* out) {
+  if (!local || !out) return fail(SPCG_ERR_ARG, "null argument");
+  if (int rc = on_device(local->device)) return rc;
+  std::lock_guard<std::mutex> lk(local->mu);
+  return plan_create(local, rank, nranks, npeers, peers, recv_off, send_off, send_idx, out);
+}
+
+int spcg_dist_plan_destroy(spcg_dist_plan_t plan) {
+  if (!plan) return SPCG_OK;
+  cudaDeviceSynchronize();
+  free_plan(plan);
+  delete plan;
+  return SPCG_OK;
+}
+
+int spcg_dist_plan_export(spcg_dist_plan_t plan, unsigned char* blob) {
+  if (!plan || !blob) return fail(SPCG_ERR_ARG, "null argument");
+  if (int rc = on_device(plan->m->device)) return rc;
+  return plan_export(plan, blob);
+}
+
+int spcg_dist_plan_connect(spcg_dist_plan_t plan, const unsigned char* blobs) {
+  if (!plan || !blobs) return fail(SPCG_ERR_ARG, "null argument");
+  if (int rc = on_device(plan->m->device)) return rc;
+  std::lock_guard<std::mutex> lk(plan->m->mu);
+  return plan_connect(plan, blobs);
+}
+
+int spcg_dist_plan_solve(spcg_dist_plan_t plan, const double* d_b, const double* d_x0, double* d_x,
+                         double* d_hist, const spcg_cg_options* opts, spcg_cg_result* result,
+                         void* stream) {
+  if (!plan || !opts || !result) return fail(SPCG_ERR_ARG, "null argument");
+  if (plan->m->n > 0 && (!d_b || !d_x)) return fail(SPCG_ERR_ARG, "null vector");
+  std::lock_guard<std::mutex> lk(plan->m->mu);
+  spcg_dist_plan_s* P[1] = {plan};
+  const double* b[1] = {d_b};
+  const double* x0[1] = {d_x0};
+  double* x[1] = {d_x};
+  return plan_solve_checked(1, P, b, d_x0 ? x0 : nullptr, x, d_hist, opts, result,
+                            (cudaStream_t)stream);
+}
+
+int spcg_dist_group_solve(int nranks, spcg_dist_plan_t* plans, const double* const* d_b,
+                          const double* const* d_x0, double* const* d_x, double* d_hist,
+                          const spcg_cg_options* opts, spcg_cg_result* results, void* stream) {
+  if (nranks < 1 || !plans || !d_b || !d_x || !opts || !results)
+    return fail(SPCG_ERR_ARG, "null argument");
+  for (int r = 0; r < nranks; ++r) {
+    if (!plans[r] || plans[r]->rank != r || plans[r]->nranks != nranks)
+      return fail(SPCG_ERR_ARG, "plans[r] must be rank r of this group");
+    if (plans[r]->m->n > 0 && (!d_b[r] || !d_x[r])) return fail(SPCG_ERR_ARG, "null vector");
+  }
+  if (d_x0) {
+    int given = 0;
+    for (int r = 0; r < nranks; ++r) given += d_x0[r] != nullptr || plans[r]->m->n == 0;
+    if (given != nranks) return fail(SPCG_ERR_ARG, "x0 must be given for every rank or none");
+  }
+  return plan_solve_checked(nranks, plans, d_b, d_x0, d_x, d_hist, opts, results,
+                            (cudaStream_t)stream);
 }
 
 }  // extern "C"

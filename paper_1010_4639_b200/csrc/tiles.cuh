@@ -73,6 +73,7 @@ struct MatView {
   int tree;              // split long lines: per-lane partial sums + a fixed shuffle tree
                          // (reassociated, deterministic) instead of the in-order sum
   int wide;              // tiles may exceed kBlock lines (launch the WIDE instantiation)
+  int cta0, ncta;        // CTAs [cta0, cta0 + ncta) work this view (ncta 0: the grid)
 };
 
 struct StageMeta {
@@ -95,12 +96,17 @@ struct __align__(16) Smem {
   double bcast;
 };
 
+__device__ __forceinline__ int view_cta(const MatView& M) { return (int)blockIdx.x - M.cta0; }
+__device__ __forceinline__ int view_ctas(const MatView& M) {
+  return M.ncta ? M.ncta : (int)gridDim.x;
+}
 __device__ __forceinline__ int my_tile(const MatView& M, int j) {
-  const int t = blockIdx.x + j * gridDim.x;
+  const int t = view_cta(M) + j * view_ctas(M);
   return M.rev ? M.ntiles - 1 - t : t;
 }
-__device__ __forceinline__ int my_tile_count(int ntiles) {
-  return (ntiles > (int)blockIdx.x) ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+__device__ __forceinline__ int my_tile_count(const MatView& M) {
+  const int b = view_cta(M), g = view_ctas(M);
+  return (M.ntiles > b) ? (M.ntiles - 1 - b) / g + 1 : 0;
 }
 
 // Tile descriptor(s), fetched ahead of the issue so thread 0 never waits on
@@ -210,7 +216,7 @@ struct Pipe {
 template <bool TWO>
 __device__ __forceinline__ void pipe_start(Pipe& P, Smem& sm, const MatView& M,
                                            bool allow_resident = true) {
-  P.m = my_tile_count(M.ntiles);
+  P.m = my_tile_count(M);
   P.resident = allow_resident && P.m <= kStages;
   P.c = 0;
 #if SPCG_TRACE

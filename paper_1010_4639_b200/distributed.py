@@ -197,14 +197,23 @@ class Comm:
             pass
 
 
-def torch_host_transport():
+def torch_host_transport(rank_order: bool = False):
     """(allreduce, sendrecv) callables for Comm.host over the default
-    torch.distributed process group (any backend, e.g. gloo on CPU tensors)."""
+    torch.distributed process group (any backend, e.g. gloo on CPU tensors).
+    rank_order: sum the ranks' partials in rank order (all-gather + ordered
+    sum), the order of the device-initiated transport's mailbox sum."""
     import torch
     import torch.distributed as dist
 
     def allreduce(a):
         t = torch.from_numpy(np.ascontiguousarray(a))
+        if rank_order:
+            parts = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+            dist.all_gather(parts, t)
+            acc = parts[0].numpy().copy()
+            for q in parts[1:]:
+                acc = acc + q.numpy()
+            return acc
         dist.all_reduce(t)
         return t.numpy()
 
@@ -269,6 +278,69 @@ class ShardedMatrix:
         return ShardedMatrix(dm, int(bounds[rank]), int(bounds[rank + 1]), int(bounds[-1]), halo,
                              plan)
 
+    @staticmethod
+    def _stencil_rows(kind, dims, fmt, bounds, rank):
+        from .device import DeviceMatrix
+
+        kinds = {"poisson2d": N.GEN_POISSON2D, "poisson3d": N.GEN_POISSON3D,
+                 "stencil27": N.GEN_STENCIL27}
+        d = list(dims) + [1] * (3 - len(dims))
+        h = ctypes.c_void_p()
+        N.check(N.load().spcg_matrix_generate_rows(kinds[kind], DeviceMatrix.FORMATS[fmt], d[0], d[1],
+                                                   d[2], int(bounds[rank]), int(bounds[rank + 1]),
+                                                   ctypes.byref(h)), "spcg_matrix_generate_rows")
+        dm = DeviceMatrix(h.value, DeviceMatrix.FORMATS[fmt], 0, 0)
+        dm._refresh()
+        return dm
+
+    @staticmethod
+    def stencil_bounds(kind: str, dims, world: int, align_planes: bool = True) -> np.ndarray:
+        d = list(dims) + [1] * (3 - len(dims))
+        n = d[0] * d[1] * d[2]
+        plane = d[0] if kind == "poisson2d" else d[0] * d[1]
+        return row_partition(n, world, align=plane if align_planes else 1)
+
+    @classmethod
+    def group_from_stencil(cls, kind: str, dims, fmt: str, world: int,
+                           align_planes: bool = True) -> list["ShardedMatrix"]:
+        """ALL `world` shards of a stencil in this process, on the current
+        device (virtual ranks of spcg_dist_group_solve): the halo plans are
+        built from every shard's halo without a process group."""
+        bounds = cls.stencil_bounds(kind, dims, world, align_planes)
+        return cls._group_finish([cls._stencil_rows(kind, dims, fmt, bounds, r)
+                                  for r in range(world)], bounds)
+
+    @staticmethod
+    def _localize(dm):
+        lib = N.load()
+        nh = ctypes.c_int64()
+        N.check(lib.spcg_matrix_localize(dm.handle, ctypes.byref(nh)), "spcg_matrix_localize")
+        halo = np.empty(nh.value, dtype=np.int64)
+        N.check(lib.spcg_matrix_halo(dm.handle, halo.ctypes.data if halo.size else None),
+                "spcg_matrix_halo")
+        return halo
+
+    @classmethod
+    def _group_finish(cls, dms, bounds) -> list["ShardedMatrix"]:
+        halos = [cls._localize(dm) for dm in dms]
+        wants = []
+        for h in halos:
+            owners = np.searchsorted(bounds, h, side="right") - 1
+            wants.append({int(q): h[owners == q] for q in np.unique(owners)})
+        out = []
+        for r, (dm, h) in enumerate(zip(dms, halos)):
+            plan = halo_plan(h, bounds, r, lambda _w: wants)
+            out.append(ShardedMatrix(dm, int(bounds[r]), int(bounds[r + 1]), int(bounds[-1]), h,
+                                     plan))
+        return out
+
+    @classmethod
+    def group_from_host(cls, a, world: int) -> list["ShardedMatrix"]:
+        """All shards of a host CsrMatrix / SymHalfMatrix in this process."""
+        bounds = row_partition(a.n, world, a.row_start)
+        dms = [cls._host_rows(a, bounds, r) for r in range(world)]
+        return cls._group_finish(dms, bounds)
+
     @classmethod
     def from_stencil(cls, kind: str, dims, fmt: str, rank: int, world: int, all_gather_object,
                      align_planes: bool = True) -> "ShardedMatrix":
@@ -298,6 +370,13 @@ class ShardedMatrix:
         from .device import DeviceMatrix
 
         bounds = row_partition(a.n, world, a.row_start)
+        return cls._finish(cls._host_rows(a, bounds, rank), bounds, rank, all_gather_object)
+
+    @staticmethod
+    def _host_rows(a, bounds, rank):
+        from .core import CsrMatrix, SymHalfMatrix, build_csr_from_triplets
+        from .device import DeviceMatrix
+
         r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
         rs = np.ascontiguousarray(a.row_start, dtype=np.int64)
         k0, k1 = int(rs[r0]), int(rs[r1])
@@ -327,7 +406,7 @@ class ShardedMatrix:
             v.ctypes.data if v.size else None, *b_args, ctypes.byref(h)), "spcg_matrix_create_rows")
         dm = DeviceMatrix(h.value, fmt, 0, 0)
         dm._refresh()
-        return cls._finish(dm, bounds, rank, all_gather_object)
+        return dm
 
     def spmv_ext(self, x_ext):
         """y_loc = A_loc x_ext for an extended vector (own + halo values)."""
@@ -375,3 +454,134 @@ def dist_cg_solve(sm: ShardedMatrix, comm: Comm, b_loc, x0_loc=None, tol: float 
     N.check(rc, "spcg_dist_cg_solve")
     h = hist[: res.iterations].cpu().numpy() if record_history else None
     return x, res, h
+
+
+# ---- device-initiated transport (spcg_dist_plan_*) ---------------------------------
+class P2PPlan:
+    """One rank's device-initiated transport: the two scalar all-reduces of
+    every iteration through epoch-tagged mailboxes in peer memory and the
+    halo of p stored by pass C straight into the neighbours' p_ext (no host
+    collective per iteration).  Bootstrap: export() -> all-gather the blobs
+    in rank order -> connect(blobs).  Ranks sharing this process and device
+    connect by plain pointers and can be solved together in one launch per
+    pass (`group_solve`)."""
+
+    BLOB = 1024  # SPCG_P2P_BLOB_BYTES
+
+    def __init__(self, sm: "ShardedMatrix", rank: int, world: int):
+        p = sm.plan
+        self.sm, self.rank, self.world = sm, rank, world
+        lib = N.load()
+        h = ctypes.c_void_p()
+
+        def ptr(a):
+            return a.ctypes.data if a.size else None
+
+        N.check(lib.spcg_dist_plan_create(sm.dm.handle, rank, world, p.npeers, ptr(p.peers),
+                                          ptr(p.recv_off), ptr(p.send_off), ptr(p.send_idx),
+                                          ctypes.byref(h)), "spcg_dist_plan_create")
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def export(self) -> bytes:
+        buf = (ctypes.c_ubyte * self.BLOB)()
+        N.check(N.load().spcg_dist_plan_export(self._h, buf), "spcg_dist_plan_export")
+        return bytes(buf)
+
+    def connect(self, blobs: list[bytes]):
+        if len(blobs) != self.world or any(len(b) != self.BLOB for b in blobs):
+            raise ValueError("connect needs one export blob per rank, in rank order")
+        buf = (ctypes.c_ubyte * (self.BLOB * self.world)).from_buffer_copy(b"".join(blobs))
+        N.check(N.load().spcg_dist_plan_connect(self._h, buf), "spcg_dist_plan_connect")
+
+    def solve(self, b_loc, x0_loc=None, tol: float = 1e-10, max_iter: int | None = None,
+              record_history: bool = False, recompute_final_residual: bool = True,
+              timing: bool = False, accumulation: str = "privatized"):
+        """This rank's share of the solve (one process per GPU)."""
+        import torch
+
+        sm = self.sm
+        mi = max_iter if max_iter else max(1, sm.n_global)
+        x = torch.empty(sm.nloc, dtype=torch.float64, device=b_loc.device)
+        hist = torch.empty(mi if record_history else 1, dtype=torch.float64, device=b_loc.device)
+        o = _options(tol, mi, record_history, recompute_final_residual, timing, accumulation)
+        res = N.CgResultC()
+        rc = N.load().spcg_dist_plan_solve(
+            self._h, b_loc.data_ptr(), x0_loc.data_ptr() if x0_loc is not None else None,
+            x.data_ptr(), hist.data_ptr() if record_history else None, o, res,
+            torch.cuda.current_stream().cuda_stream)
+        _raise(rc, res, "spcg_dist_plan_solve")
+        return x, res, (hist[: res.iterations].cpu().numpy() if record_history else None)
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            N.load().spcg_dist_plan_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _options(tol, mi, record_history, recompute_final_residual, timing, accumulation):
+    return N.CgOptionsC(tol=float(tol), max_iter=int(mi), record_history=int(record_history),
+                        recompute_final_residual=int(recompute_final_residual),
+                        accumulation=N.ACC_ATOMIC if accumulation == "atomic" else N.ACC_PRIVATIZED,
+                        engine=2, timing=int(timing))
+
+
+def _raise(rc, res, what):
+    from .solver import _BREAKDOWN
+
+    if rc in _BREAKDOWN:
+        raise _BREAKDOWN[rc](int(res.fail_iteration))
+    N.check(rc, what)
+
+
+def connect_all(plans: list[P2PPlan]):
+    """Connect the plans of ranks that all live in this process."""
+    blobs = [p.export() for p in plans]
+    for p in plans:
+        p.connect(blobs)
+
+
+def group_plans(shards: list["ShardedMatrix"]) -> list[P2PPlan]:
+    plans = [P2PPlan(sm, r, len(shards)) for r, sm in enumerate(shards)]
+    connect_all(plans)
+    return plans
+
+
+def group_solve(plans: list[P2PPlan], b_locs, x0_locs=None, tol: float = 1e-10,
+                max_iter: int | None = None, record_history: bool = False,
+                recompute_final_residual: bool = True, timing: bool = False,
+                accumulation: str = "privatized"):
+    """Every rank of `plans` (this process, this device) in ONE launch per
+    pass: the device-initiated protocol with all its waits inside single
+    launches.  Returns ([x_loc per rank], [CgResultC per rank], rank 0's
+    history or None)."""
+    import torch
+
+    R = len(plans)
+    n_global = plans[0].sm.n_global
+    mi = max_iter if max_iter else max(1, n_global)
+    dev = b_locs[0].device
+    xs = [torch.empty(p.sm.nloc, dtype=torch.float64, device=dev) for p in plans]
+    hist = torch.empty(mi if record_history else 1, dtype=torch.float64, device=dev)
+    o = _options(tol, mi, record_history, recompute_final_residual, timing, accumulation)
+    res = (N.CgResultC * R)()
+    P = (ctypes.c_void_p * R)(*[p.handle.value for p in plans])
+    B = (ctypes.c_void_p * R)(*[b.data_ptr() for b in b_locs])
+    X = (ctypes.c_void_p * R)(*[x.data_ptr() for x in xs])
+    X0 = (ctypes.c_void_p * R)(*[x.data_ptr() for x in x0_locs]) if x0_locs is not None else None
+    vp = ctypes.c_void_p
+    rc = N.load().spcg_dist_group_solve(
+        R, ctypes.cast(P, vp), ctypes.cast(B, vp), ctypes.cast(X0, vp) if X0 is not None else None,
+        ctypes.cast(X, vp), hist.data_ptr() if record_history else None, o, ctypes.cast(res, vp),
+        torch.cuda.current_stream().cuda_stream)
+    _raise(rc, res[0], "spcg_dist_group_solve")
+    return xs, list(res), (hist[: res[0].iterations].cpu().numpy() if record_history else None)

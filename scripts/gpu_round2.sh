@@ -1,0 +1,7 @@
+#!/bin/bash
+# full GPU suite + smoke + the default bench line (run under gpurun from the repo root)
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -q -m gpu --timeout 600 -p no:cacheprovider -rs > gpurun_out/pytest_gpu.log 2>&1; echo pytest_exit=$? >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke_exit=$? >> gpurun_out/smoke.log
+timeout 1200 python bench.py > gpurun_out/bench.log 2> gpurun_out/bench.err; echo bench_exit=$? >> gpurun_out/bench.err
+tail -3 gpurun_out/pytest_gpu.log; tail -1 gpurun_out/smoke.log; tail -2 gpurun_out/bench.err
