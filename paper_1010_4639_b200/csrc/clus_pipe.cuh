@@ -410,6 +410,12 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     __syncthreads();
   }
 
+  // per-phase trace (A.trace set: SPCG_TRACE / SPCG_CLUS_DEBUG): thread 0 of
+  // every CTA accumulates [partials+SpMV, wait A, send n + barrier B, scalars
+  // + update + halo + sync] ns, then records its SM id and start / end times
+  const bool tr = A.trace != nullptr && tid == 0;
+  unsigned long long tph[4] = {0, 0, 0, 0};
+  const unsigned long long tkern0 = tr ? globaltimer_ns() : 0;
   double alpha = 0.0, beta = 0.0;
   // deferred inter-cluster halo update: CSR/CSC 4.44 -> 3.95 us/iteration on
   // F; the two-segment (SCSR) build ran 10.3 us with it (unexplained, see
@@ -421,6 +427,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   for (long long it = 0; max_it > 0; ++it) {
     const int bank = (int)(epoch++ & 1u), buf = (int)(it & 1);
     const uint32_t tag = epoch;
+    const unsigned long long t0 = tr ? globaltimer_ns() : 0;
     double g = 0.0, d = 0.0;
 #pragma unroll
     for (int k = 0; k < NS; ++k)
@@ -449,7 +456,9 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     }
     double ng[NS];
     spmv(ng);  // n = A w, overlapped with the all-reduce
+    const unsigned long long t1 = tr ? globaltimer_ns() : 0;
     cluster_wait_acq();
+    const unsigned long long t2 = tr ? globaltimer_ns() : 0;
     if (comm && K > 1 && me == 0) exchange(bank, tag, SPCG_PIPE_FENCED);
 #if SPCG_PIPE_LATE_REMOTE
     // (A/B only) the tagged global halo stored after arrive(B), so the
@@ -464,6 +473,12 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     cluster_arrive_rel();  // B: cluster totals and intra-cluster halo n
 #endif
     cluster_wait_acq();
+    const unsigned long long t3 = tr ? globaltimer_ns() : 0;
+    if (tr) {
+      tph[0] += t1 - t0;
+      tph[1] += t2 - t1;
+      tph[2] += t3 - t2;
+    }
     double g_new, d_new;
     totals(bank, g_new, d_new);
     if (it >= 1) {
@@ -548,6 +563,16 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     pbuf = buf;
     ptag = tag;
     __syncthreads();
+    if (tr) tph[3] += globaltimer_ns() - t3;
+  }
+  if (tr) {
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    for (int ph = 0; ph < 4; ++ph) A.trace[gme * 8 + ph] = tph[ph];
+    A.trace[gme * 8 + 4] = smid;
+    A.trace[gme * 8 + 5] = tkern0;
+    A.trace[gme * 8 + 6] = globaltimer_ns();
+    A.trace[gme * 8 + 7] = (unsigned long long)iterations;
   }
 
   if (status != ST_OK) {

@@ -67,8 +67,22 @@ struct SendRun {
   long long dst;
 };
 
-// Everything one rank's kernels need; lives in device memory (an array of
-// them for a launch over several virtual ranks).
+// Where a rank's device-transport traffic goes: its own mailbox / halo tags
+// and the peers' buffers (device memory; only the exchange steps read it).
+struct PeerTab {
+  unsigned long long* mbox;                // own mailbox [2 banks][nranks][2]
+  unsigned long long* hflag;               // own halo tags [nranks][2]
+  int recv_from[kMaxRanks];                // ranks this one receives halo values from
+  int send_to[kMaxRanks];                  // ranks this one sends halo values to
+  unsigned long long* peer_mbox[kMaxRanks];
+  unsigned long long* peer_hflag[kMaxRanks];
+  double* peer_p[kMaxRanks];               // peers' p_ext
+  double* peer_tmp[kMaxRanks];             // peers' tmp (x0 / x halos)
+  double* peer_q[kMaxRanks];               // peers' q (reverse halo)
+};
+
+// Everything one rank's kernels need (by value as a kernel parameter for a
+// single rank; an array in device memory for a launch over virtual ranks).
 struct DistArgs {
   MatView M;          // localized rows (streaming tile view)
   StepState* S;
@@ -81,31 +95,21 @@ struct DistArgs {
   double* tmp;        // extended scratch (x0 / x with their halos)
   double* hist;
   double* part;       // per-CTA partials
-  const unsigned char* thalo;  // per tile of M: gathers halo columns
   long long nloc;
   int rank, nranks;
-  int fused;          // 1: device-initiated transport (mailbox + halo push)
   int zq;             // atomic formats: pass B re-zeroes q
   int xv;             // x is 16-byte aligned
-  int nrecv;          // ranks this one receives halo values from
-  int recv_from[kMaxRanks];
   // device transport
-  unsigned long long* mbox;                // own mailbox [2 banks][nranks][2]
-  unsigned long long* hflag;               // own halo tags [nranks][2]
-  unsigned long long* peer_mbox[kMaxRanks];
-  unsigned long long* peer_hflag[kMaxRanks];
-  double* peer_p[kMaxRanks];               // peers' p_ext
-  double* peer_tmp[kMaxRanks];             // peers' tmp (x0 / x halos)
-  double* peer_q[kMaxRanks];               // peers' q (reverse halo)
-  int nsendpeers;
-  int send_to[kMaxRanks];
-  int nruns;                               // send runs (<= kRunCache: fused into pass C)
+  const PeerTab* peer;
+  const unsigned char* thalo;  // per tile of M: gathers halo columns
+  int nrecv, nsendpeers;
+  int nruns;                   // send runs (<= kRunCache: fused into pass C)
   const SendRun* runs;
-  long long send_total;                    // generic push: every send entry
+  long long send_total;        // generic push: every send entry
   const int* send_idx;
   const int* send_peer;
   const long long* send_dst;
-  long long nghost;                        // reverse halo (SCSR atomic)
+  long long nghost;            // reverse halo (SCSR atomic)
   const int* ghost_peer;
   const int* ghost_dst;
 };
@@ -128,6 +132,14 @@ __device__ __forceinline__ MatView rank_view(const DistArgs& A, const RankCta& c
   M.ncta = c.G;
   return M;
 }
+
+// Kernel transport modes (compile time): 0 = host transport, one rank, its
+// DistArgs by value (the parameter bank, as lean as a plain kernel); 1 =
+// device transport, one rank by value; 2 = device transport, several virtual
+// ranks of one launch reading their DistArgs from the device array DAs.
+#define SPCG_RANK_ARGS(MODE)                                              \
+  const RankCta c = rank_cta(MODE == 2 ? G : (int)gridDim.x);             \
+  const DistArgs& A = (MODE == 2) ? DAs[c.v] : A1;
 
 // ---- scalar steps ------------------------------------------------------------
 // op 0: after ||b||^2          op 1: after r0.r0 (start)
@@ -255,13 +267,13 @@ __device__ __noinline__ double mailbox_allreduce(const DistArgs& A, double s) {
   const unsigned long long u = (unsigned long long)__double_as_longlong(s);
   const unsigned long long w0 = (u & 0xffffffff00000000ull) | seq, w1 = (u << 32) | seq;
   for (int k = 0; k < R; ++k) {
-    unsigned long long* dst = A.peer_mbox[k] + ((size_t)bank * R + A.rank) * 2;
+    unsigned long long* dst = A.peer->peer_mbox[k] + ((size_t)bank * R + A.rank) * 2;
     st_relaxed_sys_u64(dst, w0);
     st_relaxed_sys_u64(dst + 1, w1);
   }
   double tot = 0.0;
   for (int k = 0; k < R; ++k) {
-    const unsigned long long* src = A.mbox + ((size_t)bank * R + k) * 2;
+    const unsigned long long* src = A.peer->mbox + ((size_t)bank * R + k) * 2;
     unsigned long long a, b, spins = 0;
     do {
       a = ld_relaxed_sys_u64(src);
@@ -283,7 +295,7 @@ struct RedSmem {
   double bcast;
 };
 
-template <class SM>
+template <bool FUSED, class SM>
 __device__ __forceinline__ void rank_sum(double v, SM& sm, const DistArgs& A, const RankCta& c,
                                          int op, bool post = true) {
   const double bs = block_sum(v, sm);
@@ -303,7 +315,7 @@ __device__ __forceinline__ void rank_sum(double v, SM& sm, const DistArgs& A, co
   s = block_sum(s, sm);
   if (threadIdx.x == 0) {
     S->counter = 0;
-    if (A.fused && post && op >= 0) {
+    if (FUSED && post && op >= 0) {
       S->red = mailbox_allreduce(A, s);
       scalar_step(op, S, A.hist);
     } else {
@@ -317,7 +329,7 @@ __device__ __forceinline__ void rank_sum(double v, SM& sm, const DistArgs& A, co
 __device__ __noinline__ void wait_halo(const DistArgs& A, unsigned int tag) {
   if (threadIdx.x == 0) {
     for (int i = 0; i < A.nrecv; ++i) {
-      const unsigned long long* f = A.hflag + 2 * (size_t)A.recv_from[i];
+      const unsigned long long* f = A.peer->hflag + 2 * (size_t)A.peer->recv_from[i];
       unsigned long long spins = 0;
       while ((uint32_t)ld_acquire_sys_u64(f) < tag)
         if (++spins > kP2PSpinLimit) asm volatile("trap;");
@@ -344,14 +356,14 @@ __device__ __forceinline__ void halo_done(const DistArgs& A, const RankCta& c, S
   A.S->hseq = tag;
   fence_acq_rel_sys();
   for (int i = 0; i < A.nsendpeers; ++i)
-    st_release_sys_u64(A.peer_hflag[A.send_to[i]] + 2 * (size_t)A.rank, tag);
+    st_release_sys_u64(A.peer->peer_hflag[A.peer->send_to[i]] + 2 * (size_t)A.rank, tag);
 }
 
 // ---- pass A: q = A p_ext, red = p.q partial (skipped once done) -------------
 // WIDE: the view carries wide tiles (short-row CSR); a separate
 // instantiation so the other kernels do not pay the two-line body's registers.
 // Body of pass A over rank A's view M (M carries rev / tree / the CTA range).
-template <int FMT, bool WIDE>
+template <int FMT, bool WIDE, bool FUSED>
 __device__ __forceinline__ void spmv_pq_body(const DistArgs& A, const MatView& M, const RankCta& c,
                                              int post) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -367,7 +379,7 @@ __device__ __forceinline__ void spmv_pq_body(const DistArgs& A, const MatView& M
   smem_init(sm);
   Pipe P;
   pipe_start<TWO>(P, sm, M);
-  const bool waits = A.fused && A.nrecv > 0;
+  const bool waits = FUSED && A.nrecv > 0;
   const unsigned int htag = waits ? S->hseq : 0u;
   bool have_halo = !waits;
   SrcPlain src{A.p};
@@ -403,30 +415,30 @@ __device__ __forceinline__ void spmv_pq_body(const DistArgs& A, const MatView& M
     pipe_release<TWO>(P, sm, M, s);
   }
   pipe_drain(P, sm);
-  rank_sum(pq, sm, A, c, 2, post != 0);
+  rank_sum<FUSED>(pq, sm, A, c, 2, post != 0);
 }
 
 // pass A: q = A p_ext, red = p.q partial (skipped once done).  WIDE: the
 // view carries wide tiles (short-row CSR); a separate instantiation so the
-// other kernels do not pay the two-line body's registers.  GRP = false: one
+// other kernels do not pay the two-line body's registers.  MODE 0 / 1: one
 // rank, its DistArgs passed by value (the view stays in the parameter bank;
-// the host sets M.rev / M.tree per launch); GRP = true: several virtual
-// ranks of one launch, each reading its DistArgs from DAs.
+// the host sets M.rev / M.tree per launch); MODE 2: several virtual ranks of
+// one launch, each reading its DistArgs from DAs.
 // post = 0: leave the p.q partial for dist_ghost_push (device transport,
 // single-pass SCSR with peers: uniform over the ranks of a launch)
-template <int FMT, bool WIDE, bool GRP>
+template <int FMT, bool WIDE, int MODE>
 __global__ void __launch_bounds__(kBlock, kStreamMinBlocks)
     dist_spmv_pq(const __grid_constant__ DistArgs A1, const DistArgs* __restrict__ DAs, int G,
                  int rev, int tree, int post) {
-  const RankCta c = rank_cta(G);
-  if (GRP) {
+  if (MODE == 2) {
+    const RankCta c = rank_cta(G);
     const DistArgs& A = DAs[c.v];
     MatView M = rank_view(A, c);
     M.rev = rev;
     M.tree = tree;
-    spmv_pq_body<FMT, WIDE>(A, M, c, post);
+    spmv_pq_body<FMT, WIDE, true>(A, M, c, post);
   } else {
-    spmv_pq_body<FMT, WIDE>(A1, A1.M, c, post);
+    spmv_pq_body<FMT, WIDE, MODE == 1>(A1, A1.M, rank_cta((int)gridDim.x), post);
   }
 }
 
@@ -436,25 +448,26 @@ __global__ void __launch_bounds__(kBlock, kStreamMinBlocks)
 // anyway), the ghosts are re-zeroed, and the last CTA posts pass A's p.q.
 // op = -1: a barrier after the ghost reds (x0 / true-residual SpMVs, whose
 // q the owners read next) instead of the p.q step.
-__global__ void __launch_bounds__(kElemBlock) dist_ghost_push(const DistArgs* __restrict__ DAs,
-                                                              int G, int op) {
-  const RankCta c = rank_cta(G);
-  const DistArgs& A = DAs[c.v];
+template <int MODE>
+__global__ void __launch_bounds__(kElemBlock)
+    dist_ghost_push(const __grid_constant__ DistArgs A1, const DistArgs* __restrict__ DAs, int G,
+                    int op) {
+  SPCG_RANK_ARGS(MODE)
   StepState* S = A.S;
   if (op >= 0 && S->done) return;
   double* ghost = A.q + A.nloc;
-  const long long GT = (long long)G * blockDim.x;
+  const long long GT = (long long)c.G * blockDim.x;
   for (long long h = (long long)c.lb * blockDim.x + threadIdx.x; h < A.nghost; h += GT) {
     const double v = ghost[h];
     ghost[h] = 0.0;
-    if (v != 0.0) red_add_f64(A.peer_q[A.ghost_peer[h]] + A.ghost_dst[h], v);
+    if (v != 0.0) red_add_f64(A.peer->peer_q[A.ghost_peer[h]] + A.ghost_dst[h], v);
   }
   __shared__ bool last;
   __syncthreads();
   if (threadIdx.x == 0) {
     fence_acq_rel_sys();  // the reds are visible before the p.q post
     const unsigned int t = atomicAdd(&S->counter, 1u);
-    last = (t == (unsigned)G - 1);
+    last = (t == (unsigned)c.G - 1);
   }
   __syncthreads();
   if (!last || threadIdx.x != 0) return;
@@ -481,13 +494,13 @@ __global__ void __launch_bounds__(256) dist_unpack_add(long long total, const in
 
 // q = A tmp (plain gather; initial / true residual).  Device transport: waits
 // for the halo of the push just done (number S->hseq) first.
-template <int FMT, bool WIDE>
+template <int FMT, bool WIDE, bool FUSED>
 __device__ __forceinline__ void spmv_body(const DistArgs& A, const MatView& M) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   constexpr bool TWO = (FMT == K_SCSR_PRIV);
   smem_init(sm);
-  if (A.fused && A.nrecv > 0) wait_halo(A, A.S->hseq);
+  if (FUSED && A.nrecv > 0) wait_halo(A, A.S->hseq);
   Pipe P;
   pipe_start<TWO>(P, sm, M);
   SrcPlain src{A.tmp};
@@ -512,15 +525,16 @@ __device__ __forceinline__ void spmv_body(const DistArgs& A, const MatView& M) {
   pipe_drain(P, sm);
 }
 
-template <int FMT, bool WIDE, bool GRP>
+template <int FMT, bool WIDE, int MODE>
 __global__ void __launch_bounds__(kBlock, kStreamMinBlocks)
-    dist_spmv(const __grid_constant__ DistArgs A1, const DistArgs* __restrict__ DAs, int G) {
-  const RankCta c = rank_cta(G);
-  if (GRP) {
+    dist_spmv(const __grid_constant__ DistArgs A1, const DistArgs* __restrict__ DAs, int G,
+              int /*unused: launch-macro symmetry*/) {
+  if (MODE == 2) {
+    const RankCta c = rank_cta(G);
     const DistArgs& A = DAs[c.v];
-    spmv_body<FMT, WIDE>(A, rank_view(A, c));
+    spmv_body<FMT, WIDE, true>(A, rank_view(A, c));
   } else {
-    spmv_body<FMT, WIDE>(A1, A1.M);
+    spmv_body<FMT, WIDE, MODE == 1>(A1, A1.M);
   }
 }
 
@@ -530,11 +544,12 @@ __global__ void __launch_bounds__(kBlock, kStreamMinBlocks)
 // mode 2: r -= alpha q, red = r.r         -> op 3
 // mode 3: red = |b - q|^2 (true residual) -> op 4
 // Mode 2 moves 16-byte pairs, two in flight per thread (r, q 16-B aligned).
-__global__ void __launch_bounds__(kElemBlock) dist_elem(const DistArgs* __restrict__ DAs, int G,
-                                                        int mode, int useq, int rev) {
+template <int MODE>
+__global__ void __launch_bounds__(kElemBlock)
+    dist_elem(const __grid_constant__ DistArgs A1, const DistArgs* __restrict__ DAs, int G,
+              int mode, int useq, int rev) {
   __shared__ RedSmem sm;
-  const RankCta c = rank_cta(G);
-  const DistArgs& A = DAs[c.v];
+  SPCG_RANK_ARGS(MODE)
   StepState* S = A.S;
   if (mode == 2 && S->done) return;
   const long long nloc = A.nloc;
@@ -544,7 +559,7 @@ __global__ void __launch_bounds__(kElemBlock) dist_elem(const DistArgs* __restri
   const int zq = A.zq;
   const double alpha = S->alpha;
   const long long g = (long long)c.lb * blockDim.x + threadIdx.x;
-  const long long GT = (long long)G * blockDim.x;
+  const long long GT = (long long)c.G * blockDim.x;
   double acc = 0.0;
   if (mode == 2) {
     const double na = -alpha;
@@ -600,7 +615,7 @@ __global__ void __launch_bounds__(kElemBlock) dist_elem(const DistArgs* __restri
     }
   }
   const int op = mode == 0 ? 0 : mode == 1 ? 1 : mode == 2 ? 3 : 4;
-  rank_sum(acc, sm, A, c, op);
+  rank_sum<MODE != 0>(acc, sm, A, c, op);
 }
 
 // Send runs of this rank cached in shared memory (pass C's fused halo push).
@@ -615,7 +630,7 @@ __device__ __forceinline__ void push_row(const DistArgs& A, const RunCache& rc, 
                                          double v) {
   for (int k = 0; k < rc.n; ++k) {
     const SendRun& R = rc.run[k];
-    if (i >= R.lo && i < R.hi) A.peer_p[R.peer][R.dst + (i - R.lo)] = v;
+    if (i >= R.lo && i < R.hi) A.peer->peer_p[R.peer][R.dst + (i - R.lo)] = v;
   }
 }
 
@@ -624,17 +639,18 @@ __device__ __forceinline__ void push_row(const DistArgs& A, const RunCache& rc, 
 // end; an exhausted max_iter runs its pass C).  Device transport: the new p
 // of send rows goes straight into the neighbours' halo slots (runs <=
 // kRunCache; else dist_push afterwards), then the halo tag.
-__global__ void __launch_bounds__(kElemBlock) dist_update(const DistArgs* __restrict__ DAs, int G,
-                                                          int rev) {
+template <int MODE>
+__global__ void __launch_bounds__(kElemBlock)
+    dist_update(const __grid_constant__ DistArgs A1, const DistArgs* __restrict__ DAs, int G,
+                int rev) {
   __shared__ RunCache rc;
   __shared__ RedSmem sm;
-  const RankCta c = rank_cta(G);
-  const DistArgs& A = DAs[c.v];
+  SPCG_RANK_ARGS(MODE)
   StepState* S = A.S;
   if (S->status != 0 || S->converged || S->kc >= S->k) return;
   // device transport, send runs that fit the cache (also none): the push and
   // the halo tag happen here; otherwise dist_push does both after this pass
-  const bool push = A.fused && A.nruns <= kRunCache;
+  const bool push = MODE != 0 && A.nruns <= kRunCache;
   if (threadIdx.x == 0) rc.n = push ? A.nruns : 0;
   if (threadIdx.x < kRunCache && push && (int)threadIdx.x < A.nruns) rc.run[threadIdx.x] = A.runs[threadIdx.x];
   if (push) __syncthreads();
@@ -644,7 +660,7 @@ __global__ void __launch_bounds__(kElemBlock) dist_update(const DistArgs* __rest
   double* p = A.p;
   double* x = A.x;
   const long long g = (long long)c.lb * blockDim.x + threadIdx.x;
-  const long long GT = (long long)G * blockDim.x;
+  const long long GT = (long long)c.G * blockDim.x;
   const long long np = nloc >> 1;
   const double2* r2 = reinterpret_cast<const double2*>(r);
   double2* p2 = reinterpret_cast<double2*>(p);
@@ -680,17 +696,18 @@ __global__ void __launch_bounds__(kElemBlock) dist_update(const DistArgs* __rest
 // 2 = x) into the neighbours' extended vectors (dst: 0 = p, 1 = tmp) over the
 // whole send list, then the halo tag.  `iter`: the p push of an iteration
 // (skipped exactly when its pass C was).
-__global__ void __launch_bounds__(kElemBlock) dist_push(const DistArgs* __restrict__ DAs, int G,
-                                                        int srcsel, int dstsel, int iter) {
+template <int MODE>
+__global__ void __launch_bounds__(kElemBlock)
+    dist_push(const __grid_constant__ DistArgs A1, const DistArgs* __restrict__ DAs, int G,
+              int srcsel, int dstsel, int iter) {
   __shared__ RedSmem sm;
-  const RankCta c = rank_cta(G);
-  const DistArgs& A = DAs[c.v];
+  SPCG_RANK_ARGS(MODE)
   StepState* S = A.S;
   if (iter && (S->status != 0 || S->converged || S->kc >= S->k || A.nruns <= kRunCache)) return;
   const double* src = srcsel == 0 ? A.p : srcsel == 1 ? A.x0 : A.x;
-  const long long GT = (long long)G * blockDim.x;
+  const long long GT = (long long)c.G * blockDim.x;
   for (long long s = (long long)c.lb * blockDim.x + threadIdx.x; s < A.send_total; s += GT) {
-    double* dst = dstsel == 0 ? A.peer_p[A.send_peer[s]] : A.peer_tmp[A.send_peer[s]];
+    double* dst = dstsel == 0 ? A.peer->peer_p[A.send_peer[s]] : A.peer->peer_tmp[A.send_peer[s]];
     dst[A.send_dst[s]] = src[A.send_idx[s]];
   }
   halo_done(A, c, sm, S->hseq + 1);
@@ -705,11 +722,12 @@ __global__ void dist_pack(long long cnt, const int* idx, const double* v, double
 
 // x = x0 (or 0) and tmp = x0 (own part of the x0 gather vector); final
 // x += alpha_K p_K of a converged solve (its pass C was skipped)
-__global__ void dist_x(const DistArgs* __restrict__ DAs, int G, int mode) {
-  const RankCta c = rank_cta(G);
-  const DistArgs& A = DAs[c.v];
+template <int MODE>
+__global__ void dist_x(const __grid_constant__ DistArgs A1, const DistArgs* __restrict__ DAs,
+                       int G, int mode) {
+  SPCG_RANK_ARGS(MODE)
   const StepState* S = A.S;
-  const long long GT = (long long)G * blockDim.x;
+  const long long GT = (long long)c.G * blockDim.x;
   const double alpha = S->alpha;
   const bool upd = S->k > 0 && S->status == 0 && S->converged;
   const bool zero_b = S->b_norm == 0.0;  // solver.py:109-118: x = 0 even for x0 != 0

@@ -497,7 +497,8 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
   if (pipe && P.ghalo)  // tags restart at 1 every solve
     CUDA_TRY(cudaMemsetAsync(P.ghalo, 0, sizeof(double) * 4 * (size_t)P.C * P.hcap, st));
   static const bool tracing = getenv("SPCG_TRACE") != nullptr;
-  if (tracing && !pipe) {
+  static const char* dbg_path = getenv("SPCG_CLUS_DEBUG");  // per-solve CTA trace lines
+  if (tracing || dbg_path) {
     CUDA_TRY(cudaMalloc((void**)&a.trace, sizeof(unsigned long long) * 8 * (size_t)P.C));
     CUDA_TRY(cudaMemsetAsync(a.trace, 0, sizeof(unsigned long long) * 8 * (size_t)P.C, st));
   }
@@ -512,6 +513,42 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
   if (r.status == ST_BAD_LAUNCH)
     return fail(SPCG_ERR_CUDA, "cluster engine: kernel ran with a different cluster shape than "
                                "planned (cluster launch attribute not honoured)");
+  if (a.trace && pipe) {
+    std::vector<unsigned long long> tv(8 * (size_t)P.C);
+    CUDA_TRY(cudaMemcpy(tv.data(), a.trace, sizeof(unsigned long long) * tv.size(),
+                        cudaMemcpyDeviceToHost));
+    cudaFree(a.trace);
+    a.trace = nullptr;
+    const double it = (double)std::max<long long>(1, r.iterations) * 1e3;
+    double mean[4] = {0, 0, 0, 0}, mx[4] = {0, 0, 0, 0};
+    unsigned long long t0 = ~0ull, t1 = 0;
+    for (int c = 0; c < P.C; ++c) {
+      for (int ph = 0; ph < 4; ++ph) {
+        mean[ph] += (double)tv[8 * c + ph] / P.C;
+        mx[ph] = std::max(mx[ph], (double)tv[8 * c + ph]);
+      }
+      t0 = std::min(t0, tv[8 * c + 5]);
+      t1 = std::max(t1, tv[8 * c + 6]);
+    }
+    if (tracing)
+      fprintf(stderr,
+              "[spcg trace] engine 6 ctas=%d cs=%d two=%d us/iter mean(max): partials+spmv %.3f(%.3f) "
+              "waitA %.3f(%.3f) send+barrierB %.3f(%.3f) update %.3f(%.3f); kernel %.1f us\n",
+              P.C, P.cs, (int)P.two, mean[0] / it, mx[0] / it, mean[1] / it, mx[1] / it,
+              mean[2] / it, mx[2] / it, mean[3] / it, mx[3] / it, (double)(t1 - t0) / 1e3);
+    if (dbg_path) {
+      if (FILE* f = fopen(dbg_path, "a")) {
+        fprintf(f, "{\"engine\": 6, \"two\": %d, \"cs\": %d, \"ms\": %.6f, \"iters\": %lld, \"ctas\": [",
+                (int)P.two, P.cs, ms, (long long)r.iterations);
+        for (int c = 0; c < P.C; ++c)
+          fprintf(f, "%s[%llu, %llu, %llu, %llu, %llu, %llu, %llu]", c ? ", " : "", tv[8 * c + 4],
+                  tv[8 * c + 5] - t0, tv[8 * c + 6] - t0, tv[8 * c + 0], tv[8 * c + 1],
+                  tv[8 * c + 2], tv[8 * c + 3]);
+        fprintf(f, "]}\n");
+        fclose(f);
+      }
+    }
+  }
   if (a.trace) {
     std::vector<unsigned long long> tv(8 * (size_t)P.C);
     CUDA_TRY(cudaMemcpy(tv.data(), a.trace, sizeof(unsigned long long) * tv.size(),

@@ -307,13 +307,15 @@ struct spcg_dist_plan_s {
   unsigned char* thalo = nullptr;
   SendRun* runs = nullptr;
   int nruns = 0;
+  int nrecv = 0, nsendpeers = 0;
   int* send_peer = nullptr;
   long long* send_dst = nullptr;
   int* ghost_peer = nullptr;
   int* ghost_dst = nullptr;
   long long nghost = 0;
   bool connected = false;
-  DistArgs peer{};                   // peer pointer tables (filled by connect)
+  PeerTab peer{};                    // peer pointer tables (filled by connect)
+  PeerTab* d_peer = nullptr;         // their device copy
   std::vector<void*> opened;         // IPC mappings to close
   DistArgs* d_args = nullptr;        // device copy for solo solves
 };
@@ -325,7 +327,7 @@ void free_plan(spcg_dist_plan_s* P) {
   P->opened.clear();
   for (void* q : {(void*)P->mbox, (void*)P->hflag, (void*)P->thalo, (void*)P->runs,
                   (void*)P->send_peer, (void*)P->send_dst, (void*)P->ghost_peer,
-                  (void*)P->ghost_dst, (void*)P->d_args})
+                  (void*)P->ghost_dst, (void*)P->d_args, (void*)P->d_peer})
     if (q) cudaFree(q);
 }
 
@@ -358,7 +360,7 @@ int run_dist(const std::vector<DistArgs>& hA, DistArgs* dA, const HaloPlan* H, c
   int rc;
   if ((rc = dev_info(&di))) return rc;
   const int nv = (int)hA.size();
-  const bool fused = hA[0].fused != 0;
+  const bool fused = hA[0].peer != nullptr;
   const bool wide = FMT == K_CSR && v.wide;
   int G = 1;
   for (const DistArgs& a : hA)
@@ -388,6 +390,32 @@ int run_dist(const std::vector<DistArgs>& hA, DistArgs* dA, const HaloPlan* H, c
     if (kAtom) CUDA_TRY(cudaMemsetAsync(hA[r].q, 0, sizeof(double) * (size_t)std::max(1LL, next), st));
   }
   const int GG = nv * G, GGE = nv * GE;
+  // kernel transport mode: 0 host transport, 1 device transport (one rank
+  // per process), 2 device transport over nv virtual ranks in one launch
+  const int mode = !fused ? 0 : (nv > 1 ? 2 : 1);
+  DistArgs a1 = hA[0];  // MODE 0 / 1: the rank's arguments by value
+  a1.M.cta0 = 0;
+  a1.M.ncta = 0;
+#define SPCG_ELEM(KERNEL, ...)                                                        \
+  do {                                                                                \
+    if (mode == 0) KERNEL<0><<<GE, kElemBlock, 0, st>>>(a1, dA, GE, __VA_ARGS__);      \
+    else if (mode == 1) KERNEL<1><<<GE, kElemBlock, 0, st>>>(a1, dA, GE, __VA_ARGS__); \
+    else KERNEL<2><<<GGE, kElemBlock, 0, st>>>(a1, dA, GE, __VA_ARGS__);              \
+    ++launches;                                                                       \
+  } while (0)
+#define SPCG_TILE(KERNEL, ...)                                                                    \
+  do {                                                                                            \
+    if (wide) {                                                                                   \
+      if (mode == 0) KERNEL<K_CSR, true, 0><<<G, kBlock, sm, st>>>(a1, dA, G, __VA_ARGS__);        \
+      else if (mode == 1) KERNEL<K_CSR, true, 1><<<G, kBlock, sm, st>>>(a1, dA, G, __VA_ARGS__);   \
+      else KERNEL<K_CSR, true, 2><<<GG, kBlock, sm, st>>>(a1, dA, G, __VA_ARGS__);                \
+    } else {                                                                                      \
+      if (mode == 0) KERNEL<FMT, false, 0><<<G, kBlock, sm, st>>>(a1, dA, G, __VA_ARGS__);         \
+      else if (mode == 1) KERNEL<FMT, false, 1><<<G, kBlock, sm, st>>>(a1, dA, G, __VA_ARGS__);    \
+      else KERNEL<FMT, false, 2><<<GG, kBlock, sm, st>>>(a1, dA, G, __VA_ARGS__);                 \
+    }                                                                                             \
+    ++launches;                                                                                   \
+  } while (0)
   StepState* S0 = hA[0].S;
   double* hist0 = hA[0].hist;
   auto host_reduce = [&](int op) -> int {  // host transports: all-reduce + scalar kernel
@@ -401,36 +429,19 @@ int run_dist(const std::vector<DistArgs>& hA, DistArgs* dA, const HaloPlan* H, c
   // halo of an own vector into the neighbours' extended `dst`
   auto halo = [&](int srcsel, int dstsel, const double* hsrc, double* hdst) -> int {
     if (fused) {
-      if (hA[0].nranks > 1) {
-        dist_push<<<GGE, kElemBlock, 0, st>>>(dA, GE, srcsel, dstsel, 0);
-        ++launches;
-      }
+      if (hA[0].nranks > 1) SPCG_ELEM(dist_push, srcsel, dstsel, 0);
       return SPCG_OK;
     }
     return halo_exchange(*H, d0, hsrc, hdst, st, &launches);
   };
-  // tile kernels: one rank -> its DistArgs by value (view in the parameter
-  // bank, rev / tree set per launch); several -> the device array
-  DistArgs a1 = hA[0];
-  a1.M.cta0 = 0;
-  a1.M.ncta = 0;
-  const bool grp = nv > 1;
   auto spmv_once = [&]() -> int {  // q = A tmp (x0 / true residual)
     // device transport: the kernel waits for the halo of the push just done
     a1.M.rev = 0;
     a1.M.tree = 0;
-    if (wide) {
-      if (grp) dist_spmv<K_CSR, true, true><<<GG, kBlock, sm, st>>>(a1, dA, G);
-      else dist_spmv<K_CSR, true, false><<<G, kBlock, sm, st>>>(a1, dA, G);
-    } else {
-      if (grp) dist_spmv<FMT, false, true><<<GG, kBlock, sm, st>>>(a1, dA, G);
-      else dist_spmv<FMT, false, false><<<G, kBlock, sm, st>>>(a1, dA, G);
-    }
-    ++launches;
+    SPCG_TILE(dist_spmv, 0);
     if (kRev) {
       if (ghosts) {
-        dist_ghost_push<<<GGE, kElemBlock, 0, st>>>(dA, GE, -1);
-        ++launches;
+        SPCG_ELEM(dist_ghost_push, -1);
       } else if (!fused) {
         int rc2;
         if ((rc2 = reverse_halo(*H, d0, hA[0].q, d0.next - hA[0].nloc, st, &launches))) return rc2;
@@ -440,19 +451,16 @@ int run_dist(const std::vector<DistArgs>& hA, DistArgs* dA, const HaloPlan* H, c
   };
   CUDA_TRY(cudaEventRecord(d0.ev0, st));
   // ||b|| (solver.py:107)
-  dist_elem<<<GGE, kElemBlock, 0, st>>>(dA, GE, 0, 0, 0);
-  ++launches;
+  SPCG_ELEM(dist_elem, 0, 0, 0);
   if ((rc = host_reduce(0))) return rc;
   // x = x0, r = b - A x0, p = r (solver.py:120-124)
-  dist_x<<<GGE, kElemBlock, 0, st>>>(dA, GE, 0);
-  ++launches;
+  SPCG_ELEM(dist_x, 0);
   const bool have_x0 = hA[0].x0 != nullptr;
   if (have_x0) {
     if ((rc = halo(1, 1, hA[0].x0, hA[0].tmp))) return rc;
     if ((rc = spmv_once())) return rc;
   }
-  dist_elem<<<GGE, kElemBlock, 0, st>>>(dA, GE, 1, have_x0 ? 1 : 0, 0);
-  ++launches;
+  SPCG_ELEM(dist_elem, 1, have_x0 ? 1 : 0, 0);
   if ((rc = host_reduce(1))) return rc;
   if ((rc = halo(0, 0, hA[0].p, hA[0].p))) return rc;
   CUDA_TRY(cudaGetLastError());
@@ -484,13 +492,7 @@ int run_dist(const std::vector<DistArgs>& hA, DistArgs* dA, const HaloPlan* H, c
       const int dirA = kAlternate ? (int)((iter_enq & 1) == 0) : 0;
       a1.M.rev = dirA;
       a1.M.tree = tree;
-      if (wide) {
-        if (grp) dist_spmv_pq<K_CSR, true, true><<<GG, kBlock, sm, st>>>(a1, dA, G, dirA, tree, post);
-        else dist_spmv_pq<K_CSR, true, false><<<G, kBlock, sm, st>>>(a1, dA, G, dirA, tree, post);
-      } else {
-        if (grp) dist_spmv_pq<FMT, false, true><<<GG, kBlock, sm, st>>>(a1, dA, G, dirA, tree, post);
-        else dist_spmv_pq<FMT, false, false><<<G, kBlock, sm, st>>>(a1, dA, G, dirA, tree, post);
-      }
+      SPCG_TILE(dist_spmv_pq, dirA, tree, post);
       if (timing) CUDA_TRY(cudaEventRecord(d0.tev[bb][1][c], st));
       int rc2;
       if (!fused) {
@@ -500,23 +502,18 @@ int run_dist(const std::vector<DistArgs>& hA, DistArgs* dA, const HaloPlan* H, c
         dist_scalar<<<1, 1, 0, st>>>(2, S0, hist0);
         ++launches;
       } else if (ghosts) {
-        dist_ghost_push<<<GGE, kElemBlock, 0, st>>>(dA, GE, 2);
-        ++launches;
+        SPCG_ELEM(dist_ghost_push, 2);
       }
       if (split) CUDA_TRY(cudaEventRecord(d0.tev[bb][2][c], st));
-      dist_elem<<<GGE, kElemBlock, 0, st>>>(dA, GE, 2, 0, kAlternate ? 1 - dirA : 0);
+      SPCG_ELEM(dist_elem, 2, 0, kAlternate ? 1 - dirA : 0);
       if (split) CUDA_TRY(cudaEventRecord(d0.tev[bb][3][c], st));
       if ((rc2 = host_reduce(3))) return rc2;
       if (split) CUDA_TRY(cudaEventRecord(d0.tev[bb][4][c], st));
-      dist_update<<<GGE, kElemBlock, 0, st>>>(dA, GE, dirA);
+      SPCG_ELEM(dist_update, dirA);
       if (split) CUDA_TRY(cudaEventRecord(d0.tev[bb][5][c], st));
       ++iter_enq;
-      launches += 3;
       if (fused) {
-        if (any_push) {
-          dist_push<<<GGE, kElemBlock, 0, st>>>(dA, GE, 0, 0, 1);
-          ++launches;
-        }
+        if (any_push) SPCG_ELEM(dist_push, 0, 0, 1);
       } else if ((rc2 = halo_exchange(*H, d0, hA[0].p, hA[0].p, st, &launches))) {
         return rc2;
       }
@@ -559,17 +556,16 @@ int run_dist(const std::vector<DistArgs>& hA, DistArgs* dA, const HaloPlan* H, c
     if (!two && (rc = enqueue_chunk(bb ^ 1))) return rc;
   }
   // a converged solve skipped its pass C: x += alpha_K p_K; then the true residual
-  dist_x<<<GGE, kElemBlock, 0, st>>>(dA, GE, 1);
-  ++launches;
+  SPCG_ELEM(dist_x, 1);
   if (o->recompute_final_residual && fin.status == 0 && fin.b_norm != 0.0) {
-    dist_x<<<GGE, kElemBlock, 0, st>>>(dA, GE, 2);
-    ++launches;
+    SPCG_ELEM(dist_x, 2);
     if ((rc = halo(2, 1, hA[0].x, hA[0].tmp))) return rc;
     if ((rc = spmv_once())) return rc;
-    dist_elem<<<GGE, kElemBlock, 0, st>>>(dA, GE, 3, 0, 0);
-    ++launches;
+    SPCG_ELEM(dist_elem, 3, 0, 0);
     if ((rc = host_reduce(4))) return rc;
   }
+#undef SPCG_ELEM
+#undef SPCG_TILE
   CUDA_TRY(cudaEventRecord(d0.ev1, st));
   for (int r = 0; r < nv; ++r)
     CUDA_TRY(cudaMemcpyAsync(h_state[r], hA[r].S, sizeof(StepState), cudaMemcpyDeviceToHost, st));
@@ -791,7 +787,9 @@ int plan_connect(spcg_dist_plan_s* P, const unsigned char* blobs) {
                                     std::to_string(k) + " of " + std::to_string(R));
   }
   const int mypid = (int)getpid();
-  DistArgs& T = P->peer;
+  PeerTab& T = P->peer;
+  T.mbox = P->mbox;
+  T.hflag = P->hflag;
   auto open = [&](int k, const cudaIpcMemHandle_t& h, uint64_t raw, void** dst) -> int {
     if (k == me || B[k].pid == mypid) {
       if (B[k].device != P->m->device)
@@ -820,12 +818,14 @@ int plan_connect(spcg_dist_plan_s* P, const unsigned char* blobs) {
     }
     if (recvfrom[k] && (rc = open(k, B[k].h_q, B[k].q, (void**)&T.peer_q[k]))) return rc;
   }
-  T.nrecv = 0;
-  T.nsendpeers = 0;
+  P->nrecv = 0;
+  P->nsendpeers = 0;
   for (int k = 0; k < R; ++k) {
-    if (recvfrom[k]) T.recv_from[T.nrecv++] = k;
-    if (sendto[k]) T.send_to[T.nsendpeers++] = k;
+    if (recvfrom[k]) T.recv_from[P->nrecv++] = k;
+    if (sendto[k]) T.send_to[P->nsendpeers++] = k;
   }
+  if ((rc = dmalloc((void**)&P->d_peer, sizeof(PeerTab), nullptr))) return rc;
+  CUDA_TRY(cudaMemcpy(P->d_peer, &T, sizeof(PeerTab), cudaMemcpyHostToDevice));
   // sender tables
   const long long total = P->send_off.back();
   std::vector<int> speer((size_t)std::max(1LL, total));
@@ -888,22 +888,12 @@ int plan_args(spcg_dist_plan_s* P, int kf, const double* b, const double* x0, do
     int rc;
     if ((rc = build_thalo(m, kf, &P->thalo))) return rc;
   }
-  const DistArgs& T = P->peer;
   A.thalo = P->thalo;
   A.rank = P->rank;
   A.nranks = P->nranks;
-  A.fused = 1;
-  A.nrecv = T.nrecv;
-  memcpy(A.recv_from, T.recv_from, sizeof(A.recv_from));
-  A.mbox = P->mbox;
-  A.hflag = P->hflag;
-  memcpy(A.peer_mbox, T.peer_mbox, sizeof(A.peer_mbox));
-  memcpy(A.peer_hflag, T.peer_hflag, sizeof(A.peer_hflag));
-  memcpy(A.peer_p, T.peer_p, sizeof(A.peer_p));
-  memcpy(A.peer_tmp, T.peer_tmp, sizeof(A.peer_tmp));
-  memcpy(A.peer_q, T.peer_q, sizeof(A.peer_q));
-  A.nsendpeers = T.nsendpeers;
-  memcpy(A.send_to, T.send_to, sizeof(A.send_to));
+  A.peer = P->d_peer;
+  A.nrecv = P->nrecv;
+  A.nsendpeers = P->nsendpeers;
   A.nruns = P->nruns;
   A.runs = P->runs;
   A.send_total = P->send_off.back();

@@ -106,10 +106,12 @@ int dev_info(DevInfo** out) {
     // (these calls also raise each kernel's dynamic shared-memory limit)
     if ((rc = occupancy(spmv_kernel<K_CSR, true>, &t))) return rc;
 #define SPCG_OCC_DIST(F, W)                                                    \
-  if ((rc = occupancy(dist_spmv_pq<F, W, false>, &t))) return rc;              \
-  if ((rc = occupancy(dist_spmv_pq<F, W, true>, &t))) return rc;               \
-  if ((rc = occupancy(dist_spmv<F, W, false>, &t))) return rc;                 \
-  if ((rc = occupancy(dist_spmv<F, W, true>, &t))) return rc;
+  if ((rc = occupancy(dist_spmv_pq<F, W, 0>, &t))) return rc;                  \
+  if ((rc = occupancy(dist_spmv_pq<F, W, 1>, &t))) return rc;                  \
+  if ((rc = occupancy(dist_spmv_pq<F, W, 2>, &t))) return rc;                  \
+  if ((rc = occupancy(dist_spmv<F, W, 0>, &t))) return rc;                     \
+  if ((rc = occupancy(dist_spmv<F, W, 1>, &t))) return rc;                     \
+  if ((rc = occupancy(dist_spmv<F, W, 2>, &t))) return rc;
     SPCG_OCC_DIST(K_CSR, false)
     SPCG_OCC_DIST(K_CSR, true)
     SPCG_OCC_DIST(K_SCSR_PRIV, false)
