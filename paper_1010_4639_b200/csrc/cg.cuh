@@ -101,7 +101,10 @@ __device__ __forceinline__ double grid_allreduce(double v, Smem& sm, unsigned lo
     for (int u = 0; u < kPollPer; ++u) pend[u] = base + 32 * kPollWarps * u < (int)gridDim.x;
     bool any = true;
     unsigned long long spins = 0;
-    while (any) {
+    // warp-uniform loop (every lane until the warp's last slot is in): a
+    // divergent spin let finished lanes wait ~7 us at the reconvergence
+    // point (profiles/r02/bimodal.md)
+    while (__any_sync(0xffffffffu, any)) {
 #pragma unroll
       for (int u = 0; u < kPollPer; ++u)
         if (pend[u])
@@ -114,7 +117,7 @@ __device__ __forceinline__ double grid_allreduce(double v, Smem& sm, unsigned lo
           any |= pend[u];
         }
       if (++spins > kSpinLimit) asm volatile("trap;");
-      if (kPollSleepNs && any) __nanosleep(kPollSleepNs);
+      if (kPollSleepNs && __any_sync(0xffffffffu, any)) __nanosleep(kPollSleepNs);
     }
     double s = 0.0;
 #pragma unroll

@@ -72,7 +72,7 @@ __device__ __forceinline__ void grid_allreduce2(double& v0, double& v1, Smem& sm
     for (int u = 0; u < kPollPer; ++u) pend[u] = base + 32 * kPollWarps * u < (int)gridDim.x;
     bool any = true;
     unsigned long long spins = 0;
-    while (any) {
+    while (__any_sync(0xffffffffu, any)) {  // warp-uniform (cg.cuh grid_allreduce)
 #pragma unroll
       for (int u = 0; u < kPollPer; ++u)
         if (pend[u]) {
@@ -89,7 +89,7 @@ __device__ __forceinline__ void grid_allreduce2(double& v0, double& v1, Smem& sm
           any |= pend[u];
         }
       if (++spins > kSpinLimit) asm volatile("trap;");
-      if (kPollSleepNs && any) __nanosleep(kPollSleepNs);
+      if (kPollSleepNs && __any_sync(0xffffffffu, any)) __nanosleep(kPollSleepNs);
     }
     double s0 = 0.0, s1 = 0.0;
 #pragma unroll

@@ -46,6 +46,9 @@ constexpr int kClusSlicesPerWarp = 2048 / kClusThreads;
 constexpr int kClusMaxRows = kClusWarps * kClusSlicesPerWarp * 32;  // 2048 per CTA
 constexpr int kClusMax = 16;      // CTAs in one cluster (non-portable above 8)
 constexpr int kClusGridMax = 256;  // CTAs of a multi-cluster grid (K clusters of 8)
+#ifndef SPCG_CLUS_POST_FENCE
+#define SPCG_CLUS_POST_FENCE 0  // (A/B) fence after the leader's post
+#endif
 constexpr int kClusSlotWords = 32;  // 256-byte global slot per cluster (own L2 line pair)
 
 struct ClusCta {
@@ -293,26 +296,38 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
         dst[1] = (u0 << 32) | tag;
         dst[2] = (u1 & 0xffffffff00000000ull) | tag;
         dst[3] = (u1 << 32) | tag;
+#if SPCG_CLUS_POST_FENCE
+        // performed before this warp starts polling (see clus_pipe.cuh:
+        // an unfenced post could stay invisible to the pollers for ~6.5 us)
+        fence_acq_rel_gpu();
+#endif
       }
       if (me == 0 && wp == 0) {
         double c0 = 0.0, c1 = 0.0;
-        if (lane < K) {
-          const volatile unsigned long long* src = gb + kClusSlotWords * lane;
-          unsigned long long a, b, c, d, spins = 0;
-          for (;;) {
-            // spin on the last-written word only (one load per round keeps
-            // the pollers' pressure on the slot lines low), then validate all
-            d = src[3];
-            if ((uint32_t)d == tag) {
-              a = src[0];
-              b = src[1];
-              c = src[2];
-              if ((uint32_t)a == tag && (uint32_t)b == tag && (uint32_t)c == tag) break;
+        {
+          // warp-uniform poll (see clus_pipe.cuh: a divergent spin loop let
+          // an early leader finish ~7 us after its last slot was visible)
+          const volatile unsigned long long* src = gb + kClusSlotWords * (lane < K ? lane : 0);
+          unsigned long long a = 0, b = 0, c = 0, d = 0, spins = 0;
+          bool ok = lane >= K;
+          while (!__all_sync(0xffffffffu, ok)) {
+            if (!ok) {
+              // spin on the last-written word only (one load per round keeps
+              // the pollers' pressure on the slot lines low), then validate all
+              d = src[3];
+              if ((uint32_t)d == tag) {
+                a = src[0];
+                b = src[1];
+                c = src[2];
+                ok = (uint32_t)a == tag && (uint32_t)b == tag && (uint32_t)c == tag;
+              }
             }
             if (++spins > kSpinLimit) asm volatile("trap;");
           }
-          c0 = __longlong_as_double((long long)((a & 0xffffffff00000000ull) | (b >> 32)));
-          c1 = __longlong_as_double((long long)((c & 0xffffffff00000000ull) | (d >> 32)));
+          if (lane < K) {
+            c0 = __longlong_as_double((long long)((a & 0xffffffff00000000ull) | (b >> 32)));
+            c1 = __longlong_as_double((long long)((c & 0xffffffff00000000ull) | (d >> 32)));
+          }
         }
         fence_acq_rel_gpu();
 #if SPCG_TRACE

@@ -73,6 +73,18 @@ struct PipeShared {
 #ifndef SPCG_PIPE_ALIGNED
 #define SPCG_PIPE_ALIGNED 0
 #endif
+#ifndef SPCG_PIPE_POST
+#define SPCG_PIPE_POST 0  // 1: leader posts with st.release.gpu.v2 (A/B)
+#endif
+// (A/B) fence after the leader's slot post: a partial cure of the
+// occasional 2.2-2.5x slower solve before its cause was found (the divergent
+// spin of the leaders' poll, now warp-uniform; profiles/r02/bimodal.md)
+#ifndef SPCG_PIPE_POST_FENCE
+#define SPCG_PIPE_POST_FENCE 0  // 0: none, 1: fence.acq_rel.gpu, 2: fence.sc.gpu
+#endif
+#ifndef SPCG_PIPE_POLL_NS
+#define SPCG_PIPE_POLL_NS 0  // back-off of the leaders' slot polls (A/B)
+#endif
 __device__ __forceinline__ void cluster_arrive_rel() {
 #if SPCG_PIPE_ALIGNED
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
@@ -106,11 +118,35 @@ __device__ __forceinline__ double tagged_finish(const volatile unsigned long lon
                                                 unsigned long long a, unsigned long long b,
                                                 uint32_t tag) {
   unsigned long long spins = 0;
-  while ((uint32_t)a != tag || (uint32_t)b != tag) {
+  // warp-uniform over the lanes that arrived together: no lane spins alone
+  // while its finished neighbours wait at a reconvergence point (see the
+  // leaders' poll in exchange())
+  const unsigned m = __activemask();
+  bool ok = (uint32_t)a == tag && (uint32_t)b == tag;
+  while (!__all_sync(m, ok)) {
 #if SPCG_PIPE_SPIN_NS > 0
     __nanosleep(SPCG_PIPE_SPIN_NS);  // back off: spinners slow the lines' writers
 #endif
-    tagged_issue(src, a, b);
+    if (!ok) {
+      tagged_issue(src, a, b);
+      ok = (uint32_t)a == tag && (uint32_t)b == tag;
+    }
+    if (++spins > kSpinLimit) asm volatile("trap;");
+  }
+  return __longlong_as_double((long long)((a & 0xffffffff00000000ull) | (b >> 32)));
+}
+// Warp-uniform tagged load: all 32 lanes call it; lanes with act = false
+// only keep the loop uniform.
+__device__ __forceinline__ double tagged_load_warp(bool act, const volatile unsigned long long* src,
+                                                   uint32_t tag) {
+  unsigned long long a = 0, b = 0, spins = 0;
+  if (act) tagged_issue(src, a, b);
+  bool ok = !act || ((uint32_t)a == tag && (uint32_t)b == tag);
+  while (!__all_sync(0xffffffffu, ok)) {
+    if (!ok) {
+      tagged_issue(src, a, b);
+      ok = (uint32_t)a == tag && (uint32_t)b == tag;
+    }
     if (++spins > kSpinLimit) asm volatile("trap;");
   }
   return __longlong_as_double((long long)((a & 0xffffffff00000000ull) | (b >> 32)));
@@ -234,7 +270,13 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   // fenced: the exchange also publishes the CTAs' earlier global stores
   // (setup / tail: scratch and x windows); inside the loop it carries only
   // its own epoch-tagged words, so it needs no fence
+  long long cur_it = -1;  // loop iteration of the exchange (exchange trace)
   auto exchange = [&](int bank, uint32_t tag, bool fenced) {
+    // exchange trace (A.trace): iterations 100..107 of every cluster leader:
+    // [post time, done time, time lane k saw cluster k's slot]
+    unsigned long long* xr = (A.trace && cur_it >= 100 && cur_it < 108)
+        ? A.trace + 8 * (size_t)gridDim.x + ((size_t)kc * 8 + (size_t)(cur_it - 100)) * 34
+        : nullptr;
     double t0 = 0.0, t1 = 0.0;
     for (int c = 0; c < C; ++c) {
       t0 += cs.slot[bank][c][0];
@@ -246,27 +288,55 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       volatile unsigned long long* dst = gb + kClusSlotWords * kc;
       const unsigned long long u0 = (unsigned long long)__double_as_longlong(t0);
       const unsigned long long u1 = (unsigned long long)__double_as_longlong(t1);
+#if SPCG_PIPE_POST == 1
+      // one 16-byte store per value pair, release at gpu scope
+      asm volatile("st.release.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(dst),
+                   "l"((u0 & 0xffffffff00000000ull) | tag), "l"((u0 << 32) | tag) : "memory");
+      asm volatile("st.release.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(dst + 2),
+                   "l"((u1 & 0xffffffff00000000ull) | tag), "l"((u1 << 32) | tag) : "memory");
+#else
       dst[0] = (u0 & 0xffffffff00000000ull) | tag;
       dst[1] = (u0 << 32) | tag;
       dst[2] = (u1 & 0xffffffff00000000ull) | tag;
       dst[3] = (u1 << 32) | tag;
+#endif
+#if SPCG_PIPE_POST_FENCE == 1
+      fence_acq_rel_gpu();  // the post is performed before the poll starts
+#elif SPCG_PIPE_POST_FENCE == 2
+      asm volatile("fence.sc.gpu;" ::: "memory");
+#endif
+      if (xr) xr[0] = globaltimer_ns();
     }
     double c0 = 0.0, c1 = 0.0;
-    if (lane < K) {
-      const volatile unsigned long long* src = gb + kClusSlotWords * lane;
-      unsigned long long a, b, c, d, spins = 0;
-      for (;;) {
-        d = src[3];
-        if ((uint32_t)d == tag) {
-          a = src[0];
-          b = src[1];
-          c = src[2];
-          if ((uint32_t)a == tag && (uint32_t)b == tag && (uint32_t)c == tag) break;
+    {
+      // warp-uniform poll: every lane stays in the loop until all K slots
+      // are in (__all_sync), so no lane spins alone while finished lanes
+      // wait at a reconvergence point -- a divergent spin loop let a leader
+      // that arrived early finish ~7 us after its last slot was visible
+      // (profiles/r02/bimodal.md)
+      const volatile unsigned long long* src = gb + kClusSlotWords * (lane < K ? lane : 0);
+      unsigned long long a = 0, b = 0, c = 0, d = 0, spins = 0;
+      bool ok = lane >= K;
+      while (!__all_sync(0xffffffffu, ok)) {
+        if (!ok) {
+          d = src[3];
+          if ((uint32_t)d == tag) {
+            a = src[0];
+            b = src[1];
+            c = src[2];
+            ok = (uint32_t)a == tag && (uint32_t)b == tag && (uint32_t)c == tag;
+            if (ok && xr) xr[2 + lane] = globaltimer_ns();
+          }
         }
+#if SPCG_PIPE_POLL_NS > 0
+        __nanosleep(SPCG_PIPE_POLL_NS);
+#endif
         if (++spins > kSpinLimit) asm volatile("trap;");
       }
-      c0 = __longlong_as_double((long long)((a & 0xffffffff00000000ull) | (b >> 32)));
-      c1 = __longlong_as_double((long long)((c & 0xffffffff00000000ull) | (d >> 32)));
+      if (lane < K) {
+        c0 = __longlong_as_double((long long)((a & 0xffffffff00000000ull) | (b >> 32)));
+        c1 = __longlong_as_double((long long)((c & 0xffffffff00000000ull) | (d >> 32)));
+      }
     }
     if (fenced) fence_acq_rel_gpu();
     double s0 = 0.0, s1 = 0.0;
@@ -279,6 +349,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       d2[0] = s0;
       d2[1] = s1;
     }
+    if (xr && lane == 0) xr[1] = globaltimer_ns();
   };
   auto totals = [&](int bank, double& v0, double& v1) {
     if (K > 1) {
@@ -310,9 +381,12 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     const int hrow = h < P.hlo ? P.wlo + h : P.row_hi + (h - P.hlo);
     return hrow >= P.clo && hrow < P.chi;
   };
-  auto halo_n = [&](int buf, int h, uint32_t tag) {
-    if (halo_local(h)) return nhalo[(size_t)buf * A.hcap + h];
-    return tagged_load(gh + (((size_t)buf * G + gme) * A.hcap + h) * 2, tag);
+  // warp-uniform: every lane of a row warp calls it (act = false: no halo row)
+  auto halo_n = [&](bool act, int buf, int h, uint32_t tag) {
+    const bool loc = act && halo_local(h);
+    const double r = tagged_load_warp(act && !loc,
+                                      gh + (((size_t)buf * G + gme) * A.hcap + (act ? h : 0)) * 2, tag);
+    return loc ? nhalo[(size_t)buf * A.hcap + h] : r;
   };
   // remote: the epoch-tagged global part (other clusters), else the DSMEM part
   auto send_n = [&](const double* nv, int buf, uint32_t tag, bool remote) {
@@ -428,6 +502,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     const int bank = (int)(epoch++ & 1u), buf = (int)(it & 1);
     const uint32_t tag = epoch;
     const unsigned long long t0 = tr ? globaltimer_ns() : 0;
+    cur_it = it;
     double g = 0.0, d = 0.0;
 #pragma unroll
     for (int k = 0; k < NS; ++k)
@@ -443,13 +518,17 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       // instead of sitting before the barrier; the SpMV waits for them
       if (!comm) {
         const double na = -alpha;
-        for (int h = tid; h < nh; h += kPipeRowThreads)
-          if (!halo_local(h)) {
-            const double zh = mul_add_rn(halo_n(pbuf, h, ptag), beta, zhalo[h]);
+        for (int hb = tid - lane; hb < nh; hb += kPipeRowThreads) {  // warp-uniform trip count
+          const int h = hb + lane;
+          const bool act = h < nh && !halo_local(h);
+          const double nv = halo_n(act, pbuf, h, ptag);
+          if (act) {
+            const double zh = mul_add_rn(nv, beta, zhalo[h]);
             zhalo[h] = zh;
             const int j = halo_win(h);
             wwin[j] = mul_add_rn(wwin[j], na, zh);
           }
+        }
         asm volatile("bar.sync 1, %0;" ::"r"(kPipeRowThreads) : "memory");
       }
       pend = false;
@@ -549,15 +628,18 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
         wwin[own0 + rrow[k] - P.row_lo] = wg[k];
       }
     if (!comm)
-      for (int h = tid; h < nh; h += kPipeRowThreads) {
+      for (int hb = tid - lane; hb < nh; hb += kPipeRowThreads) {  // warp-uniform trip count
         // read after the own rows' update: one round trip (both tagged words
         // issued together); issuing it right after barrier B measured slower
-        if (kDefer && !halo_local(h)) continue;
-        const double nv = halo_n(buf, h, tag);
-        const double zh = mul_add_rn(nv, beta, zhalo[h]);
-        zhalo[h] = zh;
-        const int j = halo_win(h);
-        wwin[j] = mul_add_rn(wwin[j], na, zh);
+        const int h = hb + lane;
+        const bool act = h < nh && !(kDefer && !halo_local(h));
+        const double nv = halo_n(act, buf, h, tag);
+        if (act) {
+          const double zh = mul_add_rn(nv, beta, zhalo[h]);
+          zhalo[h] = zh;
+          const int j = halo_win(h);
+          wwin[j] = mul_add_rn(wwin[j], na, zh);
+        }
       }
     pend = true;
     pbuf = buf;

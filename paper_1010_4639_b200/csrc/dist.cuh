@@ -327,12 +327,15 @@ __device__ __forceinline__ void rank_sum(double v, SM& sm, const DistArgs& A, co
 // Device transport: wait (thread 0, then the CTA) for the halo of push number
 // `tag` from every rank this one receives from.
 __device__ __noinline__ void wait_halo(const DistArgs& A, unsigned int tag) {
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < A.nrecv; ++i) {
-      const unsigned long long* f = A.peer->hflag + 2 * (size_t)A.peer->recv_from[i];
-      unsigned long long spins = 0;
-      while ((uint32_t)ld_acquire_sys_u64(f) < tag)
-        if (++spins > kP2PSpinLimit) asm volatile("trap;");
+  if (threadIdx.x < 32) {  // warp 0, lane i polls source i (warp-uniform loop)
+    const int lane = threadIdx.x;
+    const unsigned long long* f =
+        lane < A.nrecv ? A.peer->hflag + 2 * (size_t)A.peer->recv_from[lane] : nullptr;
+    bool ok = f == nullptr;
+    unsigned long long spins = 0;
+    while (!__all_sync(0xffffffffu, ok)) {
+      if (!ok) ok = (uint32_t)ld_acquire_sys_u64(f) >= tag;
+      if (++spins > kP2PSpinLimit) asm volatile("trap;");
     }
   }
   __syncthreads();

@@ -498,9 +498,11 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
     CUDA_TRY(cudaMemsetAsync(P.ghalo, 0, sizeof(double) * 4 * (size_t)P.C * P.hcap, st));
   static const bool tracing = getenv("SPCG_TRACE") != nullptr;
   static const char* dbg_path = getenv("SPCG_CLUS_DEBUG");  // per-solve CTA trace lines
+  // [C][8] per-CTA phases + [K][8 iterations][34] exchange trace (engine 6)
+  const size_t trace_words = 8 * (size_t)P.C + (size_t)(P.C / std::max(1, P.cs)) * 8 * 34;
   if (tracing || dbg_path) {
-    CUDA_TRY(cudaMalloc((void**)&a.trace, sizeof(unsigned long long) * 8 * (size_t)P.C));
-    CUDA_TRY(cudaMemsetAsync(a.trace, 0, sizeof(unsigned long long) * 8 * (size_t)P.C, st));
+    CUDA_TRY(cudaMalloc((void**)&a.trace, sizeof(unsigned long long) * trace_words));
+    CUDA_TRY(cudaMemsetAsync(a.trace, 0, sizeof(unsigned long long) * trace_words, st));
   }
   CUDA_TRY(cudaEventRecord(w.ev0, st));
   if ((rc = launch_clus(P, a, st, pipe))) return rc;
@@ -514,7 +516,7 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
     return fail(SPCG_ERR_CUDA, "cluster engine: kernel ran with a different cluster shape than "
                                "planned (cluster launch attribute not honoured)");
   if (a.trace && pipe) {
-    std::vector<unsigned long long> tv(8 * (size_t)P.C);
+    std::vector<unsigned long long> tv(trace_words);
     CUDA_TRY(cudaMemcpy(tv.data(), a.trace, sizeof(unsigned long long) * tv.size(),
                         cudaMemcpyDeviceToHost));
     cudaFree(a.trace);
@@ -544,7 +546,12 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
           fprintf(f, "%s[%llu, %llu, %llu, %llu, %llu, %llu, %llu]", c ? ", " : "", tv[8 * c + 4],
                   tv[8 * c + 5] - t0, tv[8 * c + 6] - t0, tv[8 * c + 0], tv[8 * c + 1],
                   tv[8 * c + 2], tv[8 * c + 3]);
-        fprintf(f, "]}\n");
+        fprintf(f, "], \"xch\": [");
+        const int K = P.C / std::max(1, P.cs);
+        for (size_t w = 8 * (size_t)P.C; w < trace_words; ++w)
+          fprintf(f, "%s%lld", w > 8 * (size_t)P.C ? ", " : "",
+                  tv[w] ? (long long)(tv[w] - t0) : -1LL);
+        fprintf(f, "], \"K\": %d}\n", K);
         fclose(f);
       }
     }

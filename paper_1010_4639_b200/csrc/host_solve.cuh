@@ -43,13 +43,13 @@ int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double
     // auto only when (nearly) everything stays in shared memory: streamed
     // slices are re-read from L2 every iteration at L2 latency
     const bool resident = m->cp.streamed * 9 <= m->cp.resident;
-    // auto picks the pipelined form (engine 6) for single-segment rows (CSR,
-    // CSC) when its row slots hold the plan: F 3.97-4.31 vs 5.74 us/iteration.
-    // Two-segment SCSR rows stay on engine 5: engine 6 ran them at 4.7 us on
-    // one box but 7-11 us on another (profiles/r01/s4/pipe_two.log), engine 5
-    // at a steady 6.25
+    // auto picks the pipelined form (engine 6) when its row slots hold the
+    // plan, for single- and two-segment rows alike: F 4.6 vs 5.7 us per
+    // iteration, S 5.3 vs 6.3 (round 1 kept SCSR on engine 5 because engine 6
+    // ran it at 7-11 us on some boxes: the divergent spin of the leaders'
+    // poll, fixed in round 2 -- profiles/r02/bimodal.md)
     if (m->cp.ok && (o->engine == 5 || resident)) {
-      const bool pipe = o->engine == 0 && !m->cp.two && m->cp.max_slices <= kPipeMaxSlices;
+      const bool pipe = o->engine == 0 && m->cp.max_slices <= kPipeMaxSlices;
       return do_clus_cg(m, b, x0, x, hist, o, out, st, pipe, /*guard=*/pipe);
     }
     if (o->engine == 5)

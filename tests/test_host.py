@@ -239,3 +239,19 @@ def test_spcg_backend_env_is_honoured():
             assert p.stdout.strip() == "cuda"
         else:
             assert "unknown backend" in p.stderr
+
+
+def test_bench_report_schema_round_trips():
+    """The Table-I report keeps the reference's schema (spcg bench.py:27-128)."""
+    from paper_1010_4639_b200.table1 import BenchReport, CgTiming, OpTiming
+
+    rep = BenchReport(meta={"n": 9, "nnz_full": 33, "nnz_sym": 21, "storage_kind": "full",
+                            "backend": "cuda", "precision": "float64", "accumulation": "atomic",
+                            "reps": 3, "load_time_ms": 0.5},
+                      ops=[OpTiming("dotProd", 1, 0.0123, 1.0), OpTiming("SpMV", 1, 0.02, 1.0)],
+                      cg=[CgTiming("full", 1, 1.5, 7, True, 3.2e-11, 1.0),
+                          CgTiming("sym", 1, 1.7, 7, False, 2.0e-9, 1.0)])
+    assert BenchReport.from_json(rep.to_json()) == rep
+    assert BenchReport.from_csv(rep.to_csv()) == rep
+    txt = rep.to_text()
+    assert "CG/ # int (full)" in txt and "[NOT CONVERGED]" in txt and "workers=1" in txt
