@@ -89,6 +89,24 @@ int spcg_matrix_create_host_u32(int fmt, int64_t n, int64_t nnz,
 int spcg_matrix_generate(int kind, int fmt, int64_t d0, int64_t d1, int64_t d2,
                          spcg_matrix_t* out);
 
+/* Assemble in HBM the symmetric SPD matrix of genprob.random_spd / the
+ * FEM-shaped generator (genprob.py:96-129) from the generator's own random
+ * draws: m strictly-lower pairs (h_I[k] > h_J[k]) with values h_v[k] in draw
+ * order, mirrored; diagonal i = the |v| of row i's entries summed in the
+ * order [I-occurrences, J-occurrences] (np.bincount's order) + diag_shift.
+ * Sorting, mirroring, the diagonal and the CSR / SCSR (+ L^T) / CSC layout
+ * run on the device; the result is bitwise the host generator's matrix. */
+int spcg_matrix_assemble_pairs(int fmt, int64_t n, int64_t m, const int64_t* h_I,
+                               const int64_t* h_J, const double* h_v, double diag_shift,
+                               spcg_matrix_t* out);
+
+/* From DEVICE arrays in the .spcg layout (u64 offsets, u32 indices, fp64
+ * values; matio.py:162-168): converted and validated on the device (the
+ * checks of spcg_matrix_create_host); SCSR's L^T built by a device radix
+ * sort.  The caller keeps ownership of its arrays (copied). */
+int spcg_matrix_create_device_u32(int fmt, int64_t n, int64_t nnz, const uint64_t* d_ptr,
+                                  const uint32_t* d_idx, const double* d_val, spcg_matrix_t* out);
+
 int spcg_matrix_destroy(spcg_matrix_t m);
 
 /* n, stored entries, format, number of row tiles, device bytes held. */

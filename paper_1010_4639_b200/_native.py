@@ -78,6 +78,8 @@ SIGNATURES = {
     "spcg_matrix_create_host": (_i32, [_i32, _i64, _i64, _vp, _vp, _vp, ctypes.POINTER(_vp)]),
     "spcg_matrix_create_host_u32": (_i32, [_i32, _i64, _i64, _vp, _vp, _vp, ctypes.POINTER(_vp)]),
     "spcg_matrix_generate": (_i32, [_i32, _i32, _i64, _i64, _i64, ctypes.POINTER(_vp)]),
+    "spcg_matrix_assemble_pairs": (_i32, [_i32, _i64, _i64, _vp, _vp, _vp, _d, ctypes.POINTER(_vp)]),
+    "spcg_matrix_create_device_u32": (_i32, [_i32, _i64, _i64, _vp, _vp, _vp, ctypes.POINTER(_vp)]),
     "spcg_matrix_destroy": (_i32, [_vp]),
     "spcg_matrix_info": (
         _i32,

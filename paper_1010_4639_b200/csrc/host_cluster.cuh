@@ -423,7 +423,9 @@ double lanczos_cond(const std::vector<double>& ab, long long k) {
   };
   auto kth = [&](int idx) {  // idx-th smallest eigenvalue (0-based)
     double a = lo, z = hi;
-    for (int it = 0; it < 200 && z - a > 1e-15 * std::max(std::fabs(a), std::fabs(z)); ++it) {
+    // 1e-4 relative is ample for a guard threshold (and keeps the host time
+    // of an F solve's guard at a few microseconds)
+    for (int it = 0; it < 200 && z - a > 1e-4 * std::max(std::fabs(a), std::fabs(z)); ++it) {
       const double mid = 0.5 * (a + z);
       if (below(mid) > idx) z = mid;
       else a = mid;

@@ -113,30 +113,6 @@ int upload_tiles(Tiles& t, const std::vector<int4>& desc, const std::vector<int2
   return SPCG_OK;
 }
 
-// CSR of L^T from L+D host arrays: stable counting sort of the strictly
-// lower entries by column (rows ascending within a column).
-void transpose_strict_lower(int n, const std::vector<int>& ptr, const int* idx, const double* val,
-                            std::vector<int>& tptr, std::vector<int>& tidx,
-                            std::vector<double>& tval) {
-  tptr.assign((size_t)n + 1, 0);
-  for (int i = 0; i < n; ++i)
-    for (int k = ptr[i]; k < ptr[i + 1]; ++k)
-      if (idx[k] < i) tptr[idx[k] + 1]++;
-  for (int j = 0; j < n; ++j) tptr[j + 1] += tptr[j];
-  tidx.resize((size_t)tptr[n]);
-  tval.resize((size_t)tptr[n]);
-  std::vector<int> fill(tptr.begin(), tptr.end() - 1);
-  for (int i = 0; i < n; ++i)
-    for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
-      const int j = idx[k];
-      if (j < i) {
-        tidx[fill[j]] = i;
-        tval[fill[j]] = val[k];
-        fill[j]++;
-      }
-    }
-}
-
 // (Re)compute the per-tile leading-edge windows from the device indices.
 int compute_windows(Tiles& t, const Seg& A, const Seg* B, long long* acct) {
   if (t.ntiles == 0) return SPCG_OK;

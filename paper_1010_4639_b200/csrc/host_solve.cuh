@@ -166,70 +166,13 @@ int check_csr_host(int fmt, int64_t n, int64_t nnz) {
   return SPCG_OK;
 }
 
+// Host arrays -> a matrix handle: the raw offsets / indices / values go to
+// the device as they are (no host conversion loop), where create_from_device
+// (host_assemble.cuh) converts them to int32 and validates them in parallel
+// and builds SCSR's L^T by a device radix sort.
 template <class PT, class IT>
 int create_from_host(int fmt, int64_t n, int64_t nnz, const PT* hp, const IT* hi, const double* hv,
-                     spcg_matrix_t* out) {
-  int rc;
-  if ((rc = check_csr_host(fmt, n, nnz))) return rc;
-  if (n > 0 && (hp == nullptr)) return fail(SPCG_ERR_ARG, "null offsets");
-  if (nnz > 0 && (hi == nullptr || hv == nullptr)) return fail(SPCG_ERR_ARG, "null arrays");
-  std::vector<int> ptr((size_t)n + 1);
-  if (n == 0) {
-    ptr[0] = 0;
-  } else {
-    if ((long long)hp[0] != 0 || (long long)hp[n] != nnz)
-      return fail(SPCG_ERR_ARG, "offsets must start at 0 and end at nnz");
-    for (int64_t i = 0; i <= n; ++i) {
-      if (i > 0 && hp[i] < hp[i - 1]) return fail(SPCG_ERR_ARG, "offsets must be non-decreasing");
-      ptr[(size_t)i] = (int)hp[i];
-    }
-  }
-  std::vector<int> idx((size_t)nnz);
-  for (int64_t k = 0; k < nnz; ++k) {
-    const long long c = (long long)hi[k];
-    if (c < 0 || c >= n) return fail(SPCG_ERR_ARG, "index out of range at entry " + std::to_string(k));
-    idx[(size_t)k] = (int)c;
-  }
-  if (fmt == SPCG_FMT_SCSR) {
-    for (int64_t i = 0; i < n; ++i) {
-      const int a = ptr[i], b = ptr[i + 1];
-      if (b <= a || idx[b - 1] != (int)i)
-        return fail(SPCG_ERR_ARG, "row " + std::to_string(i) + " has no stored diagonal entry");
-      for (int k = a; k < b; ++k)
-        if (idx[k] > (int)i) return fail(SPCG_ERR_ARG, "symmetric-half storage requires col <= row");
-    }
-  }
-  DevInfo* d;
-  if ((rc = dev_info(&d))) return rc;
-  spcg_matrix_s* m = new spcg_matrix_s();
-  m->fmt = fmt;
-  m->n = (int)n;
-  m->nnz = nnz;
-  CUDA_TRY(cudaGetDevice(&m->device));
-  if ((rc = finish_matrix(m, ptr, idx.data(), hv, false))) {
-    free_matrix(m);
-    delete m;
-    return rc;
-  }
-  if (fmt == SPCG_FMT_SCSR) {
-    std::vector<int> tptr, tidx;
-    std::vector<double> tval;
-    transpose_strict_lower((int)n, ptr, idx.data(), hv, tptr, tidx, tval);
-    if ((rc = finish_transpose(m, ptr, tptr, tidx.data(), tval.data(), false))) {
-      free_matrix(m);
-      delete m;
-      return rc;
-    }
-  }
-  if ((rc = refresh_windows(m))) {
-    free_matrix(m);
-    delete m;
-    return rc;
-  }
-  *out = m;
-  return SPCG_OK;
-}
-
+                     spcg_matrix_t* out);
 // Device generator: counts -> host prefix sum -> ptr upload -> device fill.
 int gen_seg(int kind, int part, long long row0, long long n, int nx, int ny, int nz, Seg& s,
             std::vector<int>& ptr, long long* acct) {

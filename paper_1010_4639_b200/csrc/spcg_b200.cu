@@ -24,6 +24,7 @@
 #include "clus_pipe.cuh"
 #include "dist.cuh"
 #include "ops.cuh"
+#include "assemble.cuh"
 
 using namespace spcg;
 
@@ -247,6 +248,7 @@ namespace {
 #include "host_matrix.cuh"
 #include "host_cluster.cuh"
 #include "host_solve.cuh"
+#include "host_assemble.cuh"
 #include "host_dist.cuh"
 
 }  // namespace
@@ -322,6 +324,19 @@ int spcg_matrix_generate(int kind, int fmt, int64_t d0, int64_t d1, int64_t d2,
   }
   *out = m;
   return SPCG_OK;
+}
+
+int spcg_matrix_assemble_pairs(int fmt, int64_t n, int64_t m, const int64_t* h_I,
+                               const int64_t* h_J, const double* h_v, double diag_shift,
+                               spcg_matrix_t* out) {
+  if (!out) return fail(SPCG_ERR_ARG, "null out");
+  return assemble_pairs(fmt, n, m, h_I, h_J, h_v, diag_shift, out);
+}
+
+int spcg_matrix_create_device_u32(int fmt, int64_t n, int64_t nnz, const uint64_t* d_ptr,
+                                  const uint32_t* d_idx, const double* d_val, spcg_matrix_t* out) {
+  if (!out) return fail(SPCG_ERR_ARG, "null out");
+  return create_from_device(fmt, n, nnz, d_ptr, d_idx, d_val, out);
 }
 
 int spcg_matrix_destroy(spcg_matrix_t m) {

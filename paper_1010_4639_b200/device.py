@@ -81,6 +81,36 @@ class DeviceMatrix:
         return cls(h.value, fmt, n, int(val.shape[0]))
 
     @classmethod
+    def from_pairs(cls, n: int, I: np.ndarray, J: np.ndarray, v: np.ndarray, diag_shift: float,
+                   fmt: str = "csr") -> "DeviceMatrix":
+        """Assemble a generator's mirrored pairs in HBM (spcg_matrix_assemble_pairs)."""
+        I = np.ascontiguousarray(I, dtype=np.int64)
+        J = np.ascontiguousarray(J, dtype=np.int64)
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        if not (I.shape == J.shape == v.shape):
+            raise ValueError("I, J and v must have the same length")
+        h = ctypes.c_void_p()
+        N.check(N.load().spcg_matrix_assemble_pairs(cls.FORMATS[fmt], int(n), int(I.size), _ptr(I),
+                                                    _ptr(J), _ptr(v), float(diag_shift),
+                                                    ctypes.byref(h)), "spcg_matrix_assemble_pairs")
+        dm = cls(h.value, cls.FORMATS[fmt], 0, 0)
+        dm._refresh()
+        return dm
+
+    @classmethod
+    def from_device_arrays_u32(cls, fmt: int, n: int, nnz: int, d_ptr: int, d_idx: int,
+                               d_val: int) -> "DeviceMatrix":
+        """From device arrays in the .spcg layout (u64 offsets, u32 indices, f64
+        values; raw device pointers), converted and validated on the device."""
+        h = ctypes.c_void_p()
+        N.check(N.load().spcg_matrix_create_device_u32(fmt, int(n), int(nnz), d_ptr, d_idx, d_val,
+                                                       ctypes.byref(h)),
+                "spcg_matrix_create_device_u32")
+        dm = cls(h.value, fmt, 0, 0)
+        dm._refresh()
+        return dm
+
+    @classmethod
     def generate(cls, kind: str, dims: tuple[int, ...], fmt: str = "csr") -> "DeviceMatrix":
         """In-HBM generator: kind in {'poisson2d','poisson3d','stencil27'}."""
         kinds = {"poisson2d": N.GEN_POISSON2D, "poisson3d": N.GEN_POISSON3D,

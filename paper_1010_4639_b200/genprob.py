@@ -120,33 +120,54 @@ def stencil27(nx: int, ny: int, nz: int, part: str = "full", dtype=np.float64):
     return _stencil_csr((nx, ny, nz), _OFF27, 26.0, part, dtype)
 
 
-def random_spd(n: int, density: float, seed: int, dtype=np.float64) -> CsrMatrix:
-    """Seeded strictly diagonally dominant symmetric matrix (genprob.py:96-129):
-    m = round(density*n^2/2) distinct strictly-lower pairs drawn by
-    rng.choice over the row-major pair enumeration, values U(-1,0), mirrored,
-    diagonal = absolute row sum + 1."""
+def random_spd_pairs(n: int, density: float, seed: int):
+    """The random draws of random_spd (genprob.py:96-129): m distinct
+    strictly-lower pairs (I > J) by rng.choice over the row-major pair
+    enumeration and their values U(-1, 0), in draw order."""
     if n < 1:
         raise ValueError("n must be >= 1")
     rng = np.random.default_rng(seed)
     npairs = n * (n - 1) // 2
     m = min(npairs, int(round(density * n * n / 2)))
-    if m > 0:
-        ids = rng.choice(npairs, size=m, replace=False).astype(INDEX_DTYPE)
-        # pair id -> (i, j): row i owns ids [i(i-1)/2, i(i+1)/2)
-        i = ((1 + np.sqrt(1 + 8 * ids.astype(np.float64))) // 2).astype(INDEX_DTYPE)
-        i -= (i * (i - 1) // 2 > ids)
-        i += ((i + 1) * i // 2 <= ids)
-        j = ids - i * (i - 1) // 2
-        v = rng.uniform(-1.0, 0.0, size=m)
-        rows, cols, vals = np.concatenate([i, j]), np.concatenate([j, i]), np.concatenate([v, v])
-    else:
-        rows = cols = np.empty(0, dtype=INDEX_DTYPE)
-        vals = np.empty(0)
-    diag = np.bincount(rows, weights=np.abs(vals), minlength=n) + 1.0
+    if m == 0:
+        e = np.empty(0, dtype=INDEX_DTYPE)
+        return e, e.copy(), np.empty(0)
+    ids = rng.choice(npairs, size=m, replace=False).astype(INDEX_DTYPE)
+    # pair id -> (i, j): row i owns ids [i(i-1)/2, i(i+1)/2)
+    i = ((1 + np.sqrt(1 + 8 * ids.astype(np.float64))) // 2).astype(INDEX_DTYPE)
+    i -= (i * (i - 1) // 2 > ids)
+    i += ((i + 1) * i // 2 <= ids)
+    j = ids - i * (i - 1) // 2
+    v = rng.uniform(-1.0, 0.0, size=m)
+    return i, j, v
+
+
+def _assemble_pairs(n, I, J, v, shift, dtype):
+    rows, cols, vals = np.concatenate([I, J]), np.concatenate([J, I]), np.concatenate([v, v])
+    diag = np.bincount(rows, weights=np.abs(vals), minlength=n) + shift
     ar = np.arange(n, dtype=INDEX_DTYPE)
     return build_csr_from_triplets(
         (np.concatenate([rows, ar]), np.concatenate([cols, ar]), np.concatenate([vals, diag])),
         n, dtype=dtype)
+
+
+def random_spd(n: int, density: float, seed: int, dtype=np.float64) -> CsrMatrix:
+    """Seeded strictly diagonally dominant symmetric matrix (genprob.py:96-129):
+    m = round(density*n^2/2) distinct strictly-lower pairs drawn by
+    rng.choice over the row-major pair enumeration, values U(-1,0), mirrored,
+    diagonal = absolute row sum + 1."""
+    I, J, v = random_spd_pairs(n, density, seed)
+    return _assemble_pairs(n, I, J, v, 1.0, dtype)
+
+
+def random_spd_device(n: int, density: float, seed: int, fmt: str = "csr"):
+    """random_spd assembled in HBM (the draws on the host, numpy PCG64 like the
+    reference; mirroring, diagonal and CSR / SCSR / CSC layout on the device):
+    bitwise the host generator's matrix.  Returns a DeviceMatrix."""
+    from .device import DeviceMatrix
+
+    I, J, v = random_spd_pairs(n, density, seed)
+    return DeviceMatrix.from_pairs(n, I, J, v, 1.0, fmt)
 
 
 def _lower_edges(nx, ny, nz, offsets):
@@ -167,6 +188,21 @@ def _lower_edges(nx, ny, nz, offsets):
     return np.concatenate(I), np.concatenate(J)
 
 
+def fem_mesh_pairs(nx: int = 16, ny: int = 10, nz: int = 193, extra: int = 121_997,
+                   seed: int = 1):
+    """(n, I, J, v): the lower pairs of fem_mesh in draw order (I > J)."""
+    off7 = [o for o in _OFF27 if sum(c != 0 for c in o) == 1]
+    offx = [o for o in _OFF27 if sum(c != 0 for c in o) > 1]
+    i7, j7 = _lower_edges(nx, ny, nz, off7)
+    ie, je = _lower_edges(nx, ny, nz, offx)
+    rng = np.random.default_rng(seed)
+    pick = rng.choice(ie.shape[0], size=extra, replace=False)
+    I = np.concatenate([i7, ie[pick]])
+    J = np.concatenate([j7, je[pick]])
+    v = -rng.uniform(0.5, 1.0, size=I.shape[0])
+    return nx * ny * nz, I, J, v
+
+
 def fem_mesh(nx: int = 16, ny: int = 10, nz: int = 193, extra: int = 121_997,
              shift: float = 0.004, seed: int = 1, dtype=np.float64) -> CsrMatrix:
     """FEM-shaped SPD matrix (SURVEY.md §8d "F-mesh"); defaults give the
@@ -179,24 +215,18 @@ def fem_mesh(nx: int = 16, ny: int = 10, nz: int = 193, extra: int = 121_997,
     Values -U(0.5, 1) from the same generator, mirrored; diagonal = sum of
     |off-diagonals| + shift.
     """
-    off7 = [o for o in _OFF27 if sum(c != 0 for c in o) == 1]
-    offx = [o for o in _OFF27 if sum(c != 0 for c in o) > 1]
-    i7, j7 = _lower_edges(nx, ny, nz, off7)
-    ie, je = _lower_edges(nx, ny, nz, offx)
-    rng = np.random.default_rng(seed)
-    pick = rng.choice(ie.shape[0], size=extra, replace=False)
-    I = np.concatenate([i7, ie[pick]])
-    J = np.concatenate([j7, je[pick]])
-    v = -rng.uniform(0.5, 1.0, size=I.shape[0])
-    n = nx * ny * nz
-    rows = np.concatenate([I, J])
-    cols = np.concatenate([J, I])
-    vals = np.concatenate([v, v])
-    diag = np.bincount(rows, weights=np.abs(vals), minlength=n) + shift
-    ar = np.arange(n, dtype=INDEX_DTYPE)
-    return build_csr_from_triplets(
-        (np.concatenate([rows, ar]), np.concatenate([cols, ar]), np.concatenate([vals, diag])),
-        n, dtype=dtype)
+    n, I, J, v = fem_mesh_pairs(nx, ny, nz, extra, seed)
+    return _assemble_pairs(n, I, J, v, shift, dtype)
+
+
+def fem_mesh_device(nx: int = 16, ny: int = 10, nz: int = 193, extra: int = 121_997,
+                    shift: float = 0.004, seed: int = 1, fmt: str = "csr"):
+    """fem_mesh assembled in HBM (draws on the host, assembly on the device):
+    bitwise the host generator's matrix.  Returns a DeviceMatrix."""
+    from .device import DeviceMatrix
+
+    n, I, J, v = fem_mesh_pairs(nx, ny, nz, extra, seed)
+    return DeviceMatrix.from_pairs(n, I, J, v, shift, fmt)
 
 
 def rhs_for(a, seed: int = 1) -> tuple[np.ndarray, np.ndarray]:

@@ -255,3 +255,29 @@ def test_bench_report_schema_round_trips():
     assert BenchReport.from_csv(rep.to_csv()) == rep
     txt = rep.to_text()
     assert "CG/ # int (full)" in txt and "[NOT CONVERGED]" in txt and "workers=1" in txt
+
+
+def test_csc_container_carries_its_own_version(tmp_path):
+    """CSC .spcg files (new) are VERSION_CSC, so the reference reader (which
+    accepts only VERSION and ignores unknown flags) rejects them rather than
+    reading the CSC arrays as CSR; this reader round-trips both."""
+    import struct
+
+    from paper_1010_4639_b200.genprob import poisson2d
+    from paper_1010_4639_b200.matio import (VERSION, VERSION_CSC, FileFormatError, LinearSystem,
+                                            read_system, write_system)
+
+    a = poisson2d(4, 3)
+    for m, ver in ((a, VERSION), (a.to_csc(), VERSION_CSC)):
+        p = tmp_path / f"v{ver}.spcg"
+        write_system(LinearSystem(matrix=m, b=np.arange(a.n, dtype=float)), p)
+        raw = p.read_bytes()
+        assert struct.unpack_from("<I", raw, 4)[0] == ver
+        back = read_system(p).matrix
+        assert type(back) is type(m) and (back.values == m.values).all()
+    # a CSC payload labelled VERSION 1 is refused
+    raw = bytearray((tmp_path / f"v{VERSION_CSC}.spcg").read_bytes())
+    raw[4:8] = struct.pack("<I", VERSION)
+    (tmp_path / "bad.spcg").write_bytes(bytes(raw))
+    with pytest.raises(FileFormatError):
+        read_system(tmp_path / "bad.spcg")
