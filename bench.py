@@ -444,12 +444,12 @@ def run_ours(args):
     peak, peak_src = peaks()
     m = measure_ours(args.workload, args.steps, args.warmup, peak, args.max_iter, clocks=True,
                      spmv=True)
-    tfile = ROOT / "profiles" / "r01" / "p3_spmv_traffic.json"
+    tfile = ROOT / "profiles" / "r02" / "p3_spmv_traffic.json"
     if args.workload == "p3" and m["engine"] == "per-pass" and tfile.exists():
         # DRAM bytes of one dist_spmv_pq launch on this system (ncu --metrics
         # dram__bytes_read.sum,dram__bytes_write.sum; profiles/r01)
         m["roofline"]["traffic"] = int(json.loads(tfile.read_text())["dram_bytes_per_launch"])
-        m["roofline"]["traffic_source"] = ("profiles/r01/p3_spmv_traffic.json (ncu dram__bytes "
+        m["roofline"]["traffic_source"] = ("profiles/r02/p3_spmv_traffic.json (ncu dram__bytes "
                                            "of one launch)")
     m["roofline"]["peak_source"] = peak_src
     _, _, _, _, desc = WORKLOADS[args.workload]
@@ -569,10 +569,21 @@ def run_distributed(args):
     nnz_tot = int(sum(gather(nnz_loc))) if world > 1 else nnz_loc
 
     accum = "atomic" if acc == 0 else "privatized"  # SCSR shards: reverse halo vs stored L^T
+    # transport of the per-iteration exchange: "nccl" (host-enqueued NCCL
+    # all-reduces + send/recv) or "p2p" (device-initiated: mailbox all-reduce
+    # and halo stores in CUDA-IPC-mapped peer memory, no host collective)
+    plan = None
+    if args.transport == "p2p":
+        plan = D.P2PPlan(sm, rank, world)
+        plan.connect(gather(plan.export()) if world > 1 else [plan.export()])
 
     def step():
-        x, res, _ = D.dist_cg_solve(sm, comm, b_loc, max_iter=args.max_iter or None, timing=True,
-                                    accumulation=accum)
+        if plan is not None:
+            x, res, _ = plan.solve(b_loc, max_iter=args.max_iter or None, timing=True,
+                                   accumulation=accum)
+        else:
+            x, res, _ = D.dist_cg_solve(sm, comm, b_loc, max_iter=args.max_iter or None,
+                                        timing=True, accumulation=accum)
         return x, res
 
     for _ in range(args.warmup):
@@ -610,8 +621,11 @@ def run_distributed(args):
     e2e_its = 0
     for _ in range(args.steps):
         bd = bh.to("cuda", non_blocking=True)
-        xd, r, _ = D.dist_cg_solve(sm, comm, bd, max_iter=args.max_iter or None,
-                                   accumulation=accum)
+        if plan is not None:
+            xd, r, _ = plan.solve(bd, max_iter=args.max_iter or None, accumulation=accum)
+        else:
+            xd, r, _ = D.dist_cg_solve(sm, comm, bd, max_iter=args.max_iter or None,
+                                       accumulation=accum)
         xh.copy_(xd, non_blocking=True)
         e2e_its += r.iterations
     e3.record(st)
@@ -626,9 +640,14 @@ def run_distributed(args):
             "data": "synthetic (reference generator rebuilt in HBM per shard; b = A x_gen)",
             "config": {"workload": desc, "n": n, "nnz_stored": nnz_tot, "tol": 1e-10,
                        "iterations_per_solve": it_per, "step": "one full cg_solve",
-                       "parallelism": f"row-sharded over {world} GPU(s): z-slabs, NCCL halo "
-                                      "send/recv + 2 all-reduces per iteration",
-                       "engine": "per-pass kernels + NCCL (spcg_dist_cg_solve)"},
+                       "parallelism": (f"row-sharded over {world} GPU(s): z-slabs, NCCL halo "
+                                       "send/recv + 2 all-reduces per iteration")
+                                      if plan is None else
+                                      (f"row-sharded over {world} GPU(s): z-slabs, device-initiated "
+                                       "exchange (mailbox all-reduce + halo stores in peer memory)"),
+                       "engine": "per-pass kernels + NCCL (spcg_dist_cg_solve)" if plan is None
+                                 else "per-pass kernels, device transport (spcg_dist_plan_solve)",
+                       "transport": args.transport},
             "e2e": {"value": round(e2e_its / (e2e_ms / 1e3), 3), "unit": "iterations/s",
                     "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
                     "path": "spcg_dist_cg_solve per rank, pinned host b -> x"},
@@ -840,6 +859,8 @@ def main():
                     help="paper Table-I per-op rows (F matrix) on GPU vs the reference CPU path")
     ap.add_argument("--engine", choices=("auto", "sharded"), default="auto",
                     help="sharded: run the row-sharded engine even on one GPU")
+    ap.add_argument("--transport", choices=("nccl", "p2p"), default="nccl",
+                    help="sharded runs: host-enqueued NCCL or the device-initiated transport")
     ap.add_argument("--dry-run", action="store_true",
                     help="CPU check of the N-rank plumbing (gloo), no GPU and no measurement")
     args = ap.parse_args()

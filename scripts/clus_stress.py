@@ -1,6 +1,9 @@
-"""Dev stress: many cluster-engine solves of F / S, every run must be bitwise
-identical (x, iterations) -- a race in the inter-cluster exchange shows up as
-a differing run or a breakdown."""
+"""Stress: many resident-engine solves of F / S / CSC, every run must be
+bitwise identical (x, iterations) -- a race in the inter-cluster exchange,
+the DSMEM halos or the grid all-reduce shows up as a differing run or a
+breakdown.  (compute-sanitizer is closed on this GPU pool; this and the
+bimodal traces are the race evidence, profiles/r02/stress.log.)
+    python scripts/clus_stress.py RUNS 6,5,3"""
 import sys
 from pathlib import Path
 
@@ -17,20 +20,29 @@ b, _ = rhs_for(F, seed=1)
 bt = torch.from_numpy(b).cuda()
 lib = N.load()
 runs = int(sys.argv[1]) if len(sys.argv) > 1 else 200
-for name, m in (("F", F), ("S", extract_lower(F))):
+engines = [int(e) for e in sys.argv[2].split(",")] if len(sys.argv) > 2 else [5]
+for eng, (name, m) in ((e, nm) for e in engines for nm in (("F", F), ("S", extract_lower(F)),
+                                                          ("C", F.to_csc()))):
     dm = m.device()
     ref = None
     bad = 0
     for i in range(runs):
         x = torch.empty_like(bt)
         o = N.CgOptionsC(tol=1e-10, max_iter=0, record_history=0, recompute_final_residual=1,
-                         accumulation=1, engine=5)
+                         accumulation=1, engine=eng)
         r = N.CgResultC()
         rc = lib.spcg_cg_solve(dm.handle, bt.data_ptr(), None, x.data_ptr(), None, o, r, 0)
         xs = x.cpu().numpy()
-        if rc != 0 or (ref is not None and (r.iterations != ref[0] or not np.array_equal(xs, ref[1]))):
+        # engine 3 runs CSC as a column scatter with fp64 atomics: its order is
+        # unspecified by contract (like the reference's atomic mode), so only
+        # iterations and x to 1e-12 must repeat; every other case bitwise
+        exact = not (eng == 3 and name == "C")
+        same = ref is not None and r.iterations == ref[0] and (
+            np.array_equal(xs, ref[1]) if exact
+            else np.linalg.norm(xs - ref[1]) <= 1e-12 * np.linalg.norm(ref[1]))
+        if rc != 0 or (ref is not None and not same):
             bad += 1
             print(name, "run", i, "rc", rc, "its", r.iterations, flush=True)
         if ref is None and rc == 0:
             ref = (r.iterations, xs)
-    print(name, "runs", runs, "bad", bad, "its", ref[0] if ref else None, flush=True)
+    print("engine", eng, name, "runs", runs, "bad", bad, "its", ref[0] if ref else None, flush=True)
