@@ -663,6 +663,8 @@ def run_distributed(args):
                                                  (peak * world), 4), "solve_ms": solve_ms},
             "clocks": clocks, "final_relative_residual": results[-1][3],
             "max_abs_err_vs_xgen": err, "setup_s": round(setup_s, 2)}), flush=True)
+    if plan is not None:
+        plan.close()
     comm.close()
     if world > 1:
         dist.destroy_process_group()

@@ -56,6 +56,10 @@ struct StepState {
   int status, converged, done, x0_given;
   unsigned int counter;  // last-CTA-done ticket
   int record;
+  // K_SCSR_FIX: bits of max|p| per iteration parity (pass C fills the next
+  // slot, pass A / B read the current one, pass B clears the next); slot 2:
+  // the x0 / true-residual SpMVs
+  unsigned long long pmax[3];
   unsigned int rseq;  // device transport: reductions done (mailbox tag/bank)
   unsigned int hseq;  // device transport: halo pushes done (halo tag)
 };
@@ -99,6 +103,7 @@ struct DistArgs {
   int rank, nranks;
   int zq;             // atomic formats: pass B re-zeroes q
   int xv;             // x is 16-byte aligned
+  unsigned long long* txnext;  // K_SCSR_FIX: the max|p| slot pass C fills (pass B clears it)
   // device transport
   const PeerTab* peer;
   const unsigned char* thalo;  // per tile of M: gathers halo columns
@@ -563,20 +568,44 @@ __global__ void __launch_bounds__(kElemBlock)
   const double alpha = S->alpha;
   const long long g = (long long)c.lb * blockDim.x + threadIdx.x;
   const long long GT = (long long)c.G * blockDim.x;
+  // K_SCSR_FIX: q = gather part + fixed-point transposed part (then cleared)
+  unsigned long long* Y = A.M.ytx;
+  const double iy = (Y && mode != 0) ? 1.0 / fix_scale(A.M.txmax, A.M.tx_eM) : 0.0;  // exact
+  if (Y && mode == 2 && c.lb == 0 && threadIdx.x == 0 && A.txnext) *A.txnext = 0ull;
   double acc = 0.0;
   if (mode == 2) {
     const double na = -alpha;
     const long long np = nloc >> 1;
     const double2* q2 = reinterpret_cast<const double2*>(q);
     double2* r2 = reinterpret_cast<double2*>(r);
+    // every load of a round is issued before its stores (the Y / q stores
+    // may alias later loads as far as the compiler knows: interleaving them
+    // serialised the round -- 0.43 ms instead of 0.2 for Q27's pass B)
+    auto fixq = [&](double2 qv, ulonglong2 t) {
+      qv.x = __dadd_rn(qv.x, s64_to_f64((long long)t.x) * iy);
+      qv.y = __dadd_rn(qv.y, s64_to_f64((long long)t.y) * iy);
+      return qv;
+    };
+    ulonglong2* y2 = reinterpret_cast<ulonglong2*>(Y);
+    const ulonglong2 z2 = make_ulonglong2(0ull, 0ull);
     long long i = g;
     for (; i + GT < np; i += 2 * GT) {
       const long long ia = rev ? np - 1 - i : i, ib = rev ? np - 1 - (i + GT) : i + GT;
-      const double2 qa = q2[ia], qb = q2[ib], ra = r2[ia], rb = r2[ib];
+      double2 qa = q2[ia], qb = q2[ib];
+      const double2 ra = r2[ia], rb = r2[ib];
+      if (Y) {
+        const ulonglong2 ya = y2[ia], yb = y2[ib];
+        qa = fixq(qa, ya);
+        qb = fixq(qb, yb);
+      }
       const double2 oa = make_double2(mul_add_rn(ra.x, na, qa.x), mul_add_rn(ra.y, na, qa.y));
       const double2 ob = make_double2(mul_add_rn(rb.x, na, qb.x), mul_add_rn(rb.y, na, qb.y));
       r2[ia] = oa;
       r2[ib] = ob;
+      if (Y) {
+        y2[ia] = z2;
+        y2[ib] = z2;
+      }
       if (zq) {
         reinterpret_cast<double2*>(q)[ia] = make_double2(0.0, 0.0);
         reinterpret_cast<double2*>(q)[ib] = make_double2(0.0, 0.0);
@@ -588,15 +617,23 @@ __global__ void __launch_bounds__(kElemBlock)
     }
     if (i < np) {
       const long long ia = rev ? np - 1 - i : i;
-      const double2 qa = q2[ia], ra = r2[ia];
+      double2 qa = q2[ia];
+      const double2 ra = r2[ia];
+      if (Y) qa = fixq(qa, y2[ia]);
       const double2 oa = make_double2(mul_add_rn(ra.x, na, qa.x), mul_add_rn(ra.y, na, qa.y));
       r2[ia] = oa;
+      if (Y) y2[ia] = z2;
       if (zq) reinterpret_cast<double2*>(q)[ia] = make_double2(0.0, 0.0);
       acc = fma(oa.x, oa.x, acc);
       acc = fma(oa.y, oa.y, acc);
     }
     if ((nloc & 1) && g == 0) {
-      const double v = mul_add_rn(r[nloc - 1], na, q[nloc - 1]);
+      double qv = q[nloc - 1];
+      if (Y) {
+        qv = __dadd_rn(qv, s64_to_f64((long long)Y[nloc - 1]) * iy);
+        Y[nloc - 1] = 0ull;
+      }
+      const double v = mul_add_rn(r[nloc - 1], na, qv);
       if (zq) q[nloc - 1] = 0.0;
       r[nloc - 1] = v;
       acc = fma(v, v, acc);
@@ -604,15 +641,23 @@ __global__ void __launch_bounds__(kElemBlock)
   } else {
     for (long long i = g; i < nloc; i += GT) {
       double v;
+      double qv = 0.0;
+      if (mode != 0 && (mode == 3 || useq)) {
+        qv = q[i];
+        if (Y) {
+          qv = __dadd_rn(qv, s64_to_f64((long long)Y[i]) * iy);
+          Y[i] = 0ull;
+        }
+      }
       if (mode == 0) {
         v = b[i];
       } else if (mode == 1) {
-        v = useq ? mul_add_rn(b[i], -1.0, q[i]) : b[i];
+        v = useq ? mul_add_rn(b[i], -1.0, qv) : b[i];
         if (useq && zq) q[i] = 0.0;
         r[i] = v;
         A.p[i] = v;
       } else {
-        v = mul_add_rn(b[i], -1.0, q[i]);
+        v = mul_add_rn(b[i], -1.0, qv);
       }
       acc = fma(v, v, acc);
     }
@@ -667,6 +712,7 @@ __global__ void __launch_bounds__(kElemBlock)
   const long long np = nloc >> 1;
   const double2* r2 = reinterpret_cast<const double2*>(r);
   double2* p2 = reinterpret_cast<double2*>(p);
+  double pm = 0.0;
   for (long long j = g; j < np; j += GT) {
     const long long i = rev ? np - 1 - j : j;
     const double2 pv = p2[i], rv = r2[i];
@@ -680,6 +726,7 @@ __global__ void __launch_bounds__(kElemBlock)
     }
     const double2 pn = make_double2(mul_add_rn(rv.x, beta, pv.x), mul_add_rn(rv.y, beta, pv.y));
     p2[i] = pn;
+    pm = fmax(pm, fmax(fabs(pn.x), fabs(pn.y)));
     if (push) {
       push_row(A, rc, 2 * i, pn.x);
       push_row(A, rc, 2 * i + 1, pn.y);
@@ -691,6 +738,12 @@ __global__ void __launch_bounds__(kElemBlock)
     x[i] = mul_add_rn(x[i], alpha, pv);
     p[i] = mul_add_rn(r[i], beta, pv);
     if (push) push_row(A, rc, i, p[i]);
+    pm = fmax(pm, fabs(p[i]));
+  }
+  if (A.txnext) {  // K_SCSR_FIX: max|p| of the new direction (bits are monotone for >= 0)
+    pm = warp_max(pm);
+    if ((threadIdx.x & 31) == 0 && pm > 0.0)
+      atomicMax(A.txnext, (unsigned long long)__double_as_longlong(pm));
   }
   if (push) halo_done(A, c, sm, S->hseq + 1);
 }
@@ -745,6 +798,32 @@ __global__ void dist_x(const __grid_constant__ DistArgs A1, const DistArgs* __re
       A.tmp[i] = A.x[i];
     }
   }
+}
+
+// out = bits of max |v| (atomicMax on the bit patterns of non-negative
+// doubles: exact and order-independent); *out must be cleared first
+__global__ void vec_absmax_kernel(long long n, const double* v, unsigned long long* out) {
+  double m = 0.0;
+  const long long G = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += G)
+    m = fmax(m, fabs(v[i]));
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+// 2^eM bound of max_j sum_i |a_ij| over the strictly lower part, from the
+// rows of L^T summed in storage order: out = bits of the max row sum
+__global__ void lt_rowsum_max_kernel(int n, const int* ptr, const double* val,
+                                     unsigned long long* out) {
+  double m = 0.0;
+  const int G = gridDim.x * blockDim.x;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += G) {
+    double s = 0.0;
+    for (int k = ptr[j]; k < ptr[j + 1]; ++k) s = __dadd_rn(s, fabs(val[k]));
+    m = fmax(m, s);
+  }
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
 }
 
 // Per tile of a localized view: 1 when any of its entries gathers a halo

@@ -390,12 +390,31 @@ int run_dist(const std::vector<DistArgs>& hA, DistArgs* dA, const HaloPlan* H, c
     if (kAtom) CUDA_TRY(cudaMemsetAsync(hA[r].q, 0, sizeof(double) * (size_t)std::max(1LL, next), st));
   }
   const int GG = nv * G, GGE = nv * GE;
+  // K_SCSR_FIX (one rank): the max|p| slots of StepState and the accumulator
+  constexpr bool kFix = (FMT == K_SCSR_FIX);
+  auto pmax_slot = [&](int k) {
+    return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(hA[0].S) +
+                                                 offsetof(StepState, pmax) + 8 * (size_t)k);
+  };
+  if (kFix) {
+    if (nv != 1 || hA[0].M.ytx == nullptr) return fail(SPCG_ERR_ARG, "fixed-point SCSR: one rank");
+    CUDA_TRY(cudaMemsetAsync(hA[0].M.ytx, 0, sizeof(unsigned long long) *
+                                                 (size_t)std::max<long long>(2, hA[0].nloc + 1), st));
+  }
+  auto absmax = [&](const double* v, int slot) -> int {  // max|v| into a pmax slot
+    CUDA_TRY(cudaMemsetAsync(pmax_slot(slot), 0, sizeof(unsigned long long), st));
+    vec_absmax_kernel<<<GE, kElemBlock, 0, st>>>(hA[0].nloc, v, pmax_slot(slot));
+    CUDA_TRY(cudaGetLastError());
+    return SPCG_OK;
+  };
   // kernel transport mode: 0 host transport, 1 device transport (one rank
   // per process), 2 device transport over nv virtual ranks in one launch
   const int mode = !fused ? 0 : (nv > 1 ? 2 : 1);
   DistArgs a1 = hA[0];  // MODE 0 / 1: the rank's arguments by value
   a1.M.cta0 = 0;
   a1.M.ncta = 0;
+  a1.txnext = nullptr;
+  if (kFix) a1.M.txmax = pmax_slot(2);  // always a valid slot
 #define SPCG_ELEM(KERNEL, ...)                                                        \
   do {                                                                                \
     if (mode == 0) KERNEL<0><<<GE, kElemBlock, 0, st>>>(a1, dA, GE, __VA_ARGS__);      \
@@ -438,6 +457,13 @@ int run_dist(const std::vector<DistArgs>& hA, DistArgs* dA, const HaloPlan* H, c
     // device transport: the kernel waits for the halo of the push just done
     a1.M.rev = 0;
     a1.M.tree = 0;
+    if (kFix) {  // slot 2: max|tmp|, read by this SpMV and the elementwise pass after it
+      int rc2;
+      if ((rc2 = absmax(hA[0].tmp, 2))) return rc2;
+      a1.M.txmax = pmax_slot(2);
+      a1.txnext = nullptr;
+  if (kFix) a1.M.txmax = pmax_slot(2);  // always a valid slot
+    }
     SPCG_TILE(dist_spmv, 0);
     if (kRev) {
       if (ghosts) {
@@ -462,6 +488,7 @@ int run_dist(const std::vector<DistArgs>& hA, DistArgs* dA, const HaloPlan* H, c
   }
   SPCG_ELEM(dist_elem, 1, have_x0 ? 1 : 0, 0);
   if ((rc = host_reduce(1))) return rc;
+  if (kFix && (rc = absmax(hA[0].p, 0))) return rc;  // p_1 = r_0 -> slot 0
   if ((rc = halo(0, 0, hA[0].p, hA[0].p))) return rc;
   CUDA_TRY(cudaGetLastError());
   // CG loop; the host enqueues chunks of iterations and polls the device-side
@@ -492,6 +519,10 @@ int run_dist(const std::vector<DistArgs>& hA, DistArgs* dA, const HaloPlan* H, c
       const int dirA = kAlternate ? (int)((iter_enq & 1) == 0) : 0;
       a1.M.rev = dirA;
       a1.M.tree = tree;
+      if (kFix) {  // iteration parity: A / B read slot k&1, C fills (B clears) slot (k+1)&1
+        a1.M.txmax = pmax_slot((int)(iter_enq & 1));
+        a1.txnext = pmax_slot((int)((iter_enq + 1) & 1));
+      }
       SPCG_TILE(dist_spmv_pq, dirA, tree, post);
       if (timing) CUDA_TRY(cudaEventRecord(d0.tev[bb][1][c], st));
       int rc2;
@@ -627,7 +658,40 @@ DistArgs base_args(spcg_matrix_s* m, int kf, const double* b, const double* x0, 
   A.nranks = 1;
   A.zq = (kf == K_SCSR_ATOMIC || kf == K_CSC) ? 1 : 0;
   A.xv = (((uintptr_t)x) & 15) == 0;
+  if (kf == K_SCSR_FIX) {
+    A.M.ytx = d.ytx;
+    A.M.tx_eM = m->tx_eM;
+  }
   return A;
+}
+
+// K_SCSR_FIX setup: the accumulator and 2^eM >= max_j sum_{i>j} |a_ij| (from
+// the rows of L^T, summed in order: deterministic), once per handle.
+int ensure_fix(spcg_matrix_s* m) {
+  DistWorkspace& d = m->dw;
+  int rc;
+  if (d.ytx_n < (long long)m->n + 2) {
+    if (d.ytx) cudaFree(d.ytx);
+    d.ytx = nullptr;
+    if ((rc = dmalloc((void**)&d.ytx, sizeof(unsigned long long) * ((size_t)m->n + 2), nullptr)))
+      return rc;
+    d.ytx_n = (long long)m->n + 2;
+  }
+  if (m->tx_eM == -100000) {
+    if (!m->hasB) return fail(SPCG_ERR_UNSUPPORTED, "fixed-point SCSR needs the L^T rows");
+    unsigned long long* mx = nullptr;
+    if ((rc = dmalloc((void**)&mx, sizeof(unsigned long long), nullptr))) return rc;
+    CUDA_TRY(cudaMemset(mx, 0, sizeof(unsigned long long)));
+    if (m->n > 0) lt_rowsum_max_kernel<<<592, 256>>>(m->n, m->B.ptr, m->B.val, mx);
+    unsigned long long bits = 0;
+    CUDA_TRY(cudaMemcpy(&bits, mx, sizeof(bits), cudaMemcpyDeviceToHost));
+    cudaFree(mx);
+    int e = 0;
+    const double Mmax = __builtin_bit_cast(double, bits);
+    if (Mmax > 0.0) std::frexp(Mmax, &e);
+    m->tx_eM = e;
+  }
+  return SPCG_OK;
 }
 
 template <int FMT>
@@ -685,6 +749,14 @@ int do_dist_cg(spcg_matrix_s* m, spcg_comm_s* comm, int npeers, const int32_t* p
     out->converged = 1;
     out->engine_used = 2;
     return SPCG_OK;
+  }
+  // deterministic symmetric mode on one GPU: one pass over L+D with the
+  // transposed part accumulated exactly in fixed point (K_SCSR_FIX), unless
+  // the caller asked for the reference's sequential sums (row_sums = 1: the
+  // stored L^T, bitwise the reference privatized mode at workers = 1)
+  if (kf == K_SCSR_PRIV && npeers == 0 && alone && !m->is_rows && o->row_sums == 0) {
+    if ((rc = ensure_fix(m))) return rc;
+    return dispatch_fmt_host<K_SCSR_FIX>(m, H, b, x0, x, hist, o, out, st);
   }
   switch (kf) {
     case K_CSR: return dispatch_fmt_host<K_CSR>(m, H, b, x0, x, hist, o, out, st);

@@ -94,9 +94,13 @@ __device__ __forceinline__ double seq_sum(const double* prod, int ks, int ke) {
 // hoisted above it, and each red waits for x_i -- the line's own, usually
 // uncached, value).  Interleaving "gather u, red u" serialised the round's
 // gathers behind that x_i load.
-template <class Src>
+// FIX (K_SCSR_FIX): the transposed contributions go to the 64-bit
+// fixed-point accumulator ytx, scaled by the power of two c (exact sums).
+template <bool FIX = false, class Src>
 __device__ __forceinline__ double sym_row_atomic(const double* v, const int* ix, int ks, int ke,
-                                                 int i, double xi, const Src& src, double* y) {
+                                                 int i, double xi, const Src& src, double* y,
+                                                 unsigned long long* ytx = nullptr,
+                                                 double c = 0.0) {
   double acc = 0.0;
   for (int k = ks; k < ke; k += kUnroll) {
     int jj[kUnroll];
@@ -110,7 +114,10 @@ __device__ __forceinline__ double sym_row_atomic(const double* v, const int* ix,
     for (int u = 0; u < kUnroll; ++u) {
       if (k + u < ke) {
         const double a = v[k + u];
-        if (jj[u] != i) red_add_f64(y + jj[u], __dmul_rn(a, xi));
+        if (jj[u] != i) {
+          if (FIX) red_add_s64(ytx + jj[u], f64_to_s64_rn(__dmul_rn(a, xi) * c));
+          else red_add_f64(y + jj[u], __dmul_rn(a, xi));
+        }
         acc = __dadd_rn(acc, __dmul_rn(a, gx[u]));
       }
     }
@@ -364,7 +371,7 @@ __device__ __forceinline__ LineOut tile_line(Smem& sm, int s, const MatView& M, 
 #define SPCG_NO_XPRE 0
 #endif
     if (SPCG_NO_XPRE) xpre = nullptr;
-    if (FMT == K_SCSR_ATOMIC || FMT == K_CSC) {
+    if (FMT == K_SCSR_ATOMIC || FMT == K_SCSR_FIX || FMT == K_CSC) {
       // split lines: tiles of <= 256 (128) lines give each line 2 (4)
       // adjacent lanes (512-line tiles: one lane per line); lane g takes the g-th contiguous segment of the
       // line's entries (gather partial + its scatters), and the partials
@@ -388,6 +395,10 @@ __device__ __forceinline__ LineOut tile_line(Smem& sm, int s, const MatView& M, 
           if (xpre) o.xo = xpre[li];
           if (FMT == K_SCSR_ATOMIC) {
             acc = sym_row_atomic(sm.val[s], sm.idx[s], ks, ke, li, o.xi, src, y);
+            o.dg = (a1 > a0) ? sm.val[s][a1 - 1] : 0.0;
+          } else if (FMT == K_SCSR_FIX) {
+            acc = sym_row_atomic<true>(sm.val[s], sm.idx[s], ks, ke, li, o.xi, src, y, M.ytx,
+                                       fix_scale(M.txmax, M.tx_eM));
             o.dg = (a1 > a0) ? sm.val[s][a1 - 1] : 0.0;
           } else {
             acc = csc_col<GATHER_CSC>(sm.val[s], sm.idx[s], ks, ke, o.xi, src, y);
@@ -481,6 +492,10 @@ __device__ __forceinline__ LineOut tile_line(Smem& sm, int s, const MatView& M, 
       o.xi = src.get(i);
       o.q = sym_row_atomic(v, ix, ks, ke, i, o.xi, src, y);
       o.dg = (ke > ks) ? v[ke - 1] : 0.0;
+    } else if (FMT == K_SCSR_FIX) {
+      o.xi = src.get(i);
+      o.q = sym_row_atomic<true>(v, ix, ks, ke, i, o.xi, src, y, M.ytx, fix_scale(M.txmax, M.tx_eM));
+      o.dg = (ke > ks) ? v[ke - 1] : 0.0;
     } else {  // K_CSC
       o.xi = src.get(i);
       o.q = csc_col<GATHER_CSC>(v, ix, ks, ke, o.xi, src, y);
@@ -501,14 +516,18 @@ __device__ __forceinline__ LineOut tile_line(Smem& sm, int s, const MatView& M, 
     const double t = long_gather_seq(M.valB, M.idxB, M.ptrB[i], M.ptrB[i + 1], src, prod);
     o.q = __dadd_rn(g, t);
     o.xi = src.get(i);
-  } else if (FMT == K_SCSR_ATOMIC) {
+  } else if (FMT == K_SCSR_ATOMIC || FMT == K_SCSR_FIX) {
     const double xi = src.get(i);
+    const double c = FMT == K_SCSR_FIX ? fix_scale(M.txmax, M.tx_eM) : 0.0;
     double part = 0.0;
     for (int k = k0 + (int)threadIdx.x; k < k1; k += blockDim.x) {
       const int j = ld_stream_s32(M.idxA + k);
       const double a = ld_stream_f64(M.valA + k);
       part = __dadd_rn(part, __dmul_rn(a, src.get(j)));
-      if (j != i) red_add_f64(y + j, __dmul_rn(a, xi));
+      if (j != i) {
+        if (FMT == K_SCSR_FIX) red_add_s64(M.ytx + j, f64_to_s64_rn(__dmul_rn(a, xi) * c));
+        else red_add_f64(y + j, __dmul_rn(a, xi));
+      }
     }
     o.q = block_sum(part, sm);
     o.xi = xi;
@@ -584,7 +603,7 @@ __device__ __forceinline__ bool wide_tile(const Smem& sm, int s) {
 // Finish a line of a plain SpMV y = A x (no CG bookkeeping).
 template <int FMT>
 __device__ __forceinline__ void finish_plain(const LineOut& o, int i, double* y) {
-  if (FMT == K_CSR || FMT == K_SCSR_PRIV) y[i] = o.q;
+  if (FMT == K_CSR || FMT == K_SCSR_PRIV || FMT == K_SCSR_FIX) y[i] = o.q;  // FIX: the gather part
   else if (FMT == K_SCSR_ATOMIC) red_add_f64(y + i, o.q);
   // CSC: the column scatter already wrote everything
 }
@@ -594,7 +613,7 @@ __device__ __forceinline__ void finish_plain(const LineOut& o, int i, double* y)
 //   (p'Ap = 2 p'(L+D)p - p'Dp);  CSC: p_j g_j  (p'A p = p'A^T p).
 template <int FMT>
 __device__ __forceinline__ double line_pq(const LineOut& o) {
-  if (FMT == K_SCSR_ATOMIC) return o.xi * (2.0 * o.q - o.dg * o.xi);
+  if (FMT == K_SCSR_ATOMIC || FMT == K_SCSR_FIX) return o.xi * (2.0 * o.q - o.dg * o.xi);
   return o.xi * o.q;
 }
 

@@ -93,6 +93,54 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes
 __device__ __forceinline__ void red_add_f64(double* addr, double v) {
   asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(addr), "d"(v) : "memory");
 }
+// two's-complement 64-bit add (exact, order-independent): the fixed-point
+// transposed contributions of K_SCSR_FIX
+__device__ __forceinline__ void red_add_s64(unsigned long long* addr, long long v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(addr), "l"(v) : "memory");
+}
+// 64-bit integer <-> fp64 conversions of the fixed-point SCSR.  Native
+// I2F / F2I by default; SPCG_FIX_MAGIC=1 (A/B) builds them from fp64 adds and
+// bit moves (the 1.5 * 2^52 trick on two 31-bit halves) -- measured slower in
+// pass A (0.72 vs 0.68 ms on Q27) and equal in pass B, so off.
+#ifndef SPCG_FIX_MAGIC
+#define SPCG_FIX_MAGIC 0
+#endif
+constexpr double kMagic52 = 6755399441055744.0;           // 1.5 * 2^52
+constexpr long long kMagic52Bits = 0x4338000000000000LL;  // its bit pattern
+// correctly rounded (double)v, any v
+__device__ __forceinline__ double s64_to_f64(long long v) {
+#if SPCG_FIX_MAGIC
+  const long long hi = v >> 31, lo = v & 0x7fffffffLL;
+  const double dh = __dsub_rn(__longlong_as_double(hi + kMagic52Bits), kMagic52);
+  const double dl = __dsub_rn(__longlong_as_double(lo + kMagic52Bits), kMagic52);
+  return __dadd_rn(__dmul_rn(dh, 2147483648.0), dl);  // one rounding of the exact sum
+#else
+  return (double)v;
+#endif
+}
+// rint(x) (round half to even) for |x| <= 2^62
+__device__ __forceinline__ long long f64_to_s64_rn(double x) {
+#if SPCG_FIX_MAGIC
+  const double h = __dadd_rn(__dmul_rn(x, 4.656612873077392578125e-10), kMagic52);  // x / 2^31
+  const long long hi = __double_as_longlong(h) - kMagic52Bits;
+  const double rem = __dsub_rn(x, __dmul_rn(__dsub_rn(h, kMagic52), 2147483648.0));  // exact
+  const long long lo = __double_as_longlong(__dadd_rn(rem, kMagic52)) - kMagic52Bits;
+  return (hi << 31) + lo;
+#else
+  return __double2ll_rn(x);
+#endif
+}
+
+// Scale of the fixed-point accumulation: 2^(62 - eM - ex) with 2^ex >= max|x|
+// and 2^eM >= max_j sum_i |a_ij| (strict lower part), so every contribution
+// and every row total stays below 2^62 in magnitude; a power of two, so the
+// scaling itself is exact.
+__device__ __forceinline__ double fix_scale(const unsigned long long* xmax_bits, int eM) {
+  const double xmax = __longlong_as_double((long long)*xmax_bits);
+  int ex = 0;
+  if (xmax > 0.0) frexp(xmax, &ex);
+  return ldexp(1.0, 62 - eM - ex);
+}
 
 // Streaming read-only loads of matrix data (not written during a kernel).
 __device__ __forceinline__ double ld_stream_f64(const double* p) {

@@ -118,6 +118,7 @@ int dev_info(DevInfo** out) {
     SPCG_OCC_DIST(K_SCSR_PRIV, false)
     SPCG_OCC_DIST(K_SCSR_ATOMIC, false)
     SPCG_OCC_DIST(K_CSC, false)
+    SPCG_OCC_DIST(K_SCSR_FIX, false)
 #undef SPCG_OCC_DIST
     if (br < 1 || bp < 1) return fail(SPCG_ERR_CUDA, "CG kernel does not fit on an SM");
     d.coop_res = std::min(br * d.sms, 32 * kPollWarps * kPollPer);
@@ -186,6 +187,8 @@ struct DistWorkspace {
   // 1 = pass A only, 2 = all three passes for the spmv/dot/axpy split)
   cudaEvent_t tev[2][6][16] = {};
   DistArgs* args = nullptr;  // device copy of the rank's DistArgs (host transports)
+  unsigned long long* ytx = nullptr;  // K_SCSR_FIX: fixed-point transposed part (n words)
+  long long ytx_n = 0;
 };
 
 }  // namespace
@@ -230,6 +233,7 @@ struct spcg_matrix_s {
   std::vector<long long> halo;  // sorted global ids of the halo columns
   DistWorkspace dw;
   ClusPlan cp;
+  int tx_eM = -100000;  // K_SCSR_FIX: ceil(log2(max_j sum_i |a_ij|)) (unset: -100000)
   std::mutex mu;  // one solve at a time per handle (workspace reuse)
 };
 

@@ -54,7 +54,11 @@ constexpr int kRpCapA = kWideLines + 8;
 constexpr int kNzCap = kTileNnz + 16;
 
 // Kernel-level storage variants.
-enum KFmt : int { K_CSR = 0, K_SCSR_ATOMIC = 1, K_SCSR_PRIV = 2, K_CSC = 3 };
+// K_SCSR_FIX: the single pass over L+D of K_SCSR_ATOMIC, with the transposed
+// contributions accumulated EXACTLY in 64-bit fixed point (integer reds are
+// order-independent): the deterministic symmetric SpMV of the per-pass CG
+// engine without a stored L^T (dist.cuh).
+enum KFmt : int { K_CSR = 0, K_SCSR_ATOMIC = 1, K_SCSR_PRIV = 2, K_CSC = 3, K_SCSR_FIX = 4 };
 
 struct MatView {
   int n;
@@ -74,6 +78,11 @@ struct MatView {
                          // (reassociated, deterministic) instead of the in-order sum
   int wide;              // tiles may exceed kBlock lines (launch the WIDE instantiation)
   int cta0, ncta;        // CTAs [cta0, cta0 + ncta) work this view (ncta 0: the grid)
+  // K_SCSR_FIX: fixed-point accumulator of the transposed contributions, the
+  // bits of max|x| of the gathered vector, and ceil(log2(max_j sum_i |a_ij|))
+  unsigned long long* ytx;
+  const unsigned long long* txmax;
+  int tx_eM;
 };
 
 struct StageMeta {
@@ -286,6 +295,12 @@ __device__ __forceinline__ void smem_init(Smem& sm) {
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
 
