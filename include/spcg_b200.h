@@ -58,8 +58,12 @@ typedef enum {
 /* Accumulation contract of the symmetric scatter (config.py:13-35). */
 typedef enum {
   SPCG_ACC_ATOMIC = 0,      /* single pass over L+D, transpose scattered with fp64 red.add */
-  SPCG_ACC_PRIVATIZED = 1   /* deterministic owner-computes gather over a stored L^T;
-                               bitwise equal to the reference privatized mode at workers=1 */
+  SPCG_ACC_PRIVATIZED = 1   /* deterministic.  spcg_spmv: owner-computes gather over the
+                               stored L^T, bitwise the reference privatized mode at
+                               workers=1.  CG: resident engines gather the stored L^T
+                               rows on chip; the per-pass engine makes ONE pass over L+D
+                               and sums the transposed part exactly in 64-bit fixed
+                               point (row_sums = 1: the stored L^T instead) */
 } spcg_accumulation;
 
 typedef struct spcg_matrix_s* spcg_matrix_t;

@@ -15,6 +15,12 @@ Numerical contracts:
   spmv_sym    privatized: (L+D)x then + L^T x per row (owner-computes, no
               atomics) = reference privatized at workers=1, bit for bit;
               atomic: single pass, fp64 red.add scatter (order unspecified)
+  cg_solve    accumulation="privatized" (the default) is deterministic in
+              every engine: the streaming engine makes ONE pass over L+D
+              and accumulates the transposed part exactly in 64-bit fixed
+              point (order-independent integer reds; no L^T streamed);
+              row_sums="sequential" selects the stored-L^T rows instead
+              (bitwise the reference's privatized row sums at workers=1)
   dot         fixed-order two-level reduction (deterministic, reassociated)
   axpy        v + alpha*u with IEEE mul-then-add; alpha == 0 copies v
 """

@@ -99,9 +99,11 @@ def cg_solve(a, b, x0=None, opts: CgOptions | None = None, cfg: KernelConfig | N
 
     `b`/`x0` may be numpy arrays (x returned as numpy) or CUDA torch tensors
     (device-resident solve; x returned as a CUDA tensor).  `cfg.accumulation`
-    selects the symmetric-half mode: "privatized" (default, deterministic
-    owner-computes with a stored L^T) or "atomic" (single pass over L+D with
-    fp64 atomics).  `engine` 0 = auto.
+    selects the symmetric-half mode: "privatized" (default, deterministic:
+    resident engines use the stored L^T rows on chip, the streaming engine a
+    single pass over L+D with the transposed part summed exactly in 64-bit
+    fixed point) or "atomic" (single pass over L+D with fp64 atomics).
+    `engine` 0 = auto; `report.engine_info` names the engine that ran.
     """
     opts = opts or CgOptions()
     cfg = cfg or KernelConfig()
