@@ -108,6 +108,7 @@ struct DistArgs {
   const PeerTab* peer;
   const unsigned char* thalo;  // per tile of M: gathers halo columns
   int nrecv, nsendpeers;
+  int gpu_scope;               // every peer is on this device: gpu-scope exchange
   int nruns;                   // send runs (<= kRunCache: fused into pass C)
   const SendRun* runs;
   long long send_total;        // generic push: every send entry
@@ -238,23 +239,34 @@ __device__ __noinline__ void scalar_step(int op, StepState* S, double* hist) {
 __global__ void dist_scalar(int op, StepState* S, double* hist) { scalar_step(op, S, hist); }
 
 // ---- system-scope memory operations (peer memory over NVLink) ---------------
-__device__ __forceinline__ void fence_acq_rel_sys() {
-  asm volatile("fence.acq_rel.sys;" ::: "memory");
+// Scope of the exchange: system (peers are other GPUs: NVLink peer memory)
+// or gpu (virtual ranks of one launch on one device, DistArgs::gpu_scope).
+__device__ __forceinline__ void fence_acq_rel_sys(bool gpu = false) {
+  if (gpu) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  else asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
-__device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long* p, unsigned long long v,
+                                                   bool gpu = false) {
+  if (gpu) asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const unsigned long long* p) {
+__device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const unsigned long long* p,
+                                                                 bool gpu = false) {
   unsigned long long v;
-  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  if (gpu) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  else asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v,
+                                                   bool gpu = false) {
+  if (gpu) asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p,
+                                                                 bool gpu = false) {
   unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  if (gpu) asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  else asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 constexpr unsigned long long kP2PSpinLimit = 1ull << 34;  // ~minutes: a lost peer traps
@@ -264,29 +276,38 @@ constexpr unsigned long long kP2PSpinLimit = 1ull << 34;  // ~minutes: a lost pe
 // poll the own mailbox until all R tags are in, sum in rank order.  Two
 // banks by reduction parity make slot reuse safe (a rank can be at most one
 // reduction ahead of a slower reader).
+//
+// Called by a whole warp (lane k posts to rank k and polls rank k's slot, in
+// parallel; a warp-uniform loop, see the resident engines' exchange); the
+// rank-ordered total is returned in every lane, and lane 0 owns S.
 __device__ __noinline__ double mailbox_allreduce(const DistArgs& A, double s) {
+  const int lane = threadIdx.x & 31;
   StepState* S = A.S;
   const unsigned int seq = S->rseq + 1;
-  S->rseq = seq;
+  __syncwarp();
+  if (lane == 0) S->rseq = seq;
   const int R = A.nranks, bank = (int)(seq & 1u);
   const unsigned long long u = (unsigned long long)__double_as_longlong(s);
   const unsigned long long w0 = (u & 0xffffffff00000000ull) | seq, w1 = (u << 32) | seq;
-  for (int k = 0; k < R; ++k) {
-    unsigned long long* dst = A.peer->peer_mbox[k] + ((size_t)bank * R + A.rank) * 2;
-    st_relaxed_sys_u64(dst, w0);
-    st_relaxed_sys_u64(dst + 1, w1);
+  if (lane < R) {
+    unsigned long long* dst = A.peer->peer_mbox[lane] + ((size_t)bank * R + A.rank) * 2;
+    st_relaxed_sys_u64(dst, w0, A.gpu_scope);
+    st_relaxed_sys_u64(dst + 1, w1, A.gpu_scope);
   }
+  const unsigned long long* src = A.peer->mbox + ((size_t)bank * R + (lane < R ? lane : 0)) * 2;
+  unsigned long long a = 0, b = 0, spins = 0;
+  bool ok = lane >= R;
+  while (!__all_sync(0xffffffffu, ok)) {
+    if (!ok) {
+      a = ld_relaxed_sys_u64(src, A.gpu_scope);
+      b = ld_relaxed_sys_u64(src + 1, A.gpu_scope);
+      ok = (uint32_t)a == seq && (uint32_t)b == seq;
+    }
+    if (++spins > kP2PSpinLimit) asm volatile("trap;");
+  }
+  const double mine = __longlong_as_double((long long)((a & 0xffffffff00000000ull) | (b >> 32)));
   double tot = 0.0;
-  for (int k = 0; k < R; ++k) {
-    const unsigned long long* src = A.peer->mbox + ((size_t)bank * R + k) * 2;
-    unsigned long long a, b, spins = 0;
-    do {
-      a = ld_relaxed_sys_u64(src);
-      b = ld_relaxed_sys_u64(src + 1);
-      if (++spins > kP2PSpinLimit) asm volatile("trap;");
-    } while ((uint32_t)a != seq || (uint32_t)b != seq);
-    tot += __longlong_as_double((long long)((a & 0xffffffff00000000ull) | (b >> 32)));
-  }
+  for (int k = 0; k < R; ++k) tot += __shfl_sync(0xffffffffu, mine, k);  // rank order
   return tot;
 }
 
@@ -318,14 +339,18 @@ __device__ __forceinline__ void rank_sum(double v, SM& sm, const DistArgs& A, co
   double s = 0.0;
   for (int i = threadIdx.x; i < c.G; i += blockDim.x) s += __ldcg(A.part + i);
   s = block_sum(s, sm);
-  if (threadIdx.x == 0) {
-    S->counter = 0;
-    if (FUSED && post && op >= 0) {
-      S->red = mailbox_allreduce(A, s);
-      scalar_step(op, S, A.hist);
-    } else {
-      S->red = s;
+  if (FUSED && post && op >= 0) {
+    if (threadIdx.x < 32) {
+      const double tot = mailbox_allreduce(A, s);
+      if (threadIdx.x == 0) {
+        S->counter = 0;
+        S->red = tot;
+        scalar_step(op, S, A.hist);
+      }
     }
+  } else if (threadIdx.x == 0) {
+    S->counter = 0;
+    S->red = s;
   }
 }
 
@@ -339,7 +364,7 @@ __device__ __noinline__ void wait_halo(const DistArgs& A, unsigned int tag) {
     bool ok = f == nullptr;
     unsigned long long spins = 0;
     while (!__all_sync(0xffffffffu, ok)) {
-      if (!ok) ok = (uint32_t)ld_acquire_sys_u64(f) >= tag;
+      if (!ok) ok = (uint32_t)ld_acquire_sys_u64(f, A.gpu_scope) >= tag;
       if (++spins > kP2PSpinLimit) asm volatile("trap;");
     }
   }
@@ -354,7 +379,7 @@ __device__ __forceinline__ void halo_done(const DistArgs& A, const RankCta& c, S
   __shared__ bool last;
   __syncthreads();
   if (threadIdx.x == 0) {
-    fence_acq_rel_sys();
+    fence_acq_rel_sys(A.gpu_scope);
     const unsigned int t = atomicAdd(&A.S->counter, 1u);
     last = (t == (unsigned)c.G - 1);
   }
@@ -362,9 +387,29 @@ __device__ __forceinline__ void halo_done(const DistArgs& A, const RankCta& c, S
   if (!last || threadIdx.x != 0) return;
   A.S->counter = 0;
   A.S->hseq = tag;
-  fence_acq_rel_sys();
+  fence_acq_rel_sys(A.gpu_scope);
   for (int i = 0; i < A.nsendpeers; ++i)
-    st_release_sys_u64(A.peer->peer_hflag[A.peer->send_to[i]] + 2 * (size_t)A.rank, tag);
+    st_release_sys_u64(A.peer->peer_hflag[A.peer->send_to[i]] + 2 * (size_t)A.rank, tag,
+                       A.gpu_scope);
+}
+
+// Virtual-rank launches: the CTA's rank arguments copied into shared memory
+// (word by word by the first warps) with the rank's CTA range and the pass's
+// traversal flags patched in.
+__device__ __forceinline__ void stage_args(DistArgs& sA, const DistArgs& g, const RankCta& c,
+                                           int rev, int tree) {
+  static_assert(sizeof(DistArgs) % 8 == 0, "DistArgs copied in 8-byte words");
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&g);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(&sA);
+  for (int w = threadIdx.x; w < (int)(sizeof(DistArgs) / 8); w += blockDim.x) dst[w] = src[w];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    sA.M.cta0 = c.v * c.G;
+    sA.M.ncta = c.G;
+    sA.M.rev = rev;
+    sA.M.tree = tree;
+  }
+  __syncthreads();
 }
 
 // ---- pass A: q = A p_ext, red = p.q partial (skipped once done) -------------
@@ -439,12 +484,12 @@ __global__ void __launch_bounds__(kBlock, kStreamMinBlocks)
     dist_spmv_pq(const __grid_constant__ DistArgs A1, const DistArgs* __restrict__ DAs, int G,
                  int rev, int tree, int post) {
   if (MODE == 2) {
+    // the rank's arguments staged in shared memory (a register copy of the
+    // view spilled in the tile loop)
+    __shared__ DistArgs sA;
     const RankCta c = rank_cta(G);
-    const DistArgs& A = DAs[c.v];
-    MatView M = rank_view(A, c);
-    M.rev = rev;
-    M.tree = tree;
-    spmv_pq_body<FMT, WIDE, true>(A, M, c, post);
+    stage_args(sA, DAs[c.v], c, rev, tree);
+    spmv_pq_body<FMT, WIDE, true>(sA, sA.M, c, post);
   } else {
     spmv_pq_body<FMT, WIDE, MODE == 1>(A1, A1.M, rank_cta((int)gridDim.x), post);
   }
@@ -473,18 +518,18 @@ __global__ void __launch_bounds__(kElemBlock)
   __shared__ bool last;
   __syncthreads();
   if (threadIdx.x == 0) {
-    fence_acq_rel_sys();  // the reds are visible before the p.q post
+    fence_acq_rel_sys(A.gpu_scope);  // the reds are visible before the p.q post
     const unsigned int t = atomicAdd(&S->counter, 1u);
     last = (t == (unsigned)c.G - 1);
   }
   __syncthreads();
-  if (!last || threadIdx.x != 0) return;
+  if (!last || threadIdx.x >= 32) return;
+  const double tot = mailbox_allreduce(A, op >= 0 ? S->red : 0.0);
+  if (threadIdx.x != 0) return;
   S->counter = 0;
   if (op >= 0) {
-    S->red = mailbox_allreduce(A, S->red);
+    S->red = tot;
     scalar_step(op, S, A.hist);
-  } else {
-    mailbox_allreduce(A, 0.0);
   }
 }
 
@@ -538,9 +583,10 @@ __global__ void __launch_bounds__(kBlock, kStreamMinBlocks)
     dist_spmv(const __grid_constant__ DistArgs A1, const DistArgs* __restrict__ DAs, int G,
               int /*unused: launch-macro symmetry*/) {
   if (MODE == 2) {
+    __shared__ DistArgs sA;
     const RankCta c = rank_cta(G);
-    const DistArgs& A = DAs[c.v];
-    spmv_body<FMT, WIDE, true>(A, rank_view(A, c));
+    stage_args(sA, DAs[c.v], c, 0, 0);
+    spmv_body<FMT, WIDE, true>(sA, sA.M);
   } else {
     spmv_body<FMT, WIDE, MODE == 1>(A1, A1.M);
   }

@@ -308,6 +308,7 @@ struct spcg_dist_plan_s {
   SendRun* runs = nullptr;
   int nruns = 0;
   int nrecv = 0, nsendpeers = 0;
+  bool same_device = true;           // every peer mapped by pointer on this device
   int* send_peer = nullptr;
   long long* send_dst = nullptr;
   int* ghost_peer = nullptr;
@@ -362,10 +363,12 @@ int run_dist(const std::vector<DistArgs>& hA, DistArgs* dA, const HaloPlan* H, c
   const int nv = (int)hA.size();
   const bool fused = hA[0].peer != nullptr;
   const bool wide = FMT == K_CSR && v.wide;
+  // virtual ranks share the GPU: each gets 1/nv of the CTAs a lone rank
+  // would use, so a launch over all of them is one wave, as for one rank
   int G = 1;
   for (const DistArgs& a : hA)
-    G = std::max(G, std::min(std::max(1, a.M.ntiles), di->spmv_grid));
-  const int GE = 2 * di->sms;
+    G = std::max(G, std::min(std::max(1, a.M.ntiles), std::max(1, di->spmv_grid / nv)));
+  const int GE = std::max(1, 2 * di->sms / nv);
   const size_t sm = sizeof(Smem);
   constexpr int kAtom = (FMT == K_SCSR_ATOMIC || FMT == K_CSC) ? 1 : 0;
   constexpr bool kRev = (FMT == K_SCSR_ATOMIC);  // transposed scatters reach halo rows
@@ -409,7 +412,10 @@ int run_dist(const std::vector<DistArgs>& hA, DistArgs* dA, const HaloPlan* H, c
   };
   // kernel transport mode: 0 host transport, 1 device transport (one rank
   // per process), 2 device transport over nv virtual ranks in one launch
-  const int mode = !fused ? 0 : (nv > 1 ? 2 : 1);
+  // (SPCG_FORCE_GROUP=1: one rank through the virtual-rank kernels, to
+  // measure what the group form itself costs; scripts/p2p_overhead.py)
+  static const bool force_group = getenv("SPCG_FORCE_GROUP") != nullptr;
+  const int mode = !fused ? 0 : ((nv > 1 || force_group) ? 2 : 1);
   DistArgs a1 = hA[0];  // MODE 0 / 1: the rank's arguments by value
   a1.M.cta0 = 0;
   a1.M.ncta = 0;
@@ -871,6 +877,7 @@ int plan_connect(spcg_dist_plan_s* P, const unsigned char* blobs) {
     }
     CUDA_TRY(cudaIpcOpenMemHandle(dst, h, cudaIpcMemLazyEnablePeerAccess));
     P->opened.push_back(*dst);
+    P->same_device = false;  // another process: another GPU (system scope)
     return SPCG_OK;
   };
   int rc;
@@ -966,6 +973,7 @@ int plan_args(spcg_dist_plan_s* P, int kf, const double* b, const double* x0, do
   A.peer = P->d_peer;
   A.nrecv = P->nrecv;
   A.nsendpeers = P->nsendpeers;
+  A.gpu_scope = P->same_device ? 1 : 0;
   A.nruns = P->nruns;
   A.runs = P->runs;
   A.send_total = P->send_off.back();
