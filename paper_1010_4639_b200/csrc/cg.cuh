@@ -21,6 +21,9 @@ struct CgDevResult {
   double final_rel;
   double b_norm;
   double rec_rel;  // engine 6: the recursive rel of the last iteration
+  // resident cluster engines: the leader thread's loop time by phase (ns):
+  // [0] SpMV (with the partials' post), [1] reductions / waits, [2] updates
+  unsigned long long phase_ns[3];
 };
 
 struct CgArgs {

@@ -470,19 +470,18 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
     }
   }
 
-#if SPCG_TRACE
+  // phase times: the leader thread always (SolveReport.timings), every CTA's
+  // thread 0 when tracing
   unsigned long long tr[4] = {0, 0, 0, 0};
-  unsigned long long tlast = A.trace ? globaltimer_ns() : 0;
+  const bool tl = tid == 0 && (gme == 0 || (SPCG_TRACE && A.trace));
+  unsigned long long tlast = tl ? globaltimer_ns() : 0;
   auto mark = [&](int ph) {
-    if (A.trace && tid == 0) {
+    if (tl) {
       const unsigned long long t = globaltimer_ns();
       tr[ph] += t - tlast;
       tlast = t;
     }
   };
-#else
-  auto mark = [](int) {};
-#endif
   for (long long it = 0; status == ST_OK && it < max_it; ++it) {
     const int rb = (int)(it & 1), wb = rb ^ 1;
     const double na = -alpha;
@@ -608,6 +607,9 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
     A.res->status = ST_OK;
     A.res->final_rel = rel;
     A.res->b_norm = b_norm;
+    A.res->phase_ns[0] = tr[1];  // SpMV
+    A.res->phase_ns[1] = tr[2];  // all-reduce
+    A.res->phase_ns[2] = tr[0];  // update
   }
 }
 

@@ -487,7 +487,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   // per-phase trace (A.trace set: SPCG_TRACE / SPCG_CLUS_DEBUG): thread 0 of
   // every CTA accumulates [partials+SpMV, wait A, send n + barrier B, scalars
   // + update + halo + sync] ns, then records its SM id and start / end times
-  const bool tr = A.trace != nullptr && tid == 0;
+  // the leader thread always (SolveReport.timings), every CTA when tracing
+  const bool tr = tid == 0 && (A.trace != nullptr || gme == 0);
   unsigned long long tph[4] = {0, 0, 0, 0};
   const unsigned long long tkern0 = tr ? globaltimer_ns() : 0;
   double alpha = 0.0, beta = 0.0;
@@ -647,7 +648,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     __syncthreads();
     if (tr) tph[3] += globaltimer_ns() - t3;
   }
-  if (tr) {
+  if (tr && A.trace) {
     unsigned int smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     for (int ph = 0; ph < 4; ++ph) A.trace[gme * 8 + ph] = tph[ph];
@@ -698,6 +699,9 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     A.res->final_rel = rel;
     A.res->b_norm = b_norm;
     A.res->rec_rel = rec_rel;
+    A.res->phase_ns[0] = tph[0];            // partials + SpMV
+    A.res->phase_ns[1] = tph[1] + tph[2];   // waits, exchange, barrier B
+    A.res->phase_ns[2] = tph[3];            // update + halo rows
   }
 }
 

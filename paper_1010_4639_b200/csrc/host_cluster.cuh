@@ -622,6 +622,11 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
   out->fallbacks = 0;
   out->cond_estimate = cond;
   out->phase_ms[0] = out->phase_ms[1] = out->phase_ms[2] = 0.0;
+  if (r.status == SPCG_OK && r.iterations > 0) {  // the leader's loop phases
+    out->phase_ms[0] = (double)r.phase_ns[0] / 1e6;
+    out->phase_ms[2] = (double)r.phase_ns[2] / 1e6;
+    out->phase_ms[1] = std::max(0.0, (double)ms - out->phase_ms[0] - out->phase_ms[2]);
+  }
   if (r.status != SPCG_OK) {
     const char* what = r.status == SPCG_ERR_NOT_SPD ? "matrix not positive definite"
                        : r.status == SPCG_ERR_NONFINITE_ALPHA ? "non-finite alpha"

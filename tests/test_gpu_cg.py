@@ -250,3 +250,20 @@ def test_torch_resident_solve():
     assert r.x.is_cuda and r.converged
     o = O.cg_solve("csr", a.row_start, a.col_idx, a.values, b.cpu().numpy())
     assert np.linalg.norm(r.x.cpu().numpy() - o.x) / np.linalg.norm(o.x) <= 1e-8
+
+
+@pytest.mark.parametrize("engine,kind", [(0, "fem"), (5, "fem"), (2, "fem"), (0, "p3")])
+def test_timings_split_spmv_dot_axpy(engine, kind):
+    """SolveReport.timings carries the reference's keys (solver.py:98-105)
+    with the device time split by phase: the per-pass engine times its passes
+    with CUDA events, the cluster engines their leader thread's loop phases."""
+    from paper_1010_4639_b200 import CgOptions, cg_solve
+    from paper_1010_4639_b200.genprob import fem_mesh, poisson3d, rhs_for
+
+    a = fem_mesh() if kind == "fem" else poisson3d(40, 40, 40)
+    b, _ = rhs_for(a, seed=1)
+    r = cg_solve(a, b, opts=CgOptions(), engine=engine)
+    t = r.timings
+    assert set(t) == {"spmv", "dot", "axpy", "total"}
+    assert t["spmv"] > 0 and t["dot"] > 0 and t["axpy"] > 0, t
+    assert t["spmv"] + t["dot"] + t["axpy"] <= t["total"] * 1.001
