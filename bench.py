@@ -269,6 +269,38 @@ def cpu_sample(workload: str, steps: int, warmup: int, window: int):
             "iterations_per_step": its[0], "s_per_step": float(np.median(times))}
 
 
+def time_upload(workload: str):
+    """The drop-in path's first-use cost: cg_solve(CsrMatrix(...)) uploads the
+    host matrix once (spcg_matrix_create_host: raw int64 / fp64 arrays copied
+    to the device, converted to int32 and validated there, row tiles built).
+    Timed on the host arrays of the CPU baseline (same system)."""
+    import ctypes
+
+    import torch
+
+    from paper_1010_4639_b200 import _native as N
+
+    kind, rs, ci, v, _ = host_system(workload)
+    fmt = N.FMT_SCSR if kind == "sym" else N.FMT_CSR
+    n, nnz = len(rs) - 1, len(ci)
+    lib = N.load()
+    times = []
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        h = ctypes.c_void_p()
+        N.check(lib.spcg_matrix_create_host(fmt, n, nnz, rs.ctypes.data, ci.ctypes.data,
+                                            v.ctypes.data, ctypes.byref(h)), "upload")
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+        lib.spcg_matrix_destroy(h)
+    host_bytes = 8 * (n + 1) + 16 * nnz
+    return {"s": round(min(times), 3), "host_GB": round(host_bytes / 1e9, 2),
+            "GBs": round(host_bytes / min(times) / 1e9, 1),
+            "what": "spcg_matrix_create_host on the int64/fp64 host arrays (pageable), "
+                    "device-side conversion + validation + tiles; best of 2"}
+
+
 # ---- our arm ---------------------------------------------------------------------
 def _opts(N, acc, max_iter=0, timing=1):
     return N.CgOptionsC(tol=1e-10, max_iter=max_iter, record_history=0,
@@ -481,6 +513,7 @@ def run_ours(args):
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_sample(args.workload, steps=3, warmup=1,
                                           window=WINDOW.get(args.workload, 20))
+        line["upload"] = time_upload(args.workload)
     if not args.no_secondary and args.workload == "p3":
         line["secondary"] = secondary(peak, cpu=not args.no_cpu_baseline)
     print(json.dumps(line), flush=True)

@@ -46,6 +46,9 @@ constexpr int kClusSlicesPerWarp = 2048 / kClusThreads;
 constexpr int kClusMaxRows = kClusWarps * kClusSlicesPerWarp * 32;  // 2048 per CTA
 constexpr int kClusMax = 16;      // CTAs in one cluster (non-portable above 8)
 constexpr int kClusGridMax = 256;  // CTAs of a multi-cluster grid (K clusters of 8)
+#ifndef SPCG_PHASE_TIMERS
+#define SPCG_PHASE_TIMERS 1  // leader-thread phase times for SolveReport.timings
+#endif
 #ifndef SPCG_CLUS_POST_FENCE
 #define SPCG_CLUS_POST_FENCE 0  // (A/B) fence after the leader's post
 #endif
@@ -473,7 +476,7 @@ __global__ void __launch_bounds__(kClusThreads, 1) clus_cg_kernel(const ClusArgs
   // phase times: the leader thread always (SolveReport.timings), every CTA's
   // thread 0 when tracing
   unsigned long long tr[4] = {0, 0, 0, 0};
-  const bool tl = tid == 0 && (gme == 0 || (SPCG_TRACE && A.trace));
+  const bool tl = tid == 0 && ((SPCG_PHASE_TIMERS && gme == 0) || (SPCG_TRACE && A.trace));
   unsigned long long tlast = tl ? globaltimer_ns() : 0;
   auto mark = [&](int ph) {
     if (tl) {

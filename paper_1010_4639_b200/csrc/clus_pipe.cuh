@@ -79,6 +79,18 @@ struct PipeShared {
 // (A/B) fence after the leader's slot post: a partial cure of the
 // occasional 2.2-2.5x slower solve before its cause was found (the divergent
 // spin of the leaders' poll, now warp-uniform; profiles/r02/bimodal.md)
+// (A/B) warp-uniform tagged halo loads: not needed against the slow mode
+// (0 slow solves in 120 without them) and 0.16-0.2 us per iteration dearer
+// (profiles/r02/bimodal/ab_uniform.log), so off
+#ifndef SPCG_UNIFORM_HALO
+#define SPCG_UNIFORM_HALO 0
+#endif
+#ifndef SPCG_XCHG_TRACE
+#define SPCG_XCHG_TRACE 0  // exchange timeline of iterations 100-107 (SPCG_CLUS_DEBUG)
+#endif
+#ifndef SPCG_UNIFORM_XCHG
+#define SPCG_UNIFORM_XCHG 1  // (A/B) warp-uniform leaders' poll
+#endif
 #ifndef SPCG_PIPE_POST_FENCE
 #define SPCG_PIPE_POST_FENCE 0  // 0: none, 1: fence.acq_rel.gpu, 2: fence.sc.gpu
 #endif
@@ -121,6 +133,7 @@ __device__ __forceinline__ double tagged_finish(const volatile unsigned long lon
   // warp-uniform over the lanes that arrived together: no lane spins alone
   // while its finished neighbours wait at a reconvergence point (see the
   // leaders' poll in exchange())
+#if SPCG_UNIFORM_HALO
   const unsigned m = __activemask();
   bool ok = (uint32_t)a == tag && (uint32_t)b == tag;
   while (!__all_sync(m, ok)) {
@@ -133,6 +146,12 @@ __device__ __forceinline__ double tagged_finish(const volatile unsigned long lon
     }
     if (++spins > kSpinLimit) asm volatile("trap;");
   }
+#else
+  while ((uint32_t)a != tag || (uint32_t)b != tag) {
+    tagged_issue(src, a, b);
+    if (++spins > kSpinLimit) asm volatile("trap;");
+  }
+#endif
   return __longlong_as_double((long long)((a & 0xffffffff00000000ull) | (b >> 32)));
 }
 // Warp-uniform tagged load: all 32 lanes call it; lanes with act = false
@@ -274,7 +293,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   auto exchange = [&](int bank, uint32_t tag, bool fenced) {
     // exchange trace (A.trace): iterations 100..107 of every cluster leader:
     // [post time, done time, time lane k saw cluster k's slot]
-    unsigned long long* xr = (A.trace && cur_it >= 100 && cur_it < 108)
+    unsigned long long* xr = (SPCG_XCHG_TRACE && A.trace && cur_it >= 100 && cur_it < 108)
         ? A.trace + 8 * (size_t)gridDim.x + ((size_t)kc * 8 + (size_t)(cur_it - 100)) * 34
         : nullptr;
     double t0 = 0.0, t1 = 0.0;
@@ -317,7 +336,11 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       const volatile unsigned long long* src = gb + kClusSlotWords * (lane < K ? lane : 0);
       unsigned long long a = 0, b = 0, c = 0, d = 0, spins = 0;
       bool ok = lane >= K;
+#if SPCG_UNIFORM_XCHG
       while (!__all_sync(0xffffffffu, ok)) {
+#else
+      while (!ok) {
+#endif
         if (!ok) {
           d = src[3];
           if ((uint32_t)d == tag) {
@@ -383,10 +406,16 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   };
   // warp-uniform: every lane of a row warp calls it (act = false: no halo row)
   auto halo_n = [&](bool act, int buf, int h, uint32_t tag) {
+#if SPCG_UNIFORM_HALO
     const bool loc = act && halo_local(h);
     const double r = tagged_load_warp(act && !loc,
                                       gh + (((size_t)buf * G + gme) * A.hcap + (act ? h : 0)) * 2, tag);
     return loc ? nhalo[(size_t)buf * A.hcap + h] : r;
+#else
+    if (!act) return 0.0;
+    if (halo_local(h)) return nhalo[(size_t)buf * A.hcap + h];
+    return tagged_load(gh + (((size_t)buf * G + gme) * A.hcap + h) * 2, tag);
+#endif
   };
   // remote: the epoch-tagged global part (other clusters), else the DSMEM part
   auto send_n = [&](const double* nv, int buf, uint32_t tag, bool remote) {
@@ -488,7 +517,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   // every CTA accumulates [partials+SpMV, wait A, send n + barrier B, scalars
   // + update + halo + sync] ns, then records its SM id and start / end times
   // the leader thread always (SolveReport.timings), every CTA when tracing
-  const bool tr = tid == 0 && (A.trace != nullptr || gme == 0);
+  const bool tr = tid == 0 && (A.trace != nullptr || (SPCG_PHASE_TIMERS && gme == 0));
   unsigned long long tph[4] = {0, 0, 0, 0};
   const unsigned long long tkern0 = tr ? globaltimer_ns() : 0;
   double alpha = 0.0, beta = 0.0;
