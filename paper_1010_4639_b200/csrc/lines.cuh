@@ -1,11 +1,7 @@
 // lines.cuh — per-line SpMV bodies over a staged tile (one thread per line).
 //
-// The gathered vector is abstracted as a "source":
-//   SrcPlain  x_j            (y = A x; r0 = b - A x0; true residual)
-//   SrcFirst  r_j            (CG iteration 1: p_1 = r_0, solver.py:123)
-//   SrcFold   r_j + beta*p_j (CG iteration k>1: the p-update of solver.py:156
-//                             folded into the next SpMV's gather, so p is never
-//                             re-read and re-written in a separate pass)
+// The gathered vector is abstracted as a "source" (SrcPlain: x_j; the
+// resident single-reduction engine's folded r-update: SrcCgcg in cg1.cuh).
 // Row sums are formed sequentially in storage order with IEEE mul-then-add, so
 // a CSR row equals _ckernels.csr_gather (_ckernels.pyx:42-47) bit for bit.
 #pragma once
@@ -16,18 +12,6 @@ namespace spcg {
 struct SrcPlain {
   const double* x;
   __device__ __forceinline__ double get(int j) const { return x[j]; }
-};
-struct SrcFirst {
-  const double* r;
-  __device__ __forceinline__ double get(int j) const { return r[j]; }
-};
-struct SrcFold {
-  const double* r;
-  const double* p;
-  double beta;
-  __device__ __forceinline__ double get(int j) const {
-    return __dadd_rn(r[j], __dmul_rn(beta, p[j]));
-  }
 };
 
 #ifndef SPCG_UNROLL
