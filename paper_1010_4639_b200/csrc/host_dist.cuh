@@ -517,12 +517,20 @@ int run_dist(const std::vector<DistArgs>& hA, DistArgs* dA, const HaloPlan* H, c
   constexpr bool kAlternate = SPCG_ALTERNATE != 0;
   const int tree = o->row_sums == 0;  // auto: reassociated long-row sums in pass A
   const int post = ghosts ? 0 : 1;
+  static const int dir_mode = getenv("SPCG_PASS_DIR") ? atoi(getenv("SPCG_PASS_DIR")) : -1;
   auto enqueue_chunk = [&](int bb) -> int {
     for (int c = 0; c < chunk; ++c) {
       if (timing) CUDA_TRY(cudaEventRecord(d0.tev[bb][0][c], st));
       // alternate traversal directions pass to pass (A, B, C, A, ...): each
       // pass starts on the lines the previous one wrote last (still in L2)
-      const int dirA = kAlternate ? (int)((iter_enq & 1) == 0) : 0;
+      // pass A runs last-to-first always on the regular tiles (P3 1,676 ->
+      // 1,653 us per iteration: its reverse traversal streams 5 % faster,
+      // more than the L2 reuse alternation bought; Q27 neutral) and
+      // alternates on the wide tiles (P2 417.7 vs 420.1); scripts/phase_split.py
+      int dirA = kAlternate ? (wide ? (int)((iter_enq & 1) == 0) : 1) : 0;
+      // (A/B) SPCG_PASS_DIR: 0 / 1 a fixed pass-A direction, 2 alternate
+      if (dir_mode == 0 || dir_mode == 1) dirA = dir_mode;
+      if (dir_mode == 2) dirA = (int)((iter_enq & 1) == 0);
       a1.M.rev = dirA;
       a1.M.tree = tree;
       if (kFix) {  // iteration parity: A / B read slot k&1, C fills (B clears) slot (k+1)&1
