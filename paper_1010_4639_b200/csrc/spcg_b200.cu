@@ -61,6 +61,10 @@ struct DevInfo {
   int major = 0, minor = 0;
   int coop_res = 0;     // co-resident CTAs of the resident CG kernel
   int spmv_grid = 0;
+  // stream-ordered scratch (dot partials): a library-owned pool that keeps
+  // its memory (the default pool's release threshold of 0 would hand the
+  // pages back at every synchronize and re-map them, ~ms, at the next call)
+  cudaMemPool_t pool = nullptr;
 };
 
 std::mutex g_dev_mutex;
@@ -123,6 +127,14 @@ int dev_info(DevInfo** out) {
     if (br < 1 || bp < 1) return fail(SPCG_ERR_CUDA, "CG kernel does not fit on an SM");
     d.coop_res = std::min(br * d.sms, 32 * kPollWarps * kPollPer);
     d.spmv_grid = bp * d.sms;
+    cudaMemPoolProps pp = {};
+    pp.allocType = cudaMemAllocationTypePinned;
+    pp.handleTypes = cudaMemHandleTypeNone;
+    pp.location.type = cudaMemLocationTypeDevice;
+    pp.location.id = dev;
+    CUDA_TRY(cudaMemPoolCreate(&d.pool, &pp));
+    unsigned long long keep = ~0ULL;
+    CUDA_TRY(cudaMemPoolSetAttribute(d.pool, cudaMemPoolAttrReleaseThreshold, &keep));
     d.device = dev;
   }
   *out = &d;
@@ -402,7 +414,7 @@ int spcg_dot(int64_t n, const double* d_u, const double* d_v, double* d_out, voi
   // or on several devices, never share a buffer)
   const int nb = (int)std::min<long long>(2LL * d->sms, (n + kBlock - 1) / kBlock);
   double* part = nullptr;
-  CUDA_TRY(cudaMallocAsync((void**)&part, sizeof(double) * (size_t)nb, st));
+  CUDA_TRY(cudaMallocFromPoolAsync((void**)&part, sizeof(double) * (size_t)nb, d->pool, st));
   dot_partial_kernel<<<nb, kBlock, 0, st>>>(n, d_u, d_v, part);
   CUDA_TRY(cudaGetLastError());
   dot_final_kernel<<<1, kBlock, 0, st>>>(nb, part, d_out);
