@@ -45,11 +45,21 @@ constexpr int kPipeMaxSlices = kPipeRowWarps * kClusSlicesPerWarp;  // per CTA (
 constexpr int kPipeMaxSlices2 = kPipeRowWarps * 2;
 
 struct PipeShared {
-  double slot[2][kClusMax][2];
+  double slot[2][kClusMax][2];  // setup / tail all-reduce (cluster barriers)
   double red[2][kPipeWarps];
   double tot[2][2];
   ClusSend send[kClusSendCache];
+  // the loop's messages (by iteration parity): rank 0 gathers every row warp's
+  // partials of the cluster in wslot (mbA); every CTA receives the totals in
+  // ltot and its cluster neighbours' boundary n in nhalo (mbB)
+  double wslot[2][kClusMax][kPipeRowWarps][2];
+  double ltot[2][2];
+  uint64_t mbA[2], mbB[2];
+  int nloc;  // halo rows owned inside the cluster
 };
+// static shared memory of the larger of the two cluster kernels (the plan's
+// dynamic budget is shared by engines 5 and 6)
+constexpr size_t kClusStatic = sizeof(PipeShared) > sizeof(ClusShared) ? sizeof(PipeShared) : sizeof(ClusShared);
 
 // split cluster barrier
 #ifndef SPCG_PIPE_FENCED
@@ -84,6 +94,9 @@ struct PipeShared {
 // (profiles/r02/bimodal/ab_uniform.log), so off
 #ifndef SPCG_UNIFORM_HALO
 #define SPCG_UNIFORM_HALO 0
+#endif
+#ifndef SPCG_PIPE_FINE
+#define SPCG_PIPE_FINE 0  // (A/B build) 8 sub-phase timers per CTA into the trace's tail
 #endif
 #ifndef SPCG_XCHG_TRACE
 #define SPCG_XCHG_TRACE 0  // exchange timeline of iterations 100-107 (SPCG_CLUS_DEBUG)
@@ -247,7 +260,28 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       sbase[k] = (sres[k] ? sd.soff : sd.goff) + lane;
     }
   }
+  if (tid == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&cs.mbA[i], 1);
+      mbar_init(&cs.mbB[i], 1);
+    }
+    fence_mbar_init();  // visible to the cluster at the first cluster barrier
+    cs.nloc = 0;
+  }
   __syncthreads();
+  {
+    // bytes this CTA receives per iteration on mbB: the totals and one double
+    // per halo row owned inside the cluster
+    int cnt = 0;
+    for (int h = tid; h < nh; h += kPipeThreads) {
+      const int hrow = h < P.hlo ? P.wlo + h : P.row_hi + (h - P.hlo);
+      cnt += (hrow >= P.clo && hrow < P.chi) ? 1 : 0;
+    }
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if (lane == 0 && cnt) atomicAdd(&cs.nloc, cnt);
+  }
+  __syncthreads();
+  const int bbytes = 16 + 8 * cs.nloc;
 
   auto spmv = [&](double* out) {
 #pragma unroll
@@ -290,17 +324,14 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   // (setup / tail: scratch and x windows); inside the loop it carries only
   // its own epoch-tagged words, so it needs no fence
   long long cur_it = -1;  // loop iteration of the exchange (exchange trace)
-  auto exchange = [&](int bank, uint32_t tag, bool fenced) {
+  // v0, v1: this cluster's sums in, the grid's sums (cluster order) out
+  auto exchange_core = [&](int bank, uint32_t tag, bool fenced, double& v0, double& v1) {
     // exchange trace (A.trace): iterations 100..107 of every cluster leader:
     // [post time, done time, time lane k saw cluster k's slot]
     unsigned long long* xr = (SPCG_XCHG_TRACE && A.trace && cur_it >= 100 && cur_it < 108)
         ? A.trace + 8 * (size_t)gridDim.x + ((size_t)kc * 8 + (size_t)(cur_it - 100)) * 34
         : nullptr;
-    double t0 = 0.0, t1 = 0.0;
-    for (int c = 0; c < C; ++c) {
-      t0 += cs.slot[bank][c][0];
-      t1 += cs.slot[bank][c][1];
-    }
+    const double t0 = v0, t1 = v1;
     unsigned long long* gb = A.gslots + (size_t)bank * K * kClusSlotWords;
     if (lane == 0) {
       if (fenced) fence_acq_rel_gpu();
@@ -367,12 +398,24 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       s0 += __shfl_sync(0xffffffffu, c0, k);
       s1 += __shfl_sync(0xffffffffu, c1, k);
     }
+    if (xr && lane == 0) xr[1] = globaltimer_ns();
+    v0 = s0;
+    v1 = s1;
+  };
+  // blocking form (setup and tail): the cluster's slots in, the grid totals
+  // out to every cluster CTA's tot[bank] (DSMEM)
+  auto exchange = [&](int bank, uint32_t tag, bool fenced) {
+    double s0 = 0.0, s1 = 0.0;
+    for (int c = 0; c < C; ++c) {
+      s0 += cs.slot[bank][c][0];
+      s1 += cs.slot[bank][c][1];
+    }
+    exchange_core(bank, tag, fenced, s0, s1);
     if (lane < C) {
       double* d2 = cl.map_shared_rank(&cs.tot[bank][0], lane);
       d2[0] = s0;
       d2[1] = s1;
     }
-    if (xr && lane == 0) xr[1] = globaltimer_ns();
   };
   auto totals = [&](int bank, double& v0, double& v1) {
     if (K > 1) {
@@ -417,22 +460,26 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     return tagged_load(gh + (((size_t)buf * G + gme) * A.hcap + h) * 2, tag);
 #endif
   };
-  // remote: the epoch-tagged global part (other clusters), else the DSMEM part
-  auto send_n = [&](const double* nv, int buf, uint32_t tag, bool remote) {
+  // boundary n to the neighbours of this iteration: st.async into the cluster
+  // neighbours' nhalo[buf] (completing on their mbB[buf]), epoch-tagged global
+  // words for other clusters' CTAs
+  auto send_n = [&](const double* nv, int buf, uint32_t tag) {
     for (int e = 0; e < P.nsend; ++e) {
       const ClusSend sd = e < kClusSendCache ? cs.send[e] : A.sends[P.send0 + e];
-      if ((sd.dst / C != kc) != remote) continue;
-      if (remote) {
+      if (sd.dst / C != kc) {
         volatile unsigned long long* dst = gh + ((size_t)buf * G + sd.dst) * A.hcap * 2;
 #pragma unroll
         for (int k = 0; k < NS; ++k)
           if (rrow[k] >= sd.lo && rrow[k] < sd.hi)
             tagged_store(dst + 2 * (size_t)(sd.dst_off + rrow[k] - sd.lo), nv[k], tag);
       } else {
-        double* dst = cl.map_shared_rank(nhalo + (size_t)buf * A.hcap, sd.dst % C);
+        const uint32_t r = (uint32_t)(sd.dst % C);
+        const uint32_t base = mapa_u32(nhalo + (size_t)buf * A.hcap, r);
+        const uint32_t bar = mapa_u32(&cs.mbB[buf], r);
 #pragma unroll
         for (int k = 0; k < NS; ++k)
-          if (rrow[k] >= sd.lo && rrow[k] < sd.hi) dst[sd.dst_off + rrow[k] - sd.lo] = nv[k];
+          if (rrow[k] >= sd.lo && rrow[k] < sd.hi)
+            st_async_f64(base + 8u * (uint32_t)(sd.dst_off + rrow[k] - sd.lo), nv[k], bar);
       }
     }
   };
@@ -519,6 +566,16 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   // the leader thread always (SolveReport.timings), every CTA when tracing
   const bool tr = tid == 0 && (A.trace != nullptr || (SPCG_PHASE_TIMERS && gme == 0));
   unsigned long long tph[4] = {0, 0, 0, 0};
+  // SPCG_PIPE_FINE: [partials, arrive A, deferred halo, SpMV, wait A, send n
+  // local, send n remote, arrive B, wait B, scalars, own-row update, halo
+  // rows + sync]
+  unsigned long long tfine[15] = {}, tfl = 0;
+#define SPCG_FT(j)                                          \
+  if (SPCG_PIPE_FINE && tr) {                               \
+    const unsigned long long tn_ = clock64();               \
+    tfine[j] += tn_ - tfl;                                  \
+    tfl = tn_;                                              \
+  }
   const unsigned long long tkern0 = tr ? globaltimer_ns() : 0;
   double alpha = 0.0, beta = 0.0;
   // deferred inter-cluster halo update: CSR/CSC 4.44 -> 3.95 us/iteration on
@@ -528,25 +585,70 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   bool pend = false;  // inter-cluster halo rows of the last update still to do
   int pbuf = 0;
   uint32_t ptag = 0;
+  // in-loop messages (no cluster barrier): every row warp's partials go by
+  // st.async to cluster rank 0 (wslot, completing on its mbA); rank 0's comm
+  // warp sums them in (CTA, warp) order, runs the leaders' exchange (K > 1)
+  // and st.asyncs the totals to every CTA's ltot (completing on mbB), where
+  // the boundary n of the cluster neighbours (st.async into nhalo) land too.
+  // A CTA waits only for its own mbB: no CTA waits for the slowest of the
+  // cluster.  Buffers alternate by iteration parity; a sender is never two
+  // iterations ahead of a receiver (iteration i+2's sends need the totals of
+  // i+1, which need every CTA's partials of i+1, posted after its reads of i).
+  const uint32_t bA0 = mapa_u32(&cs.mbA[0], 0), bA1 = mapa_u32(&cs.mbA[1], 0);
+  const uint32_t wsl0 = mapa_u32(&cs.wslot[0][me][wp][0], 0);
+  const uint32_t wsl1 = mapa_u32(&cs.wslot[1][me][wp][0], 0);
   for (long long it = 0; max_it > 0; ++it) {
     const int bank = (int)(epoch++ & 1u), buf = (int)(it & 1);
     const uint32_t tag = epoch;
+    const uint32_t mpar = (uint32_t)(it >> 1) & 1u;  // mbarrier phase parity of this use
     const unsigned long long t0 = tr ? globaltimer_ns() : 0;
+    if (SPCG_PIPE_FINE) tfl = clock64();
     cur_it = it;
-    double g = 0.0, d = 0.0;
-#pragma unroll
-    for (int k = 0; k < NS; ++k)
-      if (rrow[k] >= 0) {
-        g = fma(rg[k], rg[k], g);
-        d += rg[k] * wg[k];
+    if (tid == 0) mbar_arrive_expect_tx(&cs.mbB[buf], (uint32_t)bbytes);
+    if (comm) {
+      if (me == 0) {
+        if (lane == 0) mbar_arrive_expect_tx(&cs.mbA[buf], (uint32_t)(C * kPipeRowWarps * 16));
+        const bool trc = SPCG_PIPE_FINE && A.trace && lane == 0;
+        unsigned long long tc0 = trc ? clock64() : 0;
+        mbar_wait_cluster(&cs.mbA[buf], mpar);
+        if (trc) {
+          const unsigned long long tn = clock64();
+          tfine[12] += tn - tc0;
+          tc0 = tn;
+        }
+        // lane w: warp w's partials over the cluster's CTAs; then the warps in
+        // a fixed tree (the same bits on every lane after the broadcast)
+        double c0 = 0.0, c1 = 0.0;
+        if (lane < kPipeRowWarps)
+          for (int c = 0; c < C; ++c) {
+            c0 += cs.wslot[buf][c][lane][0];
+            c1 += cs.wslot[buf][c][lane][1];
+          }
+        c0 = __shfl_sync(0xffffffffu, warp_sum(c0), 0);
+        c1 = __shfl_sync(0xffffffffu, warp_sum(c1), 0);
+        if (K > 1) exchange_core(bank, tag, SPCG_PIPE_FENCED, c0, c1);
+        if (trc) {
+          const unsigned long long tn = clock64();
+          tfine[13] += tn - tc0;
+        }
+        if (lane < C) st_async_v2f64(mapa_u32(&cs.ltot[buf][0], lane), c0, c1, mapa_u32(&cs.mbB[buf], lane));
       }
-    post_partials(g, d, bank);
-    cluster_arrive_rel();  // A: the slots of this iteration
-    if (kDefer && pend) {
-      // the last update's halo rows owned by other clusters: their n arrives
-      // through L2, so the load latency overlaps the partials' reduction
-      // instead of sitting before the barrier; the SpMV waits for them
-      if (!comm) {
+    } else {
+      double g = 0.0, d = 0.0;
+#pragma unroll
+      for (int k = 0; k < NS; ++k)
+        if (rrow[k] >= 0) {
+          g = fma(rg[k], rg[k], g);
+          d += rg[k] * wg[k];
+        }
+      g = warp_sum(g);
+      d = warp_sum(d);
+      if (lane == 0) st_async_v2f64(buf ? wsl1 : wsl0, g, d, buf ? bA1 : bA0);
+      SPCG_FT(0)
+      if (kDefer && pend) {
+        // the last update's halo rows owned by other clusters: their n arrives
+        // through L2, so the load latency overlaps the partials' reduction;
+        // the SpMV waits for them
         const double na = -alpha;
         for (int hb = tid - lane; hb < nh; hb += kPipeRowThreads) {  // warp-uniform trip count
           const int h = hb + lane;
@@ -561,35 +663,25 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
         }
         asm volatile("bar.sync 1, %0;" ::"r"(kPipeRowThreads) : "memory");
       }
-      pend = false;
+      SPCG_FT(1)
     }
+    pend = false;
     double ng[NS];
-    spmv(ng);  // n = A w, overlapped with the all-reduce
+    spmv(ng);  // n = A w (the comm warp has no rows), overlapped with the all-reduce
+    SPCG_FT(2)
     const unsigned long long t1 = tr ? globaltimer_ns() : 0;
-    cluster_wait_acq();
-    const unsigned long long t2 = tr ? globaltimer_ns() : 0;
-    if (comm && K > 1 && me == 0) exchange(bank, tag, SPCG_PIPE_FENCED);
-#if SPCG_PIPE_LATE_REMOTE
-    // (A/B only) the tagged global halo stored after arrive(B), so the
-    // release of B does not wait for it: CSR 4.31 -> 4.35, SCSR 5.06 -> 4.92
-    // us/iteration on one box (profiles/r01/s4/pipe_late.log): no clear win
-    send_n(ng, buf, tag, false);
-    cluster_arrive_rel();  // B: cluster totals and intra-cluster halo n
-    send_n(ng, buf, tag, true);
-#else
-    send_n(ng, buf, tag, false);
-    send_n(ng, buf, tag, true);
-    cluster_arrive_rel();  // B: cluster totals and intra-cluster halo n
-#endif
-    cluster_wait_acq();
+    const unsigned long long t2 = t1;
+    if (!comm) send_n(ng, buf, tag);
+    SPCG_FT(3)
+    mbar_wait_cluster(&cs.mbB[buf], mpar);  // totals + the cluster neighbours' boundary n
+    SPCG_FT(4)
     const unsigned long long t3 = tr ? globaltimer_ns() : 0;
     if (tr) {
       tph[0] += t1 - t0;
       tph[1] += t2 - t1;
       tph[2] += t3 - t2;
     }
-    double g_new, d_new;
-    totals(bank, g_new, d_new);
+    const double g_new = cs.ltot[buf][0], d_new = cs.ltot[buf][1];
     if (it >= 1) {
       rel = sqrt(g_new) / b_norm;
       if (!isfinite(rel)) {
@@ -646,21 +738,23 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       A.coef[2 * it + 1] = beta;
     }
     const double na = -alpha;
+    SPCG_FT(5)
+    if (!comm) {
 #pragma unroll
-    for (int k = 0; k < NS; ++k)
-      if (rrow[k] >= 0) {
-        zg[k] = mul_add_rn(ng[k], beta, zg[k]);
-        sg[k] = mul_add_rn(wg[k], beta, sg[k]);
-        pg[k] = mul_add_rn(rg[k], beta, pg[k]);
-        xr[k] = mul_add_rn(xr[k], alpha, pg[k]);
-        rg[k] = mul_add_rn(rg[k], na, sg[k]);
-        wg[k] = mul_add_rn(wg[k], na, zg[k]);
-        wwin[own0 + rrow[k] - P.row_lo] = wg[k];
-      }
-    if (!comm)
+      for (int k = 0; k < NS; ++k)
+        if (rrow[k] >= 0) {
+          zg[k] = mul_add_rn(ng[k], beta, zg[k]);
+          sg[k] = mul_add_rn(wg[k], beta, sg[k]);
+          pg[k] = mul_add_rn(rg[k], beta, pg[k]);
+          xr[k] = mul_add_rn(xr[k], alpha, pg[k]);
+          rg[k] = mul_add_rn(rg[k], na, sg[k]);
+          wg[k] = mul_add_rn(wg[k], na, zg[k]);
+          wwin[own0 + rrow[k] - P.row_lo] = wg[k];
+        }
+      SPCG_FT(6)
       for (int hb = tid - lane; hb < nh; hb += kPipeRowThreads) {  // warp-uniform trip count
         // read after the own rows' update: one round trip (both tagged words
-        // issued together); issuing it right after barrier B measured slower
+        // issued together); issuing it right after the wait measured slower
         const int h = hb + lane;
         const bool act = h < nh && !(kDefer && !halo_local(h));
         const double nv = halo_n(act, buf, h, tag);
@@ -671,12 +765,20 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
           wwin[j] = mul_add_rn(wwin[j], na, zh);
         }
       }
-    pend = true;
-    pbuf = buf;
-    ptag = tag;
-    __syncthreads();
+      pend = true;
+      pbuf = buf;
+      ptag = tag;
+      // the window of w is complete before the next SpMV (row warps only: the
+      // comm warp never touches it)
+      asm volatile("bar.sync 1, %0;" ::"r"(kPipeRowThreads) : "memory");
+    }
+    SPCG_FT(7)
     if (tr) tph[3] += globaltimer_ns() - t3;
   }
+  // every CTA leaves the loop at the same iteration (identical totals); the
+  // barrier retires the loop's messages before the tail reuses shared memory
+  cluster_sync_all();
+#undef SPCG_FT
   if (tr && A.trace) {
     unsigned int smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -685,7 +787,11 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     A.trace[gme * 8 + 5] = tkern0;
     A.trace[gme * 8 + 6] = globaltimer_ns();
     A.trace[gme * 8 + 7] = (unsigned long long)iterations;
+    if (SPCG_PIPE_FINE)
+      for (int j = 0; j < 12; ++j) A.trace[8 * (size_t)G + gme * 16 + j] = tfine[j];
   }
+  if (SPCG_PIPE_FINE && A.trace && comm && lane == 0 && me == 0)
+    for (int j = 12; j < 15; ++j) A.trace[8 * (size_t)G + gme * 16 + j] = tfine[j];
 
   if (status != ST_OK) {
     if (leader) {

@@ -95,7 +95,7 @@ int build_clus_plan(spcg_matrix_s* m) {
   int optin0 = 0, dev0 = 0;
   CUDA_TRY(cudaGetDevice(&dev0));
   CUDA_TRY(cudaDeviceGetAttribute(&optin0, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev0));
-  const int smem_probe = optin0 - (int)sizeof(ClusShared) - 1024;
+  const int smem_probe = optin0 - (int)kClusStatic - 1024;
   auto max_clusters = [&](int csz) -> int {
     CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_probe));
     if (csz > 8) CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -232,7 +232,7 @@ int build_clus_plan(spcg_matrix_s* m) {
   P.off_whalo = (int)off;
   off = al(off + sizeof(double) * 2 * (size_t)hcap);
   P.off_val = (int)off;
-  const long long budget = (long long)optin - (long long)sizeof(ClusShared) - (long long)off - 1024;
+  const long long budget = (long long)optin - (long long)kClusStatic - (long long)off - 1024;
   if (budget < 0) return clus_fail(P, "window does not fit shared memory");
   const long long E = budget / 10;  // 8 B value + 2 B column per resident entry
   long long goff = 0;
@@ -501,7 +501,9 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
   static const bool tracing = getenv("SPCG_TRACE") != nullptr;
   static const char* dbg_path = getenv("SPCG_CLUS_DEBUG");  // per-solve CTA trace lines
   // [C][8] per-CTA phases + [K][8 iterations][34] exchange trace (engine 6)
-  const size_t trace_words = 8 * (size_t)P.C + (size_t)(P.C / std::max(1, P.cs)) * 8 * 34;
+  // (SPCG_PIPE_FINE builds: [C][16] sub-phase totals in place of the exchange trace)
+  const size_t trace_words = 8 * (size_t)P.C +
+                             std::max((size_t)(P.C / std::max(1, P.cs)) * 8 * 34, 16 * (size_t)P.C);
   if (tracing || dbg_path) {
     CUDA_TRY(cudaMalloc((void**)&a.trace, sizeof(unsigned long long) * trace_words));
     CUDA_TRY(cudaMemsetAsync(a.trace, 0, sizeof(unsigned long long) * trace_words, st));
@@ -550,9 +552,12 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
                   tv[8 * c + 2], tv[8 * c + 3]);
         fprintf(f, "], \"xch\": [");
         const int K = P.C / std::max(1, P.cs);
-        for (size_t w = 8 * (size_t)P.C; w < trace_words; ++w)
+        for (size_t w = 8 * (size_t)P.C; w < 8 * (size_t)P.C + (size_t)K * 8 * 34; ++w)
           fprintf(f, "%s%lld", w > 8 * (size_t)P.C ? ", " : "",
                   tv[w] ? (long long)(tv[w] - t0) : -1LL);
+        fprintf(f, "], \"fine\": [");
+        for (size_t w = 0; w < 16 * (size_t)P.C; ++w)
+          fprintf(f, "%s%llu", w ? ", " : "", tv[8 * (size_t)P.C + w]);
         fprintf(f, "], \"K\": %d}\n", K);
         fclose(f);
       }
