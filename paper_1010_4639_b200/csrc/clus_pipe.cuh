@@ -53,9 +53,10 @@ struct PipeShared {
   // partials of the cluster in wslot (mbA); every CTA receives the totals in
   // ltot and its cluster neighbours' boundary n in nhalo (mbB)
   double wslot[2][kClusMax][kPipeRowWarps][2];
-  double ltot[2][2];
-  uint64_t mbA[2], mbB[2];
+  double ltot[3][2];
+  uint64_t mbA[2], mbB[3];
   int nloc;  // halo rows owned inside the cluster
+  unsigned long long fine[16];  // SPCG_PIPE_FINE sub-phase totals
 };
 // static shared memory of the larger of the two cluster kernels (the plan's
 // dynamic budget is shared by engines 5 and 6)
@@ -217,7 +218,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   const ClusCta P = A.ctas[gme];
   double* wwin = reinterpret_cast<double*>(smem_raw + A.off_rwin);   // window of w (SpMV input)
   double* zhalo = reinterpret_cast<double*>(smem_raw + A.off_shalo); // z of the halo rows
-  double* nhalo = reinterpret_cast<double*>(smem_raw + A.off_whalo); // [2][hcap] halo n (DSMEM)
+  double* nhalo = reinterpret_cast<double*>(smem_raw + A.off_whalo); // [3][hcap] halo n (DSMEM)
   double* sval = reinterpret_cast<double*>(smem_raw + A.off_val);
   unsigned short* scol = reinterpret_cast<unsigned short*>(smem_raw + A.off_col);
   const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   const bool leader = gme == 0 && tid == 0;
   const int nh = P.wn - (P.row_hi - P.row_lo);
   const int own0 = P.row_lo - P.wlo;
-  unsigned long long* gh = reinterpret_cast<unsigned long long*>(A.ghalo);  // [2][G][hcap][2]
+  unsigned long long* gh = reinterpret_cast<unsigned long long*>(A.ghalo);  // [3][G][hcap][2]
 
   for (int s = 0; s < P.nslices; ++s) {
     const ClusSlice sd = A.slices[P.slice0 + s];
@@ -261,8 +262,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     }
   }
   if (tid == 0) {
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&cs.mbA[i], 1);
+    for (int i = 0; i < 3; ++i) {
+      if (i < 2) mbar_init(&cs.mbA[i], 1);
       mbar_init(&cs.mbB[i], 1);
     }
     fence_mbar_init();  // visible to the cluster at the first cluster barrier
@@ -566,10 +567,15 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   // the leader thread always (SolveReport.timings), every CTA when tracing
   const bool tr = tid == 0 && (A.trace != nullptr || (SPCG_PHASE_TIMERS && gme == 0));
   unsigned long long tph[4] = {0, 0, 0, 0};
-  // SPCG_PIPE_FINE: [partials, arrive A, deferred halo, SpMV, wait A, send n
-  // local, send n remote, arrive B, wait B, scalars, own-row update, halo
-  // rows + sync]
-  unsigned long long tfine[15] = {}, tfl = 0;
+  // SPCG_PIPE_FINE (SM cycles), thread 0: [partials, deferred halo, SpMV,
+  // send n, wait mbB, scalars, own-row update, halo rows + sync]; the leader
+  // CTA's comm warp: [12] iteration start -> partials in, [13] sum + exchange
+  unsigned long long* tfine = cs.fine;  // (shared: no registers in the loop)
+  unsigned long long tfl = 0;
+  if (SPCG_PIPE_FINE) {
+    if (tid < 16) cs.fine[tid] = 0;
+    __syncthreads();
+  }
 #define SPCG_FT(j)                                          \
   if (SPCG_PIPE_FINE && tr) {                               \
     const unsigned long long tn_ = clock64();               \
@@ -586,31 +592,53 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   int pbuf = 0;
   uint32_t ptag = 0;
   // in-loop messages (no cluster barrier): every row warp's partials go by
-  // st.async to cluster rank 0 (wslot, completing on its mbA); rank 0's comm
-  // warp sums them in (CTA, warp) order, runs the leaders' exchange (K > 1)
-  // and st.asyncs the totals to every CTA's ltot (completing on mbB), where
-  // the boundary n of the cluster neighbours (st.async into nhalo) land too.
-  // A CTA waits only for its own mbB: no CTA waits for the slowest of the
-  // cluster.  Buffers alternate by iteration parity; a sender is never two
-  // iterations ahead of a receiver (iteration i+2's sends need the totals of
-  // i+1, which need every CTA's partials of i+1, posted after its reads of i).
+  // st.async to cluster rank 0 (wslot[it & 1], completing on its mbA); rank
+  // 0's comm warp sums them in (CTA, warp) order, runs the leaders' exchange
+  // (K > 1) and st.asyncs the totals to every CTA's ltot (completing on mbB),
+  // where the boundary n of the cluster neighbours (st.async into nhalo) land
+  // too.  A CTA waits only for its own mbB: no CTA waits for the slowest of
+  // the cluster.  The partials of iteration i+1 leave right after the own
+  // rows' update of i, before the halo rows, so the reduction starts ~0.4 us
+  // earlier.  Reuse distances (causality, not timing): partials by parity (a
+  // CTA posts those of i+2 after the totals of i+1, i.e. after rank 0 read
+  // i's); totals and halo n (nhalo, mbB, ghalo) by iteration mod 3 (the sends
+  // of i+3 need the totals of i+2, i.e. every CTA's partials of i+2, posted
+  // after that CTA's reads of i's halo rows, deferred ones included).
   const uint32_t bA0 = mapa_u32(&cs.mbA[0], 0), bA1 = mapa_u32(&cs.mbA[1], 0);
   const uint32_t wsl0 = mapa_u32(&cs.wslot[0][me][wp][0], 0);
   const uint32_t wsl1 = mapa_u32(&cs.wslot[1][me][wp][0], 0);
-  for (long long it = 0; max_it > 0; ++it) {
-    const int bank = (int)(epoch++ & 1u), buf = (int)(it & 1);
+  auto post_msg = [&](int pb) {  // row warps: this warp's (r.r, w.r) -> rank 0
+    double g = 0.0, d = 0.0;
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+      if (rrow[k] >= 0) {
+        g = fma(rg[k], rg[k], g);
+        d += rg[k] * wg[k];
+      }
+    g = warp_sum(g);
+    d = warp_sum(d);
+    if (lane == 0) st_async_v2f64(pb ? wsl1 : wsl0, g, d, pb ? bA1 : bA0);
+  };
+  if (!comm && max_it > 0) post_msg(0);
+  int h3 = 0;  // iteration mod 3
+  for (long long it = 0; max_it > 0; ++it, h3 = h3 == 2 ? 0 : h3 + 1) {
+    const int bank = (int)(epoch++ & 1u), pb = (int)(it & 1);
     const uint32_t tag = epoch;
-    const uint32_t mpar = (uint32_t)(it >> 1) & 1u;  // mbarrier phase parity of this use
+    const uint32_t parA = (uint32_t)(it >> 1) & 1u;  // mbA[pb]'s phase parity
+    const uint32_t parB = (uint32_t)(it / 3) & 1u;   // mbB[h3]'s
     const unsigned long long t0 = tr ? globaltimer_ns() : 0;
     if (SPCG_PIPE_FINE) tfl = clock64();
     cur_it = it;
-    if (tid == 0) mbar_arrive_expect_tx(&cs.mbB[buf], (uint32_t)bbytes);
+    if (tid == 0) mbar_arrive_expect_tx(&cs.mbB[h3], (uint32_t)bbytes);
+    // reciprocals of the last step's scalars, off the critical path: the
+    // scalar step after the wait is then one division deep
+    const double inv_gam = 1.0 / gam, inv_alpha = 1.0 / alpha;
     if (comm) {
       if (me == 0) {
-        if (lane == 0) mbar_arrive_expect_tx(&cs.mbA[buf], (uint32_t)(C * kPipeRowWarps * 16));
+        if (lane == 0) mbar_arrive_expect_tx(&cs.mbA[pb], (uint32_t)(C * kPipeRowWarps * 16));
         const bool trc = SPCG_PIPE_FINE && A.trace && lane == 0;
         unsigned long long tc0 = trc ? clock64() : 0;
-        mbar_wait_cluster(&cs.mbA[buf], mpar);
+        mbar_wait_cluster(&cs.mbA[pb], parA);
         if (trc) {
           const unsigned long long tn = clock64();
           tfine[12] += tn - tc0;
@@ -621,8 +649,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
         double c0 = 0.0, c1 = 0.0;
         if (lane < kPipeRowWarps)
           for (int c = 0; c < C; ++c) {
-            c0 += cs.wslot[buf][c][lane][0];
-            c1 += cs.wslot[buf][c][lane][1];
+            c0 += cs.wslot[pb][c][lane][0];
+            c1 += cs.wslot[pb][c][lane][1];
           }
         c0 = __shfl_sync(0xffffffffu, warp_sum(c0), 0);
         c1 = __shfl_sync(0xffffffffu, warp_sum(c1), 0);
@@ -631,24 +659,14 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
           const unsigned long long tn = clock64();
           tfine[13] += tn - tc0;
         }
-        if (lane < C) st_async_v2f64(mapa_u32(&cs.ltot[buf][0], lane), c0, c1, mapa_u32(&cs.mbB[buf], lane));
+        if (lane < C) st_async_v2f64(mapa_u32(&cs.ltot[h3][0], lane), c0, c1, mapa_u32(&cs.mbB[h3], lane));
       }
     } else {
-      double g = 0.0, d = 0.0;
-#pragma unroll
-      for (int k = 0; k < NS; ++k)
-        if (rrow[k] >= 0) {
-          g = fma(rg[k], rg[k], g);
-          d += rg[k] * wg[k];
-        }
-      g = warp_sum(g);
-      d = warp_sum(d);
-      if (lane == 0) st_async_v2f64(buf ? wsl1 : wsl0, g, d, buf ? bA1 : bA0);
       SPCG_FT(0)
       if (kDefer && pend) {
         // the last update's halo rows owned by other clusters: their n arrives
-        // through L2, so the load latency overlaps the partials' reduction;
-        // the SpMV waits for them
+        // through L2, so the load latency overlaps the reduction; the SpMV
+        // waits for them
         const double na = -alpha;
         for (int hb = tid - lane; hb < nh; hb += kPipeRowThreads) {  // warp-uniform trip count
           const int h = hb + lane;
@@ -671,9 +689,9 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     SPCG_FT(2)
     const unsigned long long t1 = tr ? globaltimer_ns() : 0;
     const unsigned long long t2 = t1;
-    if (!comm) send_n(ng, buf, tag);
+    if (!comm) send_n(ng, h3, tag);
     SPCG_FT(3)
-    mbar_wait_cluster(&cs.mbB[buf], mpar);  // totals + the cluster neighbours' boundary n
+    mbar_wait_cluster(&cs.mbB[h3], parB);  // totals + the cluster neighbours' boundary n
     SPCG_FT(4)
     const unsigned long long t3 = tr ? globaltimer_ns() : 0;
     if (tr) {
@@ -681,9 +699,15 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       tph[1] += t2 - t1;
       tph[2] += t3 - t2;
     }
-    const double g_new = cs.ltot[buf][0], d_new = cs.ltot[buf][1];
+    const double g_new = cs.ltot[h3][0], d_new = cs.ltot[h3][1];
     if (it >= 1) {
-      rel = sqrt(g_new) / b_norm;
+      // every value first, then the checks in the reference's order
+      // (solver.py:132-157), so the square root and the divisions overlap
+      const double sgn = sqrt(g_new);
+      const double beta_n = g_new * inv_gam;
+      const double eta = d_new - beta_n * g_new * inv_alpha;  // p.Ap of iteration it+1
+      const double alpha_n = g_new / eta;
+      rel = sgn / b_norm;
       if (!isfinite(rel)) {
         status = ST_NF_RES;
         fail_iter = it;
@@ -691,24 +715,21 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       }
       if (A.record_history && leader) A.hist[it - 1] = rel;
       iterations = it;
-      if (sqrt(g_new) <= tol_b) {
+      if (sgn <= tol_b) {
         converged = 1;
         break;
       }
-      const double beta_n = g_new / gam;
       if (!isfinite(beta_n)) {
         status = ST_NF_BETA;
         fail_iter = it;
         break;
       }
       if (it >= max_it) break;
-      const double eta = d_new - beta_n * g_new / alpha;  // p.Ap of iteration it+1
       if (eta <= 0.0) {
         status = ST_NOT_SPD;
         fail_iter = it + 1;
         break;
       }
-      const double alpha_n = g_new / eta;
       if (!isfinite(alpha_n)) {
         status = ST_NF_ALPHA;
         fail_iter = it + 1;
@@ -751,13 +772,12 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
           wg[k] = mul_add_rn(wg[k], na, zg[k]);
           wwin[own0 + rrow[k] - P.row_lo] = wg[k];
         }
+      post_msg(pb ^ 1);  // the partials of iteration it+1
       SPCG_FT(6)
       for (int hb = tid - lane; hb < nh; hb += kPipeRowThreads) {  // warp-uniform trip count
-        // read after the own rows' update: one round trip (both tagged words
-        // issued together); issuing it right after the wait measured slower
         const int h = hb + lane;
         const bool act = h < nh && !(kDefer && !halo_local(h));
-        const double nv = halo_n(act, buf, h, tag);
+        const double nv = halo_n(act, h3, h, tag);
         if (act) {
           const double zh = mul_add_rn(nv, beta, zhalo[h]);
           zhalo[h] = zh;
@@ -766,7 +786,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
         }
       }
       pend = true;
-      pbuf = buf;
+      pbuf = h3;
       ptag = tag;
       // the window of w is complete before the next SpMV (row warps only: the
       // comm warp never touches it)
@@ -788,10 +808,10 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     A.trace[gme * 8 + 6] = globaltimer_ns();
     A.trace[gme * 8 + 7] = (unsigned long long)iterations;
     if (SPCG_PIPE_FINE)
-      for (int j = 0; j < 12; ++j) A.trace[8 * (size_t)G + gme * 16 + j] = tfine[j];
+      for (int j = 0; j < 12; ++j) A.trace[8 * (size_t)G + gme * 16 + j] = tfine[j];  // (tid 0's)
   }
   if (SPCG_PIPE_FINE && A.trace && comm && lane == 0 && me == 0)
-    for (int j = 12; j < 15; ++j) A.trace[8 * (size_t)G + gme * 16 + j] = tfine[j];
+    for (int j = 12; j < 14; ++j) A.trace[8 * (size_t)G + gme * 16 + j] = tfine[j];
 
   if (status != ST_OK) {
     if (leader) {

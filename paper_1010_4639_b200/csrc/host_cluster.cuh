@@ -230,7 +230,7 @@ int build_clus_plan(spcg_matrix_s* m) {
   P.off_shalo = (int)off;
   off = al(off + sizeof(double) * (size_t)hcap);
   P.off_whalo = (int)off;
-  off = al(off + sizeof(double) * 2 * (size_t)hcap);
+  off = al(off + sizeof(double) * 3 * (size_t)hcap);  // engine 6: 3 buffers of halo n
   P.off_val = (int)off;
   const long long budget = (long long)optin - (long long)kClusStatic - (long long)off - 1024;
   if (budget < 0) return clus_fail(P, "window does not fit shared memory");
@@ -342,13 +342,13 @@ int build_clus_plan(spcg_matrix_s* m) {
   CUDA_TRY(cudaMemcpy(P.gval, gval.data(), sizeof(double) * gval.size(), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(P.gcol, gcol.data(), sizeof(unsigned short) * gcol.size(), cudaMemcpyHostToDevice));
   if (C > csz) {
-    // [2][C][hcap] doubles (engine 5) or epoch-tagged word pairs (engine 6)
-    if ((rc = dmalloc((void**)&P.ghalo, sizeof(double) * 4 * (size_t)C * hcap, &acct)) ||
+    // [2][C][hcap] doubles (engine 5) or [3][C][hcap] epoch-tagged word pairs (engine 6)
+    if ((rc = dmalloc((void**)&P.ghalo, sizeof(double) * 6 * (size_t)C * hcap, &acct)) ||
         (rc = dmalloc((void**)&P.gslots,
                       sizeof(unsigned long long) * 2 * kClusSlotWords * (size_t)(C / csz),
                       &acct)))
       return rc;
-    CUDA_TRY(cudaMemset(P.ghalo, 0, sizeof(double) * 4 * (size_t)C * hcap));
+    CUDA_TRY(cudaMemset(P.ghalo, 0, sizeof(double) * 6 * (size_t)C * hcap));
   }
   m->bytes += acct;
   P.hcap = hcap;
@@ -497,7 +497,7 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
                              sizeof(unsigned long long) * 2 * kClusSlotWords * (size_t)(P.C / P.cs),
                              st));
   if (pipe && P.ghalo)  // tags restart at 1 every solve
-    CUDA_TRY(cudaMemsetAsync(P.ghalo, 0, sizeof(double) * 4 * (size_t)P.C * P.hcap, st));
+    CUDA_TRY(cudaMemsetAsync(P.ghalo, 0, sizeof(double) * 6 * (size_t)P.C * P.hcap, st));
   static const bool tracing = getenv("SPCG_TRACE") != nullptr;
   static const char* dbg_path = getenv("SPCG_CLUS_DEBUG");  // per-solve CTA trace lines
   // [C][8] per-CTA phases + [K][8 iterations][34] exchange trace (engine 6)
