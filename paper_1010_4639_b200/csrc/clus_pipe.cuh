@@ -108,6 +108,9 @@ constexpr size_t kClusStatic = sizeof(PipeShared) > sizeof(ClusShared) ? sizeof(
 #ifndef SPCG_PIPE_POST_FENCE
 #define SPCG_PIPE_POST_FENCE 0  // 0: none, 1: fence.acq_rel.gpu, 2: fence.sc.gpu
 #endif
+#ifndef SPCG_XCHG_V2
+#define SPCG_XCHG_V2 1  // leaders' poll: the slot's 4 words per load round (0: tag word first)
+#endif
 #ifndef SPCG_PIPE_POLL_NS
 #define SPCG_PIPE_POLL_NS 0  // back-off of the leaders' slot polls (A/B)
 #endif
@@ -374,6 +377,16 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       while (!ok) {
 #endif
         if (!ok) {
+#if SPCG_XCHG_V2
+          // the slot's four words in one round trip (two 16-byte loads in
+          // flight together); every word carries the tag
+          asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+                       : "=l"(a), "=l"(b) : "l"(src) : "memory");
+          asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+                       : "=l"(c), "=l"(d) : "l"(src + 2) : "memory");
+          ok = (uint32_t)a == tag && (uint32_t)b == tag && (uint32_t)c == tag && (uint32_t)d == tag;
+          if (ok && xr) xr[2 + lane] = globaltimer_ns();
+#else
           d = src[3];
           if ((uint32_t)d == tag) {
             a = src[0];
@@ -382,6 +395,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
             ok = (uint32_t)a == tag && (uint32_t)b == tag && (uint32_t)c == tag;
             if (ok && xr) xr[2 + lane] = globaltimer_ns();
           }
+#endif
         }
 #if SPCG_PIPE_POLL_NS > 0
         __nanosleep(SPCG_PIPE_POLL_NS);
@@ -539,8 +553,16 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   allreduce2(part, dummy);
   double gam = part;
   const double tol_b = A.tol * b_norm;
+  // the largest g with sqrt(g) <= tol_b (sqrt is monotone: that set is [0, gthr])
+  double gthr = tol_b * tol_b;
+  for (int i = 0; i < 64 && gthr > 0.0 && sqrt(gthr) > tol_b; ++i) gthr = nextafter(gthr, 0.0);
+  for (int i = 0; i < 64 && sqrt(nextafter(gthr, HUGE_VAL)) <= tol_b; ++i) gthr = nextafter(gthr, HUGE_VAL);
   long long max_it = A.max_iter;
   double rel = sqrt(gam) / b_norm;
+  double g_rel = gam;  // r.r of the last relative residual (rel, computed after the loop)
+  auto hist_w = [&](long long i, double g) {
+    if (A.record_history && leader) A.hist[i - 1] = sqrt(g) / b_norm;
+  };
   int converged = 0, status = ST_OK;
   long long iterations = 0, fail_iter = 0;
   if (sqrt(gam) <= tol_b) {
@@ -633,6 +655,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     // reciprocals of the last step's scalars, off the critical path: the
     // scalar step after the wait is then one division deep
     const double inv_gam = 1.0 / gam, inv_alpha = 1.0 / alpha;
+    asm volatile("" ::"d"(inv_gam), "d"(inv_alpha));  // computed here, before the waits
     if (comm) {
       if (me == 0) {
         if (lane == 0) mbar_arrive_expect_tx(&cs.mbA[pb], (uint32_t)(C * kPipeRowWarps * 16));
@@ -701,38 +724,44 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     }
     const double g_new = cs.ltot[h3][0], d_new = cs.ltot[h3][1];
     if (it >= 1) {
-      // every value first, then the checks in the reference's order
-      // (solver.py:132-157), so the square root and the divisions overlap
-      const double sgn = sqrt(g_new);
+      // one division deep: beta and eta from last step's reciprocals; the
+      // convergence test sqrt(g) <= tol ||b|| as g <= gthr (the same set of
+      // doubles); rel = sqrt(g) / ||b|| (history, report) off the path
       const double beta_n = g_new * inv_gam;
       const double eta = d_new - beta_n * g_new * inv_alpha;  // p.Ap of iteration it+1
       const double alpha_n = g_new / eta;
-      rel = sgn / b_norm;
-      if (!isfinite(rel)) {
+      g_rel = g_new;
+      if (!isfinite(g_new)) {  // rel non-finite (||b|| > 0 finite)
         status = ST_NF_RES;
         fail_iter = it;
         break;
       }
-      if (A.record_history && leader) A.hist[it - 1] = rel;
       iterations = it;
-      if (sgn <= tol_b) {
+      if (g_new <= gthr) {
         converged = 1;
+        hist_w(it, g_new);
         break;
       }
       if (!isfinite(beta_n)) {
         status = ST_NF_BETA;
         fail_iter = it;
+        hist_w(it, g_new);
         break;
       }
-      if (it >= max_it) break;
+      if (it >= max_it) {
+        hist_w(it, g_new);
+        break;
+      }
       if (eta <= 0.0) {
         status = ST_NOT_SPD;
         fail_iter = it + 1;
+        hist_w(it, g_new);
         break;
       }
       if (!isfinite(alpha_n)) {
         status = ST_NF_ALPHA;
         fail_iter = it + 1;
+        hist_w(it, g_new);
         break;
       }
       alpha = alpha_n;
@@ -773,6 +802,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
           wwin[own0 + rrow[k] - P.row_lo] = wg[k];
         }
       post_msg(pb ^ 1);  // the partials of iteration it+1
+      if (it >= 1) hist_w(it, g_new);
       SPCG_FT(6)
       for (int hb = tid - lane; hb < nh; hb += kPipeRowThreads) {  // warp-uniform trip count
         const int h = hb + lane;
@@ -798,6 +828,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   // every CTA leaves the loop at the same iteration (identical totals); the
   // barrier retires the loop's messages before the tail reuses shared memory
   cluster_sync_all();
+  rel = sqrt(g_rel) / b_norm;
 #undef SPCG_FT
   if (tr && A.trace) {
     unsigned int smid;
