@@ -61,6 +61,7 @@ struct ClusCta {
   int nslices, slice0; // slices [slice0, slice0 + nslices) of the global table
   int nsend, send0;    // DSMEM sends of boundary w
   int hlo;             // lower-halo rows (row_lo - wlo); halo index h -> row
+  int nrecv;           // halo rows received from this cluster's CTAs per iteration
 };
 struct ClusSlice {
   int width;  // entries per row slot (max row length in the slice)

@@ -55,7 +55,6 @@ struct PipeShared {
   double wslot[2][kClusMax][kPipeRowWarps][2];
   double ltot[3][2];
   uint64_t mbA[2], mbB[3];
-  int nloc;  // halo rows owned inside the cluster
   unsigned long long fine[16];  // SPCG_PIPE_FINE sub-phase totals
 };
 // static shared memory of the larger of the two cluster kernels (the plan's
@@ -270,22 +269,11 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       mbar_init(&cs.mbB[i], 1);
     }
     fence_mbar_init();  // visible to the cluster at the first cluster barrier
-    cs.nloc = 0;
   }
   __syncthreads();
-  {
-    // bytes this CTA receives per iteration on mbB: the totals and one double
-    // per halo row owned inside the cluster
-    int cnt = 0;
-    for (int h = tid; h < nh; h += kPipeThreads) {
-      const int hrow = h < P.hlo ? P.wlo + h : P.row_hi + (h - P.hlo);
-      cnt += (hrow >= P.clo && hrow < P.chi) ? 1 : 0;
-    }
-    cnt = __reduce_add_sync(0xffffffffu, cnt);
-    if (lane == 0 && cnt) atomicAdd(&cs.nloc, cnt);
-  }
-  __syncthreads();
-  const int bbytes = 16 + 8 * cs.nloc;
+  // bytes this CTA receives per iteration on mbB: the totals and one double
+  // per halo row its cluster neighbours send (host-counted from the sends)
+  const int bbytes = 16 + 8 * P.nrecv;
 
   auto spmv = [&](double* out) {
 #pragma unroll
@@ -790,6 +778,10 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     const double na = -alpha;
     SPCG_FT(5)
     if (!comm) {
+      // every row warp's SpMV has read the window of w before any warp writes
+      // it (a warp with two slices is still reading when a one-slice warp
+      // gets here; the cluster barrier of the barrier protocol did this)
+      asm volatile("bar.sync 1, %0;" ::"r"(kPipeRowThreads) : "memory");
 #pragma unroll
       for (int k = 0; k < NS; ++k)
         if (rrow[k] >= 0) {
@@ -818,6 +810,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       pend = true;
       pbuf = h3;
       ptag = tag;
+
       // the window of w is complete before the next SpMV (row warps only: the
       // comm warp never touches it)
       asm volatile("bar.sync 1, %0;" ::"r"(kPipeRowThreads) : "memory");

@@ -123,8 +123,9 @@ int build_clus_plan(spcg_matrix_s* m) {
     C = csz = (int)std::min<long long>(kClusMax, std::max<long long>(1, want));
     if (max_clusters(csz) < 1) return clus_fail(P, "cluster not launchable");
   } else {
-    csz = 8;
-    const int kmax = std::min(max_clusters(csz), kClusGridMax / 8);
+    static const int force_csz = getenv("SPCG_CLUS_CSZ") ? atoi(getenv("SPCG_CLUS_CSZ")) : 0;  // dev A/B
+    csz = (force_csz == 16 || force_csz == 4) ? force_csz : 8;
+    const int kmax = std::min(max_clusters(csz), kClusGridMax / csz);
     int K = (int)std::min<long long>(kmax, (want + csz - 1) / csz);
     if (force_k > 1) K = std::min(kmax, force_k);
     if (K < 1) return clus_fail(P, "cluster not launchable");
@@ -298,6 +299,21 @@ int build_clus_plan(spcg_matrix_s* m) {
     }
     ctas[dd].nsend = (int)sends.size() - ctas[dd].send0;
   }
+  // per receiver: the in-cluster halo rows its neighbours send each iteration
+  // (engine 6 expects exactly these bytes on its mbarrier)
+  for (int c = 0; c < C; ++c) ctas[c].nrecv = 0;
+  for (int dd = 0; dd < C; ++dd)
+    for (int e = ctas[dd].send0; e < ctas[dd].send0 + ctas[dd].nsend; ++e)
+      if (dd / csz == sends[e].dst / csz) ctas[sends[e].dst].nrecv += sends[e].hi - sends[e].lo;
+  if (getenv("SPCG_CLUS_DEBUG"))
+    for (int c = 0; c < C; ++c) {  // against the halo rows the receiver counts as in-cluster
+      int nl = 0;
+      const int clo = lo[(c / csz) * csz], chi = hi[(c / csz) * csz + csz - 1];
+      for (int r = wlo[c]; r < whi[c]; ++r)
+        if ((r < lo[c] || r >= hi[c]) && r >= clo && r < chi) ++nl;
+      if (nl != ctas[c].nrecv)
+        fprintf(stderr, "[spcg plan] cta %d: %d in-cluster halo rows, %d sent\n", c, nl, ctas[c].nrecv);
+    }
   if (sends.empty()) sends.push_back(ClusSend{0, 0, 0, 0});
   // the grid of C CTAs in clusters of csz must be co-resident with this smem
   CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
