@@ -95,6 +95,9 @@ constexpr size_t kClusStatic = sizeof(PipeShared) > sizeof(ClusShared) ? sizeof(
 #ifndef SPCG_UNIFORM_HALO
 #define SPCG_UNIFORM_HALO 0
 #endif
+#ifndef SPCG_PIPE_EARLY
+#define SPCG_PIPE_EARLY 1  // remote halo n: loads issued right after the wait (0: deferral)
+#endif
 #ifndef SPCG_PIPE_FINE
 #define SPCG_PIPE_FINE 0  // (A/B build) 8 sub-phase timers per CTA into the trace's tail
 #endif
@@ -597,7 +600,10 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   // deferred inter-cluster halo update: CSR/CSC 4.44 -> 3.95 us/iteration on
   // F; the two-segment (SCSR) build ran 10.3 us with it (unexplained, see
   // DESIGN), so it keeps the update in place
-  constexpr bool kDefer = SPCG_PIPE_DEFER && (!TWO || SPCG_PIPE_DEFER_TWO);
+  // one-segment rows: remote halo loads issued early (2.94 vs 3.12 us on F
+  // with the deferral); two-segment rows: neither (3.79 vs 3.84 early)
+  constexpr bool kEarly = SPCG_PIPE_EARLY && !TWO;
+  constexpr bool kDefer = !kEarly && SPCG_PIPE_DEFER && (!TWO || SPCG_PIPE_DEFER_TWO);
   bool pend = false;  // inter-cluster halo rows of the last update still to do
   int pbuf = 0;
   uint32_t ptag = 0;
@@ -703,6 +709,13 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     if (!comm) send_n(ng, h3, tag);
     SPCG_FT(3)
     mbar_wait_cluster(&cs.mbB[h3], parB);  // totals + the cluster neighbours' boundary n
+    // SPCG_PIPE_EARLY: the first halo row of this thread, if another cluster
+    // owns it: its tagged words are loaded now, consumed after the scalars,
+    // the update and the partials' post (the L2 round trip off the path)
+    unsigned long long ea = 0, eb = 0;
+    const bool e_act = kEarly && !comm && tid < nh && !halo_local(tid);
+    const volatile unsigned long long* esrc = gh + (((size_t)h3 * G + gme) * A.hcap + (e_act ? tid : 0)) * 2;
+    if (e_act) tagged_issue(esrc, ea, eb);
     SPCG_FT(4)
     const unsigned long long t3 = tr ? globaltimer_ns() : 0;
     if (tr) {
@@ -799,7 +812,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       for (int hb = tid - lane; hb < nh; hb += kPipeRowThreads) {  // warp-uniform trip count
         const int h = hb + lane;
         const bool act = h < nh && !(kDefer && !halo_local(h));
-        const double nv = halo_n(act, h3, h, tag);
+        const double nv = (kEarly && e_act && h == tid) ? tagged_finish(esrc, ea, eb, tag)
+                                                                 : halo_n(act, h3, h, tag);
         if (act) {
           const double zh = mul_add_rn(nv, beta, zhalo[h]);
           zhalo[h] = zh;
