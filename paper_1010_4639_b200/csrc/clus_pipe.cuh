@@ -80,6 +80,19 @@ constexpr size_t kClusStatic = sizeof(PipeShared) > sizeof(ClusShared) ? sizeof(
 #ifndef SPCG_PIPE_UNROLL_TWO
 #define SPCG_PIPE_UNROLL_TWO 2
 #endif
+#ifndef SPCG_PIPE_UNROLL_TWO2
+#define SPCG_PIPE_UNROLL_TWO2 8  // two-segment rows, 2 row slots per thread
+#endif
+#ifndef SPCG_PIPE_UNROLL_ONE2
+#define SPCG_PIPE_UNROLL_ONE2 8  // one-segment rows, 2 row slots per thread (4: 2.91 vs 2.86 us on F)
+#endif
+// Engine 6 sums a symmetric-half row (stored L+D entries, then the L^T ones)
+// in ONE chain, like a full row: its recurrences already differ from the
+// reference's, so the privatized two-sum order buys nothing there, and the
+// one-chain SpMV runs S at F's speed (0: the two-sum kernel, A/B)
+#ifndef SPCG_PIPE_ONECHAIN
+#define SPCG_PIPE_ONECHAIN 1
+#endif
 #ifndef SPCG_PIPE_ALIGNED
 #define SPCG_PIPE_ALIGNED 0
 #endif
@@ -284,7 +297,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       out[k] = 0.0;
       if (swidth[k] > 0) {
         // two-segment rows: unroll 2 (unroll 4 spilled at the 128-register cap)
-        constexpr int U = TWO ? SPCG_PIPE_UNROLL_TWO : SPCG_CLUS_UNROLL;
+        constexpr int U = NS == 2 ? (TWO ? SPCG_PIPE_UNROLL_TWO2 : SPCG_PIPE_UNROLL_ONE2)
+                                  : (TWO ? SPCG_PIPE_UNROLL_TWO : SPCG_CLUS_UNROLL);
         const double q = sres[k] ? clus_row<TWO, U>(sval, scol, sbase[k], swidth[k], rlen[k], rlenA[k], wwin)
                                  : clus_row<TWO, U>(A.gval, A.gcol, sbase[k], swidth[k], rlen[k], rlenA[k], wwin);
         out[k] = rrow[k] >= 0 ? q : 0.0;
