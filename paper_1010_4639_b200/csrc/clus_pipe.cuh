@@ -413,11 +413,9 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       }
     }
     if (fenced) fence_acq_rel_gpu();
-    double s0 = 0.0, s1 = 0.0;
-    for (int k = 0; k < K; ++k) {
-      s0 += __shfl_sync(0xffffffffu, c0, k);
-      s1 += __shfl_sync(0xffffffffu, c1, k);
-    }
+    // the K cluster sums in a fixed xor tree: IEEE addition commutes, so every
+    // lane -- and every leader -- ends with the same bits
+    const double s0 = warp_sum(c0), s1 = warp_sum(c1);
     if (xr && lane == 0) xr[1] = globaltimer_ns();
     v0 = s0;
     v1 = s1;
@@ -683,8 +681,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
             c0 += cs.wslot[pb][c][lane][0];
             c1 += cs.wslot[pb][c][lane][1];
           }
-        c0 = __shfl_sync(0xffffffffu, warp_sum(c0), 0);
-        c1 = __shfl_sync(0xffffffffu, warp_sum(c1), 0);
+        c0 = warp_sum(c0);  // (xor tree: the same bits on every lane)
+        c1 = warp_sum(c1);
         if (K > 1) exchange_core(bank, tag, SPCG_PIPE_FENCED, c0, c1);
         if (trc) {
           const unsigned long long tn = clock64();

@@ -125,7 +125,8 @@ int build_clus_plan(spcg_matrix_s* m) {
   } else {
     static const int force_csz = getenv("SPCG_CLUS_CSZ") ? atoi(getenv("SPCG_CLUS_CSZ")) : 0;  // dev A/B
     csz = (force_csz == 16 || force_csz == 4) ? force_csz : 8;
-    const int kmax = std::min(max_clusters(csz), kClusGridMax / csz);
+    // <= 32 clusters: the leaders' exchange polls one cluster slot per lane
+    const int kmax = std::min(std::min(max_clusters(csz), kClusGridMax / csz), 32);
     int K = (int)std::min<long long>(kmax, (want + csz - 1) / csz);
     if (force_k > 1) K = std::min(kmax, force_k);
     if (K < 1) return clus_fail(P, "cluster not launchable");
