@@ -111,6 +111,9 @@ constexpr size_t kClusStatic = sizeof(PipeShared) > sizeof(ClusShared) ? sizeof(
 #ifndef SPCG_PIPE_EARLY
 #define SPCG_PIPE_EARLY 1  // remote halo n: loads issued right after the wait (0: deferral)
 #endif
+#ifndef SPCG_PIPE_ALLPOLL
+#define SPCG_PIPE_ALLPOLL 0  // (A/B) every CTA polls the leaders' global slots
+#endif
 #ifndef SPCG_PIPE_FINE
 #define SPCG_PIPE_FINE 0  // (A/B build) 8 sub-phase timers per CTA into the trace's tail
 #endif
@@ -334,7 +337,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   // its own epoch-tagged words, so it needs no fence
   long long cur_it = -1;  // loop iteration of the exchange (exchange trace)
   // v0, v1: this cluster's sums in, the grid's sums (cluster order) out
-  auto exchange_core = [&](int bank, uint32_t tag, bool fenced, double& v0, double& v1) {
+  auto exchange_core = [&](int bank, uint32_t tag, bool fenced, double& v0, double& v1, bool post = true) {
     // exchange trace (A.trace): iterations 100..107 of every cluster leader:
     // [post time, done time, time lane k saw cluster k's slot]
     unsigned long long* xr = (SPCG_XCHG_TRACE && A.trace && cur_it >= 100 && cur_it < 108)
@@ -342,7 +345,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
         : nullptr;
     const double t0 = v0, t1 = v1;
     unsigned long long* gb = A.gslots + (size_t)bank * K * kClusSlotWords;
-    if (lane == 0) {
+    if (post && lane == 0) {
       if (fenced) fence_acq_rel_gpu();
       volatile unsigned long long* dst = gb + kClusSlotWords * kc;
       const unsigned long long u0 = (unsigned long long)__double_as_longlong(t0);
@@ -688,7 +691,16 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
           const unsigned long long tn = clock64();
           tfine[13] += tn - tc0;
         }
-        if (lane < C) st_async_v2f64(mapa_u32(&cs.ltot[h3][0], lane), c0, c1, mapa_u32(&cs.mbB[h3], lane));
+        if (SPCG_PIPE_ALLPOLL && K > 1) {
+          if (lane == 0) st_async_v2f64(mapa_u32(&cs.ltot[h3][0], 0), c0, c1, mapa_u32(&cs.mbB[h3], 0));
+        } else if (lane < C) {
+          st_async_v2f64(mapa_u32(&cs.ltot[h3][0], lane), c0, c1, mapa_u32(&cs.mbB[h3], lane));
+        }
+      } else if (SPCG_PIPE_ALLPOLL && K > 1) {
+        // (A/B) every CTA polls the leaders' slots itself: no broadcast hop
+        double c0 = 0.0, c1 = 0.0;
+        exchange_core(bank, tag, false, c0, c1, false);
+        if (lane == 0) st_async_v2f64(mapa_u32(&cs.ltot[h3][0], me), c0, c1, mapa_u32(&cs.mbB[h3], me));
       }
     } else {
       SPCG_FT(0)
