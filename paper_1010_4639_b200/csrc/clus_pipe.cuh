@@ -147,19 +147,35 @@ __device__ __forceinline__ void cluster_wait_acq() {
 #endif
 }
 
+// gpu-scope relaxed 16-byte accesses for the tagged words (0: volatile, i.e.
+// system-scope 8-byte accesses; A/B)
+#ifndef SPCG_PIPE_GPU_SCOPE
+#define SPCG_PIPE_GPU_SCOPE 1
+#endif
 // one 64-bit word of an epoch-tagged double: {hi32|tag} or {lo32|tag}
 __device__ __forceinline__ void tagged_store(volatile unsigned long long* dst, double v, uint32_t tag) {
   const unsigned long long u = (unsigned long long)__double_as_longlong(v);
+#if SPCG_PIPE_GPU_SCOPE
+  // both words in one 16-byte relaxed store at gpu scope (each 8-byte word is
+  // single-copy atomic and carries the tag)
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(dst),
+               "l"((u & 0xffffffff00000000ull) | tag), "l"((u << 32) | tag) : "memory");
+#else
   dst[0] = (u & 0xffffffff00000000ull) | tag;
   dst[1] = (u << 32) | tag;
+#endif
 }
 // both words of a tagged double: two independent volatile loads (one round
 // trip); tagged_finish validates them when the value is consumed and re-polls
 // (rarely: the barrier that precedes the read usually outlasts the sender)
 __device__ __forceinline__ void tagged_issue(const volatile unsigned long long* src,
                                              unsigned long long& a, unsigned long long& b) {
+#if SPCG_PIPE_GPU_SCOPE
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(src) : "memory");
+#else
   a = src[0];
   b = src[1];
+#endif
 }
 __device__ __forceinline__ double tagged_finish(const volatile unsigned long long* src,
                                                 unsigned long long a, unsigned long long b,
@@ -357,10 +373,17 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       asm volatile("st.release.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(dst + 2),
                    "l"((u1 & 0xffffffff00000000ull) | tag), "l"((u1 << 32) | tag) : "memory");
 #else
+#if SPCG_PIPE_GPU_SCOPE
+      asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(dst),
+                   "l"((u0 & 0xffffffff00000000ull) | tag), "l"((u0 << 32) | tag) : "memory");
+      asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(dst + 2),
+                   "l"((u1 & 0xffffffff00000000ull) | tag), "l"((u1 << 32) | tag) : "memory");
+#else
       dst[0] = (u0 & 0xffffffff00000000ull) | tag;
       dst[1] = (u0 << 32) | tag;
       dst[2] = (u1 & 0xffffffff00000000ull) | tag;
       dst[3] = (u1 << 32) | tag;
+#endif
 #endif
 #if SPCG_PIPE_POST_FENCE == 1
       fence_acq_rel_gpu();  // the post is performed before the poll starts
