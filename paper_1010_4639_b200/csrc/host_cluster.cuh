@@ -54,6 +54,17 @@ int build_clus_plan(spcg_matrix_s* m) {
   ClusPlan& P = m->cp;
   if (P.built) return SPCG_OK;
   P.built = true;
+  // (dev) SPCG_PLAN_TIMING: host time of the plan's steps on stderr
+  static const bool ptime = getenv("SPCG_PLAN_TIMING") != nullptr;
+  auto tnow = [] { return std::chrono::steady_clock::now(); };
+  auto t_last = tnow();
+  auto mark = [&](const char* what) {
+    if (!ptime) return;
+    const auto t = tnow();
+    fprintf(stderr, "[spcg plan] %-14s %.3f ms\n", what,
+            std::chrono::duration<double, std::milli>(t - t_last).count());
+    t_last = t;
+  };
   const int n = m->n;
   if (m->is_rows) return clus_fail(P, "row block");
   if (n <= 0) return clus_fail(P, "empty");
@@ -78,6 +89,7 @@ int build_clus_plan(spcg_matrix_s* m) {
       host_transpose(n, pA, iA, vA, true, pB, iB, vB);
     }
   }
+  mark("download");
   auto lenA = [&](int i) { return pA[(size_t)i + 1] - pA[i]; };
   auto lenB = [&](int i) { return P.two ? pB[(size_t)i + 1] - pB[i] : 0; };
   long long tot = 0;
@@ -117,6 +129,7 @@ int build_clus_plan(spcg_matrix_s* m) {
     }
     return ncl;
   };
+  mark("row lengths");
   int C, csz;
   static const int force_k = getenv("SPCG_CLUS_K") ? atoi(getenv("SPCG_CLUS_K")) : 0;  // dev A/B
   if ((want <= kClusMax && force_k <= 1) || force_k == 1) {
@@ -138,6 +151,7 @@ int build_clus_plan(spcg_matrix_s* m) {
     }
     C = K * csz;
   }
+  mark("cluster shape");
   // contiguous row blocks balanced by entries + rows, <= kClusMaxRows each
   std::vector<int> lo(C), hi(C);
   {
@@ -220,6 +234,7 @@ int build_clus_plan(spcg_matrix_s* m) {
       }
     }
   }
+  mark("blocks+slices");
   // shared-memory layout and the resident budget
   DevInfo* d;
   if ((rc = dev_info(&d))) return rc;
@@ -287,6 +302,7 @@ int build_clus_plan(spcg_matrix_s* m) {
       }
     }
   }
+  mark("SELL pack");
   // halo sends: owner d -> every CTA c whose window holds d's rows
   std::vector<ClusSend> sends;
   for (int dd = 0; dd < C; ++dd) {
@@ -348,6 +364,7 @@ int build_clus_plan(spcg_matrix_s* m) {
       return clus_fail(P, "clusters not co-resident");
     }
   }
+  mark("sends+attrs");
   long long acct = 0;
   if ((rc = dmalloc((void**)&P.ctas, sizeof(ClusCta) * ctas.size(), &acct)) ||
       (rc = dmalloc((void**)&P.slices, sizeof(ClusSlice) * slices.size(), &acct)) ||
@@ -371,6 +388,7 @@ int build_clus_plan(spcg_matrix_s* m) {
       return rc;
     CUDA_TRY(cudaMemset(P.ghalo, 0, sizeof(double) * 6 * (size_t)C * hcap));
   }
+  mark("upload");
   m->bytes += acct;
   P.hcap = hcap;
   P.C = C;
