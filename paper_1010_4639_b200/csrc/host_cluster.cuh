@@ -365,28 +365,45 @@ int build_clus_plan(spcg_matrix_s* m) {
     }
   }
   mark("sends+attrs");
+  // one device arena for the plan (one allocation, one copy of a host image
+  // of the read-only part, one memset of the halo words): the first solve of
+  // a matrix pays ~2 ms here instead of ~6 (SPCG_PLAN_TIMING)
+  auto al256 = [](size_t v) { return (v + 255) & ~(size_t)255; };
+  size_t o_ctas = 0;
+  size_t o_slices = al256(o_ctas + sizeof(ClusCta) * ctas.size());
+  size_t o_sends = al256(o_slices + sizeof(ClusSlice) * slices.size());
+  size_t o_rowmeta = al256(o_sends + sizeof(ClusSend) * sends.size());
+  size_t o_gval = al256(o_rowmeta + sizeof(int2) * rowmeta.size());
+  size_t o_gcol = al256(o_gval + sizeof(double) * gval.size());
+  const size_t ro_bytes = al256(o_gcol + sizeof(unsigned short) * gcol.size());
+  const bool multi = C > csz;
+  // [2][C][hcap] doubles (engine 5) or [3][C][hcap] epoch-tagged word pairs (engine 6)
+  const size_t ghalo_bytes = multi ? sizeof(double) * 6 * (size_t)C * hcap : 0;
+  const size_t gslot_bytes = multi ? sizeof(unsigned long long) * 2 * kClusSlotWords * (size_t)(C / csz) : 0;
+  const size_t o_ghalo = ro_bytes, o_gslots = al256(o_ghalo + ghalo_bytes);
+  const size_t total = al256(o_gslots + gslot_bytes);
   long long acct = 0;
-  if ((rc = dmalloc((void**)&P.ctas, sizeof(ClusCta) * ctas.size(), &acct)) ||
-      (rc = dmalloc((void**)&P.slices, sizeof(ClusSlice) * slices.size(), &acct)) ||
-      (rc = dmalloc((void**)&P.sends, sizeof(ClusSend) * sends.size(), &acct)) ||
-      (rc = dmalloc((void**)&P.rowmeta, sizeof(int2) * rowmeta.size(), &acct)) ||
-      (rc = dmalloc((void**)&P.gval, sizeof(double) * gval.size(), &acct)) ||
-      (rc = dmalloc((void**)&P.gcol, sizeof(unsigned short) * gcol.size(), &acct)))
-    return rc;
-  CUDA_TRY(cudaMemcpy(P.ctas, ctas.data(), sizeof(ClusCta) * ctas.size(), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(P.slices, slices.data(), sizeof(ClusSlice) * slices.size(), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(P.sends, sends.data(), sizeof(ClusSend) * sends.size(), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(P.rowmeta, rowmeta.data(), sizeof(int2) * rowmeta.size(), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(P.gval, gval.data(), sizeof(double) * gval.size(), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(P.gcol, gcol.data(), sizeof(unsigned short) * gcol.size(), cudaMemcpyHostToDevice));
-  if (C > csz) {
-    // [2][C][hcap] doubles (engine 5) or [3][C][hcap] epoch-tagged word pairs (engine 6)
-    if ((rc = dmalloc((void**)&P.ghalo, sizeof(double) * 6 * (size_t)C * hcap, &acct)) ||
-        (rc = dmalloc((void**)&P.gslots,
-                      sizeof(unsigned long long) * 2 * kClusSlotWords * (size_t)(C / csz),
-                      &acct)))
-      return rc;
-    CUDA_TRY(cudaMemset(P.ghalo, 0, sizeof(double) * 6 * (size_t)C * hcap));
+  unsigned char* base = nullptr;
+  if ((rc = dmalloc((void**)&base, total, &acct))) return rc;
+  P.arena = base;
+  std::vector<unsigned char> img(ro_bytes, 0);
+  memcpy(img.data() + o_ctas, ctas.data(), sizeof(ClusCta) * ctas.size());
+  memcpy(img.data() + o_slices, slices.data(), sizeof(ClusSlice) * slices.size());
+  memcpy(img.data() + o_sends, sends.data(), sizeof(ClusSend) * sends.size());
+  memcpy(img.data() + o_rowmeta, rowmeta.data(), sizeof(int2) * rowmeta.size());
+  memcpy(img.data() + o_gval, gval.data(), sizeof(double) * gval.size());
+  memcpy(img.data() + o_gcol, gcol.data(), sizeof(unsigned short) * gcol.size());
+  CUDA_TRY(cudaMemcpy(base, img.data(), ro_bytes, cudaMemcpyHostToDevice));
+  P.ctas = reinterpret_cast<ClusCta*>(base + o_ctas);
+  P.slices = reinterpret_cast<ClusSlice*>(base + o_slices);
+  P.sends = reinterpret_cast<ClusSend*>(base + o_sends);
+  P.rowmeta = reinterpret_cast<int2*>(base + o_rowmeta);
+  P.gval = reinterpret_cast<double*>(base + o_gval);
+  P.gcol = reinterpret_cast<unsigned short*>(base + o_gcol);
+  if (multi) {
+    P.ghalo = reinterpret_cast<double*>(base + o_ghalo);
+    P.gslots = reinterpret_cast<unsigned long long*>(base + o_gslots);
+    CUDA_TRY(cudaMemset(P.ghalo, 0, ghalo_bytes));
   }
   mark("upload");
   m->bytes += acct;

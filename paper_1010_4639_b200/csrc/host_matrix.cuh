@@ -214,8 +214,7 @@ void free_matrix(spcg_matrix_s* m) {
   DistWorkspace& d = m->dw;
   F(d.r_ext); F(d.p_ext[0]); F(d.p_ext[1]); F(d.tmp_ext); F(d.q); F(d.part); F(d.S);
   F(d.send_buf); F(d.send_idx); F(d.args); F(d.ytx);
-  F(m->cp.ctas); F(m->cp.slices); F(m->cp.sends); F(m->cp.rowmeta); F(m->cp.gval); F(m->cp.gcol);
-  F(m->cp.ghalo); F(m->cp.gslots);
+  F(m->cp.arena);  // every device array of the cluster plan
   if (d.h_S) cudaFreeHost(d.h_S);
   if (d.ev0) cudaEventDestroy(d.ev0);
   if (d.ev1) cudaEventDestroy(d.ev1);
