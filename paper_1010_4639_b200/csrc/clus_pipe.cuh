@@ -16,15 +16,18 @@
 // single-reduction engines, fp64; scripts/pipecg_numerics.py: F converges in
 // the reference's 329 iterations, x within 4.9e-11 of the reference).
 //
-// Synchronisation per iteration (one CTA per SM, 15 row warps + 1 comm warp):
-//   row warps: partials -> every cluster CTA's slot (DSMEM), arrive(A);
-//              n = A w from the shared window of w;  wait(A);
-//              boundary n -> neighbours (DSMEM inside the cluster, epoch-tagged
-//              64-bit words in global memory between clusters);
-//              arrive(B), wait(B); scalars; update; __syncthreads
-//   comm warp (cluster rank 0, K > 1 clusters): wait(A); cluster sum -> own
-//              global slot (epoch-tagged); poll the K slots; sum in cluster
-//              order; DSMEM broadcast to the cluster; arrive(B), wait(B)
+// Synchronisation per iteration i (one CTA per SM, 15 row warps + 1 comm
+// warp; no cluster barrier inside the loop):
+//   row warps: n = A w from the shared window of w; boundary n -> the cluster
+//              neighbours' shared memory by st.async (completing on their
+//              mbarrier mbB) and to other clusters as epoch-tagged words in
+//              global memory; wait on the own mbB (totals + neighbours' n);
+//              scalars; update; (r.r, w.r) of i+1 -> rank 0 by st.async (mbA);
+//              halo rows; named barrier of the row warps
+//   comm warp (cluster rank 0): wait on mbA (every row warp's partials),
+//              sum in fixed order; K > 1: post to the own epoch-tagged global
+//              slot, poll the K slots, sum; st.async the totals to every
+//              cluster CTA (mbB)
 // so the leaders' global exchange runs while the row warps do the SpMV.
 // Halo rows of w advance redundantly in every CTA that gathers them
 // (z = n + beta z, w -= alpha z: the owner's operations on the owner's
@@ -61,167 +64,49 @@ struct PipeShared {
 // dynamic budget is shared by engines 5 and 6)
 constexpr size_t kClusStatic = sizeof(PipeShared) > sizeof(ClusShared) ? sizeof(PipeShared) : sizeof(ClusShared);
 
-// split cluster barrier
-#ifndef SPCG_PIPE_FENCED
-#define SPCG_PIPE_FENCED 0
-#endif
-#ifndef SPCG_PIPE_DEFER
-#define SPCG_PIPE_DEFER 1
-#endif
-#ifndef SPCG_PIPE_LATE_REMOTE
-#define SPCG_PIPE_LATE_REMOTE 0
-#endif
-#ifndef SPCG_PIPE_SPIN_NS
-#define SPCG_PIPE_SPIN_NS 0
-#endif
-#ifndef SPCG_PIPE_DEFER_TWO
-#define SPCG_PIPE_DEFER_TWO 0
-#endif
-#ifndef SPCG_PIPE_UNROLL_TWO
-#define SPCG_PIPE_UNROLL_TWO 2
-#endif
-#ifndef SPCG_PIPE_UNROLL_TWO2
-#define SPCG_PIPE_UNROLL_TWO2 8  // two-segment rows, 2 row slots per thread
-#endif
+// SpMV unroll of the 2-slot kernel (4: 2.91 vs 2.86 us per iteration on F);
+// the 4-slot kernel uses SPCG_CLUS_UNROLL (clus.cuh)
 #ifndef SPCG_PIPE_UNROLL_ONE2
-#define SPCG_PIPE_UNROLL_ONE2 8  // one-segment rows, 2 row slots per thread (4: 2.91 vs 2.86 us on F)
+#define SPCG_PIPE_UNROLL_ONE2 8
 #endif
-// Engine 6 sums a symmetric-half row (stored L+D entries, then the L^T ones)
-// in ONE chain, like a full row: its recurrences already differ from the
-// reference's, so the privatized two-sum order buys nothing there, and the
-// one-chain SpMV runs S at F's speed (0: the two-sum kernel, A/B)
-#ifndef SPCG_PIPE_ONECHAIN
-#define SPCG_PIPE_ONECHAIN 1
-#endif
-#ifndef SPCG_PIPE_ALIGNED
-#define SPCG_PIPE_ALIGNED 0
-#endif
-#ifndef SPCG_PIPE_POST
-#define SPCG_PIPE_POST 0  // 1: leader posts with st.release.gpu.v2 (A/B)
-#endif
-// (A/B) fence after the leader's slot post: a partial cure of the
-// occasional 2.2-2.5x slower solve before its cause was found (the divergent
-// spin of the leaders' poll, now warp-uniform; profiles/r02/bimodal.md)
-// (A/B) warp-uniform tagged halo loads: not needed against the slow mode
-// (0 slow solves in 120 without them) and 0.16-0.2 us per iteration dearer
-// (profiles/r02/bimodal/ab_uniform.log), so off
-#ifndef SPCG_UNIFORM_HALO
-#define SPCG_UNIFORM_HALO 0
-#endif
-#ifndef SPCG_PIPE_EARLY
-#define SPCG_PIPE_EARLY 1  // remote halo n: loads issued right after the wait (0: deferral)
-#endif
-#ifndef SPCG_PIPE_ALLPOLL
-#define SPCG_PIPE_ALLPOLL 0  // (A/B) every CTA polls the leaders' global slots
-#endif
+// instrumented builds (dev): SM-cycle sub-phase timers; the leaders' exchange
+// timeline of iterations 100-107 (both written through SPCG_CLUS_DEBUG)
 #ifndef SPCG_PIPE_FINE
-#define SPCG_PIPE_FINE 0  // (A/B build) 8 sub-phase timers per CTA into the trace's tail
+#define SPCG_PIPE_FINE 0
 #endif
 #ifndef SPCG_XCHG_TRACE
-#define SPCG_XCHG_TRACE 0  // exchange timeline of iterations 100-107 (SPCG_CLUS_DEBUG)
+#define SPCG_XCHG_TRACE 0
 #endif
-#ifndef SPCG_UNIFORM_XCHG
-#define SPCG_UNIFORM_XCHG 1  // (A/B) warp-uniform leaders' poll
-#endif
-#ifndef SPCG_PIPE_POST_FENCE
-#define SPCG_PIPE_POST_FENCE 0  // 0: none, 1: fence.acq_rel.gpu, 2: fence.sc.gpu
-#endif
-#ifndef SPCG_XCHG_V2
-#define SPCG_XCHG_V2 1  // leaders' poll: the slot's 4 words per load round (0: tag word first)
-#endif
-#ifndef SPCG_PIPE_POLL_NS
-#define SPCG_PIPE_POLL_NS 0  // back-off of the leaders' slot polls (A/B)
-#endif
-__device__ __forceinline__ void cluster_arrive_rel() {
-#if SPCG_PIPE_ALIGNED
-  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-#else
-  asm volatile("barrier.cluster.arrive.release;\n" ::: "memory");
-#endif
-}
-__device__ __forceinline__ void cluster_wait_acq() {
-#if SPCG_PIPE_ALIGNED
-  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-#else
-  asm volatile("barrier.cluster.wait.acquire;\n" ::: "memory");
-#endif
-}
-
-// gpu-scope relaxed 16-byte accesses for the tagged words (0: volatile, i.e.
-// system-scope 8-byte accesses; A/B)
-#ifndef SPCG_PIPE_GPU_SCOPE
-#define SPCG_PIPE_GPU_SCOPE 1
-#endif
-// one 64-bit word of an epoch-tagged double: {hi32|tag} or {lo32|tag}
-__device__ __forceinline__ void tagged_store(volatile unsigned long long* dst, double v, uint32_t tag) {
+// Measured and removed A/B variants: deferral of the remote halo
+// rows to the next iteration (replaced by loads issued right after the wait),
+// the privatized two-sum SpMV of symmetric-half rows (one chain instead),
+// warp-uniform tagged halo loads, back-off in the polls, a fence or a release
+// store on the leaders' post, aligned cluster barriers, every CTA polling the
+// leaders' slots, system-scope 8-byte tagged words.
+// An epoch-tagged double: {hi32 | tag, lo32 << 32 | tag}, written as one
+// 16-byte relaxed store at gpu scope (each 8-byte word is single-copy atomic
+// and carries the tag, so a reader never takes a torn value for a new one)
+__device__ __forceinline__ void tagged_store(unsigned long long* dst, double v, uint32_t tag) {
   const unsigned long long u = (unsigned long long)__double_as_longlong(v);
-#if SPCG_PIPE_GPU_SCOPE
-  // both words in one 16-byte relaxed store at gpu scope (each 8-byte word is
-  // single-copy atomic and carries the tag)
   asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(dst),
                "l"((u & 0xffffffff00000000ull) | tag), "l"((u << 32) | tag) : "memory");
-#else
-  dst[0] = (u & 0xffffffff00000000ull) | tag;
-  dst[1] = (u << 32) | tag;
-#endif
 }
-// both words of a tagged double: two independent volatile loads (one round
-// trip); tagged_finish validates them when the value is consumed and re-polls
-// (rarely: the barrier that precedes the read usually outlasts the sender)
-__device__ __forceinline__ void tagged_issue(const volatile unsigned long long* src,
-                                             unsigned long long& a, unsigned long long& b) {
-#if SPCG_PIPE_GPU_SCOPE
+// both words in one 16-byte load; tagged_finish validates them when the
+// value is consumed and re-polls until both carry the tag
+__device__ __forceinline__ void tagged_issue(const unsigned long long* src, unsigned long long& a,
+                                             unsigned long long& b) {
   asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(src) : "memory");
-#else
-  a = src[0];
-  b = src[1];
-#endif
 }
-__device__ __forceinline__ double tagged_finish(const volatile unsigned long long* src,
-                                                unsigned long long a, unsigned long long b,
-                                                uint32_t tag) {
+__device__ __forceinline__ double tagged_finish(const unsigned long long* src, unsigned long long a,
+                                                unsigned long long b, uint32_t tag) {
   unsigned long long spins = 0;
-  // warp-uniform over the lanes that arrived together: no lane spins alone
-  // while its finished neighbours wait at a reconvergence point (see the
-  // leaders' poll in exchange())
-#if SPCG_UNIFORM_HALO
-  const unsigned m = __activemask();
-  bool ok = (uint32_t)a == tag && (uint32_t)b == tag;
-  while (!__all_sync(m, ok)) {
-#if SPCG_PIPE_SPIN_NS > 0
-    __nanosleep(SPCG_PIPE_SPIN_NS);  // back off: spinners slow the lines' writers
-#endif
-    if (!ok) {
-      tagged_issue(src, a, b);
-      ok = (uint32_t)a == tag && (uint32_t)b == tag;
-    }
-    if (++spins > kSpinLimit) asm volatile("trap;");
-  }
-#else
   while ((uint32_t)a != tag || (uint32_t)b != tag) {
     tagged_issue(src, a, b);
     if (++spins > kSpinLimit) asm volatile("trap;");
   }
-#endif
   return __longlong_as_double((long long)((a & 0xffffffff00000000ull) | (b >> 32)));
 }
-// Warp-uniform tagged load: all 32 lanes call it; lanes with act = false
-// only keep the loop uniform.
-__device__ __forceinline__ double tagged_load_warp(bool act, const volatile unsigned long long* src,
-                                                   uint32_t tag) {
-  unsigned long long a = 0, b = 0, spins = 0;
-  if (act) tagged_issue(src, a, b);
-  bool ok = !act || ((uint32_t)a == tag && (uint32_t)b == tag);
-  while (!__all_sync(0xffffffffu, ok)) {
-    if (!ok) {
-      tagged_issue(src, a, b);
-      ok = (uint32_t)a == tag && (uint32_t)b == tag;
-    }
-    if (++spins > kSpinLimit) asm volatile("trap;");
-  }
-  return __longlong_as_double((long long)((a & 0xffffffff00000000ull) | (b >> 32)));
-}
-__device__ __forceinline__ double tagged_load(const volatile unsigned long long* src, uint32_t tag) {
+__device__ __forceinline__ double tagged_load(const unsigned long long* src, uint32_t tag) {
   unsigned long long a, b;
   tagged_issue(src, a, b);
   return tagged_finish(src, a, b, tag);
@@ -229,7 +114,7 @@ __device__ __forceinline__ double tagged_load(const volatile unsigned long long*
 
 // NS: row slots per thread (2 when the plan's CTAs have <= 30 slices: fewer
 // live registers, no spills; 4 otherwise)
-template <bool TWO, int NS>
+template <int NS>
 __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArgs A) {
   namespace cgp = cooperative_groups;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -316,10 +201,14 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       out[k] = 0.0;
       if (swidth[k] > 0) {
         // two-segment rows: unroll 2 (unroll 4 spilled at the 128-register cap)
-        constexpr int U = NS == 2 ? (TWO ? SPCG_PIPE_UNROLL_TWO2 : SPCG_PIPE_UNROLL_ONE2)
-                                  : (TWO ? SPCG_PIPE_UNROLL_TWO : SPCG_CLUS_UNROLL);
-        const double q = sres[k] ? clus_row<TWO, U>(sval, scol, sbase[k], swidth[k], rlen[k], rlenA[k], wwin)
-                                 : clus_row<TWO, U>(A.gval, A.gcol, sbase[k], swidth[k], rlen[k], rlenA[k], wwin);
+        // a symmetric-half row (stored L+D entries, then its L^T entries:
+        // column order) is summed in ONE chain like a full row -- engine 6's
+        // recurrences differ from the reference's anyway, so the privatized
+        // two-sum order bought nothing (S: 3.77 -> 2.86 us per iteration,
+        // bitwise the full-row solve)
+        constexpr int U = NS == 2 ? SPCG_PIPE_UNROLL_ONE2 : SPCG_CLUS_UNROLL;
+        const double q = sres[k] ? clus_row<false, U>(sval, scol, sbase[k], swidth[k], rlen[k], rlenA[k], wwin)
+                                 : clus_row<false, U>(A.gval, A.gcol, sbase[k], swidth[k], rlen[k], rlenA[k], wwin);
         out[k] = rrow[k] >= 0 ? q : 0.0;
       }
     }
@@ -363,33 +252,13 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     unsigned long long* gb = A.gslots + (size_t)bank * K * kClusSlotWords;
     if (post && lane == 0) {
       if (fenced) fence_acq_rel_gpu();
-      volatile unsigned long long* dst = gb + kClusSlotWords * kc;
+      unsigned long long* dst = gb + kClusSlotWords * kc;
       const unsigned long long u0 = (unsigned long long)__double_as_longlong(t0);
       const unsigned long long u1 = (unsigned long long)__double_as_longlong(t1);
-#if SPCG_PIPE_POST == 1
-      // one 16-byte store per value pair, release at gpu scope
-      asm volatile("st.release.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(dst),
-                   "l"((u0 & 0xffffffff00000000ull) | tag), "l"((u0 << 32) | tag) : "memory");
-      asm volatile("st.release.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(dst + 2),
-                   "l"((u1 & 0xffffffff00000000ull) | tag), "l"((u1 << 32) | tag) : "memory");
-#else
-#if SPCG_PIPE_GPU_SCOPE
       asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(dst),
                    "l"((u0 & 0xffffffff00000000ull) | tag), "l"((u0 << 32) | tag) : "memory");
       asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(dst + 2),
                    "l"((u1 & 0xffffffff00000000ull) | tag), "l"((u1 << 32) | tag) : "memory");
-#else
-      dst[0] = (u0 & 0xffffffff00000000ull) | tag;
-      dst[1] = (u0 << 32) | tag;
-      dst[2] = (u1 & 0xffffffff00000000ull) | tag;
-      dst[3] = (u1 << 32) | tag;
-#endif
-#endif
-#if SPCG_PIPE_POST_FENCE == 1
-      fence_acq_rel_gpu();  // the post is performed before the poll starts
-#elif SPCG_PIPE_POST_FENCE == 2
-      asm volatile("fence.sc.gpu;" ::: "memory");
-#endif
       if (xr) xr[0] = globaltimer_ns();
     }
     double c0 = 0.0, c1 = 0.0;
@@ -399,16 +268,11 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       // wait at a reconvergence point -- a divergent spin loop let a leader
       // that arrived early finish ~7 us after its last slot was visible
       // (profiles/r02/bimodal.md)
-      const volatile unsigned long long* src = gb + kClusSlotWords * (lane < K ? lane : 0);
+      const unsigned long long* src = gb + kClusSlotWords * (lane < K ? lane : 0);
       unsigned long long a = 0, b = 0, c = 0, d = 0, spins = 0;
       bool ok = lane >= K;
-#if SPCG_UNIFORM_XCHG
       while (!__all_sync(0xffffffffu, ok)) {
-#else
-      while (!ok) {
-#endif
         if (!ok) {
-#if SPCG_XCHG_V2
           // the slot's four words in one round trip (two 16-byte loads in
           // flight together); every word carries the tag
           asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
@@ -417,20 +281,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
                        : "=l"(c), "=l"(d) : "l"(src + 2) : "memory");
           ok = (uint32_t)a == tag && (uint32_t)b == tag && (uint32_t)c == tag && (uint32_t)d == tag;
           if (ok && xr) xr[2 + lane] = globaltimer_ns();
-#else
-          d = src[3];
-          if ((uint32_t)d == tag) {
-            a = src[0];
-            b = src[1];
-            c = src[2];
-            ok = (uint32_t)a == tag && (uint32_t)b == tag && (uint32_t)c == tag;
-            if (ok && xr) xr[2 + lane] = globaltimer_ns();
-          }
-#endif
         }
-#if SPCG_PIPE_POLL_NS > 0
-        __nanosleep(SPCG_PIPE_POLL_NS);
-#endif
         if (++spins > kSpinLimit) asm volatile("trap;");
       }
       if (lane < K) {
@@ -491,18 +342,10 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     const int hrow = h < P.hlo ? P.wlo + h : P.row_hi + (h - P.hlo);
     return hrow >= P.clo && hrow < P.chi;
   };
-  // warp-uniform: every lane of a row warp calls it (act = false: no halo row)
   auto halo_n = [&](bool act, int buf, int h, uint32_t tag) {
-#if SPCG_UNIFORM_HALO
-    const bool loc = act && halo_local(h);
-    const double r = tagged_load_warp(act && !loc,
-                                      gh + (((size_t)buf * G + gme) * A.hcap + (act ? h : 0)) * 2, tag);
-    return loc ? nhalo[(size_t)buf * A.hcap + h] : r;
-#else
     if (!act) return 0.0;
     if (halo_local(h)) return nhalo[(size_t)buf * A.hcap + h];
     return tagged_load(gh + (((size_t)buf * G + gme) * A.hcap + h) * 2, tag);
-#endif
   };
   // boundary n to the neighbours of this iteration: st.async into the cluster
   // neighbours' nhalo[buf] (completing on their mbB[buf]), epoch-tagged global
@@ -511,7 +354,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     for (int e = 0; e < P.nsend; ++e) {
       const ClusSend sd = e < kClusSendCache ? cs.send[e] : A.sends[P.send0 + e];
       if (sd.dst / C != kc) {
-        volatile unsigned long long* dst = gh + ((size_t)buf * G + sd.dst) * A.hcap * 2;
+        unsigned long long* dst = gh + ((size_t)buf * G + sd.dst) * A.hcap * 2;
 #pragma unroll
         for (int k = 0; k < NS; ++k)
           if (rrow[k] >= sd.lo && rrow[k] < sd.hi)
@@ -635,16 +478,6 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   }
   const unsigned long long tkern0 = tr ? globaltimer_ns() : 0;
   double alpha = 0.0, beta = 0.0;
-  // deferred inter-cluster halo update: CSR/CSC 4.44 -> 3.95 us/iteration on
-  // F; the two-segment (SCSR) build ran 10.3 us with it (unexplained, see
-  // DESIGN), so it keeps the update in place
-  // one-segment rows: remote halo loads issued early (2.94 vs 3.12 us on F
-  // with the deferral); two-segment rows: neither (3.79 vs 3.84 early)
-  constexpr bool kEarly = SPCG_PIPE_EARLY && !TWO;
-  constexpr bool kDefer = !kEarly && SPCG_PIPE_DEFER && (!TWO || SPCG_PIPE_DEFER_TWO);
-  bool pend = false;  // inter-cluster halo rows of the last update still to do
-  int pbuf = 0;
-  uint32_t ptag = 0;
   // in-loop messages (no cluster barrier): every row warp's partials go by
   // st.async to cluster rank 0 (wslot[it & 1], completing on its mbA); rank
   // 0's comm warp sums them in (CTA, warp) order, runs the leaders' exchange
@@ -709,45 +542,17 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
           }
         c0 = warp_sum(c0);  // (xor tree: the same bits on every lane)
         c1 = warp_sum(c1);
-        if (K > 1) exchange_core(bank, tag, SPCG_PIPE_FENCED, c0, c1);
+        if (K > 1) exchange_core(bank, tag, false, c0, c1);
         if (trc) {
           const unsigned long long tn = clock64();
           tfine[13] += tn - tc0;
         }
-        if (SPCG_PIPE_ALLPOLL && K > 1) {
-          if (lane == 0) st_async_v2f64(mapa_u32(&cs.ltot[h3][0], 0), c0, c1, mapa_u32(&cs.mbB[h3], 0));
-        } else if (lane < C) {
-          st_async_v2f64(mapa_u32(&cs.ltot[h3][0], lane), c0, c1, mapa_u32(&cs.mbB[h3], lane));
-        }
-      } else if (SPCG_PIPE_ALLPOLL && K > 1) {
-        // (A/B) every CTA polls the leaders' slots itself: no broadcast hop
-        double c0 = 0.0, c1 = 0.0;
-        exchange_core(bank, tag, false, c0, c1, false);
-        if (lane == 0) st_async_v2f64(mapa_u32(&cs.ltot[h3][0], me), c0, c1, mapa_u32(&cs.mbB[h3], me));
+        if (lane < C) st_async_v2f64(mapa_u32(&cs.ltot[h3][0], lane), c0, c1, mapa_u32(&cs.mbB[h3], lane));
       }
     } else {
       SPCG_FT(0)
-      if (kDefer && pend) {
-        // the last update's halo rows owned by other clusters: their n arrives
-        // through L2, so the load latency overlaps the reduction; the SpMV
-        // waits for them
-        const double na = -alpha;
-        for (int hb = tid - lane; hb < nh; hb += kPipeRowThreads) {  // warp-uniform trip count
-          const int h = hb + lane;
-          const bool act = h < nh && !halo_local(h);
-          const double nv = halo_n(act, pbuf, h, ptag);
-          if (act) {
-            const double zh = mul_add_rn(nv, beta, zhalo[h]);
-            zhalo[h] = zh;
-            const int j = halo_win(h);
-            wwin[j] = mul_add_rn(wwin[j], na, zh);
-          }
-        }
-        asm volatile("bar.sync 1, %0;" ::"r"(kPipeRowThreads) : "memory");
-      }
       SPCG_FT(1)
     }
-    pend = false;
     double ng[NS];
     spmv(ng);  // n = A w (the comm warp has no rows), overlapped with the all-reduce
     SPCG_FT(2)
@@ -756,12 +561,14 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     if (!comm) send_n(ng, h3, tag);
     SPCG_FT(3)
     mbar_wait_cluster(&cs.mbB[h3], parB);  // totals + the cluster neighbours' boundary n
-    // SPCG_PIPE_EARLY: the first halo row of this thread, if another cluster
-    // owns it: its tagged words are loaded now, consumed after the scalars,
-    // the update and the partials' post (the L2 round trip off the path)
+    // the first halo row of this thread, if another cluster owns it: its
+    // tagged words are loaded now and consumed after the scalars, the update
+    // and the partials' post (the L2 round trip off the path: 2.94 vs 3.12 us
+    // per iteration on F against deferring the remote rows to the next
+    // iteration's start)
     unsigned long long ea = 0, eb = 0;
-    const bool e_act = kEarly && !comm && tid < nh && !halo_local(tid);
-    const volatile unsigned long long* esrc = gh + (((size_t)h3 * G + gme) * A.hcap + (e_act ? tid : 0)) * 2;
+    const bool e_act = !comm && tid < nh && !halo_local(tid);
+    const unsigned long long* esrc = gh + (((size_t)h3 * G + gme) * A.hcap + (e_act ? tid : 0)) * 2;
     if (e_act) tagged_issue(esrc, ea, eb);
     SPCG_FT(4)
     const unsigned long long t3 = tr ? globaltimer_ns() : 0;
@@ -858,8 +665,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       SPCG_FT(6)
       for (int hb = tid - lane; hb < nh; hb += kPipeRowThreads) {  // warp-uniform trip count
         const int h = hb + lane;
-        const bool act = h < nh && !(kDefer && !halo_local(h));
-        const double nv = (kEarly && e_act && h == tid) ? tagged_finish(esrc, ea, eb, tag)
+        const bool act = h < nh;
+        const double nv = (e_act && h == tid) ? tagged_finish(esrc, ea, eb, tag)
                                                                  : halo_n(act, h3, h, tag);
         if (act) {
           const double zh = mul_add_rn(nv, beta, zhalo[h]);
@@ -868,9 +675,6 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
           wwin[j] = mul_add_rn(wwin[j], na, zh);
         }
       }
-      pend = true;
-      pbuf = h3;
-      ptag = tag;
 
       // the window of w is complete before the next SpMV (row warps only: the
       // comm warp never touches it)

@@ -336,12 +336,7 @@ int build_clus_plan(spcg_matrix_s* m) {
   CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
   if (csz > 8) CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   // the pipelined kernel (engine 6) runs the same plan with one more warp
-#if SPCG_PIPE_ONECHAIN
-  const void* kpipes[2] = {(const void*)clus_pcg_kernel<false, 2>, (const void*)clus_pcg_kernel<false, 4>};
-#else
-  const void* kpipes[4] = {(const void*)clus_pcg_kernel<false, 2>, (const void*)clus_pcg_kernel<false, 4>,
-                           (const void*)clus_pcg_kernel<true, 2>, (const void*)clus_pcg_kernel<true, 4>};
-#endif
+  const void* kpipes[2] = {(const void*)clus_pcg_kernel<2>, (const void*)clus_pcg_kernel<4>};
   for (const void* kp : kpipes) {
     CUDA_TRY(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
     if (csz > 8) CUDA_TRY(cudaFuncSetAttribute(kp, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -435,13 +430,9 @@ int launch_clus(const ClusPlan& P, const ClusArgs& a, cudaStream_t st, bool pipe
   cfg.numAttrs = (P.C > P.cs && !noncoop) ? 2 : 1;
   if (pipe) {
     const bool ns2 = P.max_slices <= kPipeMaxSlices2;
-#if !SPCG_PIPE_ONECHAIN
-    if (P.two && ns2) CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_pcg_kernel<true, 2>, a));
-    else if (P.two) CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_pcg_kernel<true, 4>, a));
-    else
-#endif
-    if (ns2) CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_pcg_kernel<false, 2>, a));
-    else CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_pcg_kernel<false, 4>, a));
+    // (two-segment plans too: engine 6 sums their rows in one chain)
+    if (ns2) CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_pcg_kernel<2>, a));
+    else CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_pcg_kernel<4>, a));
   } else if (P.two) {
     CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_cg_kernel<true>, a));
   } else {
