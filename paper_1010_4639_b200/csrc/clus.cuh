@@ -13,8 +13,10 @@
 //   keeps the window [wlo, wlo+wn) of r that its rows gather, in shared
 //   memory: own rows plus a lower and an upper halo (banded matrices: the
 //   FEM mesh's bandwidth is 177 rows).
-// * Its rows are stored as SELL-32 slices sorted by length (the binning
-//   of rows by length): entry u of the slice's 32 rows is contiguous, so a
+// * Its rows are stored as SELL-32 slices of 32 consecutive rows (natural
+//   order: the window gathers of banded rows hit consecutive banks; sorting
+//   by length saved padding but cost more in bank conflicts, host_cluster.cuh):
+//   entry u of the slice's 32 rows is contiguous, so a
 //   warp reads values and 16-bit window-relative columns conflict-free.  Each
 //   row keeps its storage order, so a row sum is the reference's sequential
 //   sum (bitwise equal to csr_gather / the privatized two-segment sum).
