@@ -145,10 +145,11 @@ typedef struct {
   int32_t recompute_final_residual; /* default 1 (solver.py:159-162)           */
   int32_t accumulation;          /* spcg_accumulation, SCSR only               */
   int32_t engine;                /* 0 = auto: banded systems whose rows fit
-                                    the co-resident clusters -> 6 (single-
-                                    segment rows) or 5 (two-segment SCSR
-                                    rows); other systems resident on chip
-                                    -> 3; everything else -> 2.
+                                    the co-resident clusters -> 6 (guarded,
+                                    falls back to 5); other systems resident
+                                    on chip -> 3; full CSR with <= 16 tiles
+                                    per co-resident CTA (~1 M rows) -> 7;
+                                    everything else -> 2.
                                     2 = per-pass kernels (the sharded engine),
                                     3 = persistent single-reduction CG
                                         (Chronopoulos-Gear, resident only),
@@ -156,7 +157,11 @@ typedef struct {
                                         (banded systems),
                                     6 = engine 5's plan with pipelined CG
                                         (Ghysels-Vanroose: the SpMV overlaps
-                                        the all-reduce).
+                                        the all-reduce),
+                                    7 = engine 3's recurrences in one
+                                        persistent kernel that streams the
+                                        tiles every iteration (gather formats:
+                                        CSR, privatized symmetric half).
                                     Other values: SPCG_ERR_ARG.             */
   int32_t timing;                /* per-pass engine: CUDA-event time of every
                                     SpMV pass -> result.spmv_ms / launches   */

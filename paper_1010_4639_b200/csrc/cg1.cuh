@@ -387,5 +387,199 @@ __global__ void __launch_bounds__(kBlock, 1) cg1_kernel(const Cg1Args G) {
   pipe_drain(P, sm);
 }
 
+
+// ---- engine 7: the same single-reduction CG for systems that do NOT fit on
+// chip (mid-size: ~0.25-4 M rows).  The per-pass engine pays three launches
+// and three tails per iteration (~30 us at 262 K rows, where the bytes take
+// ~3 us from L2); here ONE persistent cooperative kernel streams the tiles
+// every iteration through the TMA ring (the matrix of a mid-size system stays
+// in the 126 MB L2) and the only grid-wide wait is the fused all-reduce.  The
+// per-line state lives in global memory (x in A.x, p in G.Pv, and the
+// published r, s, w of cg1_kernel) instead of registers: a CTA's tile list is
+// unbounded.  Gather formats only (CSR, privatized symmetric half), so every
+// value is bitwise the one cg1_kernel computes.
+struct Cg1sArgs {
+  Cg1Args g;
+  double* Pv;  // p, own lines
+};
+
+template <int FMT>
+__global__ void __launch_bounds__(kBlock, 1) cg1s_kernel(const Cg1sArgs S1) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  constexpr bool TWO = (FMT == K_SCSR_PRIV);
+  static_assert(FMT == K_CSR || FMT == K_SCSR_PRIV, "engine 7: gather formats");
+  const Cg1Args& G = S1.g;
+  const CgArgs& A = G.base;
+  const MatView& M = A.M;
+  double* X = A.x;
+  double* Pv = S1.Pv;
+  const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+  const long long n = M.n;
+  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long GT = (long long)gridDim.x * blockDim.x;
+
+  smem_init(sm);
+  Pipe P;
+  pipe_start<TWO>(P, sm, M, false);  // streamed: the pass overwrites staged values
+  uint32_t epoch = 0;
+
+  // ||b||
+  double part = 0.0, part2 = 0.0;
+  for (long long i = gt; i < n; i += GT) part = fma(A.b[i], A.b[i], part);
+  const double b_norm = sqrt(grid_allreduce(part, sm, A.slots, epoch));
+  if (b_norm == 0.0) {  // solver.py:109-118
+    for (long long i = gt; i < n; i += GT) X[i] = 0.0;
+    if (leader) {
+      A.res->iterations = 0;
+      A.res->fail_iter = 0;
+      A.res->converged = 1;
+      A.res->status = ST_OK;
+      A.res->final_rel = 0.0;
+      A.res->b_norm = 0.0;
+    }
+    pipe_drain(P, sm);
+    return;
+  }
+  // x = x0, r0 = b - A x0 (solver.py:120-124), published in R[0]
+  part = 0.0;
+  if (A.x0 != nullptr) {
+    SrcPlain sx{A.x0};
+    run_tiles<FMT, false, TWO, false>(P, sm, M, sx, A.q, [&](int, int i, const LineOut& o) {
+      const double ri = mul_add_rn(A.b[i], -1.0, o.q);
+      X[i] = A.x0[i];
+      G.R[0][i] = ri;
+      part = fma(ri, ri, part);
+    });
+  } else {
+    for (long long i = gt; i < n; i += GT) {
+      const double ri = A.b[i];
+      X[i] = 0.0;
+      G.R[0][i] = ri;
+      part = fma(ri, ri, part);
+    }
+  }
+  double gam = grid_allreduce(part, sm, A.slots, epoch);  // publishes R[0]
+  const double tol_b = A.tol * b_norm;
+  long long max_it = A.max_iter;
+  double rel = sqrt(gam) / b_norm;
+  int converged = 0, status = ST_OK;
+  long long iterations = 0, fail_iter = 0;
+  double alpha = 0.0, beta = 0.0;
+  if (sqrt(gam) <= tol_b) {
+    converged = 1;
+    max_it = 0;
+  } else {
+    // w0 = A r0, d0 = r0.w0 (p0 = r0)
+    SrcPlain sr{G.R[0]};
+    part = 0.0;
+    run_tiles<FMT, true, TWO, false>(P, sm, M, sr, G.W[0], [&](int, int i, const LineOut& o) {
+      G.W[0][i] = o.q;
+      part += line_pq<FMT>(o);
+    });
+    const double d0 = grid_allreduce(part, sm, A.slots, epoch);  // publishes W[0]
+    if (d0 <= 0.0) {
+      status = ST_NOT_SPD;
+      fail_iter = 1;
+    } else {
+      alpha = gam / d0;
+      if (!isfinite(alpha)) {
+        status = ST_NF_ALPHA;
+        fail_iter = 1;
+      }
+    }
+  }
+  for (long long it = 0; status == ST_OK && it < max_it; ++it) {
+    const int cur = (int)(it & 1), nxt = cur ^ 1;
+    const int wc = (int)(it % 3), wn = (int)((it + 1) % 3);
+    SrcCgcg src{G.R[cur], G.W[wc], G.S[cur], -alpha, beta};
+    part = 0.0;
+    part2 = 0.0;
+    // own line i: p, s, x from its published r_i, w_i, s_{i-1} (the same
+    // operations as cg1_kernel's registers), r_{i+1} = the gathered value,
+    // w_{i+1} = A r_{i+1}
+    run_tiles<FMT, true, TWO, false>(P, sm, M, src, G.W[wn], [&](int, int i, const LineOut& o) {
+      const double pi = mul_add_rn(G.R[cur][i], beta, Pv[i]);
+      const double si = mul_add_rn(G.W[wc][i], beta, G.S[cur][i]);
+      Pv[i] = pi;
+      G.S[nxt][i] = si;
+      X[i] = mul_add_rn(X[i], alpha, pi);
+      G.W[wn][i] = o.q;
+      G.R[nxt][i] = o.xi;  // r_{i+1,i}, bitwise the gathered value
+      part = fma(o.xi, o.xi, part);
+      part2 += line_pq<FMT>(o);
+    });
+    double g_new = part, d_new = part2;
+    grid_allreduce2(g_new, d_new, sm, A.slots, epoch);
+    const long long k = it + 1;  // reference iteration number
+    rel = sqrt(g_new) / b_norm;
+    if (!isfinite(rel)) {
+      status = ST_NF_RES;
+      fail_iter = k;
+      break;
+    }
+    if (A.record_history && leader) A.hist[k - 1] = rel;
+    iterations = k;
+    if (sqrt(g_new) <= tol_b) {
+      converged = 1;
+      break;
+    }
+    const double beta_n = g_new / gam;
+    if (!isfinite(beta_n)) {
+      status = ST_NF_BETA;
+      fail_iter = k;
+      break;
+    }
+    if (k < max_it) {  // p.Ap of iteration k+1 (solver.py:135-139)
+      const double eta = d_new - beta_n * g_new / alpha;
+      if (eta <= 0.0) {
+        status = ST_NOT_SPD;
+        fail_iter = k + 1;
+        break;
+      }
+      const double alpha_n = g_new / eta;
+      if (!isfinite(alpha_n)) {
+        status = ST_NF_ALPHA;
+        fail_iter = k + 1;
+        break;
+      }
+      alpha = alpha_n;
+    }
+    beta = beta_n;
+    gam = g_new;
+  }
+  if (status != ST_OK) {
+    if (leader) {
+      A.res->iterations = iterations;
+      A.res->fail_iter = fail_iter;
+      A.res->converged = 0;
+      A.res->status = status;
+      A.res->final_rel = rel;
+      A.res->b_norm = b_norm;
+    }
+    pipe_drain(P, sm);
+    return;
+  }
+  if (A.recompute) {  // true residual ||b - A x|| / ||b||
+    grid_allreduce(0.0, sm, A.slots, epoch);  // publishes x
+    SrcPlain sx{X};
+    part = 0.0;
+    run_tiles<FMT, false, TWO, false>(P, sm, M, sx, A.q, [&](int, int i, const LineOut& o) {
+      const double tr = mul_add_rn(A.b[i], -1.0, o.q);
+      part = fma(tr, tr, part);
+    });
+    rel = sqrt(grid_allreduce(part, sm, A.slots, epoch)) / b_norm;
+  }
+  if (leader) {
+    A.res->iterations = iterations;
+    A.res->fail_iter = 0;
+    A.res->converged = converged;
+    A.res->status = ST_OK;
+    A.res->final_rel = rel;
+    A.res->b_norm = b_norm;
+  }
+  pipe_drain(P, sm);
+}
+
 }  // namespace spcg
 

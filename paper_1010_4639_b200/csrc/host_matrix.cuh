@@ -297,6 +297,30 @@ int launch_cg1(const Cg1Args& a, int grid, cudaStream_t st) {
   return SPCG_OK;
 }
 
+// engine 7: co-resident CTAs of cg1s_kernel<FMT> on this device (cooperative)
+template <int FMT>
+int cg1s_grid(const DevInfo* d, int* grid) {
+  static int cached[64] = {0};
+  int& c = cached[d->device & 63];
+  if (c == 0) {
+    int per_sm = 0;
+    const void* fn = (const void*)cg1s_kernel<FMT>;
+    CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem)));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, sizeof(Smem)));
+    // the grid all-reduce polls at most 384 slots (cg.cuh kPollPer)
+    c = std::max(1, std::min(per_sm * d->sms, 384));
+  }
+  *grid = c;
+  return SPCG_OK;
+}
+template <int FMT>
+int launch_cg1s(const Cg1sArgs& a, int grid, cudaStream_t st) {
+  void* args[] = {(void*)&a};
+  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)cg1s_kernel<FMT>, dim3(grid), dim3(kBlock), args,
+                                       sizeof(Smem), st));
+  return SPCG_OK;
+}
+
 template <int FMT>
 int launch_spmv(const MatView& v, const double* x, double* y, int grid, cudaStream_t st) {
   if (FMT == K_CSR && v.wide) spmv_kernel<K_CSR, true><<<grid, kBlock, sizeof(Smem), st>>>(v, x, y);

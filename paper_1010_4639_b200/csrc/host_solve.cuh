@@ -3,6 +3,72 @@
 // (one translation unit: the kernels' templates are instantiated there).
 #pragma once
 
+// engine 7 (cg1.cuh cg1s_kernel): streamed single-reduction CG, one
+// persistent cooperative launch per solve
+int do_cg1s(spcg_matrix_s* m, int kf, const double* b, const double* x0, double* x, double* hist,
+            const spcg_cg_options* o, spcg_cg_result* out, cudaStream_t st) {
+  DevInfo* d;
+  int rc;
+  if ((rc = dev_info(&d))) return rc;
+  int grid = 1;
+  if ((rc = kf == K_CSR ? cg1s_grid<K_CSR>(d, &grid) : cg1s_grid<K_SCSR_PRIV>(d, &grid))) return rc;
+  const MatView v = view(m, kf == K_SCSR_PRIV);
+  grid = std::max(1, std::min(grid, v.ntiles));
+  if ((rc = ensure_ws(m, grid))) return rc;
+  Workspace& w = m->ws;
+  if (o->record_history && hist == nullptr)
+    return fail(SPCG_ERR_ARG, "record_history needs a history buffer");
+  const size_t vb = sizeof(double) * (size_t)std::max(1, m->n);
+  if (!w.cg1 && (rc = dmalloc((void**)&w.cg1, 8 * vb, nullptr))) return rc;
+  CUDA_TRY(cudaMemsetAsync(w.cg1, 0, 8 * vb, st));  // s_{-1} = 0, p_{-1} = 0
+  CUDA_TRY(cudaMemsetAsync(w.slots, 0, sizeof(unsigned long long) * 2 * kSlotWords * (size_t)grid, st));
+  Cg1sArgs a{};
+  CgArgs& c = a.g.base;
+  c.M = v;
+  c.b = b;
+  c.x0 = x0;
+  c.x = x;
+  c.q = w.q;
+  c.hist = hist;
+  c.slots = w.slots;
+  c.res = w.res;
+  c.tol = o->tol;
+  c.max_iter = o->max_iter > 0 ? o->max_iter : std::max(1, m->n);
+  c.record_history = o->record_history;
+  c.recompute = o->recompute_final_residual;
+  for (int k = 0; k < 2; ++k) a.g.R[k] = w.cg1 + (size_t)k * std::max(1, m->n);
+  for (int k = 0; k < 2; ++k) a.g.S[k] = w.cg1 + (size_t)(2 + k) * std::max(1, m->n);
+  for (int k = 0; k < 3; ++k) a.g.W[k] = w.cg1 + (size_t)(4 + k) * std::max(1, m->n);
+  a.Pv = w.cg1 + (size_t)7 * std::max(1, m->n);
+  CUDA_TRY(cudaEventRecord(w.ev0, st));
+  if ((rc = kf == K_CSR ? launch_cg1s<K_CSR>(a, grid, st) : launch_cg1s<K_SCSR_PRIV>(a, grid, st)))
+    return rc;
+  CUDA_TRY(cudaEventRecord(w.ev1, st));
+  CUDA_TRY(cudaMemcpyAsync(w.h_res, w.res, sizeof(CgDevResult), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
+  const CgDevResult& r = *w.h_res;
+  *out = spcg_cg_result{};
+  out->iterations = r.iterations;
+  out->converged = r.converged;
+  out->status = r.status;
+  out->fail_iteration = r.fail_iter;
+  out->final_relative_residual = r.final_rel;
+  out->b_norm = r.b_norm;
+  out->device_ms = ms;
+  out->kernel_launches = 1;
+  out->engine_used = 7;
+  if (r.status != SPCG_OK) {
+    const char* what = r.status == SPCG_ERR_NOT_SPD ? "matrix not positive definite"
+                       : r.status == SPCG_ERR_NONFINITE_ALPHA ? "non-finite alpha"
+                       : r.status == SPCG_ERR_NONFINITE_RESIDUAL ? "non-finite residual"
+                                                                  : "non-finite beta";
+    return fail(r.status, std::string(what) + " at iteration " + std::to_string(r.fail_iter));
+  }
+  return SPCG_OK;
+}
+
 int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double* hist,
           const spcg_cg_options* o, spcg_cg_result* out, cudaStream_t st) {
   DevInfo* d;
@@ -17,13 +83,31 @@ int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double
   }
   const int kf = kfmt_of(m, o->accumulation);
   if (kf == K_SCSR_PRIV && !m->hasB) return fail(SPCG_ERR_UNSUPPORTED, "no L^T for privatized mode");
-  if (o->engine != 0 && o->engine != 2 && o->engine != 3 && o->engine != 5 && o->engine != 6)
-    return fail(SPCG_ERR_ARG, "engine must be 0 (auto), 2, 3, 5 or 6");
+  if (o->engine != 0 && o->engine != 2 && o->engine != 3 && o->engine != 5 && o->engine != 6 &&
+      o->engine != 7)
+    return fail(SPCG_ERR_ARG, "engine must be 0 (auto), 2, 3, 5, 6 or 7");
   const MatView v = view(m, kf == K_SCSR_PRIV);
   const bool fits = v.ntiles <= d->coop_res * kStages;
+  if (o->engine == 7) {
+    if (kf != K_CSR && kf != K_SCSR_PRIV)
+      return fail(SPCG_ERR_UNSUPPORTED, "engine 7 takes gather formats (CSR, privatized symmetric half)");
+    return do_cg1s(m, kf, b, x0, x, hist, o, out, st);
+  }
   // engine 2, and auto for systems that stream from HBM: per-pass kernels
   // (the sharded engine with no peers) — each pass keeps the whole register
   // budget, which a persistent kernel cannot (P3: 0.99 vs 0.82 of roofline)
+  // auto, full CSR that does not fit on chip but whose tile list is short
+  // (<= 16 tiles per co-resident CTA, ~1 M rows): engine 7's one persistent
+  // launch beats three launches per iteration (2-D Poisson 512^2 12.7 vs
+  // 30.6 us per iteration, 3-D 100^3 42.9 vs 50.0); beyond that the per-pass
+  // kernels stream faster (3-D 128^3 73.8 vs 103.6); symmetric-half
+  // privatized would stream L^T too (27-point 64^3 57.6 vs 45.6), so not
+  // there (scripts/engine7_ab.py)
+  if (o->engine == 0 && !fits && kf == K_CSR) {
+    int g7 = 1;
+    if ((rc = cg1s_grid<K_CSR>(d, &g7))) return rc;
+    if (v.ntiles <= 16 * g7) return do_cg1s(m, kf, b, x0, x, hist, o, out, st);
+  }
   if (o->engine == 2 || (o->engine == 0 && !fits))
     return do_dist_cg(m, nullptr, 0, nullptr, nullptr, nullptr, nullptr, b, x0, x, hist, o, out, st);
   // engine 5, and auto for banded systems whose rows fit the co-resident
@@ -94,7 +178,7 @@ int do_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double
   a.recompute = o->recompute_final_residual;
   Cg1Args g{};
   const size_t vb = sizeof(double) * (size_t)std::max(1, m->n);
-  if (!w.cg1 && (rc = dmalloc((void**)&w.cg1, 7 * vb, nullptr))) return rc;
+  if (!w.cg1 && (rc = dmalloc((void**)&w.cg1, 8 * vb, nullptr))) return rc;  // (+ p of engine 7)
   CUDA_TRY(cudaMemsetAsync(w.cg1, 0, 7 * vb, st));
   g.base = a;
   for (int k = 0; k < 2; ++k) g.R[k] = w.cg1 + (size_t)k * std::max(1, m->n);

@@ -13,7 +13,8 @@ from paper_1010_4639_b200.device import DeviceMatrix  # noqa: E402
 
 CFG = {"P3": ("poisson3d", (400, 400, 400), "csr", 1), "P2": ("poisson2d", (4096, 4096), "csr", 1),
        "Q27": ("stencil27", (256, 256, 256), "scsr", 0), "Q27P": ("stencil27", (256, 256, 256), "scsr", 1),
-       "Q27S": ("stencil27", (256, 256, 256), "scsr", 1)}
+       "Q27S": ("stencil27", (256, 256, 256), "scsr", 1),
+       "M512": ("poisson2d", (512, 512), "csr", 1), "M1024": ("poisson2d", (1024, 1024), "csr", 1)}
 name = sys.argv[1]
 kind, dims, fmt, acc = CFG[name]
 dm = DeviceMatrix.generate(kind, dims, fmt)

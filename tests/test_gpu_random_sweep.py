@@ -102,7 +102,7 @@ def _arrow(n):
                                     np.concatenate([vals, diag])), n)
 
 
-@pytest.mark.parametrize("engine", [0, 2, 3, 5])
+@pytest.mark.parametrize("engine", [0, 2, 3, 5, 7])
 @pytest.mark.parametrize("storage", ["csr", "sym_priv", "sym_atomic", "csc"])
 @pytest.mark.parametrize("n,density,seed", [(300, 0.05, 1), (2500, 0.004, 2), (12000, 0.0008, 3),
                                             (6000, -1.0, 4)])
@@ -116,15 +116,17 @@ def test_random_spd_all_engines(engine, storage, n, density, seed):
     m, cfg = _storage(a, storage)
     try:
         r = cg_solve(m, b, opts=CgOptions(record_history=True), cfg=cfg, engine=engine)
-    except Exception as e:  # engine 5 may decline unbanded systems; auto never does
-        assert engine == 5 and "not applicable" in str(e), e
+    except Exception as e:  # engine 5 may decline unbanded systems, engine 7 the
+        # scatter formats; auto never declines
+        assert (engine == 5 and "not applicable" in str(e)) or (
+            engine == 7 and storage in ("sym_atomic", "csc") and "gather formats" in str(e)), e
         return
     assert abs(r.iterations - ref.iterations) <= max(1, ref.iterations // 100)
     assert np.linalg.norm(r.x - ref.x) / np.linalg.norm(ref.x) <= 1e-8
     assert r.final_relative_residual <= 1e-10
 
 
-@pytest.mark.parametrize("engine", [0, 2, 3, 5])
+@pytest.mark.parametrize("engine", [0, 2, 3, 5, 7])
 def test_degenerate_sizes(engine):
     """n = 0 (empty system: b = 0 -> x = [] converged, as solver.py:109-118)
     and n = 1 through every engine and storage."""
@@ -137,7 +139,7 @@ def test_degenerate_sizes(engine):
     assert r0.iterations == 0 and r0.converged and r0.x.shape == (0,)
     assert spmv_full(a0, np.empty(0)).shape == (0,)
     a1 = build_csr_from_triplets((np.array([0]), np.array([0]), np.array([4.0])), 1)
-    for kind in ("csr", "sym_priv", "sym_atomic", "csc"):
+    for kind in ("csr", "sym_priv") if engine == 7 else ("csr", "sym_priv", "sym_atomic", "csc"):
         m, cfg = _storage(a1, kind)
         r1 = cg_solve(m, np.array([2.0]), opts=CgOptions(record_history=True), cfg=cfg,
                       engine=engine)
@@ -167,7 +169,7 @@ def test_row_sums_modes_long_rows(storage):
         KernelConfig(row_sums="fast")
 
 
-@pytest.mark.parametrize("engine", [0, 2])
+@pytest.mark.parametrize("engine", [0, 2, 7])
 @pytest.mark.parametrize("storage", ["csr", "sym_priv", "sym_atomic", "csc"])
 def test_streaming_engines_all_storages(engine, storage):
     """A system too large for the resident kernels (auto routes it to the
@@ -181,13 +183,17 @@ def test_streaming_engines_all_storages(engine, storage):
     ref = O.cg_solve("csr", a.row_start, a.col_idx, a.values, b)
     m, cfg = _storage(a, storage)
     assert m.device().info()["ntiles"] > 2 * 148
+    if engine == 7 and storage in ("sym_atomic", "csc"):
+        with pytest.raises(Exception, match="gather formats"):
+            cg_solve(m, b, cfg=cfg, engine=engine)
+        return
     r = cg_solve(m, b, opts=CgOptions(record_history=True), cfg=cfg, engine=engine)
     assert abs(r.iterations - ref.iterations) <= max(1, ref.iterations // 100)
     assert np.linalg.norm(r.x - ref.x) / np.linalg.norm(ref.x) <= 1e-8
     assert r.final_relative_residual <= 1e-10
 
 
-@pytest.mark.parametrize("engine", [1, 4, 7, -1])
+@pytest.mark.parametrize("engine", [1, 4, 8, -1])
 def test_removed_engines_are_rejected(engine):
     from paper_1010_4639_b200 import cg_solve
     from paper_1010_4639_b200.genprob import poisson2d
@@ -195,3 +201,22 @@ def test_removed_engines_are_rejected(engine):
     a = poisson2d(8, 8)
     with pytest.raises(ValueError, match="engine must be"):
         cg_solve(a, np.ones(a.n), engine=engine)
+
+
+@pytest.mark.parametrize("dims,engine_expected", [((512, 512), 7), ((1448, 1448), 2)])
+def test_auto_routes_midsize_csr(dims, engine_expected):
+    """Auto on full CSR that does not fit on chip: engine 7 (one persistent
+    streamed launch) up to ~1 M rows, the per-pass engine beyond; both follow
+    the serial reference CG's iteration count (capped) and each other's x."""
+    from paper_1010_4639_b200 import CgOptions, cg_solve
+    from paper_1010_4639_b200.genprob import poisson2d
+
+    a = poisson2d(*dims)
+    b = np.random.default_rng(11).standard_normal(a.n)
+    r0 = cg_solve(a, b, opts=CgOptions(max_iter=300, record_history=True))
+    assert r0.engine_info["engine"] == engine_expected
+    other = 2 if engine_expected == 7 else 7
+    r1 = cg_solve(a, b, opts=CgOptions(max_iter=300, record_history=True), engine=other)
+    assert r0.iterations == r1.iterations == 300
+    assert np.linalg.norm(r0.x - r1.x) / np.linalg.norm(r1.x) <= 1e-12
+    assert np.allclose(r0.residual_history, r1.residual_history, rtol=1e-6)
