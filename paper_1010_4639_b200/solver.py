@@ -68,7 +68,7 @@ class SolveReport:
     residual_history: list[float] | None = None
     timings: dict[str, float] = field(default_factory=dict)
     # (new, not in the reference's record) which device engine produced x:
-    # {"engine": 2|3|5|6, "fallback": bool, "cond_estimate": float}
+    # {"engine": 2|3|5|6|7, "fallback": bool, "cond_estimate": float}
     engine_info: dict = field(default_factory=dict, compare=False, repr=False)
 
 
