@@ -460,6 +460,16 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   // + update + halo + sync] ns, then records its SM id and start / end times
   // the leader thread always (SolveReport.timings), every CTA when tracing
   const bool tr = tid == 0 && (A.trace != nullptr || (SPCG_PHASE_TIMERS && gme == 0));
+  // (SPCG_XCHG_TRACE) thread 0's timeline of iterations 100-107: [start,
+  // SpMV done, sends done, totals in, partials posted, halo rows + barrier]
+  unsigned long long* const tl_base =
+      (SPCG_XCHG_TRACE && A.trace && tid == 0)
+          ? A.trace + 8 * (size_t)G + (size_t)max(K * 8 * 34, 16 * G) + (size_t)gme * 8 * 6
+          : nullptr;
+  long long tl_it = -1;
+#define SPCG_TL(j)                                                              \
+  if (SPCG_XCHG_TRACE && tl_base && tl_it >= 100 && tl_it < 108)                \
+    tl_base[(tl_it - 100) * 6 + (j)] = globaltimer_ns();
   unsigned long long tph[4] = {0, 0, 0, 0};
   // SPCG_PIPE_FINE (SM cycles), thread 0: [partials, deferred halo, SpMV,
   // send n, wait mbB, scalars, own-row update, halo rows + sync]; the leader
@@ -516,6 +526,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     const unsigned long long t0 = tr ? globaltimer_ns() : 0;
     if (SPCG_PIPE_FINE) tfl = clock64();
     cur_it = it;
+    tl_it = it;
+    SPCG_TL(0)
     if (tid == 0) mbar_arrive_expect_tx(&cs.mbB[h3], (uint32_t)bbytes);
     // reciprocals of the last step's scalars, off the critical path: the
     // scalar step after the wait is then one division deep
@@ -556,11 +568,14 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     double ng[NS];
     spmv(ng);  // n = A w (the comm warp has no rows), overlapped with the all-reduce
     SPCG_FT(2)
+    SPCG_TL(1)
     const unsigned long long t1 = tr ? globaltimer_ns() : 0;
     const unsigned long long t2 = t1;
     if (!comm) send_n(ng, h3, tag);
     SPCG_FT(3)
+    SPCG_TL(2)
     mbar_wait_cluster(&cs.mbB[h3], parB);  // totals + the cluster neighbours' boundary n
+    SPCG_TL(3)
     // the first halo row of this thread, if another cluster owns it: its
     // tagged words are loaded now and consumed after the scalars, the update
     // and the partials' post (the L2 round trip off the path: 2.94 vs 3.12 us
@@ -661,6 +676,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
           wwin[own0 + rrow[k] - P.row_lo] = wg[k];
         }
       post_msg(pb ^ 1);  // the partials of iteration it+1
+      SPCG_TL(4)
       if (it >= 1) hist_w(it, g_new);
       SPCG_FT(6)
       for (int hb = tid - lane; hb < nh; hb += kPipeRowThreads) {  // warp-uniform trip count
@@ -681,6 +697,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       asm volatile("bar.sync 1, %0;" ::"r"(kPipeRowThreads) : "memory");
     }
     SPCG_FT(7)
+    SPCG_TL(5)
     if (tr) tph[3] += globaltimer_ns() - t3;
   }
   // every CTA leaves the loop at the same iteration (identical totals); the
@@ -688,6 +705,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   cluster_sync_all();
   rel = sqrt(g_rel) / b_norm;
 #undef SPCG_FT
+#undef SPCG_TL
   if (tr && A.trace) {
     unsigned int smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));

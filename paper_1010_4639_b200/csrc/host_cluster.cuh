@@ -565,8 +565,10 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
   static const char* dbg_path = getenv("SPCG_CLUS_DEBUG");  // per-solve CTA trace lines
   // [C][8] per-CTA phases + [K][8 iterations][34] exchange trace (engine 6)
   // (SPCG_PIPE_FINE builds: [C][16] sub-phase totals in place of the exchange trace)
-  const size_t trace_words = 8 * (size_t)P.C +
-                             std::max((size_t)(P.C / std::max(1, P.cs)) * 8 * 34, 16 * (size_t)P.C);
+  // (SPCG_XCHG_TRACE builds: + [C][8 iterations][6] per-CTA timeline)
+  const size_t tl0 = 8 * (size_t)P.C +
+                     std::max((size_t)(P.C / std::max(1, P.cs)) * 8 * 34, 16 * (size_t)P.C);
+  const size_t trace_words = tl0 + (size_t)P.C * 8 * 6;
   if (tracing || dbg_path) {
     CUDA_TRY(cudaMalloc((void**)&a.trace, sizeof(unsigned long long) * trace_words));
     CUDA_TRY(cudaMemsetAsync(a.trace, 0, sizeof(unsigned long long) * trace_words, st));
@@ -621,6 +623,9 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
         fprintf(f, "], \"fine\": [");
         for (size_t w = 0; w < 16 * (size_t)P.C; ++w)
           fprintf(f, "%s%llu", w ? ", " : "", tv[8 * (size_t)P.C + w]);
+        fprintf(f, "], \"tl\": [");
+        for (size_t w = tl0; w < trace_words; ++w)
+          fprintf(f, "%s%lld", w > tl0 ? ", " : "", tv[w] ? (long long)(tv[w] - t0) : -1LL);
         fprintf(f, "], \"K\": %d}\n", K);
         fclose(f);
       }
