@@ -35,11 +35,12 @@ for eng, (name, m) in ((e, nm) for e in engines for nm in (("F", F), ("S", extra
         xs = x.cpu().numpy()
         # engine 3 runs CSC as a column scatter with fp64 atomics: its order is
         # unspecified by contract (like the reference's atomic mode), so only
-        # iterations and x to 1e-12 must repeat; every other case bitwise
+        # iterations and x to 1e-9 (the parity bar is 1e-8 against the
+        # reference) must repeat; every other case bitwise
         exact = not (eng == 3 and name == "C")
         same = ref is not None and r.iterations == ref[0] and (
             np.array_equal(xs, ref[1]) if exact
-            else np.linalg.norm(xs - ref[1]) <= 1e-12 * np.linalg.norm(ref[1]))
+            else np.linalg.norm(xs - ref[1]) <= 1e-9 * np.linalg.norm(ref[1]))
         if rc != 0 or (ref is not None and not same):
             bad += 1
             print(name, "run", i, "rc", rc, "its", r.iterations, flush=True)
