@@ -170,3 +170,51 @@ def test_grid_shapes_deterministic(shape):
         assert "fails 0" in ln, ln
         # one outcome for all runs: {(329, '<hash>'): 6}
         assert ln.count("(329,") == 1 and ": 6}" in ln, ln
+
+
+def _banded_spd(n, bw, per_row, seed, shift=0.05):
+    """Random symmetric banded matrix, diagonally dominant (SPD): per_row
+    strictly-lower entries per row within bw of the diagonal."""
+    from paper_1010_4639_b200 import build_csr_from_triplets
+
+    rng = np.random.default_rng(seed)
+    rows, cols = [], []
+    for i in range(1, n):
+        k = min(per_row, i, bw)
+        js = rng.choice(np.arange(max(0, i - bw), i), size=k, replace=False)
+        rows.append(np.full(k, i))
+        cols.append(js)
+    I = np.concatenate(rows)
+    J = np.concatenate(cols)
+    V = -rng.uniform(0.1, 1.0, size=I.size)
+    d = np.bincount(I, weights=np.abs(V), minlength=n) + np.bincount(J, weights=np.abs(V), minlength=n)
+    d = d + shift * (1.0 + d.mean())
+    return build_csr_from_triplets((np.concatenate([I, J, np.arange(n)]),
+                                    np.concatenate([J, I, np.arange(n)]),
+                                    np.concatenate([V, V, d])), n)
+
+
+@pytest.mark.parametrize("n,bw,per_row,seed", [(5000, 40, 6, 1), (40000, 300, 8, 2),
+                                                (120000, 900, 5, 3), (200000, 60, 3, 4),
+                                                (90000, 1500, 4, 5)])
+@pytest.mark.parametrize("kind", ["csr", "sym_priv", "csc"])
+@pytest.mark.parametrize("engine", [5, 6])
+def test_cluster_engines_random_banded(n, bw, per_row, seed, kind, engine):
+    """Engines 5 and 6 on random banded SPD systems across plan shapes (one
+    cluster to K clusters, one to four row slots per thread, narrow and
+    wide halos): the reference CG's iterations and x, bitwise repeatable."""
+    from paper_1010_4639_b200 import CgOptions, cg_solve
+
+    a = _banded_spd(n, bw, per_row, seed)
+    b = np.random.default_rng(seed + 100).standard_normal(n)
+    ref = O.cg_solve("csr", a.row_start, a.col_idx, a.values, b, workers=O.host_cores())
+    m, cfg = as_storage(a, kind)
+    try:
+        r1 = cg_solve(m, b, opts=CgOptions(record_history=True), cfg=cfg, engine=engine)
+    except Exception as e:  # the plan may decline a shape (window / rows)
+        assert "not applicable" in str(e) or "too many rows" in str(e), e
+        pytest.skip(str(e))
+    r2 = cg_solve(m, b, cfg=cfg, engine=engine)
+    assert abs(r1.iterations - ref.iterations) <= max(1, ref.iterations // 100)
+    assert np.linalg.norm(r1.x - ref.x) / np.linalg.norm(ref.x) <= 1e-8
+    assert r1.iterations == r2.iterations and np.array_equal(r1.x, r2.x)
