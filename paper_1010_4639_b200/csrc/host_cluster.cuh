@@ -508,6 +508,7 @@ double lanczos_cond(const std::vector<double>& ab, long long k) {
 // Above either limit the auto mode re-solves on engine 5 (standard-order
 // single-reduction CG, within 1e-9 of the reference in the same sweep).
 constexpr double kPipeCondMax = 1.0e5;
+constexpr long long kCoefHost = 4096;  // guard coefficients copied with the result
 constexpr double kPipeTrueResMax = 2.0;  // true rel residual / tol
 
 int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, double* hist,
@@ -576,6 +577,13 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
   CUDA_TRY(cudaEventRecord(w.ev0, st));
   if ((rc = launch_clus(P, a, st, pipe))) return rc;
   CUDA_TRY(cudaEventRecord(w.ev1, st));
+  // the guard's coefficients ride along with the result (one wait, not two)
+  const long long coef_pre = guard ? std::min<long long>(max_iter, kCoefHost) : 0;
+  if (coef_pre > 0) {
+    if (!w.h_coef) CUDA_TRY(cudaMallocHost((void**)&w.h_coef, sizeof(double) * 2 * kCoefHost));
+    CUDA_TRY(cudaMemcpyAsync(w.h_coef, w.coef, sizeof(double) * 2 * (size_t)coef_pre,
+                             cudaMemcpyDeviceToHost, st));
+  }
   CUDA_TRY(cudaMemcpyAsync(w.h_res, w.res, sizeof(CgDevResult), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   float ms = 0.f;
@@ -668,7 +676,10 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
   double cond = 0.0;
   if (guard && r.status == SPCG_OK && r.iterations >= 2) {
     std::vector<double> ab(2 * (size_t)r.iterations);
-    CUDA_TRY(cudaMemcpy(ab.data(), w.coef, sizeof(double) * ab.size(), cudaMemcpyDeviceToHost));
+    if (r.iterations <= coef_pre)
+      std::copy(w.h_coef, w.h_coef + ab.size(), ab.begin());
+    else
+      CUDA_TRY(cudaMemcpy(ab.data(), w.coef, sizeof(double) * ab.size(), cudaMemcpyDeviceToHost));
     cond = lanczos_cond(ab, r.iterations);
     if (cond > kPipeCondMax || r.final_rel > kPipeTrueResMax * o->tol) {
       // re-solve on engine 5; the reported time covers both solves

@@ -209,6 +209,7 @@ void free_matrix(spcg_matrix_s* m) {
   F(w.r); F(w.p0); F(w.p1); F(w.q); F(w.part); F(w.slots); F(w.res);
   F(w.b); F(w.x); F(w.x0); F(w.hist); F(w.cg1); F(w.coef);
   if (w.h_res) cudaFreeHost(w.h_res);
+  if (w.h_coef) cudaFreeHost(w.h_coef);
   if (w.ev0) cudaEventDestroy(w.ev0);
   if (w.ev1) cudaEventDestroy(w.ev1);
   DistWorkspace& d = m->dw;

@@ -176,6 +176,7 @@ struct Workspace {
   long long hist_cap = 0;
   double* coef = nullptr;  // engine-6 guard: (alpha, beta) per update
   long long coef_cap = 0;
+  double* h_coef = nullptr;  // pinned: the first kCoefHost pairs come back with the result
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
 
