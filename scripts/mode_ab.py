@@ -14,11 +14,13 @@ from paper_1010_4639_b200.device import DeviceMatrix  # noqa: E402
 from paper_1010_4639_b200.distributed import ShardedMatrix, group_plans, group_solve  # noqa: E402
 
 lib = N.load()
-for side in [int(s) for s in sys.argv[1:]] or [64, 128, 256]:
-    dims = (side, side, side)
-    n = side ** 3
+for arg in sys.argv[1:] or ["64", "128", "256"]:
+    kind = "poisson2d" if arg.startswith("2d") else "poisson3d"
+    side = int(arg[2:]) if arg.startswith("2d") else int(arg)
+    dims = (side, side) if kind == "poisson2d" else (side, side, side)
+    n = side ** len(dims)
     its = 200
-    dm = DeviceMatrix.generate("poisson3d", dims, "csr")
+    dm = DeviceMatrix.generate(kind, dims, "csr")
     b = torch.from_numpy(np.random.default_rng(1).standard_normal(n)).cuda()
     x = torch.empty_like(b)
     t0 = []
@@ -28,7 +30,7 @@ for side in [int(s) for s in sys.argv[1:]] or [64, 128, 256]:
         r = N.CgResultC()
         N.check(lib.spcg_cg_solve(dm.handle, b.data_ptr(), None, x.data_ptr(), None, o, r, 0), "s")
         t0.append(1e3 * r.device_ms / r.iterations)
-    shards = ShardedMatrix.group_from_stencil("poisson3d", dims, "csr", 1)
+    shards = ShardedMatrix.group_from_stencil(kind, dims, "csr", 1)
     plans = group_plans(shards)
     t1 = []
     for rep in range(3):
