@@ -114,8 +114,17 @@ __device__ __forceinline__ double tagged_load(const unsigned long long* src, uin
 
 // NS: row slots per thread (2 when the plan's CTAs have <= 30 slices: fewer
 // live registers, no spills; 4 otherwise)
-template <int NS>
-__global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArgs A) {
+constexpr int kRegW = 24;  // register rows: entries per row (the F-mesh's longest row)
+constexpr int kRegThreads = 384;  // register rows: 11 row warps + the comm warp
+
+// TH: threads of the CTA (512, or 384 for the register-row variant: the
+// 168-register budget); REG: each thread keeps its row's values and columns
+// in registers (one row slot, rows of <= kRegW entries) so the SpMV reads
+// only the window gathers from shared memory
+template <int NS, int TH = kPipeThreads, bool REG = false>
+__global__ void __launch_bounds__(TH, 1) clus_pcg_kernel(const ClusArgs A) {
+  constexpr int PW_ = TH / 32, PRW_ = PW_ - 1, PRT_ = PRW_ * 32;
+  static_assert(!REG || NS == 1, "register rows: one slot per thread");
   namespace cgp = cooperative_groups;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ PipeShared cs;
@@ -144,7 +153,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   double* sval = reinterpret_cast<double*>(smem_raw + A.off_val);
   unsigned short* scol = reinterpret_cast<unsigned short*>(smem_raw + A.off_col);
   const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
-  const bool comm = wp == kPipeRowWarps;
+  const bool comm = wp == PRW_;
   const bool leader = gme == 0 && tid == 0;
   const int nh = P.wn - (P.row_hi - P.row_lo);
   const int own0 = P.row_lo - P.wlo;
@@ -154,7 +163,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     const ClusSlice sd = A.slices[P.slice0 + s];
     if (sd.soff < 0) continue;
     const int cnt = sd.width * 32;
-    for (int e = tid; e < cnt; e += kPipeThreads) {
+    for (int e = tid; e < cnt; e += TH) {
       sval[sd.soff + e] = A.gval[sd.goff + e];
       scol[sd.soff + e] = A.gcol[sd.goff + e];
     }
@@ -167,7 +176,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       sg[NS], wg[NS], zg[NS];
 #pragma unroll
   for (int k = 0; k < NS; ++k) {
-    const int s = wp + kPipeRowWarps * k;
+    const int s = wp + PRW_ * k;
     rrow[k] = -1;
     rlen[k] = rlenA[k] = swidth[k] = sbase[k] = 0;
     sres[k] = false;
@@ -181,6 +190,22 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       swidth[k] = sd.width;
       sres[k] = sd.soff >= 0;
       sbase[k] = (sres[k] ? sd.soff : sd.goff) + lane;
+    }
+  }
+  // REG: the row's values and window-relative columns, read once
+  double vreg[REG ? kRegW : 1];
+  uint32_t creg[REG ? kRegW / 2 : 1];
+  if (REG) {
+    // from the global SELL arrays: the shared-memory copy above is still in
+    // flight in other threads (no barrier yet)
+    const int gb = (!comm && wp < P.nslices) ? A.slices[P.slice0 + wp].goff + lane : 0;
+#pragma unroll
+    for (int u = 0; u < kRegW; ++u) {
+      const bool in = u < rlen[0];
+      vreg[u] = in ? A.gval[gb + u * 32] : 0.0;
+      const uint32_t c = in ? (uint32_t)A.gcol[gb + u * 32] : 0u;
+      if (u & 1) creg[u >> 1] |= c << 16;
+      else creg[u >> 1] = c;
     }
   }
   if (tid == 0) {
@@ -207,8 +232,19 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
         // two-sum order bought nothing (S: 3.77 -> 2.86 us per iteration,
         // bitwise the full-row solve)
         constexpr int U = NS == 2 ? SPCG_PIPE_UNROLL_ONE2 : SPCG_CLUS_UNROLL;
-        const double q = sres[k] ? clus_row<false, U>(sval, scol, sbase[k], swidth[k], rlen[k], rlenA[k], wwin)
-                                 : clus_row<false, U>(A.gval, A.gcol, sbase[k], swidth[k], rlen[k], rlenA[k], wwin);
+        double q;
+        if (REG) {  // the same storage-order sum, operands from registers
+          q = 0.0;
+#pragma unroll
+          for (int u = 0; u < kRegW; ++u)
+            if (u < rlen[k]) {
+              const uint32_t c = (u & 1) ? (creg[u >> 1] >> 16) : (creg[u >> 1] & 0xffffu);
+              q = __dadd_rn(q, __dmul_rn(vreg[u], wwin[c]));
+            }
+        } else {
+          q = sres[k] ? clus_row<false, U>(sval, scol, sbase[k], swidth[k], rlen[k], rlenA[k], wwin)
+                      : clus_row<false, U>(A.gval, A.gcol, sbase[k], swidth[k], rlen[k], rlenA[k], wwin);
+        }
         out[k] = rrow[k] >= 0 ? q : 0.0;
       }
     }
@@ -223,8 +259,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     }
     __syncthreads();
     if (wp == 0) {
-      double b0 = lane < kPipeWarps ? cs.red[0][lane] : 0.0;
-      double b1 = lane < kPipeWarps ? cs.red[1][lane] : 0.0;
+      double b0 = lane < PW_ ? cs.red[0][lane] : 0.0;
+      double b1 = lane < PW_ ? cs.red[1][lane] : 0.0;
       b0 = warp_sum(b0);
       b1 = warp_sum(b1);
       if (lane < C) {
@@ -397,7 +433,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
   }
   // x = x0, r0 = b - A x0 (solver.py:120-124)
   if (A.x0 != nullptr) {
-    for (int j = tid; j < P.wn; j += kPipeThreads) wwin[j] = A.x0[P.wlo + j];
+    for (int j = tid; j < P.wn; j += TH) wwin[j] = A.x0[P.wlo + j];
     __syncthreads();
     double qv[NS];
     spmv(qv);
@@ -441,8 +477,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     converged = 1;
     max_it = 0;
   } else {
-    for (int j = tid; j < P.wn; j += kPipeThreads) wwin[j] = __ldcg(A.scratch + P.wlo + j);
-    for (int h = tid; h < A.hcap; h += kPipeThreads) zhalo[h] = 0.0;
+    for (int j = tid; j < P.wn; j += TH) wwin[j] = __ldcg(A.scratch + P.wlo + j);
+    for (int h = tid; h < A.hcap; h += TH) zhalo[h] = 0.0;
     __syncthreads();
     spmv(wg);  // w0 = A r0
     part = dummy = 0.0;
@@ -451,7 +487,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     for (int k = 0; k < NS; ++k)
       if (rrow[k] >= 0) A.scratch[rrow[k]] = wg[k];
     allreduce2(part, dummy);
-    for (int j = tid; j < P.wn; j += kPipeThreads) wwin[j] = __ldcg(A.scratch + P.wlo + j);
+    for (int j = tid; j < P.wn; j += TH) wwin[j] = __ldcg(A.scratch + P.wlo + j);
     __syncthreads();
   }
 
@@ -535,7 +571,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     asm volatile("" ::"d"(inv_gam), "d"(inv_alpha));  // computed here, before the waits
     if (comm) {
       if (me == 0) {
-        if (lane == 0) mbar_arrive_expect_tx(&cs.mbA[pb], (uint32_t)(C * kPipeRowWarps * 16));
+        if (lane == 0) mbar_arrive_expect_tx(&cs.mbA[pb], (uint32_t)(C * PRW_ * 16));
         const bool trc = SPCG_PIPE_FINE && A.trace && lane == 0;
         unsigned long long tc0 = trc ? clock64() : 0;
         mbar_wait_cluster(&cs.mbA[pb], parA);
@@ -547,7 +583,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
         // lane w: warp w's partials over the cluster's CTAs; then the warps in
         // a fixed tree (the same bits on every lane after the broadcast)
         double c0 = 0.0, c1 = 0.0;
-        if (lane < kPipeRowWarps)
+        if (lane < PRW_)
           for (int c = 0; c < C; ++c) {
             c0 += cs.wslot[pb][c][lane][0];
             c1 += cs.wslot[pb][c][lane][1];
@@ -663,7 +699,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       // every row warp's SpMV has read the window of w before any warp writes
       // it (a warp with two slices is still reading when a one-slice warp
       // gets here; the cluster barrier of the barrier protocol did this)
-      asm volatile("bar.sync 1, %0;" ::"r"(kPipeRowThreads) : "memory");
+      asm volatile("bar.sync 1, %0;" ::"r"(PRT_) : "memory");
 #pragma unroll
       for (int k = 0; k < NS; ++k)
         if (rrow[k] >= 0) {
@@ -679,7 +715,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
       SPCG_TL(4)
       if (it >= 1) hist_w(it, g_new);
       SPCG_FT(6)
-      for (int hb = tid - lane; hb < nh; hb += kPipeRowThreads) {  // warp-uniform trip count
+      for (int hb = tid - lane; hb < nh; hb += PRT_) {  // warp-uniform trip count
         const int h = hb + lane;
         const bool act = h < nh;
         const double nv = (e_act && h == tid) ? tagged_finish(esrc, ea, eb, tag)
@@ -694,7 +730,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
 
       // the window of w is complete before the next SpMV (row warps only: the
       // comm warp never touches it)
-      asm volatile("bar.sync 1, %0;" ::"r"(kPipeRowThreads) : "memory");
+      asm volatile("bar.sync 1, %0;" ::"r"(PRT_) : "memory");
     }
     SPCG_FT(7)
     SPCG_TL(5)
@@ -739,7 +775,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) clus_pcg_kernel(const ClusArg
     part = 0.0;
     dummy = 0.0;
     allreduce2(part, dummy);
-    for (int j = tid; j < P.wn; j += kPipeThreads) wwin[j] = __ldcg(A.x + P.wlo + j);
+    for (int j = tid; j < P.wn; j += TH) wwin[j] = __ldcg(A.x + P.wlo + j);
     __syncthreads();
     double qv[NS];
     spmv(qv);

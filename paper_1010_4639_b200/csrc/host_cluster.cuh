@@ -234,6 +234,7 @@ int build_clus_plan(spcg_matrix_s* m) {
         if (q < (int)o.size()) wdt = std::max(wdt, lenA(o[q]) + lenB(o[q]));
       }
       sd.width = wdt;
+      P.max_width = std::max(P.max_width, wdt);
       sd.soff = -1;
       slices.push_back(sd);
       for (int l = 0; l < 32; ++l) {
@@ -349,7 +350,8 @@ int build_clus_plan(spcg_matrix_s* m) {
   CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
   if (csz > 8) CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   // the pipelined kernel (engine 6) runs the same plan with one more warp
-  const void* kpipes[2] = {(const void*)clus_pcg_kernel<2>, (const void*)clus_pcg_kernel<4>};
+  const void* kpipes[3] = {(const void*)clus_pcg_kernel<2>, (const void*)clus_pcg_kernel<4>,
+                           (const void*)clus_pcg_kernel<1, kRegThreads, true>};
   for (const void* kp : kpipes) {
     CUDA_TRY(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
     if (csz > 8) CUDA_TRY(cudaFuncSetAttribute(kp, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -425,7 +427,11 @@ int build_clus_plan(spcg_matrix_s* m) {
 int launch_clus(const ClusPlan& P, const ClusArgs& a, cudaStream_t st, bool pipe) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(P.C);
-  cfg.blockDim = dim3(pipe ? kPipeThreads : kClusThreads);
+  // engine 6 with register rows: every slice in one 384-thread CTA's 11 row
+  // warps (one slot each) and rows of <= kRegW entries (SPCG_PIPE_REG=0: off)
+  static const bool reg_ok = !getenv("SPCG_PIPE_REG") || atoi(getenv("SPCG_PIPE_REG")) != 0;
+  const bool reg = pipe && reg_ok && P.max_slices <= kRegThreads / 32 - 1 && P.max_width <= kRegW;
+  cfg.blockDim = dim3(reg ? kRegThreads : pipe ? kPipeThreads : kClusThreads);
   cfg.dynamicSmemBytes = P.smem;
   cfg.stream = st;
   cudaLaunchAttribute at[2];
@@ -441,7 +447,9 @@ int launch_clus(const ClusPlan& P, const ClusArgs& a, cudaStream_t st, bool pipe
   // once, and the kernel refuses a launch whose cluster size is not the plan's
   static const bool noncoop = getenv("SPCG_CLUS_NONCOOP") != nullptr;
   cfg.numAttrs = (P.C > P.cs && !noncoop) ? 2 : 1;
-  if (pipe) {
+  if (reg) {
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_pcg_kernel<1, kRegThreads, true>, a));
+  } else if (pipe) {
     const bool ns2 = P.max_slices <= kPipeMaxSlices2;
     // (two-segment plans too: engine 6 sums their rows in one chain)
     if (ns2) CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_pcg_kernel<2>, a));

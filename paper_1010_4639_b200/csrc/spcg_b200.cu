@@ -227,6 +227,7 @@ struct ClusPlan {
   size_t smem = 0;
   long long resident = 0, streamed = 0;  // entries (stats)
   int max_slices = 0;                     // SELL-32 slices of the fullest CTA
+  int max_width = 0;                      // longest row (entries) of the plan
   void* arena = nullptr;                  // the one allocation the pointers above live in
 };
 
