@@ -492,9 +492,10 @@ __global__ void __launch_bounds__(TH, 1) clus_pcg_kernel(const ClusArgs A) {
   }
 
   // per-phase trace (A.trace set: SPCG_TRACE / SPCG_CLUS_DEBUG): thread 0 of
-  // every CTA accumulates [partials+SpMV, wait A, send n + barrier B, scalars
-  // + update + halo + sync] ns, then records its SM id and start / end times
-  // the leader thread always (SolveReport.timings), every CTA when tracing
+  // every CTA accumulates [iteration start + SpMV, -, sends + wait for the
+  // totals, scalars + update + halo rows + barrier] ns, then records its SM
+  // id and start / end times; the leader thread always (SolveReport.timings),
+  // every CTA when tracing
   const bool tr = tid == 0 && (A.trace != nullptr || (SPCG_PHASE_TIMERS && gme == 0));
   // (SPCG_XCHG_TRACE) thread 0's timeline of iterations 100-107: [start,
   // SpMV done, sends done, totals in, partials posted, halo rows + barrier]
@@ -507,8 +508,8 @@ __global__ void __launch_bounds__(TH, 1) clus_pcg_kernel(const ClusArgs A) {
   if (SPCG_XCHG_TRACE && tl_base && tl_it >= 100 && tl_it < 108)                \
     tl_base[(tl_it - 100) * 6 + (j)] = globaltimer_ns();
   unsigned long long tph[4] = {0, 0, 0, 0};
-  // SPCG_PIPE_FINE (SM cycles), thread 0: [partials, deferred halo, SpMV,
-  // send n, wait mbB, scalars, own-row update, halo rows + sync]; the leader
+  // SPCG_PIPE_FINE (SM cycles), thread 0: [iteration start, -, SpMV, send n,
+  // wait mbB, scalars, own-row update + partials, halo rows + sync]; the leader
   // CTA's comm warp: [12] iteration start -> partials in, [13] sum + exchange
   unsigned long long* tfine = cs.fine;  // (shared: no registers in the loop)
   unsigned long long tfl = 0;
@@ -536,7 +537,7 @@ __global__ void __launch_bounds__(TH, 1) clus_pcg_kernel(const ClusArgs A) {
   // CTA posts those of i+2 after the totals of i+1, i.e. after rank 0 read
   // i's); totals and halo n (nhalo, mbB, ghalo) by iteration mod 3 (the sends
   // of i+3 need the totals of i+2, i.e. every CTA's partials of i+2, posted
-  // after that CTA's reads of i's halo rows, deferred ones included).
+  // after that CTA's reads of i's halo rows).
   const uint32_t bA0 = mapa_u32(&cs.mbA[0], 0), bA1 = mapa_u32(&cs.mbA[1], 0);
   const uint32_t wsl0 = mapa_u32(&cs.wslot[0][me][wp][0], 0);
   const uint32_t wsl1 = mapa_u32(&cs.wslot[1][me][wp][0], 0);
@@ -797,9 +798,9 @@ __global__ void __launch_bounds__(TH, 1) clus_pcg_kernel(const ClusArgs A) {
     A.res->final_rel = rel;
     A.res->b_norm = b_norm;
     A.res->rec_rel = rec_rel;
-    A.res->phase_ns[0] = tph[0];            // partials + SpMV
-    A.res->phase_ns[1] = tph[1] + tph[2];   // waits, exchange, barrier B
-    A.res->phase_ns[2] = tph[3];            // update + halo rows
+    A.res->phase_ns[0] = tph[0];            // SpMV
+    A.res->phase_ns[1] = tph[1] + tph[2];   // sends + wait for the totals (exchange)
+    A.res->phase_ns[2] = tph[3];            // scalars, update, partials, halo rows
   }
 }
 
