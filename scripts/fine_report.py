@@ -4,7 +4,7 @@ import sys
 
 import numpy as np
 
-names = ['recips+early', 'defer-halo', 'spmv', 'send n', 'wait mbB', 'scalars', 'own-upd+partials',
+names = ['start', '-', 'spmv', 'send n', 'wait mbB', 'scalars', 'own-upd+partials',
          'halo+sync', '-', '-', '-', '-', 'C:start->partials in', 'C:sum+exchange']
 recs = [json.loads(ln) for ln in open(sys.argv[1] if len(sys.argv) > 1 else 'gpurun_out/fine.jsonl')]
 for two in (0, 1):
