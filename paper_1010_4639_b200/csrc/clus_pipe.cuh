@@ -114,8 +114,16 @@ __device__ __forceinline__ double tagged_load(const unsigned long long* src, uin
 
 // NS: row slots per thread (2 when the plan's CTAs have <= 30 slices: fewer
 // live registers, no spills; 4 otherwise)
-constexpr int kRegW = 24;  // register rows: entries per row (the F-mesh's longest row)
-constexpr int kRegThreads = 384;  // register rows: 11 row warps + the comm warp
+// (A/B knobs) register rows: entries per row and CTA threads; 320 threads
+// (9 row warps) never applied to F, whose fullest CTA has 10 slices
+#ifndef SPCG_REG_W
+#define SPCG_REG_W 24
+#endif
+#ifndef SPCG_REG_THREADS
+#define SPCG_REG_THREADS 384
+#endif
+constexpr int kRegW = SPCG_REG_W;  // register rows: entries per row (the F-mesh's longest row)
+constexpr int kRegThreads = SPCG_REG_THREADS;  // register rows: 11 row warps + the comm warp
 
 // TH: threads of the CTA (512, or 384 for the register-row variant: the
 // 168-register budget); REG: each thread keeps its row's values and columns
