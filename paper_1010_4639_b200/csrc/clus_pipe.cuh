@@ -124,15 +124,16 @@ __device__ __forceinline__ double tagged_load(const unsigned long long* src, uin
 #endif
 constexpr int kRegW = SPCG_REG_W;  // register rows: entries per row (the F-mesh's longest row)
 constexpr int kRegThreads = SPCG_REG_THREADS;  // register rows: 11 row warps + the comm warp
+constexpr int kRegW2 = 8;  // register rows with two slots per thread: short rows (stencils)
 
 // TH: threads of the CTA (512, or 384 for the register-row variant: the
 // 168-register budget); REG: each thread keeps its row's values and columns
 // in registers (one row slot, rows of <= kRegW entries) so the SpMV reads
 // only the window gathers from shared memory
-template <int NS, int TH = kPipeThreads, bool REG = false>
+template <int NS, int TH = kPipeThreads, int RW = 0>
 __global__ void __launch_bounds__(TH, 1) clus_pcg_kernel(const ClusArgs A) {
   constexpr int PW_ = TH / 32, PRW_ = PW_ - 1, PRT_ = PRW_ * 32;
-  static_assert(!REG || NS == 1, "register rows: one slot per thread");
+  constexpr bool REG = RW > 0;  // RW: register-row width (entries), 0: rows from shared memory
   namespace cgp = cooperative_groups;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ PipeShared cs;
@@ -200,20 +201,25 @@ __global__ void __launch_bounds__(TH, 1) clus_pcg_kernel(const ClusArgs A) {
       sbase[k] = (sres[k] ? sd.soff : sd.goff) + lane;
     }
   }
-  // REG: the row's values and window-relative columns, read once
-  double vreg[REG ? kRegW : 1];
-  uint32_t creg[REG ? kRegW / 2 : 1];
+  // REG: each slot's row values and window-relative columns, read once
+  constexpr int RWA = REG ? RW : 2;
+  double vreg[NS][RWA];
+  uint32_t creg[NS][RWA / 2];
   if (REG) {
     // from the global SELL arrays: the shared-memory copy above is still in
     // flight in other threads (no barrier yet)
-    const int gb = (!comm && wp < P.nslices) ? A.slices[P.slice0 + wp].goff + lane : 0;
 #pragma unroll
-    for (int u = 0; u < kRegW; ++u) {
-      const bool in = u < rlen[0];
-      vreg[u] = in ? A.gval[gb + u * 32] : 0.0;
-      const uint32_t c = in ? (uint32_t)A.gcol[gb + u * 32] : 0u;
-      if (u & 1) creg[u >> 1] |= c << 16;
-      else creg[u >> 1] = c;
+    for (int k = 0; k < NS; ++k) {
+      const int s = wp + PRW_ * k;
+      const int gb = (!comm && s < P.nslices) ? A.slices[P.slice0 + s].goff + lane : 0;
+#pragma unroll
+      for (int u = 0; u < RWA; ++u) {
+        const bool in = u < rlen[k];
+        vreg[k][u] = in ? A.gval[gb + u * 32] : 0.0;
+        const uint32_t c = in ? (uint32_t)A.gcol[gb + u * 32] : 0u;
+        if (u & 1) creg[k][u >> 1] |= c << 16;
+        else creg[k][u >> 1] = c;
+      }
     }
   }
   if (tid == 0) {
@@ -244,10 +250,10 @@ __global__ void __launch_bounds__(TH, 1) clus_pcg_kernel(const ClusArgs A) {
         if (REG) {  // the same storage-order sum, operands from registers
           q = 0.0;
 #pragma unroll
-          for (int u = 0; u < kRegW; ++u)
+          for (int u = 0; u < RWA; ++u)
             if (u < rlen[k]) {
-              const uint32_t c = (u & 1) ? (creg[u >> 1] >> 16) : (creg[u >> 1] & 0xffffu);
-              q = __dadd_rn(q, __dmul_rn(vreg[u], wwin[c]));
+              const uint32_t c = (u & 1) ? (creg[k][u >> 1] >> 16) : (creg[k][u >> 1] & 0xffffu);
+              q = __dadd_rn(q, __dmul_rn(vreg[k][u], wwin[c]));
             }
         } else {
           q = sres[k] ? clus_row<false, U>(sval, scol, sbase[k], swidth[k], rlen[k], rlenA[k], wwin)

@@ -350,8 +350,9 @@ int build_clus_plan(spcg_matrix_s* m) {
   CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
   if (csz > 8) CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   // the pipelined kernel (engine 6) runs the same plan with one more warp
-  const void* kpipes[3] = {(const void*)clus_pcg_kernel<2>, (const void*)clus_pcg_kernel<4>,
-                           (const void*)clus_pcg_kernel<1, kRegThreads, true>};
+  const void* kpipes[4] = {(const void*)clus_pcg_kernel<2>, (const void*)clus_pcg_kernel<4>,
+                           (const void*)clus_pcg_kernel<1, kRegThreads, kRegW>,
+                           (const void*)clus_pcg_kernel<2, kRegThreads, kRegW2>};
   for (const void* kp : kpipes) {
     CUDA_TRY(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
     if (csz > 8) CUDA_TRY(cudaFuncSetAttribute(kp, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -430,8 +431,11 @@ int launch_clus(const ClusPlan& P, const ClusArgs& a, cudaStream_t st, bool pipe
   // engine 6 with register rows: every slice in one 384-thread CTA's 11 row
   // warps (one slot each) and rows of <= kRegW entries (SPCG_PIPE_REG=0: off)
   static const bool reg_ok = !getenv("SPCG_PIPE_REG") || atoi(getenv("SPCG_PIPE_REG")) != 0;
-  const bool reg = pipe && reg_ok && P.max_slices <= kRegThreads / 32 - 1 && P.max_width <= kRegW;
-  cfg.blockDim = dim3(reg ? kRegThreads : pipe ? kPipeThreads : kClusThreads);
+  const int rw_ = kRegThreads / 32 - 1;  // row warps of the register variants
+  const bool reg = pipe && reg_ok && P.max_slices <= rw_ && P.max_width <= kRegW;
+  // two register rows per thread for short rows (stencils): <= 2 * 11 slices
+  const bool reg2 = pipe && reg_ok && !reg && P.max_slices <= 2 * rw_ && P.max_width <= kRegW2;
+  cfg.blockDim = dim3((reg || reg2) ? kRegThreads : pipe ? kPipeThreads : kClusThreads);
   cfg.dynamicSmemBytes = P.smem;
   cfg.stream = st;
   cudaLaunchAttribute at[2];
@@ -448,7 +452,9 @@ int launch_clus(const ClusPlan& P, const ClusArgs& a, cudaStream_t st, bool pipe
   static const bool noncoop = getenv("SPCG_CLUS_NONCOOP") != nullptr;
   cfg.numAttrs = (P.C > P.cs && !noncoop) ? 2 : 1;
   if (reg) {
-    CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_pcg_kernel<1, kRegThreads, true>, a));
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_pcg_kernel<1, kRegThreads, kRegW>, a));
+  } else if (reg2) {
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, clus_pcg_kernel<2, kRegThreads, kRegW2>, a));
   } else if (pipe) {
     const bool ns2 = P.max_slices <= kPipeMaxSlices2;
     // (two-segment plans too: engine 6 sums their rows in one chain)
