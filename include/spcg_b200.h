@@ -310,6 +310,12 @@ const char* spcg_last_error(void);
 int spcg_abi_version(void);
 /* SMs of the current device and the cooperative grid the solver uses. */
 int spcg_device_info(int* sm_count, int* coop_grid, int* cc_major, int* cc_minor);
+/* Ritz estimate of cond(A) from k CG step coefficients, h_ab[2j] = alpha_j,
+ * h_ab[2j+1] = beta_j (the beta that formed p_j; beta_0 ignored):
+ * theta_max / theta_min of the Lanczos tridiagonal, ~1e-3 relative.  The
+ * engine-6 auto guard's estimate (spcg_cg_result.cond_estimate); host only,
+ * needs no device.  *cond = 0 when k < 2 or a coefficient is not positive. */
+int spcg_cg_cond_estimate(const double* h_ab, int64_t k, double* cond);
 
 #ifdef __cplusplus
 }

@@ -125,6 +125,7 @@ SIGNATURES = {
         _i32, [_i32, _vp, _vp, _vp, _vp, _vp, ctypes.POINTER(CgOptionsC), _vp, _vp]),
     "spcg_last_error": (ctypes.c_char_p, []),
     "spcg_abi_version": (_i32, []),
+    "spcg_cg_cond_estimate": (_i32, [_vp, _i64, ctypes.POINTER(_d)]),
     "spcg_device_info": (
         _i32,
         [ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32)],
@@ -182,6 +183,23 @@ def device_info() -> dict:
     check(lib.spcg_device_info(ctypes.byref(sm), ctypes.byref(grid), ctypes.byref(ma),
                                ctypes.byref(mi)), "spcg_device_info")
     return {"sm_count": sm.value, "coop_grid": grid.value, "cc": (ma.value, mi.value)}
+
+
+def cg_cond_estimate(alpha, beta) -> float:
+    """Ritz estimate of cond(A) from CG's step coefficients (alpha_j, beta_j),
+    beta_j the coefficient that formed p_j (beta_0 ignored); the engine-6
+    guard's estimate, computed on the host (spcg_cg_cond_estimate)."""
+    import numpy as np
+
+    a = np.asarray(alpha, dtype=np.float64)
+    b = np.asarray(beta, dtype=np.float64)
+    if a.shape != b.shape or a.ndim != 1:
+        raise ValueError("alpha and beta must be 1-D arrays of the same length")
+    ab = np.ascontiguousarray(np.stack([a, b], axis=1).reshape(-1))
+    out = ctypes.c_double()
+    check(load().spcg_cg_cond_estimate(ab.ctypes.data if ab.size else None, a.size,
+                                       ctypes.byref(out)), "spcg_cg_cond_estimate")
+    return out.value
 
 
 def current_stream() -> int:

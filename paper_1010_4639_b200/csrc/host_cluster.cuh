@@ -471,7 +471,7 @@ int launch_clus(const ClusPlan& P, const ClusArgs& a, cudaStream_t st, bool pipe
 // Extreme eigenvalues of CG's Lanczos tridiagonal T_k from the step
 // coefficients (alpha_j, beta_j), beta_0 = 0:
 //   T_jj = 1/alpha_j + beta_j/alpha_{j-1},  T_{j-1,j} = sqrt(beta_j)/alpha_{j-1}
-// by Sturm-sequence bisection; returns theta_max / theta_min (the Ritz
+// by Sturm-count multisection (below); returns theta_max / theta_min (the Ritz
 // estimate of cond(A): the extreme Ritz values converge first) or 0.
 double lanczos_cond(const std::vector<double>& ab, long long k) {
   if (k < 2) return 0.0;
@@ -488,28 +488,102 @@ double lanczos_cond(const std::vector<double>& ab, long long k) {
     lo = std::min(lo, d[j] - r);
     hi = std::max(hi, d[j] + r);
   }
-  auto below = [&](double x) {  // eigenvalues of T smaller than x
-    int c = 0;
-    double q = 1.0;
-    for (long long j = 0; j < k; ++j) {
-      q = d[j] - x - (j ? e2[j] / q : 0.0);
-      if (q == 0.0) q = -1e-300;
-      if (q < 0.0) ++c;
+  // brackets: T is SPD (its extreme eigenvalues enclose the diagonal), so
+  // theta_min in [max(0, lo), min d] and theta_max in [max d, hi]
+  double dmin = d[0], dmax = d[0];
+  for (long long j = 1; j < k; ++j) {
+    dmin = std::min(dmin, d[j]);
+    dmax = std::max(dmax, d[j]);
+  }
+  // multisection with division-free Sturm counts: the leading principal
+  // minors p_j = (d_j - x) p_{j-1} - e_j^2 p_{j-2} change sign exactly
+  // (number of eigenvalues below x) times.  T is scaled by 1/hi first (the
+  // ratio is scale-free), so a step grows |p| at most ~2x and a rescale
+  // every 4 steps keeps it in range.  NP points per bracket per round, all
+  // 2 NP recurrences in one pass over T, branch-free (independent
+  // multiply-adds that vectorise), so a round narrows each bracket (NP + 1)x
+  // for about the cost of one count.  2e-3 relative is ample for a guard
+  // threshold of 1e5 (this host time sits on every auto solve's path)
+  constexpr int NP = 8, NX = 2 * NP;
+  const double sc = 1.0 / hi;
+  for (long long j = 0; j < k; ++j) {
+    d[j] *= sc;
+    e2[j] *= sc * sc;
+  }
+  double a0 = std::max(0.0, lo) * sc, z0 = dmin * sc, a1 = dmax * sc, z1 = 1.0;
+  auto done = [](double a, double z) { return z - a <= 2e-3 * std::max(std::fabs(a), std::fabs(z)); };
+  for (int round = 0; round < 64 && !(done(a0, z0) && done(a1, z1)); ++round) {
+    // (gcc vector extensions: two lanes per op on any host ISA)
+    typedef double v2d __attribute__((vector_size(16)));
+    typedef long long v2l __attribute__((vector_size(16)));
+    constexpr int NV = NX / 2;
+    alignas(64) double x[NX], c[NX];
+    for (int i = 0; i < NP; ++i) {
+      x[i] = a0 + (z0 - a0) * (i + 1) / (NP + 1);
+      x[NP + i] = a1 + (z1 - a1) * (i + 1) / (NP + 1);
     }
-    return c;
-  };
-  auto kth = [&](int idx) {  // idx-th smallest eigenvalue (0-based)
-    double a = lo, z = hi;
-    // 1e-4 relative is ample for a guard threshold (and keeps the host time
-    // of an F solve's guard at a few microseconds)
-    for (int it = 0; it < 200 && z - a > 1e-4 * std::max(std::fabs(a), std::fabs(z)); ++it) {
-      const double mid = 0.5 * (a + z);
-      if (below(mid) > idx) z = mid;
-      else a = mid;
+    v2d vx[NV], pm[NV], pc[NV], vc[NV];
+    const v2d one = {1.0, 1.0}, zero = {0.0, 0.0}, tiny = {1e-300, 1e-300};
+    for (int v = 0; v < NV; ++v) {
+      vx[v] = v2d{x[2 * v], x[2 * v + 1]};
+      pm[v] = one;  // p_{-1}
+      pc[v] = d[0] - vx[v];
+      vc[v] = (v2d)((v2l)one & (pc[v] < zero));
     }
-    return 0.5 * (a + z);
-  };
-  const double tmin = kth(0), tmax = kth((int)k - 1);
+    auto step = [&](long long j) {
+      const double dj = d[j], ej = e2[j];
+      for (int v = 0; v < NV; ++v) {
+        v2d pn = (dj - vx[v]) * pc[v] - ej * pm[v];
+        const v2l z = pn == zero;  // an exact zero takes a sign (probability ~0)
+        pn = (v2d)(((v2l)pn & ~z) | ((v2l)tiny & z));
+        vc[v] += (v2d)((v2l)one & (pn * pc[v] < zero));
+        pm[v] = pc[v];
+        pc[v] = pn;
+      }
+    };
+    long long j = 1;
+    for (; j + 4 <= k; j += 4) {
+      step(j);
+      step(j + 1);
+      step(j + 2);
+      step(j + 3);
+      for (int v = 0; v < NV; ++v) {
+        const v2d apc = (v2d)((v2l)pc[v] & 0x7fffffffffffffffLL), apm = (v2d)((v2l)pm[v] & 0x7fffffffffffffffLL);
+        const v2d m = one / (apc + apm);
+        pc[v] *= m;
+        pm[v] *= m;
+      }
+    }
+    for (; j < k; ++j) step(j);
+    for (int v = 0; v < NV; ++v) {
+      c[2 * v] = vc[v][0];
+      c[2 * v + 1] = vc[v][1];
+    }
+    // theta_min: the first point with an eigenvalue below it
+    double na = a0, nz = z0;
+    for (int i = 0; i < NP; ++i)
+      if (c[i] > 0.5) {
+        nz = x[i];
+        break;
+      } else {
+        na = x[i];
+      }
+    a0 = na;
+    z0 = nz;
+    // theta_max: the first point with every eigenvalue below it
+    na = a1;
+    nz = z1;
+    for (int i = NP; i < NX; ++i)
+      if (c[i] > (double)k - 0.5) {
+        nz = x[i];
+        break;
+      } else {
+        na = x[i];
+      }
+    a1 = na;
+    z1 = nz;
+  }
+  const double tmin = 0.5 * (a0 + z0), tmax = 0.5 * (a1 + z1);
   return tmin > 0.0 ? tmax / tmin : 0.0;
 }
 
@@ -694,7 +768,13 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
       std::copy(w.h_coef, w.h_coef + ab.size(), ab.begin());
     else
       CUDA_TRY(cudaMemcpy(ab.data(), w.coef, sizeof(double) * ab.size(), cudaMemcpyDeviceToHost));
+    static const bool gtime = getenv("SPCG_GUARD_TIMING") != nullptr;  // (dev)
+    const auto tg0 = std::chrono::steady_clock::now();
     cond = lanczos_cond(ab, r.iterations);
+    if (gtime)
+      fprintf(stderr, "[spcg guard] lanczos %.1f us (k = %lld)\n",
+              std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tg0).count(),
+              (long long)r.iterations);
     if (cond > kPipeCondMax || r.final_rel > kPipeTrueResMax * o->tol) {
       // re-solve on engine 5; the reported time covers both solves
       rc = do_clus_cg(m, b, x0, x, hist, o, out, st, false, false);

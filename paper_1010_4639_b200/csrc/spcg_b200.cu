@@ -739,4 +739,10 @@ int spcg_dist_group_solve(int nranks, spcg_dist_plan_t* plans, const double* con
                             (cudaStream_t)stream);
 }
 
+int spcg_cg_cond_estimate(const double* h_ab, int64_t k, double* cond) {
+  if (!cond || (k > 0 && !h_ab) || k < 0) return fail(SPCG_ERR_ARG, "null argument or k < 0");
+  *cond = k < 2 ? 0.0 : lanczos_cond(std::vector<double>(h_ab, h_ab + 2 * k), (long long)k);
+  return SPCG_OK;
+}
+
 }  // extern "C"

@@ -281,3 +281,54 @@ def test_csc_container_carries_its_own_version(tmp_path):
     (tmp_path / "bad.spcg").write_bytes(bytes(raw))
     with pytest.raises(FileFormatError):
         read_system(tmp_path / "bad.spcg")
+
+
+def _cg_coefficients(ev, b, iters):
+    """Textbook CG on diag(ev): (alpha_j, beta_j) with beta_j the coefficient
+    that formed p_j (beta_0 = 0)."""
+    r = b.copy()
+    p = r.copy()
+    rr = r @ r
+    alpha, beta, prev = [], [], 0.0
+    for _ in range(iters):
+        ap = ev * p
+        a = rr / (p @ ap)
+        r -= a * ap
+        rn = r @ r
+        alpha.append(a)
+        beta.append(prev)
+        prev = rn / rr
+        rr = rn
+        p = r + prev * p
+        if np.sqrt(rn) < 1e-12 * np.linalg.norm(b):
+            break
+    return np.array(alpha), np.array(beta)
+
+
+@pytest.mark.parametrize("n,cond,scale,iters", [
+    (500, 10.0, 1.0, 200), (2000, 1e3, 1e-9, 400), (30880, 1e4, 1e12, 329),
+    (3000, 1e8, 1.0, 1500), (5000, 2e5, 1.0, 600), (100, 1.0001, 1.0, 50)])
+def test_cg_cond_estimate_matches_tridiagonal_eigenvalues(n, cond, scale, iters):
+    """The engine-6 guard's Ritz estimate (host multisection over Sturm
+    counts, host_cluster.cuh lanczos_cond) equals theta_max / theta_min of
+    CG's Lanczos tridiagonal computed by LAPACK, to its stated ~1e-3."""
+    from paper_1010_4639_b200._native import cg_cond_estimate
+
+    ev = np.geomspace(1.0, cond, n) * scale
+    alpha, beta = _cg_coefficients(ev, np.random.default_rng(n).standard_normal(n), iters)
+    d = 1.0 / alpha
+    d[1:] += beta[1:] / alpha[:-1]
+    e = np.sqrt(beta[1:]) / alpha[:-1]
+    w = np.linalg.eigvalsh(np.diag(d) + np.diag(e, 1) + np.diag(e, -1))
+    got = cg_cond_estimate(alpha, beta)
+    assert abs(got / (w[-1] / w[0]) - 1.0) <= 2e-3, (got, w[-1] / w[0])
+
+
+def test_cg_cond_estimate_degenerate_inputs():
+    from paper_1010_4639_b200._native import cg_cond_estimate
+
+    assert cg_cond_estimate([], []) == 0.0
+    assert cg_cond_estimate([0.5], [0.0]) == 0.0
+    assert cg_cond_estimate([0.5, -1.0], [0.0, 0.1]) == 0.0  # not positive
+    with pytest.raises(ValueError):
+        cg_cond_estimate([0.5, 0.4], [0.0])
