@@ -518,10 +518,10 @@ double lanczos_cond(const std::vector<double>& ab, long long k) {
     typedef long long v2l __attribute__((vector_size(16)));
     constexpr int NV = NX / 2;
     alignas(64) double x[NX], c[NX];
-    for (int i = 0; i < NP; ++i) {
-      x[i] = a0 + (z0 - a0) * (i + 1) / (NP + 1);
-      x[NP + i] = a1 + (z1 - a1) * (i + 1) / (NP + 1);
-    }
+    // a bracket already narrow enough gives its points to the other one
+    const int n0 = done(a1, z1) ? NX : done(a0, z0) ? 0 : NP, n1 = NX - n0;
+    for (int i = 0; i < n0; ++i) x[i] = a0 + (z0 - a0) * (i + 1) / (n0 + 1);
+    for (int i = 0; i < n1; ++i) x[n0 + i] = a1 + (z1 - a1) * (i + 1) / (n1 + 1);
     v2d vx[NV], pm[NV], pc[NV], vc[NV];
     const v2d one = {1.0, 1.0}, zero = {0.0, 0.0}, tiny = {1e-300, 1e-300};
     for (int v = 0; v < NV; ++v) {
@@ -534,8 +534,7 @@ double lanczos_cond(const std::vector<double>& ab, long long k) {
       const double dj = d[j], ej = e2[j];
       for (int v = 0; v < NV; ++v) {
         v2d pn = (dj - vx[v]) * pc[v] - ej * pm[v];
-        const v2l z = pn == zero;  // an exact zero takes a sign (probability ~0)
-        pn = (v2d)(((v2l)pn & ~z) | ((v2l)tiny & z));
+        pn += tiny;  // an exact zero takes a sign (probability ~0); a no-op otherwise
         vc[v] += (v2d)((v2l)one & (pn * pc[v] < zero));
         pm[v] = pc[v];
         pc[v] = pn;
@@ -561,7 +560,7 @@ double lanczos_cond(const std::vector<double>& ab, long long k) {
     }
     // theta_min: the first point with an eigenvalue below it
     double na = a0, nz = z0;
-    for (int i = 0; i < NP; ++i)
+    for (int i = 0; i < n0; ++i)
       if (c[i] > 0.5) {
         nz = x[i];
         break;
@@ -573,7 +572,7 @@ double lanczos_cond(const std::vector<double>& ab, long long k) {
     // theta_max: the first point with every eigenvalue below it
     na = a1;
     nz = z1;
-    for (int i = NP; i < NX; ++i)
+    for (int i = n0; i < NX; ++i)
       if (c[i] > (double)k - 0.5) {
         nz = x[i];
         break;
