@@ -212,6 +212,7 @@ void free_matrix(spcg_matrix_s* m) {
   if (w.h_coef) cudaFreeHost(w.h_coef);
   if (w.ev0) cudaEventDestroy(w.ev0);
   if (w.ev1) cudaEventDestroy(w.ev1);
+  if (w.ev_res) cudaEventDestroy(w.ev_res);
   DistWorkspace& d = m->dw;
   F(d.r_ext); F(d.p_ext[0]); F(d.p_ext[1]); F(d.tmp_ext); F(d.q); F(d.part); F(d.S);
   F(d.send_buf); F(d.send_idx); F(d.args); F(d.ytx);
@@ -279,6 +280,7 @@ int ensure_ws(spcg_matrix_s* m, int grid) {
     CUDA_TRY(cudaMallocHost((void**)&w.h_res, sizeof(CgDevResult)));
     CUDA_TRY(cudaEventCreate(&w.ev0));
     CUDA_TRY(cudaEventCreate(&w.ev1));
+    CUDA_TRY(cudaEventCreateWithFlags(&w.ev_res, cudaEventDisableTiming));
     w.n = m->n;
   }
   if (w.slots_g < grid) {

@@ -178,6 +178,11 @@ struct Workspace {
   long long coef_cap = 0;
   double* h_coef = nullptr;  // pinned: the first kCoefHost pairs come back with the result
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev_res = nullptr;  // after the result copy (guarded solves)
+  // host-API solve: x's destination, so a guarded engine-6 solve can start
+  // x's copy before its host-side guard runs (x_early_done: it did)
+  double* h_x_early = nullptr;
+  bool x_early_done = false;
 };
 
 // Workspace of the row-sharded (per-pass) engine.
@@ -480,19 +485,34 @@ int spcg_cg_solve_host(spcg_matrix_t m, const double* h_b, const double* h_x0, d
     w.hist_cap = max_iter;
   }
   const size_t nb = sizeof(double) * (size_t)m->n;
+  static const bool etime = getenv("SPCG_E2E_TIMING") != nullptr;  // (dev)
+  const auto th0 = std::chrono::steady_clock::now();
   if (m->n) CUDA_TRY(cudaMemcpyAsync(w.b, h_b, nb, cudaMemcpyHostToDevice, st));
   if (h_x0 && m->n) CUDA_TRY(cudaMemcpyAsync(w.x0, h_x0, nb, cudaMemcpyHostToDevice, st));
+  w.h_x_early = m->n ? h_x : nullptr;
+  w.x_early_done = false;
   rc = do_cg(m, w.b, h_x0 ? w.x0 : nullptr, w.x, opts->record_history ? w.hist : nullptr, opts,
              result, st);
+  w.h_x_early = nullptr;
   if (rc != SPCG_OK && rc != SPCG_ERR_NOT_SPD && rc != SPCG_ERR_NONFINITE_ALPHA &&
-      rc != SPCG_ERR_NONFINITE_RESIDUAL && rc != SPCG_ERR_NONFINITE_BETA)
+      rc != SPCG_ERR_NONFINITE_RESIDUAL && rc != SPCG_ERR_NONFINITE_BETA) {
+    if (w.x_early_done) cudaStreamSynchronize(st);  // no copy into h_x outlives the call
+    w.x_early_done = false;
     return rc;
+  }
   const std::string err = g_last_error;
-  if (m->n) CUDA_TRY(cudaMemcpyAsync(h_x, w.x, nb, cudaMemcpyDeviceToHost, st));
+  if (m->n && !w.x_early_done) CUDA_TRY(cudaMemcpyAsync(h_x, w.x, nb, cudaMemcpyDeviceToHost, st));
+  w.x_early_done = false;
   if (opts->record_history && h_hist && result->iterations > 0)
     CUDA_TRY(cudaMemcpyAsync(h_hist, w.hist, sizeof(double) * (size_t)result->iterations,
                              cudaMemcpyDeviceToHost, st));
+  const auto th2 = std::chrono::steady_clock::now();
   CUDA_TRY(cudaStreamSynchronize(st));
+  if (etime) {
+    auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+    fprintf(stderr, "[spcg e2e] host call: to x-copy %.1f x-copy+sync %.1f us\n", us(th0, th2),
+            us(th2, std::chrono::steady_clock::now()));
+  }
   g_last_error = err;
   return rc;
 }
