@@ -643,12 +643,14 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
   a.ghalo = P.ghalo;
   a.gslots = P.gslots;
   a.cluster_size = P.cs;
-  if (P.gslots)
-    CUDA_TRY(cudaMemsetAsync(P.gslots, 0,
-                             sizeof(unsigned long long) * 2 * kClusSlotWords * (size_t)(P.C / P.cs),
-                             st));
-  if (pipe && P.ghalo)  // tags restart at 1 every solve
-    CUDA_TRY(cudaMemsetAsync(P.ghalo, 0, sizeof(double) * 6 * (size_t)P.C * P.hcap, st));
+  if (P.gslots) {
+    // tags restart at 1 every solve: engine 6 clears its halo words too, in
+    // the same memset (the arena holds ghalo right before gslots)
+    const unsigned char* end =
+        reinterpret_cast<const unsigned char*>(P.gslots + 2 * kClusSlotWords * (size_t)(P.C / P.cs));
+    unsigned char* from = reinterpret_cast<unsigned char*>(pipe && P.ghalo ? (void*)P.ghalo : (void*)P.gslots);
+    CUDA_TRY(cudaMemsetAsync(from, 0, (size_t)(end - from), st));
+  }
   static const bool tracing = getenv("SPCG_TRACE") != nullptr;
   static const char* dbg_path = getenv("SPCG_CLUS_DEBUG");  // per-solve CTA trace lines
   // [C][8] per-CTA phases + [K][8 iterations][34] exchange trace (engine 6)
