@@ -602,6 +602,7 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
                const spcg_cg_options* o, spcg_cg_result* out, cudaStream_t st, bool pipe = false,
                bool guard = false) {
   int rc;
+  const auto tentry = std::chrono::steady_clock::now();
   const ClusPlan& P = m->cp;
   if ((rc = ensure_ws(m, 1))) return rc;
   Workspace& w = m->ws;
@@ -695,8 +696,8 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
   CUDA_TRY(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
   if (etime) {
     auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
-    fprintf(stderr, "[spcg e2e] launch %.1f copies %.1f sync-wait %.1f (kernel %.1f) us\n", us(te0, te1),
-            us(te1, te2), us(te2, te3), 1e3 * ms);
+    fprintf(stderr, "[spcg e2e] entry->launch %.1f launch %.1f copies %.1f sync-wait %.1f (kernel %.1f) us\n",
+            us(tentry, te0), us(te0, te1), us(te1, te2), us(te2, te3), 1e3 * ms);
   }
   const CgDevResult& r = *w.h_res;
   if (r.status == ST_BAD_LAUNCH)

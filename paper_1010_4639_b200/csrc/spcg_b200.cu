@@ -489,6 +489,7 @@ int spcg_cg_solve_host(spcg_matrix_t m, const double* h_b, const double* h_x0, d
   const auto th0 = std::chrono::steady_clock::now();
   if (m->n) CUDA_TRY(cudaMemcpyAsync(w.b, h_b, nb, cudaMemcpyHostToDevice, st));
   if (h_x0 && m->n) CUDA_TRY(cudaMemcpyAsync(w.x0, h_x0, nb, cudaMemcpyHostToDevice, st));
+  const auto th1 = std::chrono::steady_clock::now();
   w.h_x_early = m->n ? h_x : nullptr;
   w.x_early_done = false;
   rc = do_cg(m, w.b, h_x0 ? w.x0 : nullptr, w.x, opts->record_history ? w.hist : nullptr, opts,
@@ -510,7 +511,8 @@ int spcg_cg_solve_host(spcg_matrix_t m, const double* h_b, const double* h_x0, d
   CUDA_TRY(cudaStreamSynchronize(st));
   if (etime) {
     auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
-    fprintf(stderr, "[spcg e2e] host call: to x-copy %.1f x-copy+sync %.1f us\n", us(th0, th2),
+    fprintf(stderr, "[spcg e2e] host call: h2d enqueue %.1f, to x-copy %.1f x-copy+sync %.1f us\n",
+            us(th0, th1), us(th0, th2),
             us(th2, std::chrono::steady_clock::now()));
   }
   g_last_error = err;
