@@ -24,7 +24,8 @@
  * default stream).  Every call returns an spcg_status; spcg_last_error()
  * gives the message of the most recent failure on the calling thread.
  * No call falls back to the CPU: without a usable sm_100 device every call
- * returns SPCG_ERR_CUDA.
+ * returns SPCG_ERR_CUDA (spcg_cg_cond_estimate, a host-side analysis of a
+ * finished solve's CG coefficients, needs no device and computes no solve).
  */
 #ifndef SPCG_B200_H
 #define SPCG_B200_H
