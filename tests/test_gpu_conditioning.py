@@ -139,3 +139,30 @@ def test_pipelined_guard_tightened_tolerance():
     assert r6.final_relative_residual > 2e-12  # the failure the guard exists for
     assert r0.engine_info["fallback"] and r0.engine_info["engine"] == 5
     assert r0.final_relative_residual <= 2e-12
+
+
+@pytest.mark.parametrize("shift", [1.0, 1e-5])
+def test_host_api_x_matches_device_api(shift):
+    """Through the host API a guarded auto solve queues x's copy to the
+    caller before the host-side guard runs, and copies again after a
+    fallback re-solve (host_cluster.cuh do_clus_cg, spcg_cg_solve_host): the
+    host API's x equals the device API's bitwise, on the engine-6 path
+    (shift 1) and on the engine-5 fallback (shift 1e-5, cond ~2e6), solve
+    after solve."""
+    import torch
+
+    from paper_1010_4639_b200 import CgOptions, KernelConfig, cg_solve
+    from paper_1010_4639_b200.genprob import fem_mesh, rhs_for
+
+    a = fem_mesh(shift=shift)
+    b, _ = rhs_for(a, seed=1)
+    rd = cg_solve(a, torch.from_numpy(b).cuda(), opts=CgOptions(), cfg=KernelConfig())
+    xd = rd.x.cpu().numpy()
+    fell_back = 19.13 / shift > PIPE_COND_MAX
+    assert rd.engine_info["engine"] == (5 if fell_back else 6), rd.engine_info
+    for _ in range(3):
+        rh = cg_solve(a, b, opts=CgOptions(), cfg=KernelConfig())
+        assert rh.engine_info["engine"] == rd.engine_info["engine"], rh.engine_info
+        assert bool(rh.engine_info.get("fallback")) == fell_back, rh.engine_info
+        assert rh.iterations == rd.iterations
+        assert np.array_equal(rh.x, xd)
