@@ -88,6 +88,7 @@ struct ClusArgs {
   const double* x0;  // nullable
   double* x;
   double* scratch;   // n doubles (window initialisation)
+  double* scratch2;  // n doubles (engine 6: the window of w0 = A r0)
   double* hist;
   CgDevResult* res;
   double tol;

@@ -421,16 +421,25 @@ __global__ void __launch_bounds__(TH, 1) clus_pcg_kernel(const ClusArgs A) {
     }
   };
 
-  // ||b||
+  // ||b||.  Without x0, r0 = b: ||b||^2 is gamma0 bit for bit (the same
+  // fmas, the same fixed-order all-reduce) and the window of r0 goes to
+  // global scratch now, so this all-reduce is also the barrier before the
+  // window reads (one blocking all-reduce fewer in the prologue)
   double part = 0.0, dummy = 0.0;
+  const bool zero_x0 = A.x0 == nullptr;
 #pragma unroll
   for (int k = 0; k < NS; ++k)
     if (rrow[k] >= 0) {
       const double bv = A.b[rrow[k]];
       part = fma(bv, bv, part);
+      if (zero_x0) {
+        rg[k] = bv;
+        A.scratch[rrow[k]] = bv;
+      }
     }
   allreduce2(part, dummy);
   const double b_norm = sqrt(part);
+  const double bb = part;
   if (b_norm == 0.0) {  // solver.py:109-118
 #pragma unroll
     for (int k = 0; k < NS; ++k)
@@ -458,22 +467,21 @@ __global__ void __launch_bounds__(TH, 1) clus_pcg_kernel(const ClusArgs A) {
         rg[k] = mul_add_rn(A.b[rrow[k]], -1.0, qv[k]);
       }
     __syncthreads();
-  } else {
-#pragma unroll
-    for (int k = 0; k < NS; ++k)
-      if (rrow[k] >= 0) rg[k] = A.b[rrow[k]];
   }
   // window of r0 (through global scratch, once), gamma0
-  part = 0.0;
-  dummy = 0.0;
+  double gam = bb;
+  if (!zero_x0) {
+    part = 0.0;
+    dummy = 0.0;
 #pragma unroll
-  for (int k = 0; k < NS; ++k)
-    if (rrow[k] >= 0) {
-      A.scratch[rrow[k]] = rg[k];
-      part = fma(rg[k], rg[k], part);
-    }
-  allreduce2(part, dummy);
-  double gam = part;
+    for (int k = 0; k < NS; ++k)
+      if (rrow[k] >= 0) {
+        A.scratch[rrow[k]] = rg[k];
+        part = fma(rg[k], rg[k], part);
+      }
+    allreduce2(part, dummy);
+    gam = part;
+  }
   const double tol_b = A.tol * b_norm;
   // the largest g with sqrt(g) <= tol_b (sqrt is monotone: that set is [0, gthr])
   double gthr = tol_b * tol_b;
@@ -495,13 +503,14 @@ __global__ void __launch_bounds__(TH, 1) clus_pcg_kernel(const ClusArgs A) {
     for (int h = tid; h < A.hcap; h += TH) zhalo[h] = 0.0;
     __syncthreads();
     spmv(wg);  // w0 = A r0
-    part = dummy = 0.0;
-    allreduce2(part, dummy);  // every CTA has read its r0 window from scratch
+    // the window of w0 through a second scratch vector: no barrier for the
+    // other CTAs' reads of r0's window first
 #pragma unroll
     for (int k = 0; k < NS; ++k)
-      if (rrow[k] >= 0) A.scratch[rrow[k]] = wg[k];
-    allreduce2(part, dummy);
-    for (int j = tid; j < P.wn; j += TH) wwin[j] = __ldcg(A.scratch + P.wlo + j);
+      if (rrow[k] >= 0) A.scratch2[rrow[k]] = wg[k];
+    part = dummy = 0.0;
+    allreduce2(part, dummy);  // (a barrier: every CTA sees the whole w0)
+    for (int j = tid; j < P.wn; j += TH) wwin[j] = __ldcg(A.scratch2 + P.wlo + j);
     __syncthreads();
   }
 

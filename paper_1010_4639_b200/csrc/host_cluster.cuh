@@ -627,6 +627,7 @@ int do_clus_cg(spcg_matrix_s* m, const double* b, const double* x0, double* x, d
   a.x0 = x0;
   a.x = x;
   a.scratch = w.q;
+  a.scratch2 = w.p0;
   a.hist = hist;
   a.res = w.res;
   a.tol = o->tol;
