@@ -20,3 +20,26 @@ for mi in (1, 2, 5, 10, 50, 100, 200, 329):
         torch.cuda.synchronize()
         ts.append(r.device_ms * 1e3)
     print(mi, r.iterations, "median us %.1f" % np.median(ts[2:]))
+# b = 0: launch + setup loads + the ||b|| all-reduce only
+bz = torch.zeros_like(bt)
+ts = []
+for rep in range(12):
+    o = N.CgOptionsC(tol=1e-10, max_iter=0, record_history=0, recompute_final_residual=0,
+                     accumulation=1, engine=6)
+    r = N.CgResultC()
+    flush.fill_(rep)
+    torch.cuda.synchronize()
+    lib.spcg_cg_solve(dm.handle, bz.data_ptr(), None, xt.data_ptr(), None, o, r, st)
+    torch.cuda.synchronize()
+    ts.append(r.device_ms * 1e3)
+print("b=0", r.iterations, "median us %.1f" % np.median(ts[2:]))
+ts = []
+for rep in range(12):
+    o = N.CgOptionsC(tol=1e-10, max_iter=0, record_history=0, recompute_final_residual=0,
+                     accumulation=1, engine=6)
+    r = N.CgResultC()
+    torch.cuda.synchronize()
+    lib.spcg_cg_solve(dm.handle, bz.data_ptr(), None, xt.data_ptr(), None, o, r, st)
+    torch.cuda.synchronize()
+    ts.append(r.device_ms * 1e3)
+print("b=0 no flush", r.iterations, "median us %.1f" % np.median(ts[2:]))
