@@ -497,7 +497,7 @@ int spcg_cg_solve_host(spcg_matrix_t m, const double* h_b, const double* h_x0, d
   w.h_x_early = nullptr;
   if (rc != SPCG_OK && rc != SPCG_ERR_NOT_SPD && rc != SPCG_ERR_NONFINITE_ALPHA &&
       rc != SPCG_ERR_NONFINITE_RESIDUAL && rc != SPCG_ERR_NONFINITE_BETA) {
-    if (w.x_early_done) cudaStreamSynchronize(st);  // no copy into h_x outlives the call
+    cudaStreamSynchronize(st);  // no copy into h_x (an early one) outlives the call
     w.x_early_done = false;
     return rc;
   }
