@@ -168,13 +168,18 @@ __global__ void __launch_bounds__(TH, 1) clus_pcg_kernel(const ClusArgs A) {
   const int own0 = P.row_lo - P.wlo;
   unsigned long long* gh = reinterpret_cast<unsigned long long*>(A.ghalo);  // [3][G][hcap][2]
 
-  for (int s = 0; s < P.nslices; ++s) {
-    const ClusSlice sd = A.slices[P.slice0 + s];
-    if (sd.soff < 0) continue;
-    const int cnt = sd.width * 32;
-    for (int e = tid; e < cnt; e += TH) {
-      sval[sd.soff + e] = A.gval[sd.goff + e];
-      scol[sd.soff + e] = A.gcol[sd.goff + e];
+  // (REG: the SpMV reads its operands from registers, loaded below; the
+  // shared-memory copy would only add a chain of dependent cold loads to the
+  // prologue)
+  if (!REG) {
+    for (int s = 0; s < P.nslices; ++s) {
+      const ClusSlice sd = A.slices[P.slice0 + s];
+      if (sd.soff < 0) continue;
+      const int cnt = sd.width * 32;
+      for (int e = tid; e < cnt; e += TH) {
+        sval[sd.soff + e] = A.gval[sd.goff + e];
+        scol[sd.soff + e] = A.gcol[sd.goff + e];
+      }
     }
   }
   if (tid < min(P.nsend, kClusSendCache)) cs.send[tid] = A.sends[P.send0 + tid];
