@@ -66,6 +66,9 @@ constexpr size_t kClusStatic = sizeof(PipeShared) > sizeof(ClusShared) ? sizeof(
 
 // SpMV unroll of the 2-slot kernel (4: 2.91 vs 2.86 us per iteration on F);
 // the 4-slot kernel uses SPCG_CLUS_UNROLL (clus.cuh)
+#ifndef SPCG_PIPE_SENDMASK
+#define SPCG_PIPE_SENDMASK 1  // per-warp mask of the send descriptors
+#endif
 #ifndef SPCG_PIPE_UNROLL_ONE2
 #define SPCG_PIPE_UNROLL_ONE2 8
 #endif
@@ -402,27 +405,50 @@ __global__ void __launch_bounds__(TH, 1) clus_pcg_kernel(const ClusArgs A) {
     if (halo_local(h)) return nhalo[(size_t)buf * A.hcap + h];
     return tagged_load(gh + (((size_t)buf * G + gme) * A.hcap + h) * 2, tag);
   };
+  // (SPCG_PIPE_SENDMASK) bit e: a row of this warp is in send descriptor e
+  // (all bits when there are more than 32 descriptors).  In a register:
+  // 2.328 vs 2.341 us per F iteration without the mask; read from shared
+  // memory in the loop instead (fewer spills) it ran 2.369.  One-slot
+  // variants only: the two-slot register variant would spill (0 -> 28 B)
+  constexpr bool kSendMask = SPCG_PIPE_SENDMASK && NS == 1;
+  uint32_t smask = 0xffffffffu;
+  if (kSendMask && P.nsend <= 32) {
+    smask = 0;
+    for (int e = 0; e < P.nsend; ++e) {
+      const ClusSend sd = e < kClusSendCache ? cs.send[e] : A.sends[P.send0 + e];
+      bool in = false;
+#pragma unroll
+      for (int k = 0; k < NS; ++k) in = in || (rrow[k] >= sd.lo && rrow[k] < sd.hi);
+      if (__ballot_sync(0xffffffffu, in)) smask |= 1u << e;
+    }
+  }
   // boundary n to the neighbours of this iteration: st.async into the cluster
   // neighbours' nhalo[buf] (completing on their mbB[buf]), epoch-tagged global
   // words for other clusters' CTAs
+  auto send_one = [&](const double* nv, int buf, uint32_t tag, int e) {
+    const ClusSend sd = e < kClusSendCache ? cs.send[e] : A.sends[P.send0 + e];
+    if (sd.dst / C != kc) {
+      unsigned long long* dst = gh + ((size_t)buf * G + sd.dst) * A.hcap * 2;
+#pragma unroll
+      for (int k = 0; k < NS; ++k)
+        if (rrow[k] >= sd.lo && rrow[k] < sd.hi)
+          tagged_store(dst + 2 * (size_t)(sd.dst_off + rrow[k] - sd.lo), nv[k], tag);
+    } else {
+      const uint32_t r = (uint32_t)(sd.dst % C);
+      const uint32_t base = mapa_u32(nhalo + (size_t)buf * A.hcap, r);
+      const uint32_t bar = mapa_u32(&cs.mbB[buf], r);
+#pragma unroll
+      for (int k = 0; k < NS; ++k)
+        if (rrow[k] >= sd.lo && rrow[k] < sd.hi)
+          st_async_f64(base + 8u * (uint32_t)(sd.dst_off + rrow[k] - sd.lo), nv[k], bar);
+    }
+  };
   auto send_n = [&](const double* nv, int buf, uint32_t tag) {
-    for (int e = 0; e < P.nsend; ++e) {
-      const ClusSend sd = e < kClusSendCache ? cs.send[e] : A.sends[P.send0 + e];
-      if (sd.dst / C != kc) {
-        unsigned long long* dst = gh + ((size_t)buf * G + sd.dst) * A.hcap * 2;
-#pragma unroll
-        for (int k = 0; k < NS; ++k)
-          if (rrow[k] >= sd.lo && rrow[k] < sd.hi)
-            tagged_store(dst + 2 * (size_t)(sd.dst_off + rrow[k] - sd.lo), nv[k], tag);
-      } else {
-        const uint32_t r = (uint32_t)(sd.dst % C);
-        const uint32_t base = mapa_u32(nhalo + (size_t)buf * A.hcap, r);
-        const uint32_t bar = mapa_u32(&cs.mbB[buf], r);
-#pragma unroll
-        for (int k = 0; k < NS; ++k)
-          if (rrow[k] >= sd.lo && rrow[k] < sd.hi)
-            st_async_f64(base + 8u * (uint32_t)(sd.dst_off + rrow[k] - sd.lo), nv[k], bar);
-      }
+    if constexpr (kSendMask) {
+      // only the descriptors some row of this warp belongs to (warp-uniform)
+      for (uint32_t msk = smask; msk; msk &= msk - 1) send_one(nv, buf, tag, __ffs(msk) - 1);
+    } else {
+      for (int e = 0; e < P.nsend; ++e) send_one(nv, buf, tag, e);
     }
   };
 
