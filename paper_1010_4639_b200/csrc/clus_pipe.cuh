@@ -453,9 +453,8 @@ __global__ void __launch_bounds__(TH, 1) clus_pcg_kernel(const ClusArgs A) {
   };
 
   // ||b||.  Without x0, r0 = b: ||b||^2 is gamma0 bit for bit (the same
-  // fmas, the same fixed-order all-reduce) and the window of r0 goes to
-  // global scratch now, so this all-reduce is also the barrier before the
-  // window reads (one blocking all-reduce fewer in the prologue)
+  // fmas, the same fixed-order all-reduce), and w0 is computed before it
+  // (three blocking all-reduces fewer in the prologue than x0 given)
   double part = 0.0, dummy = 0.0;
   const bool zero_x0 = A.x0 == nullptr;
 #pragma unroll
@@ -463,11 +462,20 @@ __global__ void __launch_bounds__(TH, 1) clus_pcg_kernel(const ClusArgs A) {
     if (rrow[k] >= 0) {
       const double bv = A.b[rrow[k]];
       part = fma(bv, bv, part);
-      if (zero_x0) {
-        rg[k] = bv;
-        A.scratch[rrow[k]] = bv;
-      }
+      if (zero_x0) rg[k] = bv;
     }
+  // x0 = 0: r0's window is b's, read straight from b, so w0 = A r0 needs no
+  // barrier first; its window goes out through scratch2 before this
+  // all-reduce, which is then also the barrier before w0's window reads
+  if (zero_x0) {
+    for (int j = tid; j < P.wn; j += TH) wwin[j] = A.b[P.wlo + j];
+    for (int h = tid; h < A.hcap; h += TH) zhalo[h] = 0.0;
+    __syncthreads();
+    spmv(wg);  // w0 = A r0
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+      if (rrow[k] >= 0) A.scratch2[rrow[k]] = wg[k];
+  }
   allreduce2(part, dummy);
   const double b_norm = sqrt(part);
   const double bb = part;
@@ -530,17 +538,19 @@ __global__ void __launch_bounds__(TH, 1) clus_pcg_kernel(const ClusArgs A) {
     converged = 1;
     max_it = 0;
   } else {
-    for (int j = tid; j < P.wn; j += TH) wwin[j] = __ldcg(A.scratch + P.wlo + j);
-    for (int h = tid; h < A.hcap; h += TH) zhalo[h] = 0.0;
-    __syncthreads();
-    spmv(wg);  // w0 = A r0
-    // the window of w0 through a second scratch vector: no barrier for the
-    // other CTAs' reads of r0's window first
+    if (!zero_x0) {
+      for (int j = tid; j < P.wn; j += TH) wwin[j] = __ldcg(A.scratch + P.wlo + j);
+      for (int h = tid; h < A.hcap; h += TH) zhalo[h] = 0.0;
+      __syncthreads();
+      spmv(wg);  // w0 = A r0
+      // the window of w0 through a second scratch vector: no barrier for the
+      // other CTAs' reads of r0's window first
 #pragma unroll
-    for (int k = 0; k < NS; ++k)
-      if (rrow[k] >= 0) A.scratch2[rrow[k]] = wg[k];
-    part = dummy = 0.0;
-    allreduce2(part, dummy);  // (a barrier: every CTA sees the whole w0)
+      for (int k = 0; k < NS; ++k)
+        if (rrow[k] >= 0) A.scratch2[rrow[k]] = wg[k];
+      part = dummy = 0.0;
+      allreduce2(part, dummy);  // (a barrier: every CTA sees the whole w0)
+    }
     for (int j = tid; j < P.wn; j += TH) wwin[j] = __ldcg(A.scratch2 + P.wlo + j);
     __syncthreads();
   }
